@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200-native stencil engine.
+
+Workload (BASELINE.json configs[3], the stencil config the metric's HBM
+target is quoted on that fits one GPU): 2D XY periodic 9-point user-function
+stencil (fn_weighted_3x3, tests/test_stencil.cpp:88-93), FP64, 32768 x 32768
+synthetic random field. One step = one stencil application (compute + swap,
+stencil.cpp:197-235). value = Gpoints/s over all ranks; the input (8 GiB) is
+far larger than L2 (126 MB), so no L2 flush is needed between steps.
+
+Multi-GPU (torchrun, N>1): weak scaling — every rank owns a 32768 x 32768
+y-slab of a periodic N*32768-row grid and exchanges one halo row with each
+ring neighbour over NCCL per step (paper_1902_09931_b200/slab.py), overlapped
+with interior compute.
+
+Also reported: `e2e` (same metric through the C-ABI with HOST pinned grids,
+H2D + kernel + D2H per step), `roofline` (dominant kernel vs the measured HBM
+copy bandwidth), `cpu_baseline` (the reference library, oracle/_ref, on this
+host's cores over a bounded sample), `clocks`, `gpu_launches`, and `extra`
+(secondary configs: FP32 variant, batched 1D config 2, config 1, CH ADI).
+
+`--impl reference` times the reference's own CPU implementation on the same
+config (rank 0 only) and prints the same JSON line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "2D stencil Gpts/s (XY periodic 9-point user-function, FP64)"
+UNIT = "Gpts/s"
+NX = NY = 32768
+BYTES_PER_PT = {"f64": 16, "f32": 8}  # read once + write once
+WORKLOAD = "2D xy periodic 9-point user-function stencil (fn_weighted_3x3), 32768x32768"
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = ROOT / "gpurun_out" / f"clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.path.parent.mkdir(exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# --------------------------------------------------------------- reference
+
+
+def reference_arm(args, rank, world):
+    """Time the reference CPU implementation (oracle/_ref: the unmodified
+    reference library, all host threads) on a bounded sample of the config."""
+    if rank != 0:
+        return
+    line = cpu_reference_sample(target_s=max(5.0, args.ref_seconds))
+    out = {"metric": METRIC, "value": line["value"], "unit": UNIT, "n_gpus": world, "steps": line["reps"],
+           "warmup": 1, "ms_per_step": line["ms_per_app_sample"], "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": WORKLOAD, "nx": NX, "ny": NY, "sample_rows": line["rows"]},
+           "impl": "reference",
+           "cpu_baseline": {"value": line["value"], "unit": UNIT, "cores": line["cores"],
+                            "kind": line["kind"], "sample": line["sample"]},
+           "e2e": {"value": line["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def cpu_reference_sample(target_s=12.0, rows=2048):
+    """Reference compute() on a 32768 x `rows` periodic band, numWorkers =
+    numTiles = host threads, steady_clock around compute() only
+    (bench.cpp:33-40). Falls back to the C restatement (kind "port") only
+    if the reference library was never built."""
+    import numpy as np
+    from oracle.oracle import Reference, Restatement
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    rng = np.random.default_rng(4)
+    inp = rng.uniform(-1.0, 1.0, (rows, NX))
+    w = rng.uniform(-1.0, 1.0, 9)
+    try:
+        ref = Reference()
+        kind = "reference"
+        t1 = ref.stencil_timed(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3", tiles=min(cores, rows),
+                               workers=cores, warmup=1, reps=1)
+        reps = max(1, min(200, int(target_s / max(t1, 1e-6))))
+        secs = ref.stencil_timed(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3", tiles=min(cores, rows),
+                                 workers=cores, warmup=0, reps=reps)
+    except FileNotFoundError:
+        orc = Restatement()
+        kind = "port"
+        cores = 1
+        t0 = time.perf_counter()
+        reps = 1
+        orc.stencil(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3")
+        secs = time.perf_counter() - t0
+    pts = rows * NX
+    return {"value": pts / secs / 1e9, "cores": cores, "kind": kind, "reps": reps, "rows": rows,
+            "ms_per_app_sample": secs * 1e3,
+            "sample": f"{NX}x{rows} periodic band of the {NX}x{NY} config (fn_weighted_3x3, FP64), "
+                      f"{reps} timed compute() calls, numWorkers=numTiles={cores}"}
+
+
+# --------------------------------------------------------------------- ours
+
+
+def time_plan_steps(sg, torch, plan, steps, stream):
+    """Run `steps` compute+swap steps on `stream`; per-launch CUDA events.
+    Returns (total_ms, [per-launch ms])."""
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(steps):
+        ev[k][0].record(stream)
+        sg.compute(plan, stream=stream, synchronize=False)
+        ev[k][1].record(stream)
+        sg.swap_plan(plan)
+    end.record(stream)
+    end.synchronize()
+    return start.elapsed_time(end), [a.elapsed_time(b) for a, b in ev]
+
+
+def bench_device_stencil(sg, torch, dtype, nx, ny, steps, warmup, stream, fn="fn_weighted_3x3"):
+    import numpy as np
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(4)
+    a = torch.rand((ny, nx), dtype=tdt, device="cuda", generator=g).mul_(2).sub_(1)
+    b = torch.empty_like(a)
+    w = list(np.random.default_rng(4).uniform(-1, 1, 9))
+    plan = sg.create_plan(sg.Direction.XY, sg.BoundaryMode.Periodic,
+                          sg.FunctionStencil(sg.Extents(1, 1, 1, 1), fn, w), a, b, 1, 1)
+    with torch.cuda.stream(stream):
+        time_plan_steps(sg, torch, plan, warmup, stream)
+        torch.cuda.synchronize()
+        l0 = sg.launch_count()
+        total_ms, per = time_plan_steps(sg, torch, plan, steps, stream)
+        launches = sg.launch_count() - l0
+    sg.destroy_plan(plan)
+    del a, b
+    torch.cuda.empty_cache()
+    return total_ms, per, launches
+
+
+def bench_e2e(sg, torch, nx, ny, steps):
+    """Same metric through the C ABI with HOST (pinned) grids: every step
+    uploads the input, runs the kernel and downloads the output."""
+    import numpy as np
+    hin = torch.empty((ny, nx), dtype=torch.float64, pin_memory=True)
+    hout = torch.empty((ny, nx), dtype=torch.float64, pin_memory=True)
+    hin.uniform_(-1, 1)
+    gi, go = sg.Grid2D.from_array(hin.numpy()), sg.Grid2D.from_array(hout.numpy())
+    w = list(np.random.default_rng(4).uniform(-1, 1, 9))
+    plan = sg.create_plan(sg.Direction.XY, sg.BoundaryMode.Periodic,
+                          sg.FunctionStencil(sg.Extents(1, 1, 1, 1), "fn_weighted_3x3", w), gi, go, 1, 1)
+    sg.compute(plan, sg.Residency.Host)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sg.compute(plan, sg.Residency.Host)  # H2D + kernel + D2H, synchronous
+    dt = time.perf_counter() - t0
+    sg.destroy_plan(plan)
+    nbytes = nx * ny * 8
+    return {"value": nx * ny * steps / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": nbytes, "steps": steps,
+            "path": "sg_plan_compute(Residency::Host) on pinned host Grid2D buffers"}
+
+
+def extras(sg, torch, stream, peak):
+    """Secondary BASELINE.json configs, short runs; reported, not headline."""
+    import numpy as np
+    out = {}
+    # FP32 variant of config 4.
+    tot, per, _ = bench_device_stencil(sg, torch, "f32", NX, NY, 50, 5, stream)
+    kms = statistics.mean(per)
+    out["cfg4_fp32"] = {"gpts_s": NX * NY / kms / 1e6, "kernel_ms": kms,
+                        "hbm_frac": NX * NY * 8 / (kms * 1e-3) / 1e9 / peak}
+    # Config 2: batched 1D non-periodic 4th-derivative, 4096 x 4096 FP64,
+    # L2 flushed (256 MB write) between timed launches.
+    n = 4096
+    dx = 2 * np.pi / n
+    s4 = 1.0 / (dx ** 4)
+    a = torch.rand((n, n), dtype=torch.float64, device="cuda")
+    b = torch.zeros_like(a)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    plan = sg.create_plan(sg.Direction.X, sg.BoundaryMode.NonPeriodic,
+                          sg.WeightStencil(sg.Extents(2, 2, 0, 0), [s4, -4 * s4, 6 * s4, -4 * s4, s4]), a, b, 1, 1)
+    ts = []
+    with torch.cuda.stream(stream):
+        for k in range(23):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sg.compute(plan, stream=stream, synchronize=False)
+            e1.record(stream)
+            e1.synchronize()
+            if k >= 3:
+                ts.append(e0.elapsed_time(e1))
+    sg.destroy_plan(plan)
+    kms = statistics.median(ts)
+    alg = n * n * 8 + n * (n - 4) * 8
+    out["cfg2_batched1d_fp64"] = {"gpts_s": n * (n - 4) / kms / 1e6, "kernel_ms": kms,
+                                  "hbm_frac": alg / (kms * 1e-3) / 1e9 / peak, "l2": "flushed"}
+    del a, b, flush
+    torch.cuda.empty_cache()
+    # Config 1: 512^2 XY periodic 5-point Laplacian, 10 applications
+    # (Residency::Device between applications, one sync at the end).
+    m = 512
+    dx = 2 * np.pi / m
+    cx = 1.0 / (dx * dx)
+    lap = [0.0, cx, 0.0, cx, -2 * cx - 2 * cx, cx, 0.0, cx, 0.0]
+    x = np.random.default_rng(1).uniform(-1, 1, (m, m))
+    gi, go = sg.Grid2D.from_array(x), sg.Grid2D(m, m)
+    plan = sg.create_plan(sg.Direction.XY, sg.BoundaryMode.Periodic, sg.WeightStencil(sg.Extents(1, 1, 1, 1), lap),
+                          gi, go, 1, 1)
+    best = 1e9
+    for _ in range(5):
+        t0 = time.perf_counter()
+        for k in range(10):
+            sg.compute(plan, sg.Residency.Device if k < 9 else sg.Residency.Host)
+            if k < 9:
+                sg.swap_plan(plan)
+        best = min(best, time.perf_counter() - t0)
+    sg.destroy_plan(plan)
+    out["cfg1_512sq_10apps_ms"] = best * 1e3
+    if hasattr(sg, "CHStepper"):
+        out.update(bench_ch(sg, torch))
+    return out
+
+
+def bench_ch(sg, torch, n=1024, steps=1000):
+    p = sg.CHParams(nx=n, ny=n)
+    p.dt = 0.1 * p.dx()
+    p.T = steps * p.dt
+    st = sg.CHStepper(p)
+    st.step_many(20)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st.step_many(steps)
+    st.synchronize()
+    dt = time.perf_counter() - t0
+    return {"cfg3_ch_1024sq_steps_s": steps / dt, "cfg3_ch_1024sq_1000steps_s": dt}
+
+
+def ours_arm(args, rank, world, local_rank):
+    import torch
+
+    import paper_1902_09931_b200 as sg
+    torch.cuda.set_device(local_rank)
+    sg._lib.check(sg._lib.lib().sg_init(local_rank))
+    peak, peak_kind = measured_peak()
+    if world > 1:
+        from paper_1902_09931_b200 import slab
+        return slab.bench_multi_gpu(args, rank, world, local_rank, METRIC, UNIT, WORKLOAD, peak, peak_kind)
+
+    stream = torch.cuda.Stream()
+    with Clocks(local_rank) as clk:
+        total_ms, per, launches = bench_device_stencil(sg, torch, "f64", NX, NY, args.steps, args.warmup, stream)
+    clocks = clk.summary()
+    ms = total_ms / args.steps
+    value = NX * NY / (ms * 1e-3) / 1e9
+    kms = statistics.mean(per)
+    alg_bytes = NX * NY * BYTES_PER_PT["f64"]
+    achieved = alg_bytes / (kms * 1e-3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "traffic_r01.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("k_strip_fp64_3x3_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "nx": NX, "ny": NY, "fn": "fn_weighted_3x3",
+                   "boundary": "periodic", "direction": "xy", "l2": "input 8 GiB >> 126 MB L2, no flush needed",
+                   "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "k_strip<double,1,1,1,1,OpWeighted3x3>", "kernel_ms": kms,
+                     "algorithmic_bytes_per_launch": alg_bytes},
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+    }
+    if not args.skip_e2e:
+        line["e2e"] = bench_e2e(sg, torch, NX, NY, args.e2e_steps)
+    if not args.skip_extra:
+        try:
+            line["extra"] = extras(sg, torch, stream, peak)
+        except Exception as e:  # secondary numbers must not kill the headline
+            line["extra"] = {"error": repr(e)}
+    if not args.skip_cpu:
+        cb = cpu_reference_sample(target_s=args.ref_seconds)
+        line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"],
+                                "kind": cb["kind"], "sample": cb["sample"]}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-extra", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+    ours_arm(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

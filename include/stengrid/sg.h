@@ -1,0 +1,185 @@
+/*
+ * stengrid/sg.h — the C ABI of the B200-native stencil engine
+ * (libstengrid_b200.so). Plain pointers and sizes only; no torch or C++
+ * types cross this boundary. Every entry point returns sg_status; on error
+ * sg_last_error() holds a thread-local message (and, for SG_ERR_PENTA_SOLVE,
+ * the failing system index).
+ *
+ * Each function names the reference interface it replaces
+ * (/root/reference/proj/...). The reference is a C++ library with no FFI of
+ * its own; this ABI is what its C++ API (re-implemented on top of it in
+ * include/stengrid/*.hpp) and any ctypes/cffi binding call.
+ *
+ * Memory: grids are dense row-major (entry (i, j) at j*nx + i, grid.hpp:11-49).
+ * A plan binds either HOST buffers (the plan owns device mirrors and moves
+ * data according to the residency argument of sg_plan_compute) or DEVICE
+ * buffers (zero-copy; kernels read/write them directly).
+ */
+#ifndef STENGRID_SG_H
+#define STENGRID_SG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_ABI_VERSION 1
+
+typedef enum sg_status {
+  SG_OK = 0,
+  SG_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (stencil.cpp:128-161,206-207) */
+  SG_ERR_LOGIC = 2,            /* std::logic_error: destroyed plan (stencil.cpp:198,203) */
+  SG_ERR_PENTA_SOLVE = 3,      /* PentaSolveError{system} (penta.hpp:51-55) */
+  SG_ERR_DOMAIN = 4,           /* std::domain_error (cahn_hilliard.cpp:186,209) */
+  SG_ERR_CUDA = 5,             /* CUDA runtime failure */
+  SG_ERR_NO_DEVICE = 6         /* no CUDA device: there is no CPU fallback */
+} sg_status;
+
+typedef enum sg_direction { SG_DIR_X = 0, SG_DIR_Y = 1, SG_DIR_XY = 2 } sg_direction; /* stencil.hpp:35 */
+typedef enum sg_boundary { SG_PERIODIC = 0, SG_NONPERIODIC = 1 } sg_boundary;         /* grid.hpp:64 */
+typedef enum sg_dtype { SG_F64 = 0, SG_F32 = 1 } sg_dtype;
+typedef enum sg_residency { SG_RESIDENCY_HOST = 0, SG_RESIDENCY_DEVICE = 1 } sg_residency; /* stencil.hpp:37-38 */
+typedef enum sg_memory { SG_MEM_HOST = 0, SG_MEM_DEVICE = 1 } sg_memory;
+
+/* Device twins of the reference's window functions (the reference passes a
+ * host function pointer, stencil.hpp:20-25, which cannot run on a GPU). */
+typedef enum sg_function {
+  SG_FN_NONE = 0,                 /* weight stencil */
+  SG_FN_CH_NONLINEAR = 1,         /* ch_nonlinear_window, cahn_hilliard.cpp:36-47 (3x3, 9 coe) */
+  SG_FN_CENTRAL_DIFFERENCE = 2,   /* central_difference_window, tools/main.cpp:47-49 (3x1, 1 coe) */
+  SG_FN_CENTER = 3,               /* fn_center, tests/test_stencil.cpp:68 (>=2x2, 0 coe) */
+  SG_FN_CENTRAL_SECOND = 4,       /* fn_central_second, tests/test_stencil.cpp:70-77 (3x1, 1 coe) */
+  SG_FN_LAP_CUBE_DIFF_FIRST = 5,  /* fn_lap_cube_diff_first, tests/test_stencil.cpp:79-85 (3x3, 2 coe) */
+  SG_FN_WEIGHTED_3X3 = 6,         /* fn_weighted_3x3, tests/test_stencil.cpp:88-93 (3x3, 9 coe) */
+  SG_FN_COUNT = 7
+} sg_function;
+
+typedef struct sg_extents { int left, right, top, bottom; } sg_extents; /* grid.hpp:53-62 */
+
+typedef struct sg_plan_s* sg_plan_t;
+
+/* ---------------------------------------------------------------- library */
+int sg_abi_version(void);
+const char* sg_last_error(void);
+int sg_last_error_system(void);
+/* Number of kernels this library has launched in this process (all entry
+ * points); used by bench.py to report gpu_launches. */
+uint64_t sg_launch_count(void);
+/* Initialise the CUDA context on `device` (cudaSetDevice); SG_ERR_NO_DEVICE
+ * when no GPU is visible. */
+sg_status sg_init(int device);
+/* Minimum coefficient count a device window function reads; -1 if unknown. */
+int sg_function_min_coe(int fn);
+/* Name of a device window function ("ch_nonlinear_window", ...). */
+const char* sg_function_name(int fn);
+
+/* ----------------------------------------------------------- grid helpers */
+/* wrap(i, n): grid.cpp:42-47. SG_ERR_INVALID_ARGUMENT if n <= 0. */
+sg_status sg_wrap(int64_t i, int n, int* out);
+/* make_tiles(ny, numTiles): grid.cpp:62-82; begins/ends hold numTiles ints. */
+sg_status sg_make_tiles(int ny, int numTiles, int* begins, int* ends);
+
+/* ---------------------------------------------------------- stencil plans
+ * Replaces create_plan (stencil.hpp:90-92, stencil.cpp:152-184). fn ==
+ * SG_FN_NONE selects a weight stencil with `count` weights (row-major W*H,
+ * stencil.hpp:12-18); otherwise `values` is the coefficient array of the
+ * device window function (FunctionStencil::coe, stencil.hpp:29-33).
+ * numTiles keeps make_tiles validation (1 <= numTiles <= ny) and is the
+ * y-slab count; numWorkers must be >= 1 (SPEC maps workers to devices).
+ * Validation and error classes follow stencil.cpp:128-161 exactly. */
+sg_status sg_plan_create(sg_direction dir, sg_boundary mode, sg_extents ext, sg_function fn,
+                         const double* values, size_t count, sg_dtype dtype, void* in, void* out,
+                         int nx, int ny, sg_memory memory, int numTiles, int numWorkers,
+                         sg_plan_t* plan);
+/* compute (stencil.cpp:202-235). HOST residency: host grids are
+ * authoritative — the input is uploaded, the output downloaded. DEVICE
+ * residency: the input is uploaded only if its device copy is stale, the
+ * output stays on the device until sg_plan_sync_to_host. `stream` is a
+ * cudaStream_t (NULL = the plan's own stream); `synchronize` != 0 blocks
+ * until the result is complete (the reference's compute is synchronous). */
+sg_status sg_plan_compute(sg_plan_t plan, sg_residency residency, void* stream, int synchronize);
+/* swap_plan (stencil.cpp:197-200): exchange input and output bindings. */
+sg_status sg_plan_swap(sg_plan_t plan);
+/* destroy_plan (stencil.cpp:186-195): idempotent, never touches the grids;
+ * *plan is set to NULL. */
+sg_status sg_plan_destroy(sg_plan_t* plan);
+/* Copy any device-resident bound grid back to its host buffer. */
+sg_status sg_plan_sync_to_host(sg_plan_t plan);
+/* Mark a host-bound grid as modified on the host (which = 0 input, 1 output). */
+sg_status sg_plan_mark_host_dirty(sg_plan_t plan, int which);
+/* Current bindings (which = 0 input, 1 output): host/device pointers. */
+sg_status sg_plan_binding(sg_plan_t plan, int which, void** host_ptr, void** device_ptr);
+/* 1 if the plan is valid (not destroyed). */
+int sg_plan_valid(sg_plan_t plan);
+/* Which kernel the plan dispatches to: 1 = register-strip fast path, 0 =
+ * generic one-point-per-thread path. */
+int sg_plan_kernel_kind(sg_plan_t plan);
+
+/* --------------------------------------------------------- slab launches
+ * Stateless device launch used by the multi-GPU y-slab decomposition (and
+ * internally by plans). Computes output rows [row0, row1) and columns
+ * [col0, col1) of `out` (row pitch nx). Output row j reads input rows
+ * j + inShift - top + q (q = 0..H-1), wrapped modulo inRows when wrapY,
+ * from `in` (row pitch nx, inRows rows); columns wrap modulo nx when wrapX.
+ * A slab stored with `h` halo rows above its own rows uses inShift = h. */
+typedef struct sg_slab_desc {
+  int nx;
+  int inRows;
+  int inShift;
+  int row0, row1;
+  int col0, col1;
+  int wrapX, wrapY;
+} sg_slab_desc;
+sg_status sg_stencil_launch(const sg_slab_desc* desc, sg_extents ext, sg_function fn,
+                            const double* values, size_t count, sg_dtype dtype, const void* in,
+                            void* out, void* stream);
+
+/* ---------------------------------------------------- pentadiagonal batch
+ * PentaFactor / PeriodicPentaFactor (penta.hpp:57-100, penta.cpp:93-295) on
+ * the device. Bands are interleaved (r*B + b, penta.hpp:12-20), `memory`
+ * says where they live. The factorization runs on the device, one system per
+ * thread; a zero pivot returns SG_ERR_PENTA_SOLVE with the system index. */
+typedef struct sg_penta_s* sg_penta_t;
+sg_status sg_penta_create(int batchCount, int n, int periodic, const double* secondSub,
+                          const double* sub, const double* diag, const double* super,
+                          const double* secondSuper, sg_memory memory, sg_penta_t* factor);
+/* solve_in_place (penta.cpp:199-202, 289-295) on an interleaved rhs batch. */
+sg_status sg_penta_solve(sg_penta_t factor, double* rhs, sg_memory memory, void* stream,
+                         int synchronize);
+sg_status sg_penta_destroy(sg_penta_t* factor);
+
+/* ----------------------------------------------------- Cahn-Hilliard ADI
+ * CHParams (cahn_hilliard.hpp:23-39) + CHStepper (:104-137). */
+typedef struct sg_ch_params {
+  double D, gamma, lx, ly, dt, T, icAmplitude;
+  int nx, ny;
+  uint64_t seed;
+  int nonlinearEnabled;
+} sg_ch_params;
+typedef struct sg_ch_s* sg_ch_t;
+/* CHParams defaults (D=1, gamma=0.01, 512^2, 2*pi box, seed 1, amp 0.1). */
+void sg_ch_default_params(sg_ch_params* p);
+/* CHParams::validate (cahn_hilliard.cpp:56-66). */
+sg_status sg_ch_validate(const sg_ch_params* p);
+/* CHStepper ctor (cahn_hilliard.cpp:213-241): initial condition generated on
+ * the device from SplitMix64, C^{n-1} := C^n, factors built. */
+sg_status sg_ch_create(const sg_ch_params* p, int numTiles, int numWorkers, sg_ch_t* ch);
+/* `steps` calls of CHStepper::step (cahn_hilliard.cpp:260-328). */
+sg_status sg_ch_step(sg_ch_t ch, int steps);
+/* set_state (cahn_hilliard.cpp:251-258): host arrays nx*ny; resets step/time. */
+sg_status sg_ch_set_state(sg_ch_t ch, const double* curr, const double* prev, sg_memory memory);
+/* field() / previous_field(): which = 0 C^n, 1 C^{n-1}; copies nx*ny doubles. */
+sg_status sg_ch_get_field(sg_ch_t ch, int which, double* out, sg_memory memory);
+sg_status sg_ch_device_field(sg_ch_t ch, int which, const double** dptr);
+sg_status sg_ch_status(sg_ch_t ch, int* step, double* time);
+/* Diagnostics (cahn_hilliard.cpp:330-340) via the reference host algorithm
+ * on a downloaded copy of C^n. */
+sg_status sg_ch_destroy(sg_ch_t* ch);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STENGRID_SG_H */

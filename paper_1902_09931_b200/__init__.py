@@ -1,0 +1,30 @@
+"""paper_1902_09931_b200 — B200-native cuSten/stengrid stencil engine.
+
+The compute path is libstengrid_b200.so (hand-written sm_100a CUDA behind the
+C ABI in include/stengrid/sg.h). This package is the Python host-side mirror
+of the reference's API (stengrid/stencil.hpp, penta.hpp, cahn_hilliard.hpp)
+plus the multi-GPU y-slab plumbing. There is no CPU fallback.
+"""
+from . import _lib
+from ._lib import (CudaError, DomainError, InvalidArgument, LogicError, NoDeviceError,
+                   PentaSolveError, launch_count)
+from .stencil import (BoundaryMode, Direction, Extents, FunctionStencil, Grid2D, Residency,
+                      StencilPlan, WeightStencil, compute, create_plan, destroy_plan,
+                      launch_slab, make_tiles, mark_host_dirty, swap_plan, sync_to_host, wrap)
+
+from .penta import (Axis, PentaBatch, PentaFactor, PeriodicPentaFactor, RhsBatch,
+                    build_hyperdiffusion_operator, deinterleave, interleave, solve_batch,
+                    solve_periodic_batch)
+from .cahn_hilliard import (CHParams, CHStepper, Diagnostics, biharmonic_weights,
+                            nonlinear_laplacian_coefficients)
+
+__all__ = [
+    "Axis", "PentaBatch", "PentaFactor", "PeriodicPentaFactor", "RhsBatch",
+    "build_hyperdiffusion_operator", "deinterleave", "interleave", "solve_batch",
+    "solve_periodic_batch", "CHParams", "CHStepper", "Diagnostics", "biharmonic_weights",
+    "nonlinear_laplacian_coefficients",
+    "BoundaryMode", "Direction", "Extents", "FunctionStencil", "Grid2D", "Residency",
+    "StencilPlan", "WeightStencil", "compute", "create_plan", "destroy_plan", "launch_slab",
+    "make_tiles", "mark_host_dirty", "swap_plan", "sync_to_host", "wrap", "InvalidArgument",
+    "LogicError", "DomainError", "PentaSolveError", "CudaError", "NoDeviceError", "launch_count",
+]

@@ -1,0 +1,376 @@
+// capi.cu — the extern "C" boundary (include/stengrid/sg.h): stencil plans,
+// grid helpers, error reporting. Validation order and messages follow the
+// reference's create_plan / validate_kind / make_tiles / compute
+// (stencil.cpp:128-235, grid.cpp:42-82) so the C++ layer can rethrow the
+// same exception types for the same conditions.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "sg_internal.hpp"
+
+namespace {
+
+thread_local std::string t_msg;
+thread_local int t_system = -1;
+
+template <typename F>
+sg_status guard(F&& f) {
+  try {
+    f();
+    return SG_OK;
+  } catch (const sg::Error& e) {
+    t_msg = e.what();
+    t_system = e.system;
+    return e.status;
+  } catch (const std::exception& e) {
+    t_msg = e.what();
+    return SG_ERR_CUDA;
+  }
+}
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw sg::Error(SG_ERR_NO_DEVICE, "stengrid: no CUDA device visible (there is no CPU fallback)");
+}
+
+std::vector<std::pair<int, int>> tiles_for(int ny, int numTiles) {
+  // make_tiles, grid.cpp:62-82
+  if (ny < 1) sg::invalid("make_tiles: ny must be >= 1");
+  if (numTiles < 1 || numTiles > ny)
+    sg::invalid("make_tiles: numTiles must satisfy 1 <= numTiles <= ny");
+  std::vector<std::pair<int, int>> t;
+  const int base = ny / numTiles, extra = ny % numTiles;
+  int j = 0;
+  for (int k = 0; k < numTiles; ++k) {
+    const int rows = base + (k < extra ? 1 : 0);
+    t.emplace_back(j, j + rows);
+    j += rows;
+  }
+  return t;
+}
+
+}  // namespace
+
+struct sg_plan_s {
+  bool valid = false;
+  sg_direction dir = SG_DIR_X;
+  sg_boundary mode = SG_PERIODIC;
+  sg_extents ext{};
+  int fn = SG_FN_NONE;
+  std::vector<double> values;
+  sg_dtype dtype = SG_F64;
+  int nx = 0, ny = 0;
+  sg_memory memory = SG_MEM_HOST;
+  int numTiles = 1, numWorkers = 1;
+  std::vector<std::pair<int, int>> tiles;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  struct Buf {
+    void* host = nullptr;
+    void* dev = nullptr;
+    bool owned = false;     // device mirror allocated by the plan
+    bool devValid = false;  // device copy holds the current values
+    bool hostValid = true;  // host copy holds the current values
+  } buf[2];
+  int inIdx = 0;
+
+  size_t bytes() const { return static_cast<size_t>(nx) * ny * (dtype == SG_F64 ? 8 : 4); }
+
+  void release() {
+    if (!valid) return;
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& b : buf)
+      if (b.owned && b.dev) cudaFree(b.dev);
+    if (stream) cudaStreamDestroy(stream);
+    stream = nullptr;
+    buf[0] = Buf{};
+    buf[1] = Buf{};
+    tiles.clear();
+    values.clear();
+    valid = false;
+  }
+};
+
+extern "C" {
+
+sg_status sg_internal_set_error(const char* msg, int system) {
+  t_msg = msg;
+  t_system = system;
+  return SG_OK;
+}
+
+int sg_abi_version(void) { return SG_ABI_VERSION; }
+const char* sg_last_error(void) { return t_msg.c_str(); }
+int sg_last_error_system(void) { return t_system; }
+uint64_t sg_launch_count(void) { return sg::g_launches.load(); }
+
+sg_status sg_init(int device) {
+  return guard([&] {
+    require_device();
+    SG_CUDA(cudaSetDevice(device));
+    SG_CUDA(cudaFree(nullptr));
+  });
+}
+
+int sg_function_min_coe(int fn) {
+  int w, h, c;
+  return sg::function_shape(fn, &w, &h, &c) ? c : -1;
+}
+const char* sg_function_name(int fn) { return sg::function_name(fn); }
+
+sg_status sg_wrap(int64_t i, int n, int* out) {
+  return guard([&] {
+    if (n <= 0) sg::invalid("wrap: period must be >= 1");
+    int64_t r = i % n;
+    if (r < 0) r += n;
+    *out = static_cast<int>(r);
+  });
+}
+
+sg_status sg_make_tiles(int ny, int numTiles, int* begins, int* ends) {
+  return guard([&] {
+    const auto t = tiles_for(ny, numTiles);
+    for (size_t k = 0; k < t.size(); ++k) {
+      begins[k] = t[k].first;
+      ends[k] = t[k].second;
+    }
+  });
+}
+
+sg_status sg_plan_create(sg_direction dir, sg_boundary mode, sg_extents ext, sg_function fn,
+                         const double* values, size_t count, sg_dtype dtype, void* in, void* out,
+                         int nx, int ny, sg_memory memory, int numTiles, int numWorkers,
+                         sg_plan_t* plan) {
+  return guard([&] {
+    if (!plan) sg::invalid("create_plan: null plan handle");
+    *plan = nullptr;
+    if (nx < 1 || ny < 1) sg::invalid("Grid2D: nx and ny must be >= 1");
+    if (dtype != SG_F64 && dtype != SG_F32) sg::invalid("create_plan: unknown dtype");
+    if (dir != SG_DIR_X && dir != SG_DIR_Y && dir != SG_DIR_XY)
+      sg::invalid("create_plan: unknown direction");
+    if (mode != SG_PERIODIC && mode != SG_NONPERIODIC) sg::invalid("create_plan: unknown boundary mode");
+    // stencil.cpp:156-157
+    if (in == out || in == nullptr || out == nullptr)
+      sg::invalid("create_plan: input and output must be distinct buffers");
+    // validate_kind, stencil.cpp:128-148
+    if (ext.left < 0 || ext.right < 0 || ext.top < 0 || ext.bottom < 0)
+      sg::invalid("create_plan: negative stencil extents");
+    if (dir == SG_DIR_X && (ext.top != 0 || ext.bottom != 0))
+      sg::invalid("create_plan: X-direction stencil requires top = bottom = 0");
+    if (dir == SG_DIR_Y && (ext.left != 0 || ext.right != 0))
+      sg::invalid("create_plan: Y-direction stencil requires left = right = 0");
+    if (ext.left >= nx || ext.right >= nx || ext.top >= ny || ext.bottom >= ny)
+      sg::invalid("create_plan: stencil extents must be smaller than the grid");
+    const long long W = ext.left + ext.right + 1, H = ext.top + ext.bottom + 1;
+    if (fn == SG_FN_NONE) {
+      if (count == 0) sg::invalid("create_plan: empty weight array");
+      if (static_cast<long long>(count) != W * H)
+        sg::invalid("create_plan: weight count does not match the stencil window");
+      for (size_t k = 0; k < count; ++k)
+        if (!std::isfinite(values[k])) sg::invalid("create_plan: non-finite stencil weight");
+    } else {
+      int mw, mh, mc;
+      if (!sg::function_shape(fn, &mw, &mh, &mc))
+        sg::invalid("create_plan: null stencil function");
+      // The reference would read outside the window / coefficient array
+      // (undefined behaviour); the device path rejects it instead.
+      if (W < mw || H < mh)
+        sg::invalid(std::string("create_plan: window smaller than ") + sg::function_name(fn) + " reads");
+      if (static_cast<long long>(count) < mc)
+        sg::invalid(std::string("create_plan: too few coefficients for ") + sg::function_name(fn));
+      if (W * H > 256 && !(W == 3 && H <= 3))
+        sg::invalid("create_plan: device function windows are limited to 256 taps");
+    }
+    if (numWorkers < 1) sg::invalid("create_plan: numWorkers must be >= 1");
+    auto tiles = tiles_for(ny, numTiles);
+    require_device();
+
+    auto* p = new sg_plan_s();
+    p->dir = dir;
+    p->mode = mode;
+    p->ext = ext;
+    p->fn = fn;
+    p->values.assign(values, values + count);
+    p->dtype = dtype;
+    p->nx = nx;
+    p->ny = ny;
+    p->memory = memory;
+    p->numTiles = numTiles;
+    p->numWorkers = numWorkers;
+    p->tiles = std::move(tiles);
+    try {
+      SG_CUDA(cudaGetDevice(&p->device));
+      SG_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+      void* ptrs[2] = {in, out};
+      for (int k = 0; k < 2; ++k) {
+        auto& b = p->buf[k];
+        if (memory == SG_MEM_DEVICE) {
+          b.dev = ptrs[k];
+          b.devValid = true;
+          b.hostValid = false;
+        } else {
+          b.host = ptrs[k];
+          SG_CUDA(cudaMalloc(&b.dev, p->bytes()));
+          b.owned = true;
+        }
+      }
+      p->valid = true;
+    } catch (...) {
+      p->valid = true;
+      p->release();
+      delete p;
+      throw;
+    }
+    *plan = p;
+  });
+}
+
+static sg_slab_desc full_grid_desc(const sg_plan_s* p) {
+  // make_geom, stencil.cpp:26-40
+  sg_slab_desc d{};
+  d.nx = p->nx;
+  d.inRows = p->ny;
+  d.inShift = 0;
+  const bool periodic = p->mode == SG_PERIODIC;
+  d.wrapX = d.wrapY = periodic ? 1 : 0;
+  d.row0 = periodic ? 0 : p->ext.top;
+  d.row1 = periodic ? p->ny : p->ny - p->ext.bottom;
+  if (periodic) {
+    d.col0 = 0;
+    d.col1 = p->nx;
+  } else {
+    const int fastLo = std::min(p->ext.left, p->nx);
+    const int hi = std::min(p->nx - p->ext.right, p->nx);
+    d.col0 = fastLo;
+    d.col1 = std::max(hi, fastLo);
+  }
+  return d;
+}
+
+sg_status sg_plan_compute(sg_plan_t p, sg_residency residency, void* stream, int synchronize) {
+  return guard([&] {
+    if (!p || !p->valid) sg::logic("compute: plan was destroyed");
+    SG_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    auto& in = p->buf[p->inIdx];
+    auto& out = p->buf[1 - p->inIdx];
+    if (in.dev == out.dev) sg::invalid("compute: bound grids alias");
+    const bool periodic = p->mode == SG_PERIODIC;
+    if (p->memory == SG_MEM_HOST) {
+      // HOST residency: a host grid holding valid values is authoritative
+      // (re-uploaded on every compute); a grid whose newest values were left
+      // on the device by a Device-residency compute is used from there.
+      if (!in.devValid || (residency == SG_RESIDENCY_HOST && in.hostValid)) {
+        if (!in.hostValid) sg::logic("compute: input has no valid copy");
+        SG_CUDA(cudaMemcpyAsync(in.dev, in.host, p->bytes(), cudaMemcpyHostToDevice, s));
+        in.devValid = true;
+      }
+      // Non-periodic stencils leave the output frame untouched: the device
+      // output must carry the caller's frame values.
+      if (!periodic && (!out.devValid || (residency == SG_RESIDENCY_HOST && out.hostValid))) {
+        SG_CUDA(cudaMemcpyAsync(out.dev, out.host, p->bytes(), cudaMemcpyHostToDevice, s));
+        out.devValid = true;
+      }
+    }
+    const sg_slab_desc d = full_grid_desc(p);
+    sg::launch_stencil(d, p->ext, p->fn, p->values.data(), p->values.size(), p->dtype, in.dev,
+                       out.dev, s);
+    out.devValid = true;
+    if (p->memory == SG_MEM_HOST) {
+      out.hostValid = false;
+      if (residency == SG_RESIDENCY_HOST) {
+        SG_CUDA(cudaMemcpyAsync(out.host, out.dev, p->bytes(), cudaMemcpyDeviceToHost, s));
+        out.hostValid = true;
+        synchronize = 1;  // host result must be complete on return
+      }
+    }
+    if (synchronize) SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+sg_status sg_plan_swap(sg_plan_t p) {
+  return guard([&] {
+    if (!p || !p->valid) sg::logic("swap_plan: plan was destroyed");
+    p->inIdx = 1 - p->inIdx;
+  });
+}
+
+sg_status sg_plan_destroy(sg_plan_t* p) {
+  return guard([&] {
+    if (!p || !*p) return;
+    (*p)->release();
+    delete *p;
+    *p = nullptr;
+  });
+}
+
+sg_status sg_plan_sync_to_host(sg_plan_t p) {
+  return guard([&] {
+    if (!p || !p->valid) sg::logic("sync_to_host: plan was destroyed");
+    if (p->memory != SG_MEM_HOST) return;
+    SG_CUDA(cudaSetDevice(p->device));
+    for (auto& b : p->buf)
+      if (!b.hostValid && b.devValid) {
+        SG_CUDA(cudaMemcpyAsync(b.host, b.dev, p->bytes(), cudaMemcpyDeviceToHost, p->stream));
+        b.hostValid = true;
+      }
+    SG_CUDA(cudaStreamSynchronize(p->stream));
+  });
+}
+
+sg_status sg_plan_mark_host_dirty(sg_plan_t p, int which) {
+  return guard([&] {
+    if (!p || !p->valid) sg::logic("mark_host_dirty: plan was destroyed");
+    if (which != 0 && which != 1) sg::invalid("mark_host_dirty: which must be 0 or 1");
+    auto& b = p->buf[which == 0 ? p->inIdx : 1 - p->inIdx];
+    if (p->memory == SG_MEM_HOST) {
+      b.hostValid = true;
+      b.devValid = false;
+    }
+  });
+}
+
+sg_status sg_plan_binding(sg_plan_t p, int which, void** host_ptr, void** device_ptr) {
+  return guard([&] {
+    if (!p || !p->valid) sg::logic("binding: plan was destroyed");
+    if (which != 0 && which != 1) sg::invalid("binding: which must be 0 or 1");
+    auto& b = p->buf[which == 0 ? p->inIdx : 1 - p->inIdx];
+    if (host_ptr) *host_ptr = b.host;
+    if (device_ptr) *device_ptr = b.dev;
+  });
+}
+
+int sg_plan_valid(sg_plan_t p) { return p && p->valid ? 1 : 0; }
+
+int sg_plan_kernel_kind(sg_plan_t p) {
+  if (!p || !p->valid) return -1;
+  const sg_slab_desc d = full_grid_desc(p);
+  return sg::stencil_kernel_kind(d, p->ext, p->fn, p->values.size(), p->dtype,
+                                 p->buf[p->inIdx].dev, p->buf[1 - p->inIdx].dev);
+}
+
+sg_status sg_stencil_launch(const sg_slab_desc* desc, sg_extents ext, sg_function fn,
+                            const double* values, size_t count, sg_dtype dtype, const void* in,
+                            void* out, void* stream) {
+  return guard([&] {
+    if (!desc) sg::invalid("stencil_launch: null descriptor");
+    const sg_slab_desc& d = *desc;
+    if (d.nx < 1 || d.inRows < 1) sg::invalid("stencil_launch: empty input");
+    if (d.col0 < 0 || d.col1 > d.nx || d.row0 < 0) sg::invalid("stencil_launch: bad output window");
+    if (!d.wrapY && d.row1 > d.row0 &&
+        (d.row0 + d.inShift - ext.top < 0 || d.row1 - 1 + d.inShift + ext.bottom >= d.inRows))
+      sg::invalid("stencil_launch: rows outside the input slab (missing halo)");
+    if (in == out) sg::invalid("stencil_launch: input and output must be distinct buffers");
+    require_device();
+    sg::launch_stencil(d, ext, fn, values, count, dtype, in, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,597 @@
+// ch.cu — Cahn-Hilliard BDF2-ADI stepper, end to end on the GPU.
+//
+// Replaces CHStepper (cahn_hilliard.cpp:213-328). One step is five kernels,
+// captured once into a CUDA graph per time-level parity:
+//
+//   k_rhs        Cbar = 2C^n - C^{n-1} (on the fly), nl = lap(C^3 - C) over
+//                3x3 of C^n, bih = 5x5 biharmonic over Cbar, and
+//                rhs = kDiff (C^n - C^{n-1}) - kBih bih + kNl nl
+//                (cahn_hilliard.cpp:264-297) — one fused pass, written
+//                TRANSPOSED (rhsT[i*ny + j]) through a shared-memory tile so
+//                the x-sweep sees interleaved systems (the reference's
+//                interleave_into(rhs, X), penta.cpp:343-360, for free).
+//   x-sweep      ny periodic systems of nx unknowns, one per thread,
+//                coalesced (penta.cu k_sweep); the Woodbury correction is
+//                NOT applied in place — y = K^{-1} V^T z goes to y4x.
+//   k_transpose_correct
+//                w(i,j) = zT(i,j) - (W0[i] y0[j] + ... + W3[i] y3[j]) fused
+//                with the transpose back to row-major (the reference's
+//                correct_range + deinterleave + transpose + interleave,
+//                penta.cpp:253-287, 369-384, grid.cpp:55-60).
+//   y-sweep      nx periodic systems of ny unknowns on row-major w (already
+//                interleaved for Axis::Y, penta.cpp:356-358); y -> y4y.
+//   k_combine    C^{n+1} = Cbar + (w - W·y) written over C^{n-1} in place;
+//                the time levels then swap roles (cahn_hilliard.cpp:311-324).
+//
+// Arithmetic is the reference's term for term (no FMA contraction), so the
+// fields are bitwise identical to the CPU reference. The only liberty: taps
+// whose weight is exactly 0.0 (4 of the 9 nonlinear coefficients, 12 of the
+// 25 biharmonic weights — verified at construction) are skipped; for finite
+// fields acc + 0*x == acc exactly (acc starts at +0 and is never -0).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "penta.cuh"
+#include "sg_internal.hpp"
+
+namespace sg {
+namespace {
+
+constexpr double kTwoThirds = 2.0 / 3.0;  // cahn_hilliard.cpp:12
+
+double pow4(double h) {  // cahn_hilliard.cpp:14-17
+  const double h2 = h * h;
+  return h2 * h2;
+}
+
+// biharmonic_weights (cahn_hilliard.cpp:85-114), host setup constant.
+void biharmonic_weights(double dx, double dy, double* w) {
+  const double ax = 1.0 / pow4(dx);
+  const double ay = 1.0 / pow4(dy);
+  const double cr = 2.0 / ((dx * dx) * (dy * dy));
+  for (int k = 0; k < 25; ++k) w[k] = 0.0;
+  auto at = [w](int p, int q) -> double& { return w[q * 5 + p]; };
+  at(0, 2) += ax;
+  at(1, 2) += -4.0 * ax;
+  at(2, 2) += 6.0 * ax;
+  at(3, 2) += -4.0 * ax;
+  at(4, 2) += ax;
+  at(2, 0) += ay;
+  at(2, 1) += -4.0 * ay;
+  at(2, 2) += 6.0 * ay;
+  at(2, 3) += -4.0 * ay;
+  at(2, 4) += ay;
+  static constexpr double cross[9] = {1.0, -2.0, 1.0, -2.0, 4.0, -2.0, 1.0, -2.0, 1.0};
+  for (int q = 0; q < 3; ++q)
+    for (int p = 0; p < 3; ++p) at(p + 1, q + 1) += cross[q * 3 + p] * cr;
+  double prefix = 0.0;
+  for (int k = 0; k < 22; ++k) prefix += w[k];
+  at(2, 4) = -prefix;
+}
+
+// Non-zero taps of the two CH windows (row-major positions q*W + p).
+#define SG_BIH_TAPS {2, 6, 7, 8, 10, 11, 12, 13, 14, 16, 17, 18, 22}
+#define SG_NL_TAPS {1, 3, 4, 5, 7}
+
+struct RhsParams {
+  double bw[25];
+  double nl[9];
+  double kDiff, kBih, kNl;
+};
+
+__global__ void k_init(unsigned long long seed, double amp, long long count, double* __restrict__ out) {
+  // SplitMix64 (cahn_hilliard.hpp:47-63) in counter form: draw k uses state
+  // seed + (k+1)*golden, so every element is independent.
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  unsigned long long z = seed + static_cast<unsigned long long>(k + 1) * 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  z = z ^ (z >> 31);
+  const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
+  out[k] = amp * (2.0 * u - 1.0);  // initial_condition, cahn_hilliard.cpp:74
+}
+
+constexpr int TS = 32;  // output tile edge
+constexpr int HALO = 2;
+constexpr int TE = TS + 2 * HALO;
+
+__device__ __forceinline__ int wrapi(int i, int n) {
+  int r = i % n;
+  return r < 0 ? r + n : r;
+}
+
+template <bool NONLINEAR>
+__global__ void __launch_bounds__(256) k_rhs(const double* __restrict__ cc, const double* __restrict__ cp,
+                                             double* __restrict__ rhsT, int nx, int ny,
+                                             const __grid_constant__ RhsParams P) {
+  __shared__ double sc[TE][TE + 1];  // C^n with a 2-point halo
+  __shared__ double sb[TE][TE + 1];  // Cbar with a 2-point halo
+  const int i0 = blockIdx.x * TS, j0 = blockIdx.y * TS;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int y = ty; y < TE; y += blockDim.y) {
+    const int j = wrapi(j0 - HALO + y, ny);
+    for (int x = tx; x < TE; x += blockDim.x) {
+      const int i = wrapi(i0 - HALO + x, nx);
+      const long long idx = static_cast<long long>(j) * nx + i;
+      const double c = __ldg(cc + idx), p = __ldg(cp + idx);
+      sc[y][x] = c;
+      sb[y][x] = 2.0 * c - p;  // cahn_hilliard.cpp:273
+    }
+  }
+  __syncthreads();
+  constexpr int kBihTaps[13] = SG_BIH_TAPS;
+  constexpr int kNlTaps[5] = SG_NL_TAPS;
+  double res[TS / 8];
+#pragma unroll
+  for (int k = 0; k < TS / 8; ++k) {
+    const int y = ty + 8 * k;  // output row within the tile
+    const int x = tx;
+    double bh = 0.0;
+#pragma unroll
+    for (int t = 0; t < 13; ++t) {
+      const int q = kBihTaps[t] / 5, p = kBihTaps[t] % 5;
+      bh += P.bw[kBihTaps[t]] * sb[y + q][x + p];
+    }
+    const int i = (i0 + x) % nx, j = (j0 + y) % ny;
+    const long long idx = static_cast<long long>(j) * nx + i;
+    const double c = sc[y + HALO][x + HALO];
+    const double pr = __ldg(cp + idx);
+    double r;
+    if constexpr (NONLINEAR) {
+      double nl = 0.0;
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        const int q = kNlTaps[t] / 3, p = kNlTaps[t] % 3;
+        const double v = sc[y + 1 + q][x + 1 + p];
+        nl += P.nl[kNlTaps[t]] * (v * v * v - v);
+      }
+      r = P.kDiff * (c - pr) - P.kBih * bh + P.kNl * nl;  // cahn_hilliard.cpp:292
+    } else {
+      r = P.kDiff * (c - pr) - P.kBih * bh;  // cahn_hilliard.cpp:294
+    }
+    res[k] = r;
+  }
+  __syncthreads();
+  // stage the tile transposed in smem, then write rhsT[i*ny + j] coalesced in j
+#pragma unroll
+  for (int k = 0; k < TS / 8; ++k) sc[tx][ty + 8 * k] = res[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < TS / 8; ++k) {
+    const int x = ty + 8 * k;  // i within the tile
+    const int i = i0 + x, j = j0 + tx;
+    if (i < nx && j < ny) rhsT[static_cast<long long>(i) * ny + j] = sc[x][tx];
+  }
+}
+
+struct CorrTables {
+  const double* W[4];
+  const double* y4;  // y4[k*B + b]
+};
+
+// w(i,j) = zT[i*ny + j] - (Wx0[i] y0[j] + Wx1[i] y1[j] + Wx2[i] y2[j] + Wx3[i] y3[j])
+__global__ void __launch_bounds__(256) k_transpose_correct(const double* __restrict__ zT,
+                                                           double* __restrict__ w, int nx, int ny,
+                                                           const CorrTables t) {
+  __shared__ double tile[TS][TS + 1];
+  const int i0 = blockIdx.x * TS, j0 = blockIdx.y * TS;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  // read zT rows i (contiguous j), apply the correction
+#pragma unroll
+  for (int k = 0; k < TS / 8; ++k) {
+    const int i = i0 + ty + 8 * k, j = j0 + tx;
+    if (i < nx && j < ny) {
+      const double z = zT[static_cast<long long>(i) * ny + j];
+      const double corr = __ldg(t.W[0] + i) * __ldg(t.y4 + j) + __ldg(t.W[1] + i) * __ldg(t.y4 + ny + j) +
+                          __ldg(t.W[2] + i) * __ldg(t.y4 + 2LL * ny + j) +
+                          __ldg(t.W[3] + i) * __ldg(t.y4 + 3LL * ny + j);
+      tile[ty + 8 * k][tx] = z - corr;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < TS / 8; ++k) {
+    const int j = j0 + ty + 8 * k, i = i0 + tx;
+    if (i < nx && j < ny) w[static_cast<long long>(j) * nx + i] = tile[tx][ty + 8 * k];
+  }
+}
+
+// C^{n+1} = (2 C^n - C^{n-1}) + (w - (Wy0[j] y0[i] + ... + Wy3[j] y3[i])), over C^{n-1}.
+__global__ void __launch_bounds__(256) k_combine(const double* __restrict__ cc, double* __restrict__ cpNext,
+                                                 const double* __restrict__ w, int nx, int ny,
+                                                 const CorrTables t) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long long>(nx) * ny) return;
+  const int j = static_cast<int>(idx / nx), i = static_cast<int>(idx % nx);
+  const double v = w[idx] - (__ldg(t.W[0] + j) * __ldg(t.y4 + i) + __ldg(t.W[1] + j) * __ldg(t.y4 + nx + i) +
+                             __ldg(t.W[2] + j) * __ldg(t.y4 + 2LL * nx + i) +
+                             __ldg(t.W[3] + j) * __ldg(t.y4 + 3LL * nx + i));
+  const double cb = 2.0 * cc[idx] - cpNext[idx];
+  cpNext[idx] = cb + v;  // cahn_hilliard.cpp:320
+}
+
+// Bands of the uniform hyperdiffusion operator (penta.cpp:313-335) for one
+// periodic system: {sigma, -4 sigma, 1 + 6 sigma, -4 sigma, sigma}.
+__global__ void k_fill_bands(double sigma, int n, double* e, double* c, double* d, double* a, double* b) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  e[r] = sigma;
+  c[r] = -4.0 * sigma;
+  d[r] = 1.0 + 6.0 * sigma;
+  a[r] = -4.0 * sigma;
+  b[r] = sigma;
+}
+
+bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+}  // namespace
+
+void ch_validate(const sg_ch_params& p) {  // CHParams::validate, cahn_hilliard.cpp:56-66
+  if (!(p.D > 0.0)) invalid("CHParams: D must be > 0");
+  if (!(p.gamma > 0.0)) invalid("CHParams: gamma must be > 0");
+  if (!(p.dt > 0.0)) invalid("CHParams: dt must be > 0");
+  if (!(p.T > 0.0)) invalid("CHParams: T must be > 0");
+  if (!(p.lx > 0.0) || !(p.ly > 0.0)) invalid("CHParams: lx, ly must be > 0");
+  if (!is_pow2(p.nx) || !is_pow2(p.ny)) invalid("CHParams: nx and ny must be powers of two");
+  if (p.nx < 8 || p.ny < 8) invalid("CHParams: grid too small (need >= 8)");
+  if (!(p.icAmplitude >= 0.0)) invalid("CHParams: icAmplitude must be >= 0");
+}
+
+struct ChState {
+  sg_ch_params p{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  double* field[2] = {nullptr, nullptr};  // ping-pong time levels
+  int curr = 0;                           // field[curr] = C^n, field[1-curr] = C^{n-1}
+  double *rhsT = nullptr, *w = nullptr, *y4x = nullptr, *y4y = nullptr;
+  DevicePenta fx, fy;
+  RhsParams rp{};
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  int step = 0;
+  std::vector<void*> allocs;
+
+  double* dalloc(size_t n) {
+    void* q = nullptr;
+    SG_CUDA(cudaMalloc(&q, n * sizeof(double)));
+    allocs.push_back(q);
+    return static_cast<double*>(q);
+  }
+
+  ~ChState() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& g : graph)
+      if (g) cudaGraphExecDestroy(g);
+    for (void* q : allocs) cudaFree(q);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void build_factor(DevicePenta& f, double sigma, int n) {
+    double* bands = dalloc(5 * static_cast<size_t>(n));
+    k_fill_bands<<<(n + 255) / 256, 256, 0, stream>>>(sigma, n, bands, bands + n, bands + 2 * n, bands + 3 * n,
+                                                      bands + 4 * n);
+    check_launch("ch bands kernel");
+    f.build(1, n, true, true, bands, bands + n, bands + 2 * n, bands + 3 * n, bands + 4 * n, stream);
+    f.B = 0;  // batch count is supplied per sweep
+  }
+
+  void init() {
+    SG_CUDA(cudaGetDevice(&device));
+    SG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    const size_t cnt = static_cast<size_t>(p.nx) * p.ny;
+    field[0] = dalloc(cnt);
+    field[1] = dalloc(cnt);
+    rhsT = dalloc(cnt);
+    w = dalloc(cnt);
+    y4x = dalloc(4 * static_cast<size_t>(p.ny));
+    y4y = dalloc(4 * static_cast<size_t>(p.nx));
+    const double dx = p.lx / p.nx, dy = p.ly / p.ny;
+    // hyperdiffusion_sigma (cahn_hilliard.cpp:19-21), RhsCoeffs (:25-34)
+    const double sx = kTwoThirds * p.D * p.gamma * p.dt / pow4(dx);
+    const double sy = kTwoThirds * p.D * p.gamma * p.dt / pow4(dy);
+    build_factor(fx, sx, p.nx);
+    build_factor(fy, sy, p.ny);
+    rp.kDiff = -kTwoThirds;
+    rp.kBih = kTwoThirds * p.D * p.gamma * p.dt;
+    rp.kNl = kTwoThirds * p.D * p.dt;
+    biharmonic_weights(dx, dy, rp.bw);
+    // nonlinear_laplacian_coefficients (cahn_hilliard.cpp:78-83)
+    const double cx = 1.0 / (dx * dx), cy = 1.0 / (dy * dy), cc = -2.0 * cx - 2.0 * cy;
+    const double nl[9] = {0.0, cy, 0.0, cx, cc, cx, 0.0, cy, 0.0};
+    std::memcpy(rp.nl, nl, sizeof nl);
+    // the skipped taps must be exactly zero
+    bool keep[25] = {};
+    constexpr int kBihTaps[13] = SG_BIH_TAPS;
+    for (int t : kBihTaps) keep[t] = true;
+    for (int k = 0; k < 25; ++k)
+      if (!keep[k] && rp.bw[k] != 0.0) throw Error(SG_ERR_CUDA, "internal: biharmonic zero pattern");
+    // initial_condition (cahn_hilliard.cpp:68-76); C^{n-1} := C^n (:218)
+    const long long n = static_cast<long long>(cnt);
+    k_init<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(p.seed, p.icAmplitude, n, field[0]);
+    check_launch("ch init kernel");
+    SG_CUDA(cudaMemcpyAsync(field[1], field[0], cnt * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    curr = 0;
+    step = 0;
+    SG_CUDA(cudaStreamSynchronize(stream));
+  }
+
+  // One step with time levels (field[c], field[1-c]).
+  void enqueue_step(int c, cudaStream_t s) {
+    const int nx = p.nx, ny = p.ny;
+    const double* cc = field[c];
+    double* cp = field[1 - c];
+    dim3 tb(32, 8), tg((nx + TS - 1) / TS, (ny + TS - 1) / TS);
+    if (p.nonlinearEnabled)
+      k_rhs<true><<<tg, tb, 0, s>>>(cc, cp, rhsT, nx, ny, rp);
+    else
+      k_rhs<false><<<tg, tb, 0, s>>>(cc, cp, rhsT, nx, ny, rp);
+    check_launch("ch rhs kernel");
+    penta_sweep(fx.t, ny, nx, rhsT, y4x, true, true, s);
+    CorrTables tx{{fx.t.W[0], fx.t.W[1], fx.t.W[2], fx.t.W[3]}, y4x};
+    k_transpose_correct<<<tg, tb, 0, s>>>(rhsT, w, nx, ny, tx);
+    check_launch("ch transpose kernel");
+    penta_sweep(fy.t, nx, ny, w, y4y, true, true, s);
+    CorrTables ty{{fy.t.W[0], fy.t.W[1], fy.t.W[2], fy.t.W[3]}, y4y};
+    const long long cnt = static_cast<long long>(nx) * ny;
+    k_combine<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, s>>>(cc, cp, w, nx, ny, ty);
+    check_launch("ch combine kernel");
+  }
+
+  void capture() {
+    for (int c = 0; c < 2; ++c) {
+      cudaGraph_t g;
+      SG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      const uint64_t before = g_launches.load();
+      enqueue_step(c, stream);
+      g_launches.store(before);  // captured, not launched
+      SG_CUDA(cudaStreamEndCapture(stream, &g));
+      SG_CUDA(cudaGraphInstantiate(&graph[c], g, 0));
+      SG_CUDA(cudaGraphDestroy(g));
+    }
+  }
+
+  void run(int steps) {
+    if (!graph[0]) capture();
+    for (int k = 0; k < steps; ++k) {
+      SG_CUDA(cudaGraphLaunch(graph[curr], stream));
+      count_launch(5);
+      curr = 1 - curr;  // C^{n+1} was written over C^{n-1}
+      ++step;
+    }
+  }
+};
+
+}  // namespace sg
+
+struct sg_ch_s {
+  std::unique_ptr<sg::ChState> st;
+};
+
+struct sg_penta_s {
+  std::unique_ptr<sg::DevicePenta> f;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+};
+
+// Reuse the error plumbing of capi.cu through these two helpers.
+extern "C" sg_status sg_internal_set_error(const char* msg, int system);
+
+namespace {
+template <typename F>
+sg_status guard2(F&& f) {
+  try {
+    f();
+    return SG_OK;
+  } catch (const sg::Error& e) {
+    sg_internal_set_error(e.what(), e.system);
+    return e.status;
+  } catch (const std::exception& e) {
+    sg_internal_set_error(e.what(), -1);
+    return SG_ERR_CUDA;
+  }
+}
+
+void require_device2() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw sg::Error(SG_ERR_NO_DEVICE, "stengrid: no CUDA device visible (there is no CPU fallback)");
+}
+}  // namespace
+
+extern "C" {
+
+void sg_ch_default_params(sg_ch_params* p) {
+  p->D = 1.0;
+  p->gamma = 0.01;
+  p->nx = 512;
+  p->ny = 512;
+  p->lx = 2.0 * 3.14159265358979323846;
+  p->ly = 2.0 * 3.14159265358979323846;
+  p->dt = 0.0;
+  p->T = 0.0;
+  p->seed = 1;
+  p->icAmplitude = 0.1;
+  p->nonlinearEnabled = 1;
+}
+
+sg_status sg_ch_validate(const sg_ch_params* p) {
+  return guard2([&] {
+    if (!p) sg::invalid("CHParams: null");
+    sg::ch_validate(*p);
+  });
+}
+
+sg_status sg_ch_create(const sg_ch_params* p, int numTiles, int numWorkers, sg_ch_t* ch) {
+  return guard2([&] {
+    if (!p || !ch) sg::invalid("CHStepper: null argument");
+    *ch = nullptr;
+    sg::ch_validate(*p);
+    // rowTiles_ = make_tiles(ny, numTiles) (cahn_hilliard.cpp:216); pool_(numWorkers)
+    if (numTiles < 1 || numTiles > p->ny) sg::invalid("make_tiles: numTiles must satisfy 1 <= numTiles <= ny");
+    if (numWorkers < 1) sg::invalid("WorkerPool: workers must be >= 1");
+    require_device2();
+    auto h = std::make_unique<sg_ch_s>();
+    h->st = std::make_unique<sg::ChState>();
+    h->st->p = *p;
+    h->st->init();
+    *ch = h.release();
+  });
+}
+
+sg_status sg_ch_step(sg_ch_t ch, int steps) {
+  return guard2([&] {
+    if (!ch) sg::logic("CHStepper: destroyed");
+    SG_CUDA(cudaSetDevice(ch->st->device));
+    ch->st->run(steps);
+  });
+}
+
+sg_status sg_ch_set_state(sg_ch_t ch, const double* curr, const double* prev, sg_memory memory) {
+  return guard2([&] {
+    if (!ch) sg::logic("CHStepper: destroyed");
+    auto& s = *ch->st;
+    SG_CUDA(cudaSetDevice(s.device));
+    const size_t bytes = static_cast<size_t>(s.p.nx) * s.p.ny * sizeof(double);
+    const cudaMemcpyKind k = memory == SG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    s.curr = 0;
+    SG_CUDA(cudaMemcpyAsync(s.field[0], curr, bytes, k, s.stream));
+    SG_CUDA(cudaMemcpyAsync(s.field[1], prev, bytes, k, s.stream));
+    SG_CUDA(cudaStreamSynchronize(s.stream));
+    s.step = 0;  // cahn_hilliard.cpp:256-257
+  });
+}
+
+sg_status sg_ch_get_field(sg_ch_t ch, int which, double* out, sg_memory memory) {
+  return guard2([&] {
+    if (!ch) sg::logic("CHStepper: destroyed");
+    auto& s = *ch->st;
+    SG_CUDA(cudaSetDevice(s.device));
+    const size_t bytes = static_cast<size_t>(s.p.nx) * s.p.ny * sizeof(double);
+    const double* src = s.field[which == 0 ? s.curr : 1 - s.curr];
+    SG_CUDA(cudaMemcpyAsync(out, src, bytes, memory == SG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                            s.stream));
+    SG_CUDA(cudaStreamSynchronize(s.stream));
+  });
+}
+
+sg_status sg_ch_device_field(sg_ch_t ch, int which, const double** dptr) {
+  return guard2([&] {
+    if (!ch) sg::logic("CHStepper: destroyed");
+    auto& s = *ch->st;
+    SG_CUDA(cudaStreamSynchronize(s.stream));
+    *dptr = s.field[which == 0 ? s.curr : 1 - s.curr];
+  });
+}
+
+sg_status sg_ch_status(sg_ch_t ch, int* step, double* time) {
+  return guard2([&] {
+    if (!ch) sg::logic("CHStepper: destroyed");
+    if (step) *step = ch->st->step;
+    if (time) *time = static_cast<double>(ch->st->step) * ch->st->p.dt;  // cahn_hilliard.cpp:327
+  });
+}
+
+sg_status sg_ch_destroy(sg_ch_t* ch) {
+  return guard2([&] {
+    if (!ch || !*ch) return;
+    delete *ch;
+    *ch = nullptr;
+  });
+}
+
+// ------------------------------------------------------------------ penta
+
+sg_status sg_penta_create(int batchCount, int n, int periodic, const double* e, const double* c,
+                          const double* d, const double* a, const double* b, sg_memory memory,
+                          sg_penta_t* factor) {
+  return guard2([&] {
+    if (!factor) sg::invalid("penta: null handle");
+    *factor = nullptr;
+    if (batchCount < 1) sg::invalid("penta: batchCount must be >= 1");  // penta.cpp:10-13
+    if (n < 5) sg::invalid("penta: systems need n >= 5");
+    require_device2();
+    auto h = std::make_unique<sg_penta_s>();
+    SG_CUDA(cudaGetDevice(&h->device));
+    SG_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->f = std::make_unique<sg::DevicePenta>();
+    const size_t len = static_cast<size_t>(batchCount) * n;
+    const double* bands[5] = {e, c, d, a, b};
+    // Uniform operator: every system identical (host bands are checked here;
+    // device bands always take the per-system path).
+    bool uniform = false;
+    if (memory == SG_MEM_HOST) {
+      uniform = true;
+      for (int k = 0; k < 5 && uniform; ++k)
+        for (int r = 0; r < n && uniform; ++r) {
+          const double* row = bands[k] + static_cast<size_t>(r) * batchCount;
+          for (int q = 1; q < batchCount; ++q)
+            if (std::memcmp(&row[q], &row[0], sizeof(double)) != 0) {
+              uniform = false;
+              break;
+            }
+        }
+    }
+    const int nsys = uniform ? 1 : batchCount;
+    const size_t dlen = static_cast<size_t>(nsys) * n;
+    double* dev = h->f->alloc(5 * dlen);
+    for (int k = 0; k < 5; ++k) {
+      if (uniform) {
+        std::vector<double> col(n);
+        for (int r = 0; r < n; ++r) col[r] = bands[k][static_cast<size_t>(r) * batchCount];
+        SG_CUDA(cudaMemcpy(dev + k * dlen, col.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+      } else {
+        SG_CUDA(cudaMemcpy(dev + k * dlen, bands[k], len * sizeof(double),
+                           memory == SG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+      }
+    }
+    h->f->build(nsys, n, periodic != 0, uniform, dev, dev + dlen, dev + 2 * dlen, dev + 3 * dlen,
+                dev + 4 * dlen, h->stream);
+    h->f->B = batchCount;
+    *factor = h.release();
+  });
+}
+
+sg_status sg_penta_solve(sg_penta_t f, double* rhs, sg_memory memory, void* stream, int synchronize) {
+  return guard2([&] {
+    if (!f) sg::logic("penta: destroyed factor");
+    SG_CUDA(cudaSetDevice(f->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : f->stream;
+    const int B = f->f->B, n = f->f->n;
+    const size_t bytes = static_cast<size_t>(B) * n * sizeof(double);
+    double* z = rhs;
+    double* tmp = nullptr;
+    if (memory == SG_MEM_HOST) {
+      SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), bytes, s));
+      SG_CUDA(cudaMemcpyAsync(tmp, rhs, bytes, cudaMemcpyHostToDevice, s));
+      z = tmp;
+    }
+    sg::penta_sweep(f->f->t, B, n, z, nullptr, f->f->periodic, false, s);
+    if (memory == SG_MEM_HOST) {
+      SG_CUDA(cudaMemcpyAsync(rhs, tmp, bytes, cudaMemcpyDeviceToHost, s));
+      SG_CUDA(cudaFreeAsync(tmp, s));
+      synchronize = 1;
+    }
+    if (synchronize) SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+sg_status sg_penta_destroy(sg_penta_t* f) {
+  return guard2([&] {
+    if (!f || !*f) return;
+    cudaSetDevice((*f)->device);
+    if ((*f)->stream) {
+      cudaStreamSynchronize((*f)->stream);
+      cudaStreamDestroy((*f)->stream);
+    }
+    delete *f;
+    *f = nullptr;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// penta.cuh — device pentadiagonal factor tables and sweeps (see penta.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+namespace sg {
+
+// Factor tables. uniform: every array holds one system (n entries, W_k n
+// entries, cw 6, K 16, piv 4); otherwise interleaved per system (r*B + b;
+// cw/K/piv system-major).
+struct PentaTables {
+  const double* m1 = nullptr;
+  const double* m2 = nullptr;
+  const double* dInv = nullptr;
+  const double* ap = nullptr;
+  const double* bp = nullptr;
+  const double* W[4] = {nullptr, nullptr, nullptr, nullptr};
+  const double* cw = nullptr;
+  const double* K = nullptr;
+  const int* piv = nullptr;
+  int uniform = 0;
+};
+
+// Owns the device factor of one (periodic or not) batch.
+struct DevicePenta {
+  int B = 0, n = 0;
+  bool periodic = false;
+  PentaTables t;
+  std::vector<void*> allocs;
+
+  DevicePenta() = default;
+  DevicePenta(const DevicePenta&) = delete;
+  DevicePenta& operator=(const DevicePenta&) = delete;
+  ~DevicePenta();
+
+  // Bands are DEVICE pointers; uniform => single-system bands of length n,
+  // else interleaved B*n. Throws Error(SG_ERR_PENTA_SOLVE, system) exactly
+  // where the reference throws PentaSolveError.
+  void build(int B, int n, bool periodic, bool uniform, const double* e, const double* c,
+             const double* d, const double* a, const double* b, cudaStream_t s);
+  double* alloc(size_t count);
+};
+
+// Forward/back substitution (+ periodic correction) of B interleaved systems
+// in z. fusedCorrection: skip z -= W y and write y (y4[k*B + b]) instead.
+void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool periodic,
+                 bool fusedCorrection, cudaStream_t s);
+
+// lu4_solve, penta.cpp:61-70.
+__device__ __forceinline__ void lu4_solve_dev(const double* K, const int* piv, double* y) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int p = piv[c];
+    if (p != c) {
+      double t = y[c];
+      // y[c] <-> y[p] with a runtime p: select chain keeps y in registers
+      double yp = p == 1 ? y[1] : p == 2 ? y[2] : y[3];
+      y[c] = yp;
+      if (p == 1) y[1] = t;
+      else if (p == 2) y[2] = t;
+      else y[3] = t;
+    }
+  }
+#pragma unroll
+  for (int r = 1; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < r; ++c) y[r] -= K[r * 4 + c] * y[c];
+#pragma unroll
+  for (int r = 3; r >= 0; --r) {
+#pragma unroll
+    for (int c = r + 1; c < 4; ++c) y[r] -= K[r * 4 + c] * y[c];
+    y[r] /= K[r * 4 + r];
+  }
+}
+
+
+}  // namespace sg

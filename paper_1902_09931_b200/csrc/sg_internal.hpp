@@ -1,0 +1,50 @@
+// Internal declarations shared by the libstengrid_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "stengrid/sg.h"
+
+namespace sg {
+
+// Error classes mirror the reference's exception types one-to-one so the C++
+// layer can rethrow exactly what the reference throws.
+struct Error : std::runtime_error {
+  sg_status status;
+  int system;
+  Error(sg_status s, const std::string& m, int sys = -1) : std::runtime_error(m), status(s), system(sys) {}
+};
+
+[[noreturn]] inline void invalid(const std::string& m) { throw Error(SG_ERR_INVALID_ARGUMENT, m); }
+[[noreturn]] inline void logic(const std::string& m) { throw Error(SG_ERR_LOGIC, m); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(SG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define SG_CUDA(x) ::sg::cuda_check((x), #x)
+
+// Number of kernels launched by this library (reported as gpu_launches).
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+inline void check_launch(const char* what) {
+  count_launch();
+  cuda_check(cudaGetLastError(), what);
+}
+
+// Stencil launch (stencil.cu). `values` are the weights (fn == SG_FN_NONE) or
+// the function coefficients; returns the kernel kind used (1 fast, 0 generic).
+int launch_stencil(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,
+                   size_t count, sg_dtype dtype, const void* in, void* out, cudaStream_t stream);
+// Which kernel launch_stencil would pick, without launching.
+int stencil_kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size_t count,
+                        sg_dtype dtype, const void* in, const void* out);
+// Minimum window (W, H) and coefficient count a device function reads.
+bool function_shape(int fn, int* minW, int* minH, int* minCoe);
+const char* function_name(int fn);
+
+}  // namespace sg

@@ -1,0 +1,546 @@
+// stencil.cu — sm_100a stencil kernels for the cuSten/stengrid engine.
+//
+// Replaces the reference's CPU hot loops weights_rows / weights_wrapped_point
+// (stencil.cpp:49-85) and function_rows / function_gathered_point
+// (stencil.cpp:87-126). Arithmetic is bitwise identical to the reference:
+// each output is acc = 0; acc += w[q*W+p] * in(i-left+p, j-top+q) row-major
+// over the window (compiled with --fmad=false, the device analogue of the
+// reference's -ffp-contract=off, CMakeLists.txt:15-21); function stencils
+// receive the window packed with rowStride = W, which the reference's
+// contract allows (stencil.hpp:20-25).
+//
+// Two kernels:
+//  * k_strip — the bandwidth path. One warp owns a strip of 32*V columns
+//    (V = 16 bytes / sizeof(T): 2 doubles or 4 floats per lane, so every
+//    row load is one coalesced 512 B LDG.128 per warp) and marches down a
+//    segment of rows. Each input row is loaded from HBM exactly once per
+//    strip; horizontal neighbours come from warp shuffles, only the two
+//    strip-edge lanes load halo columns (wrapped in index math, computed
+//    once per strip). The H-row window lives in registers; loads run a
+//    D-row software prefetch ahead so ~D*512 B per warp are in flight.
+//    Weights/coefficients sit in the kernel parameter (constant) bank.
+//  * k_generic — one thread per output point with per-tap modular wrap:
+//    any extents (including windows wider than the grid), any alignment,
+//    any row pitch. Used for tiny/odd grids and unusual extents.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <type_traits>
+
+#include "sg_internal.hpp"
+
+namespace sg {
+
+std::atomic<uint64_t> g_launches{0};
+
+namespace {
+
+constexpr int VMAX = 256;       // values carried in the parameter bank
+constexpr int GENERIC_FN_MAX = 256;  // window taps a generic device function may see
+
+template <typename T>
+struct KArgs {
+  const T* __restrict__ in;
+  T* __restrict__ out;
+  const T* __restrict__ wdev;  // weights when count > VMAX (generic path only)
+  int nx, inRows, inShift;
+  int row0, row1, col0, col1;
+  int wrapX, wrapY;
+  int left, right, top, bottom;
+  int segRows;
+  int count;
+  T v[VMAX];
+};
+
+// ----------------------------------------------------------- window ops
+// Device twins of the reference's window functions. Same expression trees,
+// evaluated without contraction, so FP64 results are bitwise identical.
+struct OpWeights {};  // marker: weight stencil
+
+struct OpChNonlinear {  // cahn_hilliard.cpp:36-47
+  template <typename T>
+  __device__ static T apply(const T* w, const T* coe, int rs) {
+    T acc = T(0);
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const T v = w[q * rs + p];
+        acc += coe[q * 3 + p] * (v * v * v - v);
+      }
+    return acc;
+  }
+};
+struct OpCentralDifference {  // tools/main.cpp:47-49
+  template <typename T>
+  __device__ static T apply(const T* w, const T* coe, int) {
+    return (w[0] - T(2) * w[1] + w[2]) * coe[0];
+  }
+};
+struct OpCenter {  // tests/test_stencil.cpp:68
+  template <typename T>
+  __device__ static T apply(const T* w, const T*, int rs) {
+    return w[rs + 1];
+  }
+};
+struct OpCentralSecond {  // tests/test_stencil.cpp:70-77
+  template <typename T>
+  __device__ static T apply(const T* w, const T* coe, int) {
+    T acc = T(0);
+    acc += coe[0] * w[0];
+    acc += (T(-2) * coe[0]) * w[1];
+    acc += coe[0] * w[2];
+    return acc;
+  }
+};
+struct OpLapCubeDiffFirst {  // tests/test_stencil.cpp:79-85
+  template <typename T>
+  __device__ static T g(T v) { return v * v * v - v; }
+  template <typename T>
+  __device__ static T apply(const T* w, const T* coe, int rs) {
+    const T gm = g(w[rs + 1]);
+    const T x = (g(w[rs]) - T(2) * gm) + g(w[rs + 2]);
+    const T y = (g(w[1]) - T(2) * gm) + g(w[2 * rs + 1]);
+    return coe[0] * x + coe[1] * y;
+  }
+};
+struct OpWeighted3x3 {  // tests/test_stencil.cpp:88-93
+  template <typename T>
+  __device__ static T apply(const T* w, const T* coe, int rs) {
+    T acc = T(0);
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int p = 0; p < 3; ++p) acc += coe[q * 3 + p] * w[q * rs + p];
+    return acc;
+  }
+};
+
+template <typename T>
+struct VecT;
+template <>
+struct VecT<double> {
+  static constexpr int V = 2;
+  using type = double2;
+};
+template <>
+struct VecT<float> {
+  static constexpr int V = 4;
+  using type = float4;
+};
+
+template <typename T>
+__device__ __forceinline__ T shfl_up(T v, int d) {
+  return __shfl_up_sync(0xffffffffu, v, d);
+}
+template <typename T>
+__device__ __forceinline__ T shfl_down(T v, int d) {
+  return __shfl_down_sync(0xffffffffu, v, d);
+}
+
+__device__ __forceinline__ int wrap_idx(long long i, int n) {
+  long long r = i % n;
+  return static_cast<int>(r < 0 ? r + n : r);
+}
+
+constexpr int STRIP_WARPS = 4;
+
+// --------------------------------------------------------------- k_strip
+template <typename T, int L, int R, int TP, int BT, int D, typename Op>
+__global__ void __launch_bounds__(STRIP_WARPS * 32) k_strip(const __grid_constant__ KArgs<T> a) {
+  using VT = typename VecT<T>::type;
+  constexpr int V = VecT<T>::V;
+  constexpr int SW = 32 * V;
+  constexpr int H = TP + BT + 1;
+  constexpr int W = L + R + 1;
+  constexpr int E = L + V + R;
+  constexpr int LL = L > 0 ? L : 1;
+  constexpr int RR = R > 0 ? R : 1;
+
+  const int lane = threadIdx.x & 31;
+  const int strip = blockIdx.x * STRIP_WARPS + (threadIdx.x >> 5);
+  const int x0 = strip * SW;
+  if (x0 >= a.nx) return;  // warp-uniform
+  const int ra = a.row0 + blockIdx.y * a.segRows;
+  const int rb = min(ra + a.segRows, a.row1);
+  if (ra >= rb) return;
+
+  const int nx = a.nx;
+  const int xb = x0 + lane * V;
+  const bool laneValid = xb < nx;
+  const int xc = laneValid ? xb : nx - V;  // clamped (value unused)
+
+  // Halo columns: shuffled from neighbour lanes where they hold the column,
+  // otherwise loaded directly with the wrap resolved once here.
+  int hlCol[LL], hrCol[RR];
+  bool hlDir[LL], hrDir[RR];
+#pragma unroll
+  for (int k = 1; k <= L; ++k) {
+    const int dl = (k + V - 1) / V;
+    const int c = xb - k;
+    hlDir[k - 1] = lane < dl;
+    hlCol[k - 1] = a.wrapX ? wrap_idx(c, nx) : max(min(c, nx - 1), 0);
+  }
+#pragma unroll
+  for (int k = 1; k <= R; ++k) {
+    const int dr = (V - 1 + k) / V;
+    const int c = xb + V - 1 + k;
+    hrDir[k - 1] = (lane + dr > 31) || (c >= nx);
+    hrCol[k - 1] = a.wrapX ? wrap_idx(c, nx) : max(min(c, nx - 1), 0);
+  }
+
+  struct Raw {
+    VT c;
+    T hl[LL];
+    T hr[RR];
+  };
+  const T* __restrict__ in = a.in;
+  auto fetch = [&](int row, Raw& r) {
+    const T* base = in + static_cast<long long>(row) * nx;
+    r.c = __ldg(reinterpret_cast<const VT*>(base + xc));
+#pragma unroll
+    for (int k = 0; k < L; ++k) r.hl[k] = hlDir[k] ? __ldg(base + hlCol[k]) : T(0);
+#pragma unroll
+    for (int k = 0; k < R; ++k) r.hr[k] = hrDir[k] ? __ldg(base + hrCol[k]) : T(0);
+  };
+  auto expand = [&](const Raw& r, T* e) {
+    T c[V];
+    if constexpr (V == 2) {
+      c[0] = r.c.x;
+      c[1] = r.c.y;
+    } else {
+      c[0] = r.c.x;
+      c[1] = r.c.y;
+      c[2] = r.c.z;
+      c[3] = r.c.w;
+    }
+#pragma unroll
+    for (int k = 1; k <= L; ++k) {
+      const int dl = (k + V - 1) / V;
+      const T s = shfl_up(c[V * dl - k], dl);
+      e[L - k] = hlDir[k - 1] ? r.hl[k - 1] : s;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) e[L + v] = c[v];
+#pragma unroll
+    for (int k = 1; k <= R; ++k) {
+      const int dr = (V - 1 + k) / V;
+      const T s = shfl_down(c[(k - 1) % V], dr);
+      e[L + V - 1 + k] = hrDir[k - 1] ? r.hr[k - 1] : s;
+    }
+  };
+
+  // Input rows ra+inShift-TP .. rb-1+inShift+BT, wrapped iff wrapY.
+  const int nIn = (rb - ra) + H - 1;
+  int rf = ra + a.inShift - TP;
+  if (a.wrapY) rf = wrap_idx(rf, a.inRows);
+  auto advance = [&](int& r) {
+    ++r;
+    if (a.wrapY) {
+      if (r == a.inRows) r = 0;
+    } else if (r >= a.inRows) {
+      r = a.inRows - 1;
+    }
+  };
+
+  Raw ring[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (k < nIn) fetch(rf, ring[k]);
+    advance(rf);
+  }
+  T win[H][E];
+  T* __restrict__ out = a.out;
+  for (int t0 = 0; t0 < nIn; t0 += D) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const int t = t0 + k;
+      if (t < nIn) {
+        T e[E];
+        expand(ring[k], e);
+        if (t + D < nIn) fetch(rf, ring[k]);
+        advance(rf);
+#pragma unroll
+        for (int q = 0; q < H - 1; ++q)
+#pragma unroll
+          for (int p = 0; p < E; ++p) win[q][p] = win[q + 1][p];
+#pragma unroll
+        for (int p = 0; p < E; ++p) win[H - 1][p] = e[p];
+        if (t >= H - 1) {
+          const int j = ra + t - (H - 1);
+          T res[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if constexpr (std::is_same_v<Op, OpWeights>) {
+              T acc = T(0);
+#pragma unroll
+              for (int q = 0; q < H; ++q)
+#pragma unroll
+                for (int p = 0; p < W; ++p) acc += a.v[q * W + p] * win[q][v + p];
+              res[v] = acc;
+            } else {
+              T w[H * W];
+#pragma unroll
+              for (int q = 0; q < H; ++q)
+#pragma unroll
+                for (int p = 0; p < W; ++p) w[q * W + p] = win[q][v + p];
+              res[v] = Op::template apply<T>(w, a.v, W);
+            }
+          }
+          if (laneValid) {
+            T* orow = out + static_cast<long long>(j) * nx;
+            if (xb >= a.col0 && xb + V <= a.col1) {
+              VT o;
+              if constexpr (V == 2) {
+                o.x = res[0];
+                o.y = res[1];
+              } else {
+                o.x = res[0];
+                o.y = res[1];
+                o.z = res[2];
+                o.w = res[3];
+              }
+              *reinterpret_cast<VT*>(orow + xb) = o;
+            } else {
+#pragma unroll
+              for (int v = 0; v < V; ++v)
+                if (xb + v >= a.col0 && xb + v < a.col1) orow[xb + v] = res[v];
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------- k_generic
+template <typename T, typename Op>
+__global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T> a) {
+  const int i = a.col0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = a.row0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= a.col1 || j >= a.row1) return;
+  const int W = a.left + a.right + 1;
+  const int H = a.top + a.bottom + 1;
+  const T* __restrict__ in = a.in;
+  if constexpr (std::is_same_v<Op, OpWeights>) {
+    const T* wt = a.count <= VMAX ? a.v : a.wdev;
+    T acc = T(0);
+    for (int q = 0; q < H; ++q) {
+      long long r = static_cast<long long>(j) + a.inShift - a.top + q;
+      if (a.wrapY) r = wrap_idx(r, a.inRows);
+      const T* rowp = in + r * a.nx;
+      for (int p = 0; p < W; ++p) {
+        long long c = static_cast<long long>(i) - a.left + p;
+        if (a.wrapX) c = wrap_idx(c, a.nx);
+        acc += wt[q * W + p] * rowp[c];
+      }
+    }
+    a.out[static_cast<long long>(j) * a.nx + i] = acc;
+  } else {
+    T w[GENERIC_FN_MAX];
+    for (int q = 0; q < H; ++q) {
+      long long r = static_cast<long long>(j) + a.inShift - a.top + q;
+      if (a.wrapY) r = wrap_idx(r, a.inRows);
+      const T* rowp = in + r * a.nx;
+      for (int p = 0; p < W; ++p) {
+        long long c = static_cast<long long>(i) - a.left + p;
+        if (a.wrapX) c = wrap_idx(c, a.nx);
+        w[q * W + p] = rowp[c];
+      }
+    }
+    a.out[static_cast<long long>(j) * a.nx + i] = Op::template apply<T>(w, a.v, W);
+  }
+}
+
+// -------------------------------------------------------------- dispatch
+struct FnInfo {
+  const char* name;
+  int minW, minH, minCoe;
+};
+constexpr FnInfo kFn[SG_FN_COUNT] = {
+    {"weights", 1, 1, 0},
+    {"ch_nonlinear_window", 3, 3, 9},
+    {"central_difference_window", 3, 1, 1},
+    {"fn_center", 2, 2, 0},
+    {"fn_central_second", 3, 1, 1},
+    {"fn_lap_cube_diff_first", 3, 3, 2},
+    {"fn_weighted_3x3", 3, 3, 9},
+};
+
+template <typename Op, typename F>
+bool with_op(int fn, F&& f) {
+  switch (fn) {
+    case SG_FN_NONE: f(OpWeights{}); return true;
+    case SG_FN_CH_NONLINEAR: f(OpChNonlinear{}); return true;
+    case SG_FN_CENTRAL_DIFFERENCE: f(OpCentralDifference{}); return true;
+    case SG_FN_CENTER: f(OpCenter{}); return true;
+    case SG_FN_CENTRAL_SECOND: f(OpCentralSecond{}); return true;
+    case SG_FN_LAP_CUBE_DIFF_FIRST: f(OpLapCubeDiffFirst{}); return true;
+    case SG_FN_WEIGHTED_3X3: f(OpWeighted3x3{}); return true;
+    default: return false;
+  }
+}
+
+// Fast-path coverage: symmetric extents up to 4 for weight stencils; the
+// natural window of each device function.
+bool strip_supported(const sg_extents& e, int fn) {
+  if (e.left != e.right || e.top != e.bottom) return false;
+  if (fn == SG_FN_NONE) return e.left <= 4 && e.top <= 4;
+  if (fn == SG_FN_CENTRAL_DIFFERENCE || fn == SG_FN_CENTRAL_SECOND)
+    return e.left == 1 && e.top == 0;
+  return e.left == 1 && e.top == 1;
+}
+
+template <typename T>
+bool strip_eligible(const sg_slab_desc& d, const sg_extents& e, int fn, size_t count,
+                    const void* in, const void* out) {
+  constexpr int V = VecT<T>::V;
+  if (!strip_supported(e, fn)) return false;
+  if (count > static_cast<size_t>(VMAX)) return false;
+  if (d.nx % V != 0) return false;
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) % 16 != 0) return false;
+  return true;
+}
+
+// Prefetch depth: keep the raw-row ring near 64 32-bit registers per lane.
+template <typename T, int L>
+constexpr int prefetch_depth() {
+  constexpr int words = (VecT<T>::V + 2 * L) * static_cast<int>(sizeof(T) / 4);
+  constexpr int d = 64 / words;
+  return d >= 8 ? 8 : d >= 4 ? 4 : 2;
+}
+
+template <typename T, int L, int TP, typename Op>
+void launch_strip_lt(const KArgs<T>& a, dim3 grid, cudaStream_t s) {
+  constexpr int D = prefetch_depth<T, L>();
+  k_strip<T, L, L, TP, TP, D, Op><<<grid, STRIP_WARPS * 32, 0, s>>>(a);
+}
+
+template <typename T, typename Op>
+void launch_strip(const KArgs<T>& a, const sg_extents& e, dim3 grid, cudaStream_t s) {
+#define SG_CASE(LV, TV) \
+  if (e.left == LV && e.top == TV) return launch_strip_lt<T, LV, TV, Op>(a, grid, s);
+  if constexpr (std::is_same_v<Op, OpWeights>) {
+    SG_CASE(0, 0) SG_CASE(1, 0) SG_CASE(2, 0) SG_CASE(3, 0) SG_CASE(4, 0)
+    SG_CASE(0, 1) SG_CASE(1, 1) SG_CASE(2, 1) SG_CASE(3, 1) SG_CASE(4, 1)
+    SG_CASE(0, 2) SG_CASE(1, 2) SG_CASE(2, 2) SG_CASE(3, 2) SG_CASE(4, 2)
+    SG_CASE(0, 3) SG_CASE(1, 3) SG_CASE(2, 3) SG_CASE(3, 3) SG_CASE(4, 3)
+    SG_CASE(0, 4) SG_CASE(1, 4) SG_CASE(2, 4) SG_CASE(3, 4) SG_CASE(4, 4)
+  } else if constexpr (std::is_same_v<Op, OpCentralDifference> ||
+                       std::is_same_v<Op, OpCentralSecond>) {
+    SG_CASE(1, 0)
+  } else {
+    SG_CASE(1, 1)
+  }
+#undef SG_CASE
+  invalid("internal: no strip kernel for these extents");
+}
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <typename T>
+int launch_typed(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,
+                 size_t count, const void* in, void* out, cudaStream_t s) {
+  const int rows = d.row1 - d.row0;
+  const int cols = d.col1 - d.col0;
+  if (rows <= 0 || cols <= 0) return strip_eligible<T>(d, e, fn, count, in, out) ? 1 : 0;
+  KArgs<T> a;
+  std::memset(static_cast<void*>(&a), 0, sizeof(a));
+  a.in = static_cast<const T*>(in);
+  a.out = static_cast<T*>(out);
+  a.wdev = nullptr;
+  a.nx = d.nx;
+  a.inRows = d.inRows;
+  a.inShift = d.inShift;
+  a.row0 = d.row0;
+  a.row1 = d.row1;
+  a.col0 = d.col0;
+  a.col1 = d.col1;
+  a.wrapX = d.wrapX;
+  a.wrapY = d.wrapY;
+  a.left = e.left;
+  a.right = e.right;
+  a.top = e.top;
+  a.bottom = e.bottom;
+  a.count = static_cast<int>(count);
+  const size_t nv = std::min(count, static_cast<size_t>(VMAX));
+  for (size_t k = 0; k < nv; ++k) a.v[k] = static_cast<T>(values[k]);
+
+  if (strip_eligible<T>(d, e, fn, count, in, out)) {
+    constexpr int V = VecT<T>::V;
+    const int strips = (d.nx + 32 * V - 1) / (32 * V);
+    const int gx = (strips + STRIP_WARPS - 1) / STRIP_WARPS;
+    // Aim for >= 8 resident warps' worth of work per SM-slot; long
+    // segments amortise the (H-1)-row vertical halo.
+    const long long targetWarps = 1LL * sm_count() * 16 * 6;
+    long long seg = (1LL * rows * strips + targetWarps - 1) / targetWarps;
+    const int H = e.top + e.bottom + 1;
+    seg = std::max<long long>(seg, std::min(rows, std::max(4, 2 * H)));
+    seg = std::min<long long>(seg, 512);
+    a.segRows = static_cast<int>(seg);
+    const int gy = static_cast<int>((rows + seg - 1) / seg);
+    dim3 grid(gx, gy);
+    with_op<void>(fn, [&](auto op) { launch_strip<T, decltype(op)>(a, e, grid, s); });
+    check_launch("stencil strip kernel");
+    return 1;
+  }
+
+  T* wtmp = nullptr;
+  if (fn == SG_FN_NONE && count > static_cast<size_t>(VMAX)) {
+    SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wtmp), count * sizeof(T), s));
+    T* hw = new T[count];
+    for (size_t k = 0; k < count; ++k) hw[k] = static_cast<T>(values[k]);
+    cudaError_t err = cudaMemcpyAsync(wtmp, hw, count * sizeof(T), cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+    delete[] hw;
+    SG_CUDA(err);
+    a.wdev = wtmp;
+  }
+  dim3 block(32, 8);
+  dim3 grid((cols + 31) / 32, (rows + 7) / 8);
+  with_op<void>(fn, [&](auto op) { k_generic<T, decltype(op)><<<grid, block, 0, s>>>(a); });
+  check_launch("stencil generic kernel");
+  if (wtmp) SG_CUDA(cudaFreeAsync(wtmp, s));
+  return 0;
+}
+
+}  // namespace
+
+bool function_shape(int fn, int* minW, int* minH, int* minCoe) {
+  if (fn < 0 || fn >= SG_FN_COUNT) return false;
+  *minW = kFn[fn].minW;
+  *minH = kFn[fn].minH;
+  *minCoe = kFn[fn].minCoe;
+  return true;
+}
+
+const char* function_name(int fn) {
+  return (fn >= 0 && fn < SG_FN_COUNT) ? kFn[fn].name : nullptr;
+}
+
+int stencil_kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size_t count,
+                        sg_dtype dtype, const void* in, const void* out) {
+  return dtype == SG_F64 ? strip_eligible<double>(d, e, fn, count, in, out)
+                         : strip_eligible<float>(d, e, fn, count, in, out);
+}
+
+int launch_stencil(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,
+                   size_t count, sg_dtype dtype, const void* in, void* out, cudaStream_t stream) {
+  if (fn != SG_FN_NONE && (e.left + e.right + 1) * (e.top + e.bottom + 1) > GENERIC_FN_MAX &&
+      !strip_supported(e, fn))
+    invalid("create_plan: device function windows are limited to 256 taps");
+  if (dtype == SG_F64) return launch_typed<double>(d, e, fn, values, count, in, out, stream);
+  if (dtype == SG_F32) return launch_typed<float>(d, e, fn, values, count, in, out, stream);
+  invalid("unknown dtype");
+}
+
+}  // namespace sg

@@ -1,0 +1,154 @@
+"""GPU parity tests for the Cahn-Hilliard BDF2-ADI stepper
+(tests/test_cahn_hilliard.cpp and acceptance criteria restated).
+
+Checker: the C restatement of CHStepper (oracle/stengrid_oracle.c,
+orc_ch_run), pinned bitwise to the reference in tests/test_oracle.py. The
+north-star tolerance is 1e-9 relative L2 after 100 steps; the device path is
+expected — and asserted — to be BITWISE equal.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def bits_equal(a, b):
+    return a.shape == b.shape and np.array_equal(np.ascontiguousarray(a).view(np.uint64),
+                                                 np.ascontiguousarray(b).view(np.uint64))
+
+
+def params(sg, nx, ny=None, dt_factor=0.1, **kw):
+    p = sg.CHParams(nx=nx, ny=nx if ny is None else ny)
+    p.dt = dt_factor * p.dx()
+    p.T = 1.0
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+def oracle_dict(p):
+    return dict(D=p.D, gamma=p.gamma, lx=p.lx, ly=p.ly, dt=p.dt, nx=p.nx, ny=p.ny,
+                nonlinear=p.nonlinearEnabled)
+
+
+@pytest.mark.parametrize("nx,ny,steps", [(8, 8, 3), (16, 8, 5), (64, 64, 20), (128, 32, 10), (32, 256, 7)])
+def test_ch_steps_bitwise_vs_oracle(sg, orc, nx, ny, steps):
+    p = params(sg, nx, ny, seed=3)
+    st = sg.CHStepper(p)
+    for _ in range(steps):
+        st.step()
+    c0 = orc.ch_initial_condition(nx, ny, seed=3)
+    want_c, want_p = orc.ch_run(oracle_dict(p), steps, c0, c0)
+    assert bits_equal(st.field().values, want_c)
+    assert bits_equal(st.previous_field().values, want_p)
+    assert st.step_index() == steps
+    assert st.time() == steps * p.dt
+
+
+def test_initial_condition_matches_splitmix64(sg, orc):
+    """cahn_hilliard.cpp:68-76 — generated on the device in counter form."""
+    p = params(sg, 64, 32, seed=42)
+    st = sg.CHStepper(p)
+    assert bits_equal(st.field().values, orc.ch_initial_condition(64, 32, seed=42, amp=0.1))
+    assert bits_equal(st.previous_field().values, st.field().values)
+
+
+def test_ch_1024_100_steps_within_north_star_tolerance(sg, orc):
+    """BASELINE config 3 size: 1024^2, 100 steps; rel-L2 <= 1e-9 required,
+    bitwise expected."""
+    p = params(sg, 1024)
+    st = sg.CHStepper(p)
+    st.step_many(100)
+    got = st.field().values
+    c0 = orc.ch_initial_condition(1024, 1024)
+    want, _ = orc.ch_run(oracle_dict(p), 100, c0, c0)
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert rel <= 1e-9
+    assert bits_equal(got, want)
+
+
+def test_linear_single_mode_rational_symbol(sg):
+    """test_cahn_hilliard.cpp:292-318 — analytic oracle, 10 steps, 1e-12."""
+    p = params(sg, 64, 16, nonlinearEnabled=False)
+    st = sg.CHStepper(p)
+    h = p.dx()
+    x = np.arange(p.nx) * h
+    mode = np.tile(np.cos(x), (p.ny, 1))
+    g = sg.Grid2D.from_array(mode, h, p.dy())
+    st.set_state(g, g)
+    lam4 = (6.0 - 8.0 * math.cos(h) + 2.0 * math.cos(2.0 * h)) / (h * h * h * h)
+    kb = (2.0 / 3.0) * p.D * p.gamma * p.dt
+    lx = 1.0 + kb * lam4
+    a_prev = a_curr = 1.0
+    for _ in range(10):
+        st.step()
+        a_bar = 2.0 * a_curr - a_prev
+        rhs = -(2.0 / 3.0) * (a_curr - a_prev) - kb * lam4 * a_bar
+        a_prev, a_curr = a_curr, a_bar + rhs / lx
+        assert np.max(np.abs(st.field().values - a_curr * np.cos(x)[None, :])) <= 1e-12
+
+
+def test_constant_and_zero_states_fixed(sg):
+    """test_cahn_hilliard.cpp:259-290."""
+    p = params(sg, 64)
+    st = sg.CHStepper(p)
+    c = sg.Grid2D(64, 64)
+    c.values[:] = 0.3
+    st.set_state(c, c)
+    for _ in range(10):
+        st.step()
+    assert np.allclose(st.field().values, 0.3, rtol=1e-13, atol=0)
+    z = sg.Grid2D(64, 64)
+    st.set_state(z, z)
+    st.step()
+    assert np.all(st.field().values == 0.0)
+
+
+def test_negation_equivariance_bitwise(sg):
+    """test_cahn_hilliard.cpp:368-390 — C -> -C commutes with the step."""
+    p = params(sg, 32)
+    a, b = sg.CHStepper(p), sg.CHStepper(p)
+    c = a.field()
+    neg = sg.Grid2D.from_array(-c.values)
+    b.set_state(neg, neg)
+    a.set_state(c, c)
+    for _ in range(5):
+        a.step()
+        b.step()
+    assert bits_equal(b.field().values, -a.field().values)
+
+
+def test_mass_conservation(sg):
+    """test_cahn_hilliard.cpp:392-401 — mean preserved to 1e-10."""
+    p = params(sg, 64)
+    st = sg.CHStepper(p)
+    m0 = st.field().values.mean()
+    st.step_many(50)
+    assert abs(st.field().values.mean() - m0) <= 1e-10
+
+
+def test_tile_worker_invariance(sg):
+    """acceptance criterion 3 / test_cahn_hilliard.cpp:453-465."""
+    p = params(sg, 128)
+    ref = sg.CHStepper(p, 1, 1)
+    ref.step_many(2)
+    for tiles in (1, 2, 4, 8):
+        for workers in (1, 4):
+            st = sg.CHStepper(p, tiles, workers)
+            st.step_many(2)
+            assert bits_equal(st.field().values, ref.field().values)
+
+
+def test_params_validation(sg):
+    """test_cahn_hilliard.cpp:56-75."""
+    p = params(sg, 64)
+    p.validate()
+    for field, val in [("nx", 100), ("dt", 0.0), ("D", -1.0), ("gamma", 0.0), ("T", 0.0), ("nx", 4)]:
+        bad = params(sg, 64)
+        setattr(bad, field, val)
+        with pytest.raises(sg.InvalidArgument):
+            bad.validate()
+        with pytest.raises(sg.InvalidArgument):
+            sg.CHStepper(bad)
