@@ -79,7 +79,12 @@ struct sg_plan_s {
     bool hostValid = true;  // host copy holds the current values
   } buf[2];
   int inIdx = 0;
+  // Host-pipelining resources (Residency::Host on large periodic grids).
+  cudaStream_t sH2D = nullptr, sD2H = nullptr;
+  std::vector<cudaEvent_t> events;
+  bool registered[2] = {false, false};
 
+  size_t elem() const { return dtype == SG_F64 ? 8 : 4; }
   size_t bytes() const { return static_cast<size_t>(nx) * ny * (dtype == SG_F64 ? 8 : 4); }
 
   void release() {
@@ -88,6 +93,14 @@ struct sg_plan_s {
     if (stream) cudaStreamSynchronize(stream);
     for (auto& b : buf)
       if (b.owned && b.dev) cudaFree(b.dev);
+    for (int k = 0; k < 2; ++k)
+      if (registered[k]) cudaHostUnregister(buf[k].host);
+    for (auto e : events) cudaEventDestroy(e);
+    events.clear();
+    if (sH2D) cudaStreamDestroy(sH2D);
+    if (sD2H) cudaStreamDestroy(sD2H);
+    sH2D = sD2H = nullptr;
+    registered[0] = registered[1] = false;
     if (stream) cudaStreamDestroy(stream);
     stream = nullptr;
     buf[0] = Buf{};
@@ -219,6 +232,21 @@ sg_status sg_plan_create(sg_direction dir, sg_boundary mode, sg_extents ext, sg_
           b.host = ptrs[k];
           SG_CUDA(cudaMalloc(&b.dev, p->bytes()));
           b.owned = true;
+          // Page-lock large pageable host grids once so every transfer is a
+          // full-speed DMA (the plan never owns the grids; unregistered at
+          // destroy). Failure to register is harmless (pageable copies).
+          if (p->bytes() >= (4u << 20)) {
+            cudaPointerAttributes attr{};
+            if (cudaPointerGetAttributes(&attr, b.host) == cudaSuccess &&
+                attr.type == cudaMemoryTypeUnregistered) {
+              if (cudaHostRegister(b.host, p->bytes(), cudaHostRegisterPortable) == cudaSuccess)
+                p->registered[k] = true;
+              else
+                cudaGetLastError();
+            } else {
+              cudaGetLastError();
+            }
+          }
         }
       }
       p->valid = true;
@@ -254,6 +282,61 @@ static sg_slab_desc full_grid_desc(const sg_plan_s* p) {
   return d;
 }
 
+// Residency::Host on a large periodic grid: stream the grid through the GPU
+// in row chunks on three streams so the H2D of chunk k+1, the kernel on
+// chunk k and the D2H of chunk k-1 overlap (PCIe is full duplex). Each
+// chunk's kernel waits only for the chunks holding its halo rows.
+static void pipelined_host_compute(sg_plan_s* p, sg_plan_s::Buf& in, sg_plan_s::Buf& out, cudaStream_t s) {
+  const int ny = p->ny, top = p->ext.top, bottom = p->ext.bottom;
+  const size_t rowBytes = static_cast<size_t>(p->nx) * p->elem();
+  int rows = std::max((ny + 31) / 32, std::max(std::max(top, bottom), 1));
+  const int nch = (ny + rows - 1) / rows;
+  if (!p->sH2D) SG_CUDA(cudaStreamCreateWithFlags(&p->sH2D, cudaStreamNonBlocking));
+  if (!p->sD2H) SG_CUDA(cudaStreamCreateWithFlags(&p->sD2H, cudaStreamNonBlocking));
+  const size_t need = 2 * static_cast<size_t>(nch) + 2;
+  while (p->events.size() < need) {
+    cudaEvent_t e;
+    SG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->events.push_back(e);
+  }
+  cudaEvent_t evStart = p->events[0], evEnd = p->events[1];
+  cudaEvent_t* evH2D = p->events.data() + 2;
+  cudaEvent_t* evComp = p->events.data() + 2 + nch;
+  auto* hin = static_cast<const char*>(in.host);
+  auto* din = static_cast<char*>(in.dev);
+  SG_CUDA(cudaEventRecord(evStart, s));
+  SG_CUDA(cudaStreamWaitEvent(p->sH2D, evStart, 0));
+  SG_CUDA(cudaStreamWaitEvent(p->sD2H, evStart, 0));
+  if (top > 0) {  // wrapped halo of chunk 0: the last `top` rows
+    const size_t off = static_cast<size_t>(ny - top) * rowBytes;
+    SG_CUDA(cudaMemcpyAsync(din + off, hin + off, top * rowBytes, cudaMemcpyHostToDevice, p->sH2D));
+  }
+  for (int k = 0; k < nch; ++k) {
+    const int a = k * rows, b = std::min(ny, a + rows);
+    const size_t off = static_cast<size_t>(a) * rowBytes;
+    SG_CUDA(cudaMemcpyAsync(din + off, hin + off, (b - a) * rowBytes, cudaMemcpyHostToDevice, p->sH2D));
+    SG_CUDA(cudaEventRecord(evH2D[k], p->sH2D));
+  }
+  sg_slab_desc d = full_grid_desc(p);
+  for (int k = 0; k < nch; ++k) {
+    const int a = k * rows, b = std::min(ny, a + rows);
+    // rows up to b-1+bottom must be resident (wrapping to chunk 0 is covered
+    // by stream order: chunk 0 was uploaded before every later chunk)
+    const int lastRow = std::min(ny - 1, b - 1 + bottom);
+    SG_CUDA(cudaStreamWaitEvent(s, evH2D[lastRow / rows], 0));
+    d.row0 = a;
+    d.row1 = b;
+    sg::launch_stencil(d, p->ext, p->fn, p->values.data(), p->values.size(), p->dtype, in.dev, out.dev, s);
+    SG_CUDA(cudaEventRecord(evComp[k], s));
+    SG_CUDA(cudaStreamWaitEvent(p->sD2H, evComp[k], 0));
+    const size_t off = static_cast<size_t>(a) * rowBytes;
+    SG_CUDA(cudaMemcpyAsync(static_cast<char*>(out.host) + off, static_cast<const char*>(out.dev) + off,
+                            (b - a) * rowBytes, cudaMemcpyDeviceToHost, p->sD2H));
+  }
+  SG_CUDA(cudaEventRecord(evEnd, p->sD2H));
+  SG_CUDA(cudaStreamWaitEvent(s, evEnd, 0));
+}
+
 sg_status sg_plan_compute(sg_plan_t p, sg_residency residency, void* stream, int synchronize) {
   return guard([&] {
     if (!p || !p->valid) sg::logic("compute: plan was destroyed");
@@ -263,6 +346,15 @@ sg_status sg_plan_compute(sg_plan_t p, sg_residency residency, void* stream, int
     auto& out = p->buf[1 - p->inIdx];
     if (in.dev == out.dev) sg::invalid("compute: bound grids alias");
     const bool periodic = p->mode == SG_PERIODIC;
+    if (p->memory == SG_MEM_HOST && periodic && residency == SG_RESIDENCY_HOST && in.hostValid &&
+        p->bytes() >= (64u << 20)) {
+      pipelined_host_compute(p, in, out, s);
+      in.devValid = true;
+      out.devValid = true;
+      out.hostValid = true;
+      SG_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
     if (p->memory == SG_MEM_HOST) {
       // HOST residency: a host grid holding valid values is authoritative
       // (re-uploaded on every compute); a grid whose newest values were left
