@@ -1,0 +1,316 @@
+// stengrid/stencil.hpp — drop-in replacement for the reference stencil API
+// (/root/reference/proj/include/stengrid/stencil.hpp:1-116): the same
+// create_plan / compute / swap_plan / destroy_plan over Grid2D fields, the
+// same kinds, enums, ownership rules and exceptions — executed by the sm_100a
+// kernels of libstengrid_b200.so through the C ABI (stengrid/sg.h).
+//
+// Differences a caller can observe:
+//  * StencilFunction pointers are host code; a FunctionStencil's fn must be
+//    registered with a device twin (register_device_function). The
+//    reference's own window functions are pre-registered (stengrid::functions).
+//    An unregistered fn throws std::invalid_argument — there is no CPU path.
+//  * Residency is real: Residency::Device leaves the output in HBM until
+//    sync_to_host(plan) (the paper's meaning); Residency::Host
+//    (the default) behaves exactly like the reference.
+#pragma once
+
+#include <cmath>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <variant>
+#include <vector>
+
+#include "stengrid/grid.hpp"
+#include "stengrid/worker_pool.hpp"
+
+namespace stengrid {
+
+/// stencil.hpp:12-18
+struct WeightStencil {
+  Extents ext;
+  std::vector<double> weights;
+};
+
+/// stencil.hpp:20-25 — entry (p, q) of the window is window[q*rowStride + p].
+using StencilFunction = double (*)(const double* window, const double* coe, int rowStride);
+
+/// stencil.hpp:29-33
+struct FunctionStencil {
+  Extents ext;
+  StencilFunction fn = nullptr;
+  std::vector<double> coe;
+};
+
+enum class Direction { X, Y, XY };
+enum class Residency { Host, Device };
+using StencilKind = std::variant<WeightStencil, FunctionStencil>;
+
+/// Host implementations of the reference's window functions (same arithmetic),
+/// pre-registered with their device twins.
+namespace functions {
+inline double ch_nonlinear_window(const double* window, const double* coe, int rowStride) {
+  double acc = 0.0;  // cahn_hilliard.cpp:36-47
+  for (int q = 0; q < 3; ++q) {
+    const double* row = window + static_cast<std::ptrdiff_t>(q) * rowStride;
+    const double* cr = coe + q * 3;
+    for (int p = 0; p < 3; ++p) {
+      const double v = row[p];
+      acc += cr[p] * (v * v * v - v);
+    }
+  }
+  return acc;
+}
+inline double central_difference_window(const double* w, const double* coe, int) {
+  return (w[0] - 2.0 * w[1] + w[2]) * coe[0];  // tools/main.cpp:47-49
+}
+inline double fn_center(const double* w, const double*, int rs) { return w[rs + 1]; }
+inline double fn_central_second(const double* w, const double* coe, int) {
+  double acc = 0.0;  // tests/test_stencil.cpp:70-77
+  acc += coe[0] * w[0];
+  acc += (-2.0 * coe[0]) * w[1];
+  acc += coe[0] * w[2];
+  return acc;
+}
+inline double fn_lap_cube_diff_first(const double* w, const double* coe, int rs) {
+  auto g = [](double v) { return v * v * v - v; };  // tests/test_stencil.cpp:79-85
+  const double gm = g(w[rs + 1]);
+  const double x = (g(w[rs]) - 2.0 * gm) + g(w[rs + 2]);
+  const double y = (g(w[1]) - 2.0 * gm) + g(w[2 * rs + 1]);
+  return coe[0] * x + coe[1] * y;
+}
+inline double fn_weighted_3x3(const double* w, const double* coe, int rs) {
+  double acc = 0.0;  // tests/test_stencil.cpp:88-93
+  for (int q = 0; q < 3; ++q)
+    for (int p = 0; p < 3; ++p) acc += coe[q * 3 + p] * w[q * rs + p];
+  return acc;
+}
+}  // namespace functions
+
+namespace detail {
+inline std::mutex& registry_mutex() {
+  static std::mutex m;
+  return m;
+}
+inline std::map<StencilFunction, int>& registry() {
+  static std::map<StencilFunction, int> r = {
+      {&functions::ch_nonlinear_window, SG_FN_CH_NONLINEAR},
+      {&functions::central_difference_window, SG_FN_CENTRAL_DIFFERENCE},
+      {&functions::fn_center, SG_FN_CENTER},
+      {&functions::fn_central_second, SG_FN_CENTRAL_SECOND},
+      {&functions::fn_lap_cube_diff_first, SG_FN_LAP_CUBE_DIFF_FIRST},
+      {&functions::fn_weighted_3x3, SG_FN_WEIGHTED_3X3},
+  };
+  return r;
+}
+}  // namespace detail
+
+/// Map a host window function to a device twin (an sg_function id). The
+/// caller asserts the two compute the same expression in the same order.
+inline void register_device_function(StencilFunction hostFn, sg_function deviceFn) {
+  if (hostFn == nullptr || deviceFn <= SG_FN_NONE || deviceFn >= SG_FN_COUNT)
+    throw std::invalid_argument("register_device_function: bad arguments");
+  std::lock_guard<std::mutex> lk(detail::registry_mutex());
+  detail::registry()[hostFn] = deviceFn;
+}
+
+inline int device_function_id(StencilFunction fn) {
+  if (fn == nullptr) return -1;
+  std::lock_guard<std::mutex> lk(detail::registry_mutex());
+  auto it = detail::registry().find(fn);
+  return it == detail::registry().end() ? -2 : it->second;
+}
+
+/// stencil.hpp:42-85 — movable, not copyable; never owns the fields.
+class StencilPlan {
+ public:
+  StencilPlan() = default;
+  StencilPlan(StencilPlan&& o) noexcept { *this = std::move(o); }
+  StencilPlan& operator=(StencilPlan&& o) noexcept {
+    if (this != &o) {
+      destroy();
+      h_ = o.h_;
+      o.h_ = nullptr;
+      direction_ = o.direction_;
+      mode_ = o.mode_;
+      ext_ = o.ext_;
+      kind_ = std::move(o.kind_);
+      tiles_ = std::move(o.tiles_);
+      input_ = o.input_;
+      output_ = o.output_;
+      numWorkers_ = o.numWorkers_;
+      numTiles_ = o.numTiles_;
+      fnId_ = o.fnId_;
+      boundIn_ = o.boundIn_;
+      boundOut_ = o.boundOut_;
+      o.input_ = o.output_ = nullptr;
+    }
+    return *this;
+  }
+  StencilPlan(const StencilPlan&) = delete;
+  StencilPlan& operator=(const StencilPlan&) = delete;
+  ~StencilPlan() { destroy(); }
+
+  bool valid() const { return input_ != nullptr; }
+  Direction direction() const { return direction_; }
+  BoundaryMode mode() const { return mode_; }
+  const Extents& extents() const { return ext_; }
+  const TilePlan& tiles() const { return tiles_; }
+  int num_workers() const { return numWorkers_; }
+  const Grid2D* input() const { return input_; }
+  const Grid2D* output() const { return output_; }
+
+  /// stencil.cpp:186-193 — idempotent; never touches the grids.
+  void destroy() {
+    if (h_) sg_plan_destroy(&h_);
+    h_ = nullptr;
+    input_ = nullptr;
+    output_ = nullptr;
+    tiles_ = TilePlan{};
+  }
+
+ private:
+  friend StencilPlan create_plan(Direction, BoundaryMode, StencilKind, Grid2D&, Grid2D&, int, int,
+                                 WorkerPool*);
+  friend void swap_plan(StencilPlan&);
+  friend void compute(StencilPlan&, Residency);
+  friend void sync_to_host(StencilPlan&);
+
+  // (Re)bind the C plan to the grids' current host buffers.
+  void bind() {
+    if (h_) sg_plan_destroy(&h_);
+    const double* vals = nullptr;
+    size_t count = 0;
+    if (const auto* ws = std::get_if<WeightStencil>(&kind_)) {
+      vals = ws->weights.data();
+      count = ws->weights.size();
+    } else {
+      const auto& fs = std::get<FunctionStencil>(kind_);
+      vals = fs.coe.data();
+      count = fs.coe.size();
+    }
+    const sg_extents e{ext_.left, ext_.right, ext_.top, ext_.bottom};
+    detail::check(sg_plan_create(static_cast<sg_direction>(direction_),
+                                 mode_ == BoundaryMode::Periodic ? SG_PERIODIC : SG_NONPERIODIC, e,
+                                 static_cast<sg_function>(fnId_), vals, count, SG_F64, input_->data(),
+                                 output_->data(), input_->nx, input_->ny, SG_MEM_HOST, numTiles_,
+                                 numWorkers_, &h_));
+    boundIn_ = input_->data();
+    boundOut_ = output_->data();
+  }
+
+  sg_plan_t h_ = nullptr;
+  Direction direction_ = Direction::X;
+  BoundaryMode mode_ = BoundaryMode::Periodic;
+  Extents ext_;
+  StencilKind kind_;
+  TilePlan tiles_;
+  Grid2D* input_ = nullptr;
+  Grid2D* output_ = nullptr;
+  int numWorkers_ = 1;
+  int numTiles_ = 1;
+  int fnId_ = SG_FN_NONE;
+  const double* boundIn_ = nullptr;
+  const double* boundOut_ = nullptr;
+};
+
+/// stencil.hpp:90-92 / stencil.cpp:152-184.
+inline StencilPlan create_plan(Direction direction, BoundaryMode mode, StencilKind kind, Grid2D& input,
+                               Grid2D& output, int numTiles, int numWorkers,
+                               WorkerPool* sharedPool = nullptr) {
+  if (!input.same_shape(output)) throw std::invalid_argument("create_plan: input and output shapes differ");
+  if (&input == &output || input.data() == output.data())
+    throw std::invalid_argument("create_plan: input and output must be distinct buffers");
+  int fnId = SG_FN_NONE;
+  if (const auto* fs = std::get_if<FunctionStencil>(&kind)) {
+    fnId = device_function_id(fs->fn);
+    if (fnId == -2 && fs->ext.valid())
+      throw std::invalid_argument(
+          "create_plan: stencil function has no registered device twin (register_device_function)");
+  }
+  if (numWorkers >= 1 && sharedPool != nullptr && sharedPool->workers() != numWorkers)
+    throw std::invalid_argument("create_plan: shared pool size does not match numWorkers");
+  StencilPlan plan;
+  plan.direction_ = direction;
+  plan.mode_ = mode;
+  plan.ext_ = std::visit([](const auto& s) { return s.ext; }, kind);
+  plan.kind_ = std::move(kind);
+  plan.input_ = &input;
+  plan.output_ = &output;
+  plan.numWorkers_ = numWorkers;
+  plan.numTiles_ = numTiles;
+  plan.fnId_ = fnId < 0 ? -1 : fnId;  // -1: null function -> invalid_argument from the ABI
+  try {
+    plan.bind();  // full validation (stencil.cpp:128-161) happens in the C ABI
+  } catch (...) {
+    plan.input_ = plan.output_ = nullptr;
+    throw;
+  }
+  plan.tiles_ = make_tiles(input.ny, numTiles, plan.ext_);
+  return plan;
+}
+
+inline void destroy_plan(StencilPlan& plan) { plan.destroy(); }
+
+/// stencil.cpp:197-200
+inline void swap_plan(StencilPlan& plan) {
+  if (!plan.valid()) throw std::logic_error("swap_plan: plan was destroyed");
+  detail::check(sg_plan_swap(plan.h_));
+  std::swap(plan.input_, plan.output_);
+  std::swap(plan.boundIn_, plan.boundOut_);
+}
+
+/// stencil.cpp:202-235 — runs on the GPU; synchronous.
+inline void compute(StencilPlan& plan, Residency hint = Residency::Host) {
+  if (!plan.valid()) throw std::logic_error("compute: plan was destroyed");
+  Grid2D& in = *plan.input_;
+  Grid2D& out = *plan.output_;
+  if (!in.same_shape(out)) throw std::invalid_argument("compute: bound grids changed shape");
+  if (in.data() == out.data()) throw std::invalid_argument("compute: bound grids alias");
+  if (in.data() != plan.boundIn_ || out.data() != plan.boundOut_) plan.bind();  // storage moved
+  detail::check(sg_plan_compute(plan.h_, hint == Residency::Host ? SG_RESIDENCY_HOST : SG_RESIDENCY_DEVICE,
+                                nullptr, 1));
+}
+
+/// Bring Device-resident results back into the bound host grids.
+inline void sync_to_host(StencilPlan& plan) {
+  if (!plan.valid()) throw std::logic_error("sync_to_host: plan was destroyed");
+  detail::check(sg_plan_sync_to_host(plan.h_));
+}
+
+/// stencil.cpp:237-260 — single-point evaluation (host; used as a checker).
+inline double apply_weights_at(const Grid2D& input, const WeightStencil& sten, int i, int j,
+                               BoundaryMode mode) {
+  const Extents& e = sten.ext;
+  const int W = e.width(), H = e.height();
+  const double* w = sten.weights.data();
+  const double* v = input.data();
+  double acc = 0.0;
+  for (int q = 0; q < H; ++q) {
+    const int jj = mode == BoundaryMode::Periodic ? wrap(j - e.top + q, input.ny) : j - e.top + q;
+    const std::ptrdiff_t base = static_cast<std::ptrdiff_t>(jj) * input.nx;
+    for (int p = 0; p < W; ++p) {
+      const int ii = mode == BoundaryMode::Periodic ? wrap(i - e.left + p, input.nx) : i - e.left + p;
+      acc += w[q * W + p] * v[base + ii];
+    }
+  }
+  return acc;
+}
+
+/// stencil.cpp:262-286
+inline double apply_function_at(const Grid2D& input, const FunctionStencil& sten, int i, int j,
+                                BoundaryMode mode) {
+  const Extents& e = sten.ext;
+  const int W = e.width(), H = e.height();
+  std::vector<double> window(static_cast<std::size_t>(W) * H);
+  for (int q = 0; q < H; ++q) {
+    const int jj = mode == BoundaryMode::Periodic ? wrap(j - e.top + q, input.ny) : j - e.top + q;
+    for (int p = 0; p < W; ++p) {
+      const int ii = mode == BoundaryMode::Periodic ? wrap(i - e.left + p, input.nx) : i - e.left + p;
+      window[static_cast<std::size_t>(q) * W + p] = input(ii, jj);
+    }
+  }
+  return sten.fn(window.data(), sten.coe.data(), W);
+}
+
+}  // namespace stengrid

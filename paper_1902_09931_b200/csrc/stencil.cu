@@ -22,10 +22,13 @@
 //  * k_generic — one thread per output point with per-tap modular wrap:
 //    any extents (including windows wider than the grid), any alignment,
 //    any row pitch. Used for tiny/odd grids and unusual extents.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -315,6 +318,236 @@ __global__ void __launch_bounds__(STRIP_WARPS * 32) k_strip(const __grid_constan
   }
 }
 
+// ---------------------------------------------------------------- k_tma
+// The TMA-staged variant of k_strip (the default fast path). Each warp owns
+// a strip as in k_strip, but rows are staged into a per-warp shared-memory
+// ring by the bulk-copy engine (cp.async.bulk, TMA 1D, completion on an
+// mbarrier per stage): ONE copy per row brings the strip's 32*V columns
+// plus the L/R halo columns (rounded out to 16 B) — halos are loaded once
+// and never shuffled; only edge strips add a 16-32 B wrap copy. Registers
+// hold just the H-row window, so occupancy is ~2.5x k_strip's and the ring
+// keeps S*RPS rows per warp in flight without register cost.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int TMA_WARPS = 4;
+
+template <typename T, int L, int R, int TP, int BT>
+struct TmaGeom {
+  static constexpr int V = VecT<T>::V;
+  static constexpr int SW = 32 * V;
+  static constexpr int LP = ((L + V - 1) / V) * V;  // left pad, 16 B granules
+  static constexpr int RP = ((R + V - 1) / V) * V;
+  static constexpr int ROW = LP + SW + RP;  // elements per staged row
+  static constexpr int H = TP + BT + 1;
+  // Rows per stage: a multiple of H so the register window is a ring whose
+  // slot for every unrolled row is a compile-time constant (no moves).
+  static constexpr int RPS = H >= 2 ? H : 2;
+  static constexpr int STAGES = (8 + RPS - 1) / RPS >= 2 ? (8 + RPS - 1) / RPS : 2;
+  // stage stride rounded to 128 B (tensor-TMA destination alignment)
+  static constexpr size_t stage_bytes = (static_cast<size_t>(RPS) * ROW * sizeof(T) + 127) / 128 * 128;
+  static constexpr int STAGE_ELEMS = static_cast<int>(stage_bytes / sizeof(T));
+  static constexpr size_t warp_bytes = static_cast<size_t>(STAGES) * stage_bytes;
+  static constexpr size_t smem_bytes = TMA_WARPS * warp_bytes + TMA_WARPS * STAGES * sizeof(uint64_t);
+};
+
+template <typename T, int L, int R, int TP, int BT, typename Op>
+__global__ void __launch_bounds__(TMA_WARPS * 32) k_tma(const __grid_constant__ KArgs<T> a,
+                                                        const __grid_constant__ CUtensorMap tmap) {
+  using G = TmaGeom<T, L, R, TP, BT>;
+  using VT = typename VecT<T>::type;
+  constexpr int V = G::V, SW = G::SW, LP = G::LP, RP = G::RP, ROW = G::ROW;
+  constexpr int H = G::H, RPS = G::RPS, STAGES = G::STAGES, SE = G::STAGE_ELEMS;
+  constexpr int W = L + R + 1;
+  constexpr int E = L + V + R;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  T* ring = reinterpret_cast<T*>(smem_raw + warp * G::warp_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + TMA_WARPS * G::warp_bytes) + warp * STAGES;
+
+  const int strip = blockIdx.x * TMA_WARPS + warp;
+  const int x0 = strip * SW;
+  if (x0 >= a.nx) return;  // warp-uniform
+  const int ra = a.row0 + blockIdx.y * a.segRows;
+  const int rb = min(ra + a.segRows, a.row1);
+  if (ra >= rb) return;
+  const int nx = a.nx;
+  const int valid = min(SW, nx - x0);  // columns of this strip inside the grid
+  const int xb = x0 + lane * V;
+  const bool laneValid = xb < nx;
+
+  // Copy plan for one row of this strip: a main span [c0, c1) placed at ring
+  // offset LP + (c0 - x0); wrapped halo spans only at the grid edges. All
+  // spans are whole 16 B granules (nx % V == 0, LP/RP multiples of V).
+  int c0 = x0 - LP, c1 = x0 + valid + RP;
+  int wl = 0, wr = 0;
+  if (c0 < 0) {
+    wl = a.wrapX ? -c0 : 0;
+    c0 = 0;
+  }
+  if (c1 > nx) {
+    wr = a.wrapX ? c1 - nx : 0;
+    c1 = nx;
+  }
+  const uint32_t rowBytes = static_cast<uint32_t>((c1 - c0 + wl + wr) * sizeof(T));
+
+  // Input rows ra+inShift-TP .. ; the stage count is rounded up so every
+  // stage is full (extra rows are clamped/wrapped reads whose outputs are
+  // never stored).
+  const int nIn = (rb - ra) + H - 1;
+  const int nStages = (nIn + RPS - 1) / RPS;
+  int rf = ra + a.inShift - TP;
+  if (a.wrapY) rf = wrap_idx(rf, a.inRows);
+  const T* __restrict__ in = a.in;
+  // Interior strips copy a whole stage (RPS rows x ROW columns incl. halos)
+  // with ONE 2D tensor-TMA when its rows do not wrap; edge strips and
+  // wrapping stages fall back to per-row 1D bulk copies.
+  const bool interiorX = (x0 - LP >= 0) && (x0 + SW + RP <= nx);
+  auto issue = [&](int g) {  // lane 0 only
+    const int slot = g % STAGES;
+    T* sstage = ring + slot * SE;
+    if (interiorX && rf + RPS <= a.inRows) {
+      mbar_expect_tx(&bars[slot], static_cast<uint32_t>(RPS * ROW * sizeof(T)));
+      tma_load_2d(sstage, &tmap, x0 - LP, rf, &bars[slot]);
+      rf += RPS;
+      if (a.wrapY && rf == a.inRows) rf = 0;
+      return;
+    }
+    mbar_expect_tx(&bars[slot], rowBytes * RPS);
+#pragma unroll 1
+    for (int k = 0; k < RPS; ++k) {
+      const T* grow = in + static_cast<long long>(rf) * nx;
+      T* srow = sstage + k * ROW;
+      bulk_g2s(srow + LP + (c0 - x0), grow + c0, (c1 - c0) * sizeof(T), &bars[slot]);
+      if (wl) bulk_g2s(srow + LP - wl, grow + nx - wl, wl * sizeof(T), &bars[slot]);
+      if (wr) bulk_g2s(srow + LP + valid, grow, wr * sizeof(T), &bars[slot]);
+      ++rf;
+      if (a.wrapY) {
+        if (rf == a.inRows) rf = 0;
+      } else if (rf >= a.inRows) {
+        rf = a.inRows - 1;
+      }
+    }
+  };
+  if (lane == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int g = 0; g < STAGES && g < nStages; ++g) issue(g);
+  }
+  __syncwarp();
+
+  T win[H][E];  // ring: input row t lives in win[t % H]
+  T* __restrict__ orow = a.out + static_cast<long long>(ra - (H - 1)) * nx + xb;
+  const bool vecStore = laneValid && xb >= a.col0 && xb + V <= a.col1;
+  const long long rowStep = nx;
+  int j = ra - (H - 1);  // output row completed by the current input row
+  for (int g = 0; g < nStages; ++g) {
+    const int slot = g % STAGES;
+    mbar_wait(&bars[slot], (g / STAGES) & 1);
+    const T* sbase = ring + slot * SE + LP + lane * V;
+#pragma unroll
+    for (int k = 0; k < RPS; ++k) {
+      const T* srow = sbase + k * ROW;
+      T* e = win[k % H];
+      const VT c = *reinterpret_cast<const VT*>(srow);
+      if constexpr (V == 2) {
+        e[L] = c.x;
+        e[L + 1] = c.y;
+      } else {
+        e[L] = c.x;
+        e[L + 1] = c.y;
+        e[L + 2] = c.z;
+        e[L + 3] = c.w;
+      }
+#pragma unroll
+      for (int p = 0; p < L; ++p) e[p] = srow[p - L];
+#pragma unroll
+      for (int p = 0; p < R; ++p) e[L + V + p] = srow[V + p];
+      // Output row j uses input rows j-TP .. j+BT = the H most recent rows,
+      // oldest in slot (k + 1) % H.
+      T res[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if constexpr (std::is_same_v<Op, OpWeights>) {
+          T acc = T(0);
+#pragma unroll
+          for (int q = 0; q < H; ++q)
+#pragma unroll
+            for (int p = 0; p < W; ++p) acc += a.v[q * W + p] * win[(k + 1 + q) % H][v + p];
+          res[v] = acc;
+        } else {
+          T w[H * W];
+#pragma unroll
+          for (int q = 0; q < H; ++q)
+#pragma unroll
+            for (int p = 0; p < W; ++p) w[q * W + p] = win[(k + 1 + q) % H][v + p];
+          res[v] = Op::template apply<T>(w, a.v, W);
+        }
+      }
+      if (j >= ra && j < rb) {  // warp-uniform
+        if (vecStore) {
+          VT o;
+          if constexpr (V == 2) {
+            o.x = res[0];
+            o.y = res[1];
+          } else {
+            o.x = res[0];
+            o.y = res[1];
+            o.z = res[2];
+            o.w = res[3];
+          }
+          *reinterpret_cast<VT*>(orow) = o;
+        } else if (laneValid) {
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            if (xb + v >= a.col0 && xb + v < a.col1) orow[v] = res[v];
+        }
+      }
+      ++j;
+      orow += rowStep;
+    }
+    __syncwarp();  // every lane has read slot `slot`
+    if (lane == 0 && g + STAGES < nStages) issue(g + STAGES);
+  }
+}
+
 // ------------------------------------------------------------- k_generic
 template <typename T, typename Op>
 __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T> a) {
@@ -412,8 +645,57 @@ constexpr int prefetch_depth() {
   return d >= 8 ? 8 : d >= 4 ? 4 : 2;
 }
 
+// 2D tensor map over the input grid (inner dim = columns), box ROW x RPS.
+template <typename T>
+CUtensorMap make_row_map(const T* base, int nx, int rows, int boxW, int boxH) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) throw Error(SG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(nx), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(nx) * sizeof(T)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(boxW), static_cast<cuuint32_t>(boxH)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                            const_cast<T*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(SG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return map;
+}
+
+// SG_STENCIL_KERNEL=reg selects the register-prefetch k_strip (kept for A/B
+// measurements); the default is the TMA-staged k_tma.
+bool use_tma() {
+  static const bool v = [] {
+    const char* e = std::getenv("SG_STENCIL_KERNEL");
+    return !(e && std::strcmp(e, "reg") == 0);
+  }();
+  return v;
+}
+
 template <typename T, int L, int TP, typename Op>
 void launch_strip_lt(const KArgs<T>& a, dim3 grid, cudaStream_t s) {
+  if (use_tma()) {
+    using G = TmaGeom<T, L, L, TP, TP>;
+    auto kern = k_tma<T, L, L, TP, TP, Op>;
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+      SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(G::smem_bytes)));
+      SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      configured = true;
+    }
+    const CUtensorMap map = make_row_map<T>(a.in, a.nx, a.inRows, G::ROW, G::RPS);
+    kern<<<grid, TMA_WARPS * 32, G::smem_bytes, s>>>(a, map);
+    return;
+  }
   constexpr int D = prefetch_depth<T, L>();
   k_strip<T, L, L, TP, TP, D, Op><<<grid, STRIP_WARPS * 32, 0, s>>>(a);
 }
