@@ -22,9 +22,12 @@
 //                   then compute y = K^{-1} V^T z (penta.cpp:262-274) and either
 //                   apply z -= W y in place (penta.cpp:279-286) or hand y to a
 //                   fused consumer (the CH transpose/combine kernels).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -287,6 +290,263 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_sweep(const PentaTables f, in
   }
 }
 
+// ------------------------------------------------------------ k_sweep_tma
+// The latency-bound recurrence path, TMA-fed: one warp = 32 systems; the
+// rows of z (and of the factor tables) stream into a shared-memory ring of
+// NSTG stages x RS rows through 2D/1D tensor copies (one elected lane, one
+// mbarrier per stage), NSTG*RS = 64 rows ahead of the dependency chain, so
+// each unknown costs only the FP64 latency of its 3 (forward) or 4
+// (backward) dependent ops. Forward results go to z with coalesced stores
+// and come back through the same ring for the backward pass (a proxy fence
+// orders the generic stores before the async-proxy reads).
+constexpr int SW_RS = 8;    // rows per stage
+constexpr int SW_NSTG = 8;  // stages in flight
+
+struct alignas(64) SweepMaps {
+  CUtensorMap z;     // 2D {B, n}, box {32, RS}
+  CUtensorMap t[5];  // m1, m2, dInv, ap, bp: uniform 1D {n} box {RS}; else 2D like z
+};
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void s_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void s_mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void s_mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(s_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void s_tma_2d(void* dst, const CUtensorMap* m, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          s_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(s_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void s_tma_1d(void* dst, const CUtensorMap* m, int x, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];" ::"r"(
+          s_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(s_u32(bar))
+      : "memory");
+}
+
+template <bool UNIFORM>
+struct SweepSmem {
+  // doubles per factor table per stage; tensor-TMA destinations must be
+  // 128 B aligned, so the uniform (SW_RS-long) tables get a 16-double slot
+  static constexpr int FAC = UNIFORM ? 16 : SW_RS * 32;
+  static constexpr int STAGE = SW_RS * 32 + 3 * FAC;             // z + up to 3 tables
+  static constexpr int STAGE_PAD = (STAGE * 8 + 127) / 128 * 16;  // doubles, 128 B aligned stride
+  static constexpr size_t bytes = static_cast<size_t>(SW_NSTG) * STAGE_PAD * 8 + SW_NSTG * 8;
+};
+
+template <bool UNIFORM, bool PERIODIC, int MODE>
+__global__ void __launch_bounds__(32) k_sweep_tma(const PentaTables f, const __grid_constant__ SweepMaps maps,
+                                                  int B, int n, double* __restrict__ z, double* __restrict__ y4) {
+  using SM = SweepSmem<UNIFORM>;
+  extern __shared__ __align__(128) double sw_smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sw_smem + SW_NSTG * SM::STAGE_PAD);
+  const int lane = threadIdx.x;
+  const int b0 = blockIdx.x * 32;
+  const int b = b0 + lane;
+  const bool active = b < B;
+  constexpr int FAC = SM::FAC;
+  constexpr uint32_t ZB = SW_RS * 32 * 8;
+  constexpr uint32_t FB = (UNIFORM ? SW_RS : SW_RS * 32) * 8;  // bytes per factor box
+  // stage g of pass `pass` (0 fwd: rows g*RS..; 1 bwd: rows n-(g+1)*RS..)
+  auto issue = [&](int gseq, int pass, int g) {
+    const int slot = gseq % SW_NSTG;
+    double* st = sw_smem + slot * SM::STAGE_PAD;
+    const int r0 = pass == 0 ? g * SW_RS : n - (g + 1) * SW_RS;
+    const int nt = pass == 0 ? 2 : 3;
+    s_mbar_expect_tx(&bars[slot], ZB + nt * FB);
+    s_tma_2d(st, &maps.z, b0, r0, &bars[slot]);
+    for (int k = 0; k < nt; ++k) {
+      const CUtensorMap* m = &maps.t[pass == 0 ? k : 2 + k];  // fwd: m1, m2; bwd: dInv, ap, bp
+      if (UNIFORM)
+        s_tma_1d(st + SW_RS * 32 + k * FAC, m, r0, &bars[slot]);
+      else
+        s_tma_2d(st + SW_RS * 32 + k * FAC, m, b0, r0, &bars[slot]);
+    }
+  };
+  auto fac = [&](const double* st, int k, int row) -> double {
+    return UNIFORM ? st[SW_RS * 32 + k * FAC + row] : st[SW_RS * 32 + k * FAC + row * 32 + lane];
+  };
+  const int nS = (n + SW_RS - 1) / SW_RS;  // stages per pass
+  const int total = 2 * nS;
+  auto issue_seq = [&](int gseq) {
+    if (gseq < nS) issue(gseq, 0, gseq);
+    else issue(gseq, 1, gseq - nS);
+  };
+  if (lane == 0) {
+    for (int k = 0; k < SW_NSTG; ++k) s_mbar_init(&bars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // prefetch forward stages only: backward stages read forward results
+    for (int g = 0; g < SW_NSTG && g < nS; ++g) issue_seq(g);
+  }
+  __syncwarp();
+  double* zc = z + b;
+  const long long sB = B;
+  // ---- forward
+  double y2 = 0.0, y1 = 0.0;
+  for (int g = 0; g < nS; ++g) {
+    const int slot = g % SW_NSTG;
+    s_mbar_wait(&bars[slot], (g / SW_NSTG) & 1);
+    const double* st = sw_smem + slot * SM::STAGE_PAD;
+#pragma unroll
+    for (int k = 0; k < SW_RS; ++k) {
+      const int r = g * SW_RS + k;
+      if (r < n) {
+        const double zr = st[k * 32 + lane];
+        double yr;
+        if (r >= 2) {
+          yr = zr - (fac(st, 0, k) * y2 + fac(st, 1, k) * y1);  // penta.cpp:180
+        } else if (r == 1) {
+          yr = zr - fac(st, 1, k) * y1;  // penta.cpp:173 (y1 holds y[0])
+        } else {
+          yr = zr;  // y[0] is not modified by the forward pass
+        }
+        if (active && r >= 1) zc[r * sB] = yr;
+        y2 = y1;
+        y1 = yr;
+      }
+    }
+    __syncwarp();
+    const int nxt = g + SW_NSTG;
+    if (nxt < nS && lane == 0) issue_seq(nxt);
+  }
+  // forward results must be visible to the async proxy before the backward
+  // pass streams them back
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __threadfence_block();
+  __syncwarp();
+  if (lane == 0)
+    for (int g = nS; g < nS + SW_NSTG && g < total; ++g) issue_seq(g);
+  __syncwarp();
+  // ---- backward (penta.cpp:183-196)
+  double s1 = 0.0, s2 = 0.0, zn1 = 0.0, zn2 = 0.0;
+  for (int g = nS; g < total; ++g) {
+    const int slot = g % SW_NSTG;
+    s_mbar_wait(&bars[slot], (g / SW_NSTG) & 1);
+    const double* st = sw_smem + slot * SM::STAGE_PAD;
+    const int r0 = n - (g - nS + 1) * SW_RS;
+#pragma unroll
+    for (int k = SW_RS - 1; k >= 0; --k) {
+      const int r = r0 + k;
+      if (r >= 0) {
+        const double yv = st[k * 32 + lane];
+        double yr;
+        if (r == n - 1) {
+          yr = yv * fac(st, 0, k);
+          zn1 = yr;
+        } else if (r == n - 2) {
+          yr = (yv - fac(st, 1, k) * s1) * fac(st, 0, k);
+          zn2 = yr;
+        } else {
+          yr = (yv - fac(st, 1, k) * s1 - fac(st, 2, k) * s2) * fac(st, 0, k);
+        }
+        if (active) zc[r * sB] = yr;
+        s2 = s1;
+        s1 = yr;
+      }
+    }
+    __syncwarp();
+    const int nxt = g + SW_NSTG;
+    if (nxt < total && lane == 0) issue_seq(nxt);
+  }
+  if constexpr (PERIODIC) {
+    const double zz0 = s1, zz1 = s2;  // y[0], y[1]
+    const int sys = UNIFORM ? 0 : b;
+    if (!active) return;
+    const double* cw = f.cw + sys * 6;
+    double y[4];
+    y[0] = cw[0] * zn2 + cw[1] * zn1;
+    y[1] = cw[2] * zn1;
+    y[2] = cw[3] * zz0;
+    y[3] = cw[4] * zz0 + cw[5] * zz1;
+    lu4_solve_dev(f.K + sys * 16, f.piv + sys * 4, y);
+    if constexpr (MODE == 1) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) y4[k * sB + b] = y[k];
+    } else {
+#pragma unroll 4
+      for (int r = 0; r < n; ++r) {
+        const long long idx = r * sB;
+        const double w0 = tab(f.W[0], r, b, B, UNIFORM), w1 = tab(f.W[1], r, b, B, UNIFORM),
+                     w2 = tab(f.W[2], r, b, B, UNIFORM), w3 = tab(f.W[3], r, b, B, UNIFORM);
+        zc[idx] -= w0 * y[0] + w1 * y[1] + w2 * y[2] + w3 * y[3];
+      }
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  return encode;
+}
+
+bool encode_map(CUtensorMap* m, const double* p, int rank, uint64_t d0, uint64_t d1, uint32_t b0, uint32_t b1) {
+  auto enc = tensor_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {d0, d1};
+  const cuuint64_t strides[1] = {d0 * 8};
+  const cuuint32_t box[2] = {b0, b1};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TMA path needs 16 B aligned rows (B even, aligned pointers) and a driver
+// tensor-map encoder; otherwise the register-prefetch k_sweep runs.
+bool sweep_maps(const PentaTables& f, int B, int n, const double* z, SweepMaps* maps) {
+  if (B % 2 != 0 || (reinterpret_cast<uintptr_t>(z) & 15)) return false;
+  if (std::getenv("SG_SWEEP_KERNEL") && std::strcmp(std::getenv("SG_SWEEP_KERNEL"), "reg") == 0) return false;
+  std::memset(maps, 0, sizeof(*maps));
+  if (!encode_map(&maps->z, z, 2, B, n, 32, SW_RS)) return false;
+  const double* t[5] = {f.m1, f.m2, f.dInv, f.ap, f.bp};
+  for (int k = 0; k < 5; ++k) {
+    if (reinterpret_cast<uintptr_t>(t[k]) & 15) return false;
+    const bool ok = f.uniform ? encode_map(&maps->t[k], t[k], 1, n, 1, SW_RS, 1)
+                              : encode_map(&maps->t[k], t[k], 2, B, n, 32, SW_RS);
+    if (!ok) return false;
+  }
+  return true;
+}
+
+template <bool U, bool P, int M>
+void launch_sweep_tma(const PentaTables& f, const SweepMaps& maps, int B, int n, double* z, double* y4,
+                      cudaStream_t s) {
+  auto kern = k_sweep_tma<U, P, M>;
+  static bool configured = false;
+  if (!configured) {
+    SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(SweepSmem<U>::bytes)));
+    configured = true;
+  }
+  const int blocks = (B + 31) / 32;
+  kern<<<blocks, 32, SweepSmem<U>::bytes, s>>>(f, maps, B, n, z, y4);
+}
+
 template <bool U, bool P, int M>
 void launch_sweep_t(const PentaTables& f, int B, int n, double* z, double* y4, cudaStream_t s) {
   const int blocks = (B + SWEEP_THREADS - 1) / SWEEP_THREADS;
@@ -297,6 +557,20 @@ void launch_sweep_t(const PentaTables& f, int B, int n, double* z, double* y4, c
 
 void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool periodic,
                  bool fusedCorrection, cudaStream_t s) {
+  SweepMaps maps;
+  if (sweep_maps(f, B, n, z, &maps)) {
+    if (f.uniform) {
+      if (!periodic) launch_sweep_tma<true, false, 0>(f, maps, B, n, z, y4, s);
+      else if (fusedCorrection) launch_sweep_tma<true, true, 1>(f, maps, B, n, z, y4, s);
+      else launch_sweep_tma<true, true, 0>(f, maps, B, n, z, y4, s);
+    } else {
+      if (!periodic) launch_sweep_tma<false, false, 0>(f, maps, B, n, z, y4, s);
+      else if (fusedCorrection) launch_sweep_tma<false, true, 1>(f, maps, B, n, z, y4, s);
+      else launch_sweep_tma<false, true, 0>(f, maps, B, n, z, y4, s);
+    }
+    check_launch("penta sweep (TMA) kernel");
+    return;
+  }
   if (f.uniform) {
     if (!periodic) launch_sweep_t<true, false, 0>(f, B, n, z, y4, s);
     else if (fusedCorrection) launch_sweep_t<true, true, 1>(f, B, n, z, y4, s);

@@ -356,123 +356,126 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   } while (!ok);
 }
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
-      : "memory");
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// The mbarrier receives one arrival when all prior cp.async of this thread land.
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// CTA geometry: TMA_WARPS consumer warps side by side cover CW columns; one
+// producer warp streams rows (CW + halos) into a STAGES x RPS ring.
 constexpr int TMA_WARPS = 4;
 
 template <typename T, int L, int R, int TP, int BT>
 struct TmaGeom {
   static constexpr int V = VecT<T>::V;
   static constexpr int SW = 32 * V;
+  static constexpr int CW = TMA_WARPS * SW;
   static constexpr int LP = ((L + V - 1) / V) * V;  // left pad, 16 B granules
   static constexpr int RP = ((R + V - 1) / V) * V;
-  static constexpr int ROW = LP + SW + RP;  // elements per staged row
+  static constexpr int ROW = LP + CW + RP;  // elements per staged row (~2 KB)
   static constexpr int H = TP + BT + 1;
   // Rows per stage: a multiple of H so the register window is a ring whose
   // slot for every unrolled row is a compile-time constant (no moves).
   static constexpr int RPS = H >= 2 ? H : 2;
-  static constexpr int STAGES = (8 + RPS - 1) / RPS >= 2 ? (8 + RPS - 1) / RPS : 2;
-  // stage stride rounded to 128 B (tensor-TMA destination alignment)
-  static constexpr size_t stage_bytes = (static_cast<size_t>(RPS) * ROW * sizeof(T) + 127) / 128 * 128;
-  static constexpr int STAGE_ELEMS = static_cast<int>(stage_bytes / sizeof(T));
-  static constexpr size_t warp_bytes = static_cast<size_t>(STAGES) * stage_bytes;
-  static constexpr size_t smem_bytes = TMA_WARPS * warp_bytes + TMA_WARPS * STAGES * sizeof(uint64_t);
+  static constexpr int STAGES = (9 + RPS - 1) / RPS >= 2 ? (9 + RPS - 1) / RPS : 2;
+  static constexpr size_t stage_bytes = static_cast<size_t>(RPS) * ROW * sizeof(T);
+  static constexpr size_t smem_bytes = STAGES * stage_bytes + 2 * STAGES * sizeof(uint64_t);
 };
 
 template <typename T, int L, int R, int TP, int BT, typename Op>
-__global__ void __launch_bounds__(TMA_WARPS * 32) k_tma(const __grid_constant__ KArgs<T> a,
-                                                        const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__((TMA_WARPS + 1) * 32) k_tma(const __grid_constant__ KArgs<T> a) {
   using G = TmaGeom<T, L, R, TP, BT>;
   using VT = typename VecT<T>::type;
-  constexpr int V = G::V, SW = G::SW, LP = G::LP, RP = G::RP, ROW = G::ROW;
-  constexpr int H = G::H, RPS = G::RPS, STAGES = G::STAGES, SE = G::STAGE_ELEMS;
+  constexpr int V = G::V, SW = G::SW, CW = G::CW, LP = G::LP, RP = G::RP, ROW = G::ROW;
+  constexpr int H = G::H, RPS = G::RPS, STAGES = G::STAGES;
   constexpr int W = L + R + 1;
   constexpr int E = L + V + R;
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * G::stage_bytes);
+  uint64_t* empty = full + STAGES;
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  T* ring = reinterpret_cast<T*>(smem_raw + warp * G::warp_bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + TMA_WARPS * G::warp_bytes) + warp * STAGES;
-
-  const int strip = blockIdx.x * TMA_WARPS + warp;
-  const int x0 = strip * SW;
-  if (x0 >= a.nx) return;  // warp-uniform
+  const int nx = a.nx;
+  const int cx0 = blockIdx.x * CW;
   const int ra = a.row0 + blockIdx.y * a.segRows;
   const int rb = min(ra + a.segRows, a.row1);
-  if (ra >= rb) return;
-  const int nx = a.nx;
-  const int valid = min(SW, nx - x0);  // columns of this strip inside the grid
-  const int xb = x0 + lane * V;
-  const bool laneValid = xb < nx;
-
-  // Copy plan for one row of this strip: a main span [c0, c1) placed at ring
-  // offset LP + (c0 - x0); wrapped halo spans only at the grid edges. All
-  // spans are whole 16 B granules (nx % V == 0, LP/RP multiples of V).
-  int c0 = x0 - LP, c1 = x0 + valid + RP;
-  int wl = 0, wr = 0;
-  if (c0 < 0) {
-    wl = a.wrapX ? -c0 : 0;
-    c0 = 0;
-  }
-  if (c1 > nx) {
-    wr = a.wrapX ? c1 - nx : 0;
-    c1 = nx;
-  }
-  const uint32_t rowBytes = static_cast<uint32_t>((c1 - c0 + wl + wr) * sizeof(T));
-
-  // Input rows ra+inShift-TP .. ; the stage count is rounded up so every
-  // stage is full (extra rows are clamped/wrapped reads whose outputs are
-  // never stored).
+  if (ra >= rb) return;  // CTA-uniform
   const int nIn = (rb - ra) + H - 1;
   const int nStages = (nIn + RPS - 1) / RPS;
-  int rf = ra + a.inShift - TP;
-  if (a.wrapY) rf = wrap_idx(rf, a.inRows);
-  const T* __restrict__ in = a.in;
-  // Interior strips copy a whole stage (RPS rows x ROW columns incl. halos)
-  // with ONE 2D tensor-TMA when its rows do not wrap; edge strips and
-  // wrapping stages fall back to per-row 1D bulk copies.
-  const bool interiorX = (x0 - LP >= 0) && (x0 + SW + RP <= nx);
-  auto issue = [&](int g) {  // lane 0 only
-    const int slot = g % STAGES;
-    T* sstage = ring + slot * SE;
-    if (interiorX && rf + RPS <= a.inRows) {
-      mbar_expect_tx(&bars[slot], static_cast<uint32_t>(RPS * ROW * sizeof(T)));
-      tma_load_2d(sstage, &tmap, x0 - LP, rf, &bars[slot]);
-      rf += RPS;
-      if (a.wrapY && rf == a.inRows) rf = 0;
-      return;
+
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < STAGES; ++k) {
+      mbar_init(&full[k], 2);  // expect_tx arrival + cp.async (halo) arrival
+      mbar_init(&empty[k], TMA_WARPS);
     }
-    mbar_expect_tx(&bars[slot], rowBytes * RPS);
-#pragma unroll 1
-    for (int k = 0; k < RPS; ++k) {
-      const T* grow = in + static_cast<long long>(rf) * nx;
-      T* srow = sstage + k * ROW;
-      bulk_g2s(srow + LP + (c0 - x0), grow + c0, (c1 - c0) * sizeof(T), &bars[slot]);
-      if (wl) bulk_g2s(srow + LP - wl, grow + nx - wl, wl * sizeof(T), &bars[slot]);
-      if (wr) bulk_g2s(srow + LP + valid, grow, wr * sizeof(T), &bars[slot]);
-      ++rf;
-      if (a.wrapY) {
-        if (rf == a.inRows) rf = 0;
-      } else if (rf >= a.inRows) {
-        rf = a.inRows - 1;
-      }
-    }
-  };
-  if (lane == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    for (int g = 0; g < STAGES && g < nStages; ++g) issue(g);
   }
-  __syncwarp();
+  __syncthreads();
 
+  if (warp == TMA_WARPS) {
+    // ---------------- producer: per row, one bulk copy of the CTA's own
+    // columns (128 B aligned, whole lines: no over-fetch) and 16 B cp.async
+    // granules for the halo columns (wrapped in index math at grid edges).
+    if (lane != 0) return;
+    const int validC = min(CW, nx - cx0);
+    const uint32_t mainBytes = static_cast<uint32_t>(validC * sizeof(T));
+    int hsrc[(LP + RP) / V > 0 ? (LP + RP) / V : 1];
+    int hdst[(LP + RP) / V > 0 ? (LP + RP) / V : 1];
+    int nh = 0;
+#pragma unroll
+    for (int k = 0; k < LP / V; ++k) {
+      const int c = cx0 - LP + k * V;
+      if (c >= 0 || a.wrapX) {
+        hsrc[nh] = c >= 0 ? c : c + nx;
+        hdst[nh++] = k * V;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < RP / V; ++k) {
+      const int c = cx0 + validC + k * V;
+      if (c < nx || a.wrapX) {
+        hsrc[nh] = c < nx ? c : c - nx;
+        hdst[nh++] = LP + validC + k * V;
+      }
+    }
+    int rf = ra + a.inShift - TP;
+    if (a.wrapY) rf = wrap_idx(rf, a.inRows);
+    const T* __restrict__ in = a.in;
+    for (int g = 0; g < nStages; ++g) {
+      const int slot = g % STAGES;
+      if (g >= STAGES) mbar_wait(&empty[slot], ((g / STAGES) + 1) & 1);
+      mbar_expect_tx(&full[slot], mainBytes * RPS);
+      T* sstage = ring + slot * (RPS * ROW);
+#pragma unroll
+      for (int k = 0; k < RPS; ++k) {
+        const T* grow = in + static_cast<long long>(rf) * nx;
+        T* srow = sstage + k * ROW;
+        bulk_g2s(srow + LP, grow + cx0, mainBytes, &full[slot]);
+        for (int h = 0; h < nh; ++h) cp_async16(srow + hdst[h], grow + hsrc[h]);
+        ++rf;
+        if (a.wrapY) {
+          if (rf == a.inRows) rf = 0;
+        } else if (rf >= a.inRows) {
+          rf = a.inRows - 1;
+        }
+      }
+      cp_async_mbar_arrive(&full[slot]);
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  const int xb = cx0 + warp * SW + lane * V;
+  const bool laneValid = xb < nx;
   T win[H][E];  // ring: input row t lives in win[t % H]
   T* __restrict__ orow = a.out + static_cast<long long>(ra - (H - 1)) * nx + xb;
   const bool vecStore = laneValid && xb >= a.col0 && xb + V <= a.col1;
@@ -480,8 +483,8 @@ __global__ void __launch_bounds__(TMA_WARPS * 32) k_tma(const __grid_constant__ 
   int j = ra - (H - 1);  // output row completed by the current input row
   for (int g = 0; g < nStages; ++g) {
     const int slot = g % STAGES;
-    mbar_wait(&bars[slot], (g / STAGES) & 1);
-    const T* sbase = ring + slot * SE + LP + lane * V;
+    mbar_wait(&full[slot], (g / STAGES) & 1);
+    const T* sbase = ring + slot * (RPS * ROW) + LP + warp * SW + lane * V;
 #pragma unroll
     for (int k = 0; k < RPS; ++k) {
       const T* srow = sbase + k * ROW;
@@ -543,8 +546,8 @@ __global__ void __launch_bounds__(TMA_WARPS * 32) k_tma(const __grid_constant__ 
       ++j;
       orow += rowStep;
     }
-    __syncwarp();  // every lane has read slot `slot`
-    if (lane == 0 && g + STAGES < nStages) issue(g + STAGES);
+    __syncwarp();  // every lane of this warp has read the stage
+    if (lane == 0) mbar_arrive(&empty[slot]);
   }
 }
 
@@ -645,31 +648,6 @@ constexpr int prefetch_depth() {
   return d >= 8 ? 8 : d >= 4 ? 4 : 2;
 }
 
-// 2D tensor map over the input grid (inner dim = columns), box ROW x RPS.
-template <typename T>
-CUtensorMap make_row_map(const T* base, int nx, int rows, int boxW, int boxH) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      fn = nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }();
-  if (!encode) throw Error(SG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  CUtensorMap map;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(nx), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(nx) * sizeof(T)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(boxW), static_cast<cuuint32_t>(boxH)};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                            const_cast<T*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw Error(SG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  return map;
-}
-
 // SG_STENCIL_KERNEL=reg selects the register-prefetch k_strip (kept for A/B
 // measurements); the default is the TMA-staged k_tma.
 bool use_tma() {
@@ -692,8 +670,8 @@ void launch_strip_lt(const KArgs<T>& a, dim3 grid, cudaStream_t s) {
       SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       configured = true;
     }
-    const CUtensorMap map = make_row_map<T>(a.in, a.nx, a.inRows, G::ROW, G::RPS);
-    kern<<<grid, TMA_WARPS * 32, G::smem_bytes, s>>>(a, map);
+    dim3 g2((a.nx + G::CW - 1) / G::CW, grid.y);
+    kern<<<g2, (TMA_WARPS + 1) * 32, G::smem_bytes, s>>>(a);
     return;
   }
   constexpr int D = prefetch_depth<T, L>();
