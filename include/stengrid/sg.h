@@ -7,8 +7,8 @@
  *
  * Each function names the reference interface it replaces
  * (/root/reference/proj/...). The reference is a C++ library with no FFI of
- * its own; this ABI is what its C++ API (re-implemented on top of it in
- * include/stengrid/*.hpp) and any ctypes/cffi binding call.
+ * its own; this ABI is what its C++ API (re-implemented on top of it by the
+ * headers in include/stengrid) and any ctypes/cffi binding call.
  *
  * Memory: grids are dense row-major (entry (i, j) at j*nx + i, grid.hpp:11-49).
  * A plan binds either HOST buffers (the plan owns device mirrors and moves
@@ -174,9 +174,30 @@ sg_status sg_ch_set_state(sg_ch_t ch, const double* curr, const double* prev, sg
 sg_status sg_ch_get_field(sg_ch_t ch, int which, double* out, sg_memory memory);
 sg_status sg_ch_device_field(sg_ch_t ch, int which, const double** dptr);
 sg_status sg_ch_status(sg_ch_t ch, int* step, double* time);
-/* Diagnostics (cahn_hilliard.cpp:330-340) via the reference host algorithm
- * on a downloaded copy of C^n. */
 sg_status sg_ch_destroy(sg_ch_t* ch);
+
+/* ------------------------------------- distributed Cahn-Hilliard (y-slabs)
+ * One process per GPU; rank r owns rows [r*ny/world, (r+1)*ny/world) of both
+ * time levels, stored as "ext" slabs with 2 halo rows above and below
+ * ((own + 4) x nx, row-major). Per step the host (ch_dist.py) runs:
+ *   halo exchange of both ext slabs (2 rows each way, periodic ring)
+ *   sg_chd_phase_x   fused RHS + x-sweep + Woodbury-corrected transpose into
+ *                    `send`, packed as world blocks of (own x nx/world)
+ *   all-to-all       send -> ycol: rank q receives columns [q*nxq,(q+1)*nxq)
+ *                    of every row, i.e. the (ny x nxq) y-sweep batch
+ *   sg_chd_phase_y   y-sweep (nxq periodic systems of ny unknowns) in place
+ *   all-to-all       ycol -> recv (packed like send)
+ *   sg_chd_combine   C^{n+1} = (2C^n - C^{n-1}) + v over C^{n-1}; roles swap.
+ * Replaces CHStepper::step (cahn_hilliard.cpp:260-328) across GPUs; the
+ * arithmetic is identical, so fields are bitwise independent of world. */
+typedef struct sg_chd_s* sg_chd_t;
+sg_status sg_chd_create(const sg_ch_params* p, int world, int rank, sg_chd_t* h);
+sg_status sg_chd_geometry(sg_chd_t h, int* own, int* nxq, int* r0);
+sg_status sg_chd_init(sg_chd_t h, double* currExt, double* prevExt, void* stream);
+sg_status sg_chd_phase_x(sg_chd_t h, const double* currExt, const double* prevExt, double* send, void* stream);
+sg_status sg_chd_phase_y(sg_chd_t h, double* ycol, void* stream);
+sg_status sg_chd_combine(sg_chd_t h, const double* currExt, double* prevExt, const double* recv, void* stream);
+sg_status sg_chd_destroy(sg_chd_t* h);
 
 #ifdef __cplusplus
 }

@@ -33,7 +33,9 @@ EXPORTED = [
     "sg_plan_mark_host_dirty", "sg_plan_binding", "sg_plan_valid", "sg_plan_kernel_kind",
     "sg_stencil_launch", "sg_penta_create", "sg_penta_solve", "sg_penta_destroy",
     "sg_ch_default_params", "sg_ch_validate", "sg_ch_create", "sg_ch_step", "sg_ch_set_state",
-    "sg_ch_get_field", "sg_ch_device_field", "sg_ch_status", "sg_ch_destroy",
+    "sg_ch_get_field", "sg_ch_device_field", "sg_ch_status", "sg_ch_destroy", "sg_chd_create",
+    "sg_chd_geometry", "sg_chd_init", "sg_chd_phase_x", "sg_chd_phase_y", "sg_chd_combine",
+    "sg_chd_destroy",
 ]
 
 
@@ -130,6 +132,13 @@ def lib():
         "sg_ch_device_field": (C.c_int, [vp, C.c_int, C.POINTER(vp)]),
         "sg_ch_status": (C.c_int, [vp, ip, dp]),
         "sg_ch_destroy": (C.c_int, [C.POINTER(vp)]),
+        "sg_chd_create": (C.c_int, [C.POINTER(SgChParams), C.c_int, C.c_int, C.POINTER(vp)]),
+        "sg_chd_geometry": (C.c_int, [vp, ip, ip, ip]),
+        "sg_chd_init": (C.c_int, [vp, vp, vp, vp]),
+        "sg_chd_phase_x": (C.c_int, [vp, vp, vp, vp, vp]),
+        "sg_chd_phase_y": (C.c_int, [vp, vp, vp]),
+        "sg_chd_combine": (C.c_int, [vp, vp, vp, vp, vp]),
+        "sg_chd_destroy": (C.c_int, [C.POINTER(vp)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name, None)

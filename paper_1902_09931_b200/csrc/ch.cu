@@ -106,22 +106,38 @@ __device__ __forceinline__ int wrapi(int i, int n) {
   return r < 0 ? r + n : r;
 }
 
+// Input geometry of the RHS kernel: output row jl (0..outRows) reads input
+// rows jl + inShift + dy, dy in [-2, 2], wrapped modulo inRows iff wrapY
+// (full periodic grid: inShift 0, wrapY 1; a y-slab with 2 halo rows above
+// and below: inShift 2, wrapY 0). Columns always wrap (periodic in x).
+struct RhsGeom {
+  int nx, outRows, inRows, inShift, wrapY;
+};
+
+__device__ __forceinline__ int wrap_once(int i, int n) {  // i in [-n, 2n)
+  return i < 0 ? i + n : (i >= n ? i - n : i);
+}
+
 template <bool NONLINEAR>
 __global__ void __launch_bounds__(256) k_rhs(const double* __restrict__ cc, const double* __restrict__ cp,
-                                             double* __restrict__ rhsT, int nx, int ny,
+                                             double* __restrict__ rhsT, const RhsGeom G,
                                              const __grid_constant__ RhsParams P) {
   __shared__ double sc[TE][TE + 1];  // C^n with a 2-point halo
   __shared__ double sb[TE][TE + 1];  // Cbar with a 2-point halo
+  __shared__ double sp[TS][TS + 1];  // C^{n-1}, tile interior
+  const int nx = G.nx;
   const int i0 = blockIdx.x * TS, j0 = blockIdx.y * TS;
   const int tx = threadIdx.x, ty = threadIdx.y;
   for (int y = ty; y < TE; y += blockDim.y) {
-    const int j = wrapi(j0 - HALO + y, ny);
+    int j = j0 - HALO + y + G.inShift;
+    j = G.wrapY ? (G.inRows >= TE ? wrap_once(j, G.inRows) : wrapi(j, G.inRows)) : min(max(j, 0), G.inRows - 1);
     for (int x = tx; x < TE; x += blockDim.x) {
-      const int i = wrapi(i0 - HALO + x, nx);
+      const int i = nx >= TE ? wrap_once(i0 - HALO + x, nx) : wrapi(i0 - HALO + x, nx);
       const long long idx = static_cast<long long>(j) * nx + i;
       const double c = __ldg(cc + idx), p = __ldg(cp + idx);
       sc[y][x] = c;
       sb[y][x] = 2.0 * c - p;  // cahn_hilliard.cpp:273
+      if (y >= HALO && y < HALO + TS && x >= HALO && x < HALO + TS) sp[y - HALO][x - HALO] = p;
     }
   }
   __syncthreads();
@@ -138,10 +154,8 @@ __global__ void __launch_bounds__(256) k_rhs(const double* __restrict__ cc, cons
       const int q = kBihTaps[t] / 5, p = kBihTaps[t] % 5;
       bh += P.bw[kBihTaps[t]] * sb[y + q][x + p];
     }
-    const int i = (i0 + x) % nx, j = (j0 + y) % ny;
-    const long long idx = static_cast<long long>(j) * nx + i;
     const double c = sc[y + HALO][x + HALO];
-    const double pr = __ldg(cp + idx);
+    const double pr = sp[y][x];
     double r;
     if constexpr (NONLINEAR) {
       double nl = 0.0;
@@ -158,7 +172,8 @@ __global__ void __launch_bounds__(256) k_rhs(const double* __restrict__ cc, cons
     res[k] = r;
   }
   __syncthreads();
-  // stage the tile transposed in smem, then write rhsT[i*ny + j] coalesced in j
+  // stage the tile transposed in smem, then write rhsT[i*outRows + jl]
+  // coalesced in jl (the x-sweep's interleaved batch)
 #pragma unroll
   for (int k = 0; k < TS / 8; ++k) sc[tx][ty + 8 * k] = res[k];
   __syncthreads();
@@ -166,7 +181,7 @@ __global__ void __launch_bounds__(256) k_rhs(const double* __restrict__ cc, cons
   for (int k = 0; k < TS / 8; ++k) {
     const int x = ty + 8 * k;  // i within the tile
     const int i = i0 + x, j = j0 + tx;
-    if (i < nx && j < ny) rhsT[static_cast<long long>(i) * ny + j] = sc[x][tx];
+    if (i < nx && j < G.outRows) rhsT[static_cast<long long>(i) * G.outRows + j] = sc[x][tx];
   }
 }
 
@@ -175,45 +190,79 @@ struct CorrTables {
   const double* y4;  // y4[k*B + b]
 };
 
-// w(i,j) = zT[i*ny + j] - (Wx0[i] y0[j] + Wx1[i] y1[j] + Wx2[i] y2[j] + Wx3[i] y3[j])
+// w(i,jl) = zT[i*own + jl] - (Wx0[i] y0[jl] + Wx1[i] y1[jl] + Wx2[i] y2[jl] + Wx3[i] y3[jl]),
+// stored PACKED for the all-to-all: block q = i / nxq holds own x nxq
+// (row jl, column i % nxq). With one rank (nxq = nx) this is row-major w.
 __global__ void __launch_bounds__(256) k_transpose_correct(const double* __restrict__ zT,
-                                                           double* __restrict__ w, int nx, int ny,
+                                                           double* __restrict__ w, int nx, int own, int nxq,
                                                            const CorrTables t) {
   __shared__ double tile[TS][TS + 1];
   const int i0 = blockIdx.x * TS, j0 = blockIdx.y * TS;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  // read zT rows i (contiguous j), apply the correction
 #pragma unroll
   for (int k = 0; k < TS / 8; ++k) {
     const int i = i0 + ty + 8 * k, j = j0 + tx;
-    if (i < nx && j < ny) {
-      const double z = zT[static_cast<long long>(i) * ny + j];
-      const double corr = __ldg(t.W[0] + i) * __ldg(t.y4 + j) + __ldg(t.W[1] + i) * __ldg(t.y4 + ny + j) +
-                          __ldg(t.W[2] + i) * __ldg(t.y4 + 2LL * ny + j) +
-                          __ldg(t.W[3] + i) * __ldg(t.y4 + 3LL * ny + j);
-      tile[ty + 8 * k][tx] = z - corr;
+    if (i < nx && j < own) {
+      const double z = zT[static_cast<long long>(i) * own + j];
+      const double corr = __ldg(t.W[0] + i) * __ldg(t.y4 + j) + __ldg(t.W[1] + i) * __ldg(t.y4 + own + j) +
+                          __ldg(t.W[2] + i) * __ldg(t.y4 + 2LL * own + j) +
+                          __ldg(t.W[3] + i) * __ldg(t.y4 + 3LL * own + j);
+      tile[ty + 8 * k][tx] = z - corr;  // penta.cpp:283-284
     }
   }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < TS / 8; ++k) {
     const int j = j0 + ty + 8 * k, i = i0 + tx;
-    if (i < nx && j < ny) w[static_cast<long long>(j) * nx + i] = tile[tx][ty + 8 * k];
+    if (i < nx && j < own) {
+      const int q = i / nxq, c = i - q * nxq;
+      w[static_cast<long long>(q) * own * nxq + static_cast<long long>(j) * nxq + c] = tile[tx][ty + 8 * k];
+    }
   }
 }
 
-// C^{n+1} = (2 C^n - C^{n-1}) + (w - (Wy0[j] y0[i] + ... + Wy3[j] y3[i])), over C^{n-1}.
+// Single GPU: C^{n+1} = (2 C^n - C^{n-1}) + (w - (Wy0[j] y0[i] + ... + Wy3[j] y3[i])), over C^{n-1}.
 __global__ void __launch_bounds__(256) k_combine(const double* __restrict__ cc, double* __restrict__ cpNext,
                                                  const double* __restrict__ w, int nx, int ny,
                                                  const CorrTables t) {
-  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= static_cast<long long>(nx) * ny) return;
-  const int j = static_cast<int>(idx / nx), i = static_cast<int>(idx % nx);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i >= nx) return;
+  const long long idx = static_cast<long long>(j) * nx + i;
   const double v = w[idx] - (__ldg(t.W[0] + j) * __ldg(t.y4 + i) + __ldg(t.W[1] + j) * __ldg(t.y4 + nx + i) +
                              __ldg(t.W[2] + j) * __ldg(t.y4 + 2LL * nx + i) +
                              __ldg(t.W[3] + j) * __ldg(t.y4 + 3LL * nx + i));
   const double cb = 2.0 * cc[idx] - cpNext[idx];
   cpNext[idx] = cb + v;  // cahn_hilliard.cpp:320
+}
+
+// y-slab: C^{n+1} = (2 C^n - C^{n-1}) + v with v the (already corrected)
+// y-sweep result received PACKED from the all-to-all; fields are ext slabs
+// (2 halo rows above the own rows).
+__global__ void __launch_bounds__(256) k_combine_packed(const double* __restrict__ ccExt, double* __restrict__ cpExt,
+                                                        const double* __restrict__ v, int nx, int own, int nxq) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jl = blockIdx.y;
+  if (i >= nx) return;
+  const long long idx = static_cast<long long>(jl + HALO) * nx + i;
+  const int q = i / nxq, c = i - q * nxq;
+  const double vv = v[static_cast<long long>(q) * own * nxq + static_cast<long long>(jl) * nxq + c];
+  const double cb = 2.0 * ccExt[idx] - cpExt[idx];
+  cpExt[idx] = cb + vv;  // cahn_hilliard.cpp:320
+}
+
+// initial_condition on a slab: global element index k = (r0 + jl)*nx + i.
+__global__ void k_init_slab(unsigned long long seed, double amp, int nx, int own, int r0, double* __restrict__ ext) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jl = blockIdx.y;
+  if (i >= nx) return;
+  const long long k = static_cast<long long>(r0 + jl) * nx + i;
+  unsigned long long z = seed + static_cast<unsigned long long>(k + 1) * 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  z = z ^ (z >> 31);
+  const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
+  ext[static_cast<long long>(jl + HALO) * nx + i] = amp * (2.0 * u - 1.0);
 }
 
 // Bands of the uniform hyperdiffusion operator (penta.cpp:313-335) for one
@@ -227,6 +276,38 @@ __global__ void k_fill_bands(double sigma, int n, double* e, double* c, double* 
   a[r] = -4.0 * sigma;
   b[r] = sigma;
 }
+
+}  // namespace
+
+static void k_init_slab_launch(unsigned long long seed, double amp, int nx, int own, int r0, double* ext,
+                        cudaStream_t s) {
+  k_init_slab<<<dim3((nx + 255) / 256, own), 256, 0, s>>>(seed, amp, nx, own, r0, ext);
+  check_launch("ch slab init kernel");
+}
+
+static void ch_phase_x(const sg_ch_params& p, const RhsParams& rp, const PentaTables& fx, int own, int nxq,
+                const double* cur, const double* prev, double* rhsT, double* y4x, double* send, cudaStream_t s) {
+  const int nx = p.nx;
+  dim3 tb(32, 8), tg((nx + TS - 1) / TS, (own + TS - 1) / TS);
+  const RhsGeom geom{nx, own, own + 2 * HALO, HALO, 0};
+  if (p.nonlinearEnabled)
+    k_rhs<true><<<tg, tb, 0, s>>>(cur, prev, rhsT, geom, rp);
+  else
+    k_rhs<false><<<tg, tb, 0, s>>>(cur, prev, rhsT, geom, rp);
+  check_launch("ch slab rhs kernel");
+  penta_sweep(fx, own, nx, rhsT, y4x, true, true, s);
+  CorrTables tx{{fx.W[0], fx.W[1], fx.W[2], fx.W[3]}, y4x};
+  k_transpose_correct<<<tg, tb, 0, s>>>(rhsT, send, nx, own, nxq, tx);
+  check_launch("ch slab transpose kernel");
+}
+
+static void ch_combine_packed(int nx, int own, int nxq, const double* cur, double* prev, const double* recv,
+                       cudaStream_t s) {
+  k_combine_packed<<<dim3((nx + 255) / 256, own), 256, 0, s>>>(cur, prev, recv, nx, own, nxq);
+  check_launch("ch slab combine kernel");
+}
+
+namespace {
 
 bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
@@ -327,19 +408,19 @@ struct ChState {
     const double* cc = field[c];
     double* cp = field[1 - c];
     dim3 tb(32, 8), tg((nx + TS - 1) / TS, (ny + TS - 1) / TS);
+    const RhsGeom geom{nx, ny, ny, 0, 1};
     if (p.nonlinearEnabled)
-      k_rhs<true><<<tg, tb, 0, s>>>(cc, cp, rhsT, nx, ny, rp);
+      k_rhs<true><<<tg, tb, 0, s>>>(cc, cp, rhsT, geom, rp);
     else
-      k_rhs<false><<<tg, tb, 0, s>>>(cc, cp, rhsT, nx, ny, rp);
+      k_rhs<false><<<tg, tb, 0, s>>>(cc, cp, rhsT, geom, rp);
     check_launch("ch rhs kernel");
     penta_sweep(fx.t, ny, nx, rhsT, y4x, true, true, s);
     CorrTables tx{{fx.t.W[0], fx.t.W[1], fx.t.W[2], fx.t.W[3]}, y4x};
-    k_transpose_correct<<<tg, tb, 0, s>>>(rhsT, w, nx, ny, tx);
+    k_transpose_correct<<<tg, tb, 0, s>>>(rhsT, w, nx, ny, nx, tx);
     check_launch("ch transpose kernel");
     penta_sweep(fy.t, nx, ny, w, y4y, true, true, s);
     CorrTables ty{{fy.t.W[0], fy.t.W[1], fy.t.W[2], fy.t.W[3]}, y4y};
-    const long long cnt = static_cast<long long>(nx) * ny;
-    k_combine<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, s>>>(cc, cp, w, nx, ny, ty);
+    k_combine<<<dim3((nx + 255) / 256, ny), 256, 0, s>>>(cc, cp, w, nx, ny, ty);
     check_launch("ch combine kernel");
   }
 
@@ -367,7 +448,70 @@ struct ChState {
   }
 };
 
+// ------------------------------------------------------------------------
+// Distributed CH (one process per GPU, y-slabs). The host orchestrates:
+//   halo exchange (2 rows of C^n, C^{n-1}) -> phase_x -> all-to-all ->
+//   phase_y -> all-to-all -> combine
+// (paper_1902_09931_b200/ch_dist.py). Each phase is the single-GPU step's
+// arithmetic on the rank's share, so results are bitwise identical for
+// every world size.
+struct ChDist {
+  sg_ch_params p{};
+  int world = 1, rank = 0, own = 0, nxq = 0, r0 = 0;
+  int device = 0;
+  DevicePenta fx, fy;
+  RhsParams rp{};
+  double *rhsT = nullptr, *y4x = nullptr, *ybuf = nullptr;
+  std::vector<void*> allocs;
+  cudaStream_t stream = nullptr;
+
+  double* dalloc(size_t n) {
+    void* q = nullptr;
+    SG_CUDA(cudaMalloc(&q, n * sizeof(double)));
+    allocs.push_back(q);
+    return static_cast<double*>(q);
+  }
+  ~ChDist() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* q : allocs) cudaFree(q);
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void build_factor(DevicePenta& f, double sigma, int n) {
+    double* bands = dalloc(5 * static_cast<size_t>(n));
+    k_fill_bands<<<(n + 255) / 256, 256, 0, stream>>>(sigma, n, bands, bands + n, bands + 2 * n, bands + 3 * n,
+                                                      bands + 4 * n);
+    check_launch("ch bands kernel");
+    f.build(1, n, true, true, bands, bands + n, bands + 2 * n, bands + 3 * n, bands + 4 * n, stream);
+  }
+  void init() {
+    SG_CUDA(cudaGetDevice(&device));
+    SG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    own = p.ny / world;
+    nxq = p.nx / world;
+    r0 = rank * own;
+    rhsT = dalloc(static_cast<size_t>(own) * p.nx);
+    y4x = dalloc(4 * static_cast<size_t>(own));
+    ybuf = dalloc(4 * static_cast<size_t>(nxq));
+    const double dx = p.lx / p.nx, dy = p.ly / p.ny;
+    build_factor(fx, kTwoThirds * p.D * p.gamma * p.dt / pow4(dx), p.nx);
+    build_factor(fy, kTwoThirds * p.D * p.gamma * p.dt / pow4(dy), p.ny);
+    rp.kDiff = -kTwoThirds;
+    rp.kBih = kTwoThirds * p.D * p.gamma * p.dt;
+    rp.kNl = kTwoThirds * p.D * p.dt;
+    biharmonic_weights(dx, dy, rp.bw);
+    const double cx = 1.0 / (dx * dx), cy = 1.0 / (dy * dy), cc = -2.0 * cx - 2.0 * cy;
+    const double nl[9] = {0.0, cy, 0.0, cx, cc, cx, 0.0, cy, 0.0};
+    std::memcpy(rp.nl, nl, sizeof nl);
+    SG_CUDA(cudaStreamSynchronize(stream));
+  }
+};
+
 }  // namespace sg
+
+struct sg_chd_s {
+  std::unique_ptr<sg::ChDist> d;
+};
 
 struct sg_ch_s {
   std::unique_ptr<sg::ChState> st;
@@ -591,6 +735,93 @@ sg_status sg_penta_destroy(sg_penta_t* f) {
     }
     delete *f;
     *f = nullptr;
+  });
+}
+
+// ------------------------------------------------------- distributed CH
+
+sg_status sg_chd_create(const sg_ch_params* p, int world, int rank, sg_chd_t* h) {
+  return guard2([&] {
+    if (!p || !h) sg::invalid("CH slab: null argument");
+    *h = nullptr;
+    sg::ch_validate(*p);
+    if (world < 1 || rank < 0 || rank >= world) sg::invalid("CH slab: bad world/rank");
+    if (p->ny % world != 0 || p->nx % world != 0)
+      sg::invalid("CH slab: world size must divide nx and ny");
+    if (p->ny / world < 2) sg::invalid("CH slab: each rank needs at least 2 rows");
+    require_device2();
+    auto o = std::make_unique<sg_chd_s>();
+    o->d = std::make_unique<sg::ChDist>();
+    o->d->p = *p;
+    o->d->world = world;
+    o->d->rank = rank;
+    o->d->init();
+    *h = o.release();
+  });
+}
+
+sg_status sg_chd_geometry(sg_chd_t h, int* own, int* nxq, int* r0) {
+  return guard2([&] {
+    if (!h) sg::logic("CH slab: destroyed");
+    if (own) *own = h->d->own;
+    if (nxq) *nxq = h->d->nxq;
+    if (r0) *r0 = h->d->r0;
+  });
+}
+
+sg_status sg_chd_init(sg_chd_t h, double* currExt, double* prevExt, void* stream) {
+  return guard2([&] {
+    if (!h) sg::logic("CH slab: destroyed");
+    auto& d = *h->d;
+    SG_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    const int nx = d.p.nx;
+    sg::k_init_slab_launch(d.p.seed, d.p.icAmplitude, nx, d.own, d.r0, currExt, s);
+    const size_t rowB = static_cast<size_t>(nx) * sizeof(double);
+    SG_CUDA(cudaMemcpyAsync(prevExt, currExt, rowB * (d.own + 4), cudaMemcpyDeviceToDevice, s));
+    if (!stream) SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+sg_status sg_chd_phase_x(sg_chd_t h, const double* currExt, const double* prevExt, double* send, void* stream) {
+  return guard2([&] {
+    if (!h) sg::logic("CH slab: destroyed");
+    auto& d = *h->d;
+    SG_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    sg::ch_phase_x(d.p, d.rp, d.fx.t, d.own, d.nxq, currExt, prevExt, d.rhsT, d.y4x, send, s);
+    if (!stream) SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+sg_status sg_chd_phase_y(sg_chd_t h, double* ycol, void* stream) {
+  return guard2([&] {
+    if (!h) sg::logic("CH slab: destroyed");
+    auto& d = *h->d;
+    SG_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    // nxq periodic systems of ny unknowns, interleaved; Woodbury in place
+    sg::penta_sweep(d.fy.t, d.nxq, d.p.ny, ycol, nullptr, true, false, s);
+    if (!stream) SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+sg_status sg_chd_combine(sg_chd_t h, const double* currExt, double* prevExt, const double* recv, void* stream) {
+  return guard2([&] {
+    if (!h) sg::logic("CH slab: destroyed");
+    auto& d = *h->d;
+    SG_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    sg::ch_combine_packed(d.p.nx, d.own, d.nxq, currExt, prevExt, recv, s);
+    if (!stream) SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+sg_status sg_chd_destroy(sg_chd_t* h) {
+  return guard2([&] {
+    if (!h || !*h) return;
+    delete *h;
+    *h = nullptr;
   });
 }
 

@@ -299,8 +299,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_sweep(const PentaTables f, in
 // (backward) dependent ops. Forward results go to z with coalesced stores
 // and come back through the same ring for the backward pass (a proxy fence
 // orders the generic stores before the async-proxy reads).
-constexpr int SW_RS = 8;    // rows per stage
-constexpr int SW_NSTG = 8;  // stages in flight
+constexpr int SW_RS = 16;   // rows per stage
+constexpr int SW_NSTG = 4;  // stages in flight
 
 struct alignas(64) SweepMaps {
   CUtensorMap z;     // 2D {B, n}, box {32, RS}
@@ -326,6 +326,9 @@ __device__ __forceinline__ void s_mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
   } while (!ok);
 }
+__device__ __forceinline__ void s_mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void s_tma_2d(void* dst, const CUtensorMap* m, int x, int y, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -345,129 +348,188 @@ template <bool UNIFORM>
 struct SweepSmem {
   // doubles per factor table per stage; tensor-TMA destinations must be
   // 128 B aligned, so the uniform (SW_RS-long) tables get a 16-double slot
-  static constexpr int FAC = UNIFORM ? 16 : SW_RS * 32;
+  static constexpr int FAC = UNIFORM ? (SW_RS + 15) / 16 * 16 : SW_RS * 32;
   static constexpr int STAGE = SW_RS * 32 + 3 * FAC;             // z + up to 3 tables
   static constexpr int STAGE_PAD = (STAGE * 8 + 127) / 128 * 16;  // doubles, 128 B aligned stride
-  static constexpr size_t bytes = static_cast<size_t>(SW_NSTG) * STAGE_PAD * 8 + SW_NSTG * 8;
+  static constexpr size_t bytes = static_cast<size_t>(SW_NSTG) * STAGE_PAD * 8 + 2 * SW_NSTG * 8;
 };
 
 template <bool UNIFORM, bool PERIODIC, int MODE>
-__global__ void __launch_bounds__(32) k_sweep_tma(const PentaTables f, const __grid_constant__ SweepMaps maps,
+__global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __grid_constant__ SweepMaps maps,
                                                   int B, int n, double* __restrict__ z, double* __restrict__ y4) {
+  // Warp 0: consumer (32 systems, the dependency chain). Warp 1 lane 0:
+  // producer (tensor-TMA issue), so the chain never stalls on issue code.
   using SM = SweepSmem<UNIFORM>;
   extern __shared__ __align__(128) double sw_smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sw_smem + SW_NSTG * SM::STAGE_PAD);
-  const int lane = threadIdx.x;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sw_smem + SW_NSTG * SM::STAGE_PAD);
+  uint64_t* empty = full + SW_NSTG;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const int b0 = blockIdx.x * 32;
   const int b = b0 + lane;
   const bool active = b < B;
   constexpr int FAC = SM::FAC;
-  constexpr uint32_t ZB = SW_RS * 32 * 8;
-  constexpr uint32_t FB = (UNIFORM ? SW_RS : SW_RS * 32) * 8;  // bytes per factor box
-  // stage g of pass `pass` (0 fwd: rows g*RS..; 1 bwd: rows n-(g+1)*RS..)
-  auto issue = [&](int gseq, int pass, int g) {
-    const int slot = gseq % SW_NSTG;
-    double* st = sw_smem + slot * SM::STAGE_PAD;
-    const int r0 = pass == 0 ? g * SW_RS : n - (g + 1) * SW_RS;
-    const int nt = pass == 0 ? 2 : 3;
-    s_mbar_expect_tx(&bars[slot], ZB + nt * FB);
-    s_tma_2d(st, &maps.z, b0, r0, &bars[slot]);
-    for (int k = 0; k < nt; ++k) {
-      const CUtensorMap* m = &maps.t[pass == 0 ? k : 2 + k];  // fwd: m1, m2; bwd: dInv, ap, bp
-      if (UNIFORM)
-        s_tma_1d(st + SW_RS * 32 + k * FAC, m, r0, &bars[slot]);
-      else
-        s_tma_2d(st + SW_RS * 32 + k * FAC, m, b0, r0, &bars[slot]);
-    }
-  };
-  auto fac = [&](const double* st, int k, int row) -> double {
-    return UNIFORM ? st[SW_RS * 32 + k * FAC + row] : st[SW_RS * 32 + k * FAC + row * 32 + lane];
-  };
-  const int nS = (n + SW_RS - 1) / SW_RS;  // stages per pass
+  constexpr int RS = SW_RS;
+  constexpr uint32_t ZB = RS * 32 * 8;
+  constexpr uint32_t FB = (UNIFORM ? RS : RS * 32) * 8;  // bytes per factor box
+  const int nS = (n + RS - 1) / RS;  // stages per pass
   const int total = 2 * nS;
-  auto issue_seq = [&](int gseq) {
-    if (gseq < nS) issue(gseq, 0, gseq);
-    else issue(gseq, 1, gseq - nS);
-  };
-  if (lane == 0) {
-    for (int k = 0; k < SW_NSTG; ++k) s_mbar_init(&bars[k], 1);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < SW_NSTG; ++k) {
+      s_mbar_init(&full[k], 1);
+      s_mbar_init(&empty[k], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    // prefetch forward stages only: backward stages read forward results
-    for (int g = 0; g < SW_NSTG && g < nS; ++g) issue_seq(g);
   }
-  __syncwarp();
+  __syncthreads();
+
+  if (warp == 1) {
+    // ------------------------------------------------------------ producer
+    for (int g = 0; g < total; ++g) {
+      const int slot = g % SW_NSTG;
+      if (g == nS) {
+        // backward stages read the forward results: wait until the consumer
+        // has stored them all and fenced them to the async proxy
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+      }
+      if (lane == 0) {
+        if (g >= SW_NSTG) s_mbar_wait(&empty[slot], ((g / SW_NSTG) + 1) & 1);
+        const int pass = g < nS ? 0 : 1;
+        const int gg = g < nS ? g : g - nS;
+        double* st = sw_smem + slot * SM::STAGE_PAD;
+        const int r0 = pass == 0 ? gg * RS : n - (gg + 1) * RS;
+        const int nt = pass == 0 ? 2 : 3;
+        s_mbar_expect_tx(&full[slot], ZB + nt * FB);
+        s_tma_2d(st, &maps.z, b0, r0, &full[slot]);
+        for (int k = 0; k < nt; ++k) {
+          const CUtensorMap* m = &maps.t[pass == 0 ? k : 2 + k];  // fwd: m1, m2; bwd: dInv, ap, bp
+          if (UNIFORM)
+            s_tma_1d(st + RS * 32 + k * FAC, m, r0, &full[slot]);
+          else
+            s_tma_2d(st + RS * 32 + k * FAC, m, b0, r0, &full[slot]);
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumer
+  auto fac = [&](const double* st, int k, int row) -> double {
+    return UNIFORM ? st[RS * 32 + k * FAC + row] : st[RS * 32 + k * FAC + row * 32 + lane];
+  };
   double* zc = z + b;
   const long long sB = B;
-  // ---- forward
+  // ---- forward (penta.cpp:171-181): stage 0 peeled (rows 0, 1 special)
   double y2 = 0.0, y1 = 0.0;
-  for (int g = 0; g < nS; ++g) {
-    const int slot = g % SW_NSTG;
-    s_mbar_wait(&bars[slot], (g / SW_NSTG) & 1);
-    const double* st = sw_smem + slot * SM::STAGE_PAD;
+  {
+    s_mbar_wait(&full[0], 0);
+    const double* st = sw_smem;
 #pragma unroll
-    for (int k = 0; k < SW_RS; ++k) {
-      const int r = g * SW_RS + k;
-      if (r < n) {
-        const double zr = st[k * 32 + lane];
-        double yr;
-        if (r >= 2) {
-          yr = zr - (fac(st, 0, k) * y2 + fac(st, 1, k) * y1);  // penta.cpp:180
-        } else if (r == 1) {
-          yr = zr - fac(st, 1, k) * y1;  // penta.cpp:173 (y1 holds y[0])
-        } else {
-          yr = zr;  // y[0] is not modified by the forward pass
-        }
-        if (active && r >= 1) zc[r * sB] = yr;
+    for (int k = 0; k < RS; ++k) {
+      const double zr = st[k * 32 + lane];
+      double yr;
+      if (k >= 2)
+        yr = zr - (fac(st, 0, k) * y2 + fac(st, 1, k) * y1);
+      else if (k == 1)
+        yr = zr - fac(st, 1, k) * y1;  // y1 holds y[0]
+      else
+        yr = zr;
+      if (active && k >= 1 && k < n) zc[k * sB] = yr;
+      y2 = y1;
+      y1 = yr;
+    }
+    __syncwarp();
+    if (lane == 0) s_mbar_arrive(&empty[0]);
+  }
+  // Full stages run branch-free with a walking store pointer (the loop is
+  // issue-bound: one warp per SM sub-partition, every instruction counts).
+  double* zp = zc + RS * sB;
+  const long long step = sB;
+  for (int g = 1; g < nS; ++g) {
+    const int slot = g % SW_NSTG;
+    s_mbar_wait(&full[slot], (g / SW_NSTG) & 1);
+    const double* st = sw_smem + slot * SM::STAGE_PAD;
+    const int r0 = g * RS;
+    if (r0 + RS <= n) {
+#pragma unroll
+      for (int k = 0; k < RS; ++k) {
+        const double yr = st[k * 32 + lane] - (fac(st, 0, k) * y2 + fac(st, 1, k) * y1);  // penta.cpp:180
+        if (active) *zp = yr;
+        zp += step;
+        y2 = y1;
+        y1 = yr;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < RS; ++k) {
+        const double yr = st[k * 32 + lane] - (fac(st, 0, k) * y2 + fac(st, 1, k) * y1);
+        if (active && r0 + k < n) *zp = yr;
+        zp += step;
         y2 = y1;
         y1 = yr;
       }
     }
     __syncwarp();
-    const int nxt = g + SW_NSTG;
-    if (nxt < nS && lane == 0) issue_seq(nxt);
+    if (lane == 0) s_mbar_arrive(&empty[slot]);
   }
-  // forward results must be visible to the async proxy before the backward
-  // pass streams them back
   asm volatile("fence.proxy.async.global;" ::: "memory");
-  __threadfence_block();
-  __syncwarp();
-  if (lane == 0)
-    for (int g = nS; g < nS + SW_NSTG && g < total; ++g) issue_seq(g);
-  __syncwarp();
-  // ---- backward (penta.cpp:183-196)
-  double s1 = 0.0, s2 = 0.0, zn1 = 0.0, zn2 = 0.0;
+  asm volatile("bar.sync 1, 64;" ::: "memory");
+  // ---- backward (penta.cpp:183-196): stage 0 (rows n-RS..n-1) peeled
+  double s1 = 0.0, s2 = 0.0, zn1 = 0.0, zn2 = 0.0, zz0 = 0.0, zz1 = 0.0;
   for (int g = nS; g < total; ++g) {
     const int slot = g % SW_NSTG;
-    s_mbar_wait(&bars[slot], (g / SW_NSTG) & 1);
+    s_mbar_wait(&full[slot], (g / SW_NSTG) & 1);
     const double* st = sw_smem + slot * SM::STAGE_PAD;
-    const int r0 = n - (g - nS + 1) * SW_RS;
+    const int r0 = n - (g - nS + 1) * RS;
+    if (g == nS) {
 #pragma unroll
-    for (int k = SW_RS - 1; k >= 0; --k) {
-      const int r = r0 + k;
-      if (r >= 0) {
+      for (int k = RS - 1; k >= 0; --k) {
+        const int r = r0 + k;
         const double yv = st[k * 32 + lane];
         double yr;
-        if (r == n - 1) {
+        if (k == RS - 1) {
           yr = yv * fac(st, 0, k);
           zn1 = yr;
-        } else if (r == n - 2) {
+        } else if (k == RS - 2) {
           yr = (yv - fac(st, 1, k) * s1) * fac(st, 0, k);
           zn2 = yr;
         } else {
           yr = (yv - fac(st, 1, k) * s1 - fac(st, 2, k) * s2) * fac(st, 0, k);
         }
-        if (active) zc[r * sB] = yr;
+        if (active && r >= 0) zc[r * sB] = yr;
+        if (r == 1) zz1 = yr;
+        if (r == 0) zz0 = yr;
+        s2 = s1;
+        s1 = yr;
+      }
+    } else if (r0 >= 2) {
+      // full stage above row 1: branch-free, walking pointer
+      double* zq = zc + static_cast<long long>(r0 + RS - 1) * sB;
+#pragma unroll
+      for (int k = RS - 1; k >= 0; --k) {
+        const double yr = (st[k * 32 + lane] - fac(st, 1, k) * s1 - fac(st, 2, k) * s2) * fac(st, 0, k);
+        if (active) *zq = yr;
+        zq -= sB;
+        s2 = s1;
+        s1 = yr;
+      }
+    } else {
+#pragma unroll
+      for (int k = RS - 1; k >= 0; --k) {
+        const int r = r0 + k;
+        const double yr = (st[k * 32 + lane] - fac(st, 1, k) * s1 - fac(st, 2, k) * s2) * fac(st, 0, k);
+        if (active && r >= 0) zc[r * sB] = yr;
+        zz1 = r == 1 ? yr : zz1;
+        zz0 = r == 0 ? yr : zz0;
         s2 = s1;
         s1 = yr;
       }
     }
     __syncwarp();
-    const int nxt = g + SW_NSTG;
-    if (nxt < total && lane == 0) issue_seq(nxt);
+    if (lane == 0) s_mbar_arrive(&empty[slot]);
   }
   if constexpr (PERIODIC) {
-    const double zz0 = s1, zz1 = s2;  // y[0], y[1]
     const int sys = UNIFORM ? 0 : b;
     if (!active) return;
     const double* cw = f.cw + sys * 6;
@@ -544,7 +606,7 @@ void launch_sweep_tma(const PentaTables& f, const SweepMaps& maps, int B, int n,
     configured = true;
   }
   const int blocks = (B + 31) / 32;
-  kern<<<blocks, 32, SweepSmem<U>::bytes, s>>>(f, maps, B, n, z, y4);
+  kern<<<blocks, 64, SweepSmem<U>::bytes, s>>>(f, maps, B, n, z, y4);
 }
 
 template <bool U, bool P, int M>

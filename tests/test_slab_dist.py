@@ -77,3 +77,41 @@ def test_partition_matches_make_tiles_and_rows():
     assert s.output_rows() == (0, 1)
     with pytest.raises(ValueError):
         Slab(16, 4, 4, 0, 2, 2, True)
+
+
+def _a2a_worker(rank, world, port, q):
+    """The packed all-to-all layout of the distributed CH step
+    (ch_dist.py): row slabs -> column slabs -> row slabs."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nx, ny = 12, 8 * world
+        own, nxq = ny // world, nx // world
+        g = np.arange(nx * ny, dtype=np.float64).reshape(ny, nx)
+        mine = g[rank * own:(rank + 1) * own]
+        # packed: block q = columns [q*nxq, (q+1)*nxq) of my rows
+        send = torch.from_numpy(np.concatenate([mine[:, qq * nxq:(qq + 1) * nxq].ravel() for qq in range(world)]))
+        ycol = torch.empty(ny * nxq, dtype=torch.float64)
+        dist.all_to_all_single(ycol, send)
+        ok = np.array_equal(ycol.numpy().reshape(ny, nxq), g[:, rank * nxq:(rank + 1) * nxq])
+        back = torch.empty(own * nx, dtype=torch.float64)
+        dist.all_to_all_single(back, ycol)
+        ok = ok and np.array_equal(back.numpy(), send.numpy())
+        q.put((rank, "ok" if ok else "bad"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_ch_alltoall_layout(world):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_a2a_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[1] == "ok" for r in res), res
