@@ -6,6 +6,7 @@
 // identical to the reference CHStepper.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <functional>
@@ -132,6 +133,29 @@ inline Grid2D biharmonic(const Grid2D& c) {
   return out;
 }
 
+/// cahn_hilliard.cpp:161-177 — composite Simpson mean, on the device
+/// (bitwise identical to the reference).
+inline double simpson_mean(const Grid2D& g) {
+  double out = 0.0;
+  detail::check(sg_simpson_mean(g.data(), g.nx, g.ny, 0, SG_MEM_HOST, &out));
+  return out;
+}
+
+/// cahn_hilliard.cpp:179-188 — s = 1/(1 - <C^2>); std::domain_error at saturation.
+inline double s_metric(const Grid2D& c) {
+  double out = 0.0;
+  detail::check(sg_s_metric(c.data(), c.nx, c.ny, SG_MEM_HOST, &out));
+  return out;
+}
+
+/// cahn_hilliard.cpp:190-211 — spectral mean wavenumber (cuFFT on the
+/// device); std::domain_error on an all-zero field.
+inline double k1_metric(const Grid2D& c) {
+  double out = 0.0;
+  detail::check(sg_k1_metric(c.data(), c.nx, c.ny, c.dx, c.dy, SG_MEM_HOST, &out));
+  return out;
+}
+
 /// cahn_hilliard.hpp:104-137 — BDF2-ADI stepper, state in HBM.
 class CHStepper {
  public:
@@ -185,6 +209,13 @@ class CHStepper {
     refresh();
     return cPrev_;
   }
+  /// cahn_hilliard.cpp:330-340 — computed on the device-resident C^n.
+  Diagnostics diagnostics() const {
+    Diagnostics d;
+    detail::check(sg_ch_diagnostics(h_, &d.t, &d.s, &d.k1Inv));
+    return d;
+  }
+
   /// Device pointer of C^n (which = 0) or C^{n-1} (which = 1).
   const double* device_field(int which = 0) const {
     const double* p = nullptr;
@@ -213,5 +244,28 @@ struct RunSink {
   std::function<void(const Diagnostics&)> onDiagnostics;
   std::function<void(const Grid2D&, int step, double t)> onSnapshot;
 };
+
+/// cahn_hilliard.cpp:342-356 — steps between sink emissions run back to
+/// back on the device (no host round trips).
+inline void run(const CHParams& params, int numTiles, int numWorkers, const RunSink& sink) {
+  CHStepper stepper(params, numTiles, numWorkers);
+  const bool diag = sink.diagEvery > 0 && sink.onDiagnostics;
+  const bool snap = sink.snapEvery > 0 && sink.onSnapshot;
+  const auto emit = [&](long step) {
+    if (diag && step % sink.diagEvery == 0) sink.onDiagnostics(stepper.diagnostics());
+    if (snap && step % sink.snapEvery == 0) sink.onSnapshot(stepper.field(), static_cast<int>(step), stepper.time());
+  };
+  emit(0);
+  const auto steps = static_cast<long>(std::ceil(params.T / params.dt - 1e-9));
+  long s = 0;
+  while (s < steps) {
+    long next = steps;
+    if (diag) next = std::min(next, (s / sink.diagEvery + 1) * sink.diagEvery);
+    if (snap) next = std::min(next, (s / sink.snapEvery + 1) * sink.snapEvery);
+    stepper.steps(static_cast<int>(next - s));
+    s = next;
+    emit(s);
+  }
+}
 
 }  // namespace stengrid

@@ -175,6 +175,19 @@ sg_status sg_ch_get_field(sg_ch_t ch, int which, double* out, sg_memory memory);
 sg_status sg_ch_device_field(sg_ch_t ch, int which, const double** dptr);
 sg_status sg_ch_status(sg_ch_t ch, int* step, double* time);
 sg_status sg_ch_destroy(sg_ch_t* ch);
+/* CHStepper::diagnostics (cahn_hilliard.cpp:330-340) on the device-resident
+ * C^n: t, s = s_metric, k1Inv = 1/k1_metric (0 for an all-zero field).
+ * SG_ERR_DOMAIN when the mixture is saturated (s_metric throws). */
+sg_status sg_ch_diagnostics(sg_ch_t ch, double* t, double* s, double* k1Inv);
+
+/* ------------------------------------------------------ field diagnostics
+ * simpson_mean (cahn_hilliard.cpp:161-177; square != 0: mean of v^2) and
+ * s_metric (:179-188) — bitwise identical to the reference — and k1_metric
+ * (:190-211; cuFFT + deterministic reduction, ~1e-13 relative). Fields are
+ * row-major nx*ny in host or device memory. */
+sg_status sg_simpson_mean(const double* field, int nx, int ny, int square, sg_memory memory, double* out);
+sg_status sg_s_metric(const double* field, int nx, int ny, sg_memory memory, double* out);
+sg_status sg_k1_metric(const double* field, int nx, int ny, double dx, double dy, sg_memory memory, double* out);
 
 /* ------------------------------------- distributed Cahn-Hilliard (y-slabs)
  * One process per GPU; rank r owns rows [r*ny/world, (r+1)*ny/world) of both

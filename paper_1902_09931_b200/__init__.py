@@ -15,14 +15,14 @@ from .stencil import (BoundaryMode, Direction, Extents, FunctionStencil, Grid2D,
 from .penta import (Axis, PentaBatch, PentaFactor, PeriodicPentaFactor, RhsBatch,
                     build_hyperdiffusion_operator, deinterleave, interleave, solve_batch,
                     solve_periodic_batch)
-from .cahn_hilliard import (CHParams, CHStepper, Diagnostics, biharmonic_weights,
-                            nonlinear_laplacian_coefficients)
+from .cahn_hilliard import (CHParams, CHStepper, Diagnostics, RunSink, biharmonic_weights, k1_metric,
+                            nonlinear_laplacian_coefficients, run, s_metric, simpson_mean)
 
 __all__ = [
     "Axis", "PentaBatch", "PentaFactor", "PeriodicPentaFactor", "RhsBatch",
     "build_hyperdiffusion_operator", "deinterleave", "interleave", "solve_batch",
     "solve_periodic_batch", "CHParams", "CHStepper", "Diagnostics", "biharmonic_weights",
-    "nonlinear_laplacian_coefficients",
+    "nonlinear_laplacian_coefficients", "RunSink", "run", "simpson_mean", "s_metric", "k1_metric",
     "BoundaryMode", "Direction", "Extents", "FunctionStencil", "Grid2D", "Residency",
     "StencilPlan", "WeightStencil", "compute", "create_plan", "destroy_plan", "launch_slab",
     "make_tiles", "mark_host_dirty", "swap_plan", "sync_to_host", "wrap", "InvalidArgument",

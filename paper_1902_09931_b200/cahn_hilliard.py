@@ -93,6 +93,38 @@ def biharmonic_weights(dx: float, dy: float):
     return w
 
 
+def _field_ptr(g):
+    """(pointer, memory kind, nx, ny, dx, dy) of a Grid2D or 2D CUDA tensor."""
+    if isinstance(g, Grid2D):
+        v = np.ascontiguousarray(g.values, dtype=np.float64)
+        return v, C.c_void_p(v.ctypes.data), 0, g.nx, g.ny, g.dx, g.dy
+    return g, C.c_void_p(g.data_ptr()), 1, int(g.shape[1]), int(g.shape[0]), 1.0, 1.0
+
+
+def simpson_mean(g) -> float:
+    """cahn_hilliard.cpp:161-177 on the device (bitwise identical)."""
+    keep, ptr, mem, nx, ny, _, _ = _field_ptr(g)
+    out = C.c_double()
+    check(_lib.lib().sg_simpson_mean(ptr, nx, ny, 0, mem, C.byref(out)))
+    return out.value
+
+
+def s_metric(g) -> float:
+    """cahn_hilliard.cpp:179-188 on the device; DomainError when saturated."""
+    keep, ptr, mem, nx, ny, _, _ = _field_ptr(g)
+    out = C.c_double()
+    check(_lib.lib().sg_s_metric(ptr, nx, ny, mem, C.byref(out)))
+    return out.value
+
+
+def k1_metric(g, dx=None, dy=None) -> float:
+    """cahn_hilliard.cpp:190-211 on the device (cuFFT); DomainError on zero."""
+    keep, ptr, mem, nx, ny, gdx, gdy = _field_ptr(g)
+    out = C.c_double()
+    check(_lib.lib().sg_k1_metric(ptr, nx, ny, dx or gdx, dy or gdy, mem, C.byref(out)))
+    return out.value
+
+
 class CHStepper:
     """cahn_hilliard.hpp:104-137 — state lives in HBM."""
 
@@ -142,6 +174,12 @@ class CHStepper:
         check(_lib.lib().sg_ch_device_field(self._h, which, C.byref(ptr)))
         return ptr.value
 
+    def diagnostics(self) -> Diagnostics:
+        """cahn_hilliard.cpp:330-340, computed on the device-resident C^n."""
+        t, s_, k = C.c_double(), C.c_double(), C.c_double()
+        check(_lib.lib().sg_ch_diagnostics(self._h, C.byref(t), C.byref(s_), C.byref(k)))
+        return Diagnostics(t.value, s_.value, k.value)
+
     def step_index(self) -> int:
         s = C.c_int()
         check(_lib.lib().sg_ch_status(self._h, C.byref(s), None))
@@ -158,3 +196,39 @@ class CHStepper:
                 _lib.lib().sg_ch_destroy(C.byref(self._h))
         except Exception:
             pass
+
+
+@dataclass
+class RunSink:
+    """cahn_hilliard.hpp:141-146."""
+    diagEvery: int = 1
+    snapEvery: int = 0
+    onDiagnostics: object = None
+    onSnapshot: object = None
+
+
+def run(params: CHParams, num_tiles: int, num_workers: int, sink: RunSink) -> None:
+    """cahn_hilliard.cpp:342-356: step to T (ceil(T/dt - 1e-9) steps),
+    emitting diagnostics / snapshots at the sink cadences; steps between
+    emissions are enqueued back to back on the device."""
+    import math as _m
+    st = CHStepper(params, num_tiles, num_workers)
+
+    def emit(step):
+        if sink.diagEvery > 0 and sink.onDiagnostics and step % sink.diagEvery == 0:
+            sink.onDiagnostics(st.diagnostics())
+        if sink.snapEvery > 0 and sink.onSnapshot and step % sink.snapEvery == 0:
+            sink.onSnapshot(st.field(), step, st.time())
+
+    emit(0)
+    steps = int(_m.ceil(params.T / params.dt - 1e-9))
+    cadences = [c for c, f in ((sink.diagEvery, sink.onDiagnostics), (sink.snapEvery, sink.onSnapshot))
+                if c > 0 and f]
+    s = 0
+    while s < steps:
+        nxt = steps
+        for c in cadences:
+            nxt = min(nxt, (s // c + 1) * c)
+        st.step_many(nxt - s)
+        s = nxt
+        emit(s)

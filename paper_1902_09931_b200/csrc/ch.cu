@@ -641,6 +641,30 @@ sg_status sg_ch_status(sg_ch_t ch, int* step, double* time) {
   });
 }
 
+sg_status sg_ch_diagnostics(sg_ch_t ch, double* t, double* s, double* k1Inv) {
+  return guard2([&] {
+    if (!ch) sg::logic("CHStepper: destroyed");
+    auto& st = *ch->st;
+    SG_CUDA(cudaSetDevice(st.device));
+    SG_CUDA(cudaStreamSynchronize(st.stream));
+    const double* f = st.field[st.curr];
+    const double dx = st.p.lx / st.p.nx, dy = st.p.ly / st.p.ny;
+    if (t) *t = static_cast<double>(st.step) * st.p.dt;
+    double m2 = 0.0;
+    sg::device_simpson(f, st.p.nx, st.p.ny, true, &m2, st.stream);
+    if (m2 >= 1.0 - 1e-12) throw sg::Error(SG_ERR_DOMAIN, "s_metric: mixture saturated, <C^2> reached 1");
+    if (s) *s = 1.0 / (1.0 - m2);
+    double k1inv = 0.0;
+    try {
+      k1inv = 1.0 / sg::device_k1(f, st.p.nx, st.p.ny, dx, dy, st.stream);
+    } catch (const sg::Error& e) {
+      if (e.status != SG_ERR_DOMAIN) throw;
+      k1inv = 0.0;  // an identically zero field has no spectral length scale
+    }
+    if (k1Inv) *k1Inv = k1inv;
+  });
+}
+
 sg_status sg_ch_destroy(sg_ch_t* ch) {
   return guard2([&] {
     if (!ch || !*ch) return;
@@ -715,7 +739,10 @@ sg_status sg_penta_solve(sg_penta_t f, double* rhs, sg_memory memory, void* stre
       SG_CUDA(cudaMemcpyAsync(tmp, rhs, bytes, cudaMemcpyHostToDevice, s));
       z = tmp;
     }
-    sg::penta_sweep(f->f->t, B, n, z, nullptr, f->f->periodic, false, s);
+    double* y4 = nullptr;
+    if (f->f->periodic) SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&y4), 4 * sizeof(double) * B, s));
+    sg::penta_sweep(f->f->t, B, n, z, y4, f->f->periodic, false, s);
+    if (y4) SG_CUDA(cudaFreeAsync(y4, s));
     if (memory == SG_MEM_HOST) {
       SG_CUDA(cudaMemcpyAsync(rhs, tmp, bytes, cudaMemcpyDeviceToHost, s));
       SG_CUDA(cudaFreeAsync(tmp, s));
@@ -801,7 +828,7 @@ sg_status sg_chd_phase_y(sg_chd_t h, double* ycol, void* stream) {
     SG_CUDA(cudaSetDevice(d.device));
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
     // nxq periodic systems of ny unknowns, interleaved; Woodbury in place
-    sg::penta_sweep(d.fy.t, d.nxq, d.p.ny, ycol, nullptr, true, false, s);
+    sg::penta_sweep(d.fy.t, d.nxq, d.p.ny, ycol, d.ybuf, true, false, s);
     if (!stream) SG_CUDA(cudaStreamSynchronize(s));
   });
 }

@@ -1,0 +1,240 @@
+// diagnostics.cu — Cahn-Hilliard diagnostics on the device.
+//
+// Replaces simpson_mean / s_metric / k1_metric (cahn_hilliard.cpp:161-211)
+// and CHStepper::diagnostics (:330-340), so a run() with a diagnostics sink
+// no longer downloads the field.
+//
+//  * simpson_mean / s_metric: bitwise identical to the reference. One thread
+//    per row accumulates rowAcc = sum_i wx_i * v_ij in the reference's order
+//    (rows staged through shared-memory tiles so loads stay coalesced), then
+//    one thread folds total += wy_j * rowAcc_j in row order.
+//  * k1_metric: 2D FFT by cuFFT (Z2Z, forward, unnormalized like fft_2d,
+//    fft.cpp:54-61) and a deterministic two-level reduction of
+//    num = sum |C_k|^2, den = sum |C_k|^2 / |k| over k != 0. The reference's
+//    radix-2 FFT and serial sums round differently: agreement is to ~1e-13
+//    relative (tests use 1e-10), which is well inside the reference's own
+//    KAT tolerances (test_cahn_hilliard.cpp:346-366: 1e-12 absolute on O(1)).
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cmath>
+#include <string>
+
+#include "sg_internal.hpp"
+
+namespace sg {
+namespace {
+
+constexpr int DT = 32;
+
+// rowAcc[j] = sum_i (i odd ? 4 : 2) * f(v_ij), f = identity or square,
+// accumulated left to right (cahn_hilliard.cpp:166-172, 179-185).
+template <bool SQUARE>
+__global__ void __launch_bounds__(DT) k_simpson_rows(const double* __restrict__ v, int nx, int ny,
+                                                      double* __restrict__ rowAcc) {
+  __shared__ double tile[DT][DT + 1];
+  const int j0 = blockIdx.x * DT;
+  const int lane = threadIdx.x;
+  double acc = 0.0;
+  for (int i0 = 0; i0 < nx; i0 += DT) {
+    for (int r = 0; r < DT; ++r) {
+      const int j = j0 + r, i = i0 + lane;
+      tile[r][lane] = (j < ny && i < nx) ? v[static_cast<long long>(j) * nx + i] : 0.0;
+    }
+    __syncwarp();
+    const int lim = min(DT, nx - i0);
+    for (int c = 0; c < lim; ++c) {
+      const int i = i0 + c;
+      const double wx = (i % 2 == 1) ? 4.0 : 2.0;
+      const double x = tile[lane][c];
+      acc += wx * (SQUARE ? x * x : x);
+    }
+    __syncwarp();
+  }
+  if (j0 + lane < ny) rowAcc[j0 + lane] = acc;
+}
+
+__global__ void k_simpson_total(const double* __restrict__ rowAcc, int nx, int ny, double* out) {
+  double total = 0.0;  // cahn_hilliard.cpp:165-176
+  for (int j = 0; j < ny; ++j) {
+    const double wy = (j % 2 == 1) ? 4.0 : 2.0;
+    total += wy * rowAcc[j];
+  }
+  *out = total / (9.0 * static_cast<double>(nx) * static_cast<double>(ny));
+}
+
+__global__ void k_to_complex(const double* __restrict__ v, long long n, cufftDoubleComplex* __restrict__ c) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) c[k] = make_cuDoubleComplex(v[k], 0.0);
+}
+
+constexpr int RB = 256;
+
+// Per-block partial sums of |C|^2 and |C|^2/|k| (k1_metric, cahn_hilliard.cpp:196-208).
+__global__ void __launch_bounds__(RB) k_k1_partial(const cufftDoubleComplex* __restrict__ s, int nx, int ny,
+                                                   double kxScale, double kyScale, double* __restrict__ part) {
+  __shared__ double sn[RB], sd[RB];
+  const long long n = static_cast<long long>(nx) * ny;
+  double num = 0.0, den = 0.0;
+  for (long long k = static_cast<long long>(blockIdx.x) * RB + threadIdx.x; k < n;
+       k += static_cast<long long>(gridDim.x) * RB) {
+    const int j = static_cast<int>(k / nx), i = static_cast<int>(k % nx);
+    if (i == 0 && j == 0) continue;
+    const int mj = (j < ny / 2) ? j : j - ny;
+    const int mi = (i < nx / 2) ? i : i - nx;
+    const cufftDoubleComplex z = s[k];
+    const double power = z.x * z.x + z.y * z.y;  // std::norm
+    const double kmag = hypot(kxScale * mi, kyScale * mj);
+    num += power;
+    den += power / kmag;
+  }
+  sn[threadIdx.x] = num;
+  sd[threadIdx.x] = den;
+  __syncthreads();
+  for (int w = RB / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      sn[threadIdx.x] += sn[threadIdx.x + w];
+      sd[threadIdx.x] += sd[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = sn[0];
+    part[2 * blockIdx.x + 1] = sd[0];
+  }
+}
+
+__global__ void k_k1_final(const double* __restrict__ part, int nb, double* out) {
+  double num = 0.0, den = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    num += part[2 * b];
+    den += part[2 * b + 1];
+  }
+  out[0] = num;
+  out[1] = den;
+}
+
+}  // namespace
+
+// Mean by composite Simpson (square: of v^2), on the device; result in *out (host).
+void device_simpson(const double* v, int nx, int ny, bool square, double* out, cudaStream_t s) {
+  if (nx % 2 != 0 || ny % 2 != 0) invalid("simpson_mean: nx and ny must be even");
+  double* buf = nullptr;
+  SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(double) * (ny + 1), s));
+  if (square)
+    k_simpson_rows<true><<<(ny + DT - 1) / DT, DT, 0, s>>>(v, nx, ny, buf);
+  else
+    k_simpson_rows<false><<<(ny + DT - 1) / DT, DT, 0, s>>>(v, nx, ny, buf);
+  check_launch("simpson rows kernel");
+  k_simpson_total<<<1, 1, 0, s>>>(buf, nx, ny, buf + ny);
+  check_launch("simpson total kernel");
+  SG_CUDA(cudaMemcpyAsync(out, buf + ny, sizeof(double), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaFreeAsync(buf, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+}
+
+// k1 = num/den over the FFT spectrum; throws domain_error-class on den == 0.
+double device_k1(const double* v, int nx, int ny, double dx, double dy, cudaStream_t s) {
+  if (nx < 1 || ny < 1 || (nx & (nx - 1)) || (ny & (ny - 1)))
+    invalid("fft_2d: grid dimensions must be powers of two");
+  const long long n = static_cast<long long>(nx) * ny;
+  cufftDoubleComplex* c = nullptr;
+  SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(cufftDoubleComplex) * n, s));
+  k_to_complex<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(v, n, c);
+  check_launch("k1 complex kernel");
+  cufftHandle plan;
+  if (cufftPlan2d(&plan, ny, nx, CUFFT_Z2Z) != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftPlan2d failed");
+  cufftSetStream(plan, s);
+  const cufftResult fr = cufftExecZ2Z(plan, c, c, CUFFT_FORWARD);
+  count_launch();
+  cufftDestroy(plan);
+  if (fr != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftExecZ2Z failed");
+  const int nb = 296;
+  double* part = nullptr;
+  SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * (2 * nb + 2), s));
+  const double kxScale = 2.0 * 3.14159265358979323846 / (dx * nx);
+  const double kyScale = 2.0 * 3.14159265358979323846 / (dy * ny);
+  k_k1_partial<<<nb, RB, 0, s>>>(c, nx, ny, kxScale, kyScale, part);
+  check_launch("k1 partial kernel");
+  k_k1_final<<<1, 1, 0, s>>>(part, nb, part + 2 * nb);
+  check_launch("k1 final kernel");
+  double nd[2];
+  SG_CUDA(cudaMemcpyAsync(nd, part + 2 * nb, sizeof nd, cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaFreeAsync(part, s));
+  SG_CUDA(cudaFreeAsync(c, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  if (nd[1] == 0.0) throw Error(SG_ERR_DOMAIN, "k1_metric: zero field has no spectral mean");
+  return nd[0] / nd[1];
+}
+
+}  // namespace sg
+
+// ------------------------------------------------------------------ C ABI
+extern "C" sg_status sg_internal_set_error(const char* msg, int system);
+
+namespace {
+template <typename F>
+sg_status dguard(F&& f) {
+  try {
+    f();
+    return SG_OK;
+  } catch (const sg::Error& e) {
+    sg_internal_set_error(e.what(), e.system);
+    return e.status;
+  } catch (const std::exception& e) {
+    sg_internal_set_error(e.what(), -1);
+    return SG_ERR_CUDA;
+  }
+}
+
+// Device view of a host or device field (uploads host data to a temporary).
+struct DevField {
+  const double* p = nullptr;
+  double* tmp = nullptr;
+  cudaStream_t s = nullptr;
+  DevField(const double* f, long long n, sg_memory m, cudaStream_t st) : s(st) {
+    if (m == SG_MEM_DEVICE) {
+      p = f;
+      return;
+    }
+    SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double) * n, s));
+    SG_CUDA(cudaMemcpyAsync(tmp, f, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    p = tmp;
+  }
+  ~DevField() {
+    if (tmp) cudaFreeAsync(tmp, s);
+  }
+};
+}  // namespace
+
+extern "C" {
+
+sg_status sg_simpson_mean(const double* field, int nx, int ny, int square, sg_memory memory, double* out) {
+  return dguard([&] {
+    if (nx < 1 || ny < 1) sg::invalid("simpson_mean: empty grid");
+    if (nx % 2 != 0 || ny % 2 != 0) sg::invalid("simpson_mean: nx and ny must be even");
+    DevField f(field, 1LL * nx * ny, memory, nullptr);
+    sg::device_simpson(f.p, nx, ny, square != 0, out, nullptr);
+  });
+}
+
+sg_status sg_s_metric(const double* field, int nx, int ny, sg_memory memory, double* out) {
+  return dguard([&] {
+    if (nx % 2 != 0 || ny % 2 != 0) sg::invalid("simpson_mean: nx and ny must be even");
+    DevField f(field, 1LL * nx * ny, memory, nullptr);
+    double m2 = 0.0;
+    sg::device_simpson(f.p, nx, ny, true, &m2, nullptr);
+    if (m2 >= 1.0 - 1e-12)  // cahn_hilliard.cpp:186
+      throw sg::Error(SG_ERR_DOMAIN, "s_metric: mixture saturated, <C^2> reached 1");
+    *out = 1.0 / (1.0 - m2);
+  });
+}
+
+sg_status sg_k1_metric(const double* field, int nx, int ny, double dx, double dy, sg_memory memory, double* out) {
+  return dguard([&] {
+    DevField f(field, 1LL * nx * ny, memory, nullptr);
+    *out = sg::device_k1(f.p, nx, ny, dx, dy, nullptr);
+  });
+}
+
+}  // extern "C"

@@ -617,8 +617,32 @@ void launch_sweep_t(const PentaTables& f, int B, int n, double* z, double* y4, c
 
 }  // namespace
 
+namespace {
+// z[r*B + b] -= W0[r] y0[b] + W1[r] y1[b] + W2[r] y2[b] + W3[r] y3[b]
+// (penta.cpp:279-286) as one fully parallel pass: the recurrence kernels
+// hand y = K^{-1} V^T z over in y4[k*B + b].
+__global__ void __launch_bounds__(256) k_penta_correct(const PentaTables f, int B, int n, double* __restrict__ z,
+                                                       const double* __restrict__ y4) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (b >= B) return;
+  const bool u = f.uniform;
+  const long long idx = static_cast<long long>(r) * B + b;
+  const double w0 = tab(f.W[0], r, b, B, u), w1 = tab(f.W[1], r, b, B, u), w2 = tab(f.W[2], r, b, B, u),
+               w3 = tab(f.W[3], r, b, B, u);
+  z[idx] -= w0 * __ldg(y4 + b) + w1 * __ldg(y4 + B + b) + w2 * __ldg(y4 + 2LL * B + b) + w3 * __ldg(y4 + 3LL * B + b);
+}
+}  // namespace
+
 void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool periodic,
                  bool fusedCorrection, cudaStream_t s) {
+  if (periodic && !fusedCorrection && y4 != nullptr) {
+    // recurrence with y handed over, then the correction as a parallel pass
+    penta_sweep(f, B, n, z, y4, true, true, s);
+    k_penta_correct<<<dim3((B + 255) / 256, n), 256, 0, s>>>(f, B, n, z, y4);
+    check_launch("penta correction kernel");
+    return;
+  }
   SweepMaps maps;
   if (sweep_maps(f, B, n, z, &maps)) {
     if (f.uniform) {

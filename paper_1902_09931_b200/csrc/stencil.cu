@@ -367,13 +367,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// CTA geometry: TMA_WARPS consumer warps side by side cover CW columns (8 KB
-// of a row: CTA-boundary halos are then ~0.4% of the traffic); one producer
-// warp streams rows (CW + halos) into a STAGES x RPS ring. The grid is
-// persistent: each CTA takes a balanced contiguous slice of the flattened
-// (column block, row) space, i.e. at most two column-block segments, so the
-// vertical halo rows are read once per slice and no wave tail remains.
-constexpr int TMA_WARPS = 16;
+// CTA geometry: TMA_WARPS consumer warps side by side cover CW columns; one
+// producer warp streams rows (CW + halos) into a STAGES x RPS ring.
+constexpr int TMA_WARPS = 4;
 
 template <typename T, int L, int R, int TP, int BT>
 struct TmaGeom {
@@ -382,31 +378,14 @@ struct TmaGeom {
   static constexpr int CW = TMA_WARPS * SW;
   static constexpr int LP = ((L + V - 1) / V) * V;  // left pad, 16 B granules
   static constexpr int RP = ((R + V - 1) / V) * V;
-  static constexpr int ROW = LP + CW + RP;  // elements per staged row
+  static constexpr int ROW = LP + CW + RP;  // elements per staged row (~2 KB)
   static constexpr int H = TP + BT + 1;
   // Rows per stage: a multiple of H so the register window is a ring whose
   // slot for every unrolled row is a compile-time constant (no moves).
   static constexpr int RPS = H >= 2 ? H : 2;
+  static constexpr int STAGES = (9 + RPS - 1) / RPS >= 2 ? (9 + RPS - 1) / RPS : 2;
   static constexpr size_t stage_bytes = static_cast<size_t>(RPS) * ROW * sizeof(T);
-  // as many stages as fit ~100 KB (two CTAs per SM), at least 2
-  static constexpr int STAGES_FIT = static_cast<int>((100u << 10) / stage_bytes);
-  static constexpr int STAGES = STAGES_FIT < 2 ? 2 : (STAGES_FIT > 8 ? 8 : STAGES_FIT);
   static constexpr size_t smem_bytes = STAGES * stage_bytes + 2 * STAGES * sizeof(uint64_t);
-};
-
-// Segment k of a CTA's slice: column block xb, rows [r0, r0 + len) relative
-// to a.row0.
-struct SliceIter {
-  long long pos, end;
-  int rows;
-  __device__ bool next(int& xb, int& r0, int& len) {
-    if (pos >= end) return false;
-    xb = static_cast<int>(pos / rows);
-    r0 = static_cast<int>(pos % rows);
-    len = static_cast<int>(min(static_cast<long long>(rows - r0), end - pos));
-    pos += len;
-    return true;
-  }
 };
 
 template <typename T, int L, int R, int TP, int BT, typename Op>
@@ -425,16 +404,12 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32) k_tma(const __grid_const
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nx = a.nx;
-  // blockIdx.x = column block, blockIdx.y = row segment: CTAs of one
-  // segment start together and advance in lockstep across column blocks, so
-  // a CTA's halo columns are read while the neighbour's copy of the same
-  // lines is still in L2.
-  const int rows = a.row1 - a.row0;
-  const long long segLen = (rows + gridDim.y - 1) / gridDim.y;
-  const long long start = static_cast<long long>(blockIdx.x) * rows + blockIdx.y * segLen;
-  const long long segEnd = (blockIdx.y + 1) * segLen;
-  const long long end = static_cast<long long>(blockIdx.x) * rows + (segEnd < rows ? segEnd : rows);
-  if (start >= end) return;  // CTA-uniform
+  const int cx0 = blockIdx.x * CW;
+  const int ra = a.row0 + blockIdx.y * a.segRows;
+  const int rb = min(ra + a.segRows, a.row1);
+  if (ra >= rb) return;  // CTA-uniform
+  const int nIn = (rb - ra) + H - 1;
+  const int nStages = (nIn + RPS - 1) / RPS;
 
   if (threadIdx.x == 0) {
     for (int k = 0; k < STAGES; ++k) {
@@ -451,145 +426,128 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32) k_tma(const __grid_const
     // columns (128 B aligned, whole lines: no over-fetch) and 16 B cp.async
     // granules for the halo columns (wrapped in index math at grid edges).
     if (lane != 0) return;
+    const int validC = min(CW, nx - cx0);
+    const uint32_t mainBytes = static_cast<uint32_t>(validC * sizeof(T));
+    int hsrc[(LP + RP) / V > 0 ? (LP + RP) / V : 1];
+    int hdst[(LP + RP) / V > 0 ? (LP + RP) / V : 1];
+    int nh = 0;
+#pragma unroll
+    for (int k = 0; k < LP / V; ++k) {
+      const int c = cx0 - LP + k * V;
+      if (c >= 0 || a.wrapX) {
+        hsrc[nh] = c >= 0 ? c : c + nx;
+        hdst[nh++] = k * V;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < RP / V; ++k) {
+      const int c = cx0 + validC + k * V;
+      if (c < nx || a.wrapX) {
+        hsrc[nh] = c < nx ? c : c - nx;
+        hdst[nh++] = LP + validC + k * V;
+      }
+    }
+    int rf = ra + a.inShift - TP;
+    if (a.wrapY) rf = wrap_idx(rf, a.inRows);
     const T* __restrict__ in = a.in;
-    SliceIter it{start, end, rows};
-    int xb, r0, len;
-    int G0 = 0;  // global stage counter (ring slot / phase)
-    while (it.next(xb, r0, len)) {
-      const int cx0 = xb * CW;
-      const int validC = min(CW, nx - cx0);
-      const uint32_t mainBytes = static_cast<uint32_t>(validC * sizeof(T));
-      int hsrc[(LP + RP) / V > 0 ? (LP + RP) / V : 1];
-      int hdst[(LP + RP) / V > 0 ? (LP + RP) / V : 1];
-      int nh = 0;
+    for (int g = 0; g < nStages; ++g) {
+      const int slot = g % STAGES;
+      if (g >= STAGES) mbar_wait(&empty[slot], ((g / STAGES) + 1) & 1);
+      mbar_expect_tx(&full[slot], mainBytes * RPS);
+      T* sstage = ring + slot * (RPS * ROW);
 #pragma unroll
-      for (int k = 0; k < LP / V; ++k) {
-        const int c = cx0 - LP + k * V;
-        if (c >= 0 || a.wrapX) {
-          hsrc[nh] = c >= 0 ? c : c + nx;
-          hdst[nh++] = k * V;
+      for (int k = 0; k < RPS; ++k) {
+        const T* grow = in + static_cast<long long>(rf) * nx;
+        T* srow = sstage + k * ROW;
+        bulk_g2s(srow + LP, grow + cx0, mainBytes, &full[slot]);
+        for (int h = 0; h < nh; ++h) cp_async16(srow + hdst[h], grow + hsrc[h]);
+        ++rf;
+        if (a.wrapY) {
+          if (rf == a.inRows) rf = 0;
+        } else if (rf >= a.inRows) {
+          rf = a.inRows - 1;
         }
       }
-#pragma unroll
-      for (int k = 0; k < RP / V; ++k) {
-        const int c = cx0 + validC + k * V;
-        if (c < nx || a.wrapX) {
-          hsrc[nh] = c < nx ? c : c - nx;
-          hdst[nh++] = LP + validC + k * V;
-        }
-      }
-      const int ra = a.row0 + r0;
-      const int nStages = (len + H - 1 + RPS - 1) / RPS;
-      int rf = ra + a.inShift - TP;
-      if (a.wrapY) rf = wrap_idx(rf, a.inRows);
-      for (int g = 0; g < nStages; ++g, ++G0) {
-        const int slot = G0 % STAGES;
-        if (G0 >= STAGES) mbar_wait(&empty[slot], ((G0 / STAGES) + 1) & 1);
-        mbar_expect_tx(&full[slot], mainBytes * RPS);
-        T* sstage = ring + slot * (RPS * ROW);
-#pragma unroll
-        for (int k = 0; k < RPS; ++k) {
-          const T* grow = in + static_cast<long long>(rf) * nx;
-          T* srow = sstage + k * ROW;
-          bulk_g2s(srow + LP, grow + cx0, mainBytes, &full[slot]);
-          for (int h = 0; h < nh; ++h) cp_async16(srow + hdst[h], grow + hsrc[h]);
-          ++rf;
-          if (a.wrapY) {
-            if (rf == a.inRows) rf = 0;
-          } else if (rf >= a.inRows) {
-            rf = a.inRows - 1;
-          }
-        }
-        cp_async_mbar_arrive(&full[slot]);
-      }
+      cp_async_mbar_arrive(&full[slot]);
     }
     return;
   }
 
   // ---------------- consumers
-  SliceIter it{start, end, rows};
-  int xbk, r0, len;
-  int G0 = 0;
-  T* __restrict__ out = a.out;
-  while (it.next(xbk, r0, len)) {
-    const int xb = xbk * CW + warp * SW + lane * V;
-    const bool laneValid = xb < nx;
-    const int ra = a.row0 + r0;
-    const int rb = ra + len;
-    const int nStages = (len + H - 1 + RPS - 1) / RPS;
-    T win[H][E];  // ring: input row t lives in win[t % H]
-    T* __restrict__ orow = out + static_cast<long long>(ra - (H - 1)) * nx + xb;
-    const bool vecStore = laneValid && xb >= a.col0 && xb + V <= a.col1;
-    const long long rowStep = nx;
-    int j = ra - (H - 1);  // output row completed by the current input row
-    for (int g = 0; g < nStages; ++g, ++G0) {
-      const int slot = G0 % STAGES;
-      mbar_wait(&full[slot], (G0 / STAGES) & 1);
-      const T* sbase = ring + slot * (RPS * ROW) + LP + warp * SW + lane * V;
+  const int xb = cx0 + warp * SW + lane * V;
+  const bool laneValid = xb < nx;
+  T win[H][E];  // ring: input row t lives in win[t % H]
+  T* __restrict__ orow = a.out + static_cast<long long>(ra - (H - 1)) * nx + xb;
+  const bool vecStore = laneValid && xb >= a.col0 && xb + V <= a.col1;
+  const long long rowStep = nx;
+  int j = ra - (H - 1);  // output row completed by the current input row
+  for (int g = 0; g < nStages; ++g) {
+    const int slot = g % STAGES;
+    mbar_wait(&full[slot], (g / STAGES) & 1);
+    const T* sbase = ring + slot * (RPS * ROW) + LP + warp * SW + lane * V;
 #pragma unroll
-      for (int k = 0; k < RPS; ++k) {
-        const T* srow = sbase + k * ROW;
-        T* e = win[k % H];
-        const VT c = *reinterpret_cast<const VT*>(srow);
-        if constexpr (V == 2) {
-          e[L] = c.x;
-          e[L + 1] = c.y;
-        } else {
-          e[L] = c.x;
-          e[L + 1] = c.y;
-          e[L + 2] = c.z;
-          e[L + 3] = c.w;
-        }
-#pragma unroll
-        for (int p = 0; p < L; ++p) e[p] = srow[p - L];
-#pragma unroll
-        for (int p = 0; p < R; ++p) e[L + V + p] = srow[V + p];
-        // Output row j uses input rows j-TP .. j+BT = the H most recent
-        // rows, oldest in slot (k + 1) % H.
-        T res[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          if constexpr (std::is_same_v<Op, OpWeights>) {
-            T acc = T(0);
-#pragma unroll
-            for (int q = 0; q < H; ++q)
-#pragma unroll
-              for (int p = 0; p < W; ++p) acc += a.v[q * W + p] * win[(k + 1 + q) % H][v + p];
-            res[v] = acc;
-          } else {
-            T w[H * W];
-#pragma unroll
-            for (int q = 0; q < H; ++q)
-#pragma unroll
-              for (int p = 0; p < W; ++p) w[q * W + p] = win[(k + 1 + q) % H][v + p];
-            res[v] = Op::template apply<T>(w, a.v, W);
-          }
-        }
-        if (j >= ra && j < rb) {  // warp-uniform
-          if (vecStore) {
-            VT o;
-            if constexpr (V == 2) {
-              o.x = res[0];
-              o.y = res[1];
-            } else {
-              o.x = res[0];
-              o.y = res[1];
-              o.z = res[2];
-              o.w = res[3];
-            }
-            *reinterpret_cast<VT*>(orow) = o;
-          } else if (laneValid) {
-#pragma unroll
-            for (int v = 0; v < V; ++v)
-              if (xb + v >= a.col0 && xb + v < a.col1) orow[v] = res[v];
-          }
-        }
-        ++j;
-        orow += rowStep;
+    for (int k = 0; k < RPS; ++k) {
+      const T* srow = sbase + k * ROW;
+      T* e = win[k % H];
+      const VT c = *reinterpret_cast<const VT*>(srow);
+      if constexpr (V == 2) {
+        e[L] = c.x;
+        e[L + 1] = c.y;
+      } else {
+        e[L] = c.x;
+        e[L + 1] = c.y;
+        e[L + 2] = c.z;
+        e[L + 3] = c.w;
       }
-      __syncwarp();  // every lane of this warp has read the stage
-      if (lane == 0) mbar_arrive(&empty[slot]);
+#pragma unroll
+      for (int p = 0; p < L; ++p) e[p] = srow[p - L];
+#pragma unroll
+      for (int p = 0; p < R; ++p) e[L + V + p] = srow[V + p];
+      // Output row j uses input rows j-TP .. j+BT = the H most recent rows,
+      // oldest in slot (k + 1) % H.
+      T res[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if constexpr (std::is_same_v<Op, OpWeights>) {
+          T acc = T(0);
+#pragma unroll
+          for (int q = 0; q < H; ++q)
+#pragma unroll
+            for (int p = 0; p < W; ++p) acc += a.v[q * W + p] * win[(k + 1 + q) % H][v + p];
+          res[v] = acc;
+        } else {
+          T w[H * W];
+#pragma unroll
+          for (int q = 0; q < H; ++q)
+#pragma unroll
+            for (int p = 0; p < W; ++p) w[q * W + p] = win[(k + 1 + q) % H][v + p];
+          res[v] = Op::template apply<T>(w, a.v, W);
+        }
+      }
+      if (j >= ra && j < rb) {  // warp-uniform
+        if (vecStore) {
+          VT o;
+          if constexpr (V == 2) {
+            o.x = res[0];
+            o.y = res[1];
+          } else {
+            o.x = res[0];
+            o.y = res[1];
+            o.z = res[2];
+            o.w = res[3];
+          }
+          *reinterpret_cast<VT*>(orow) = o;
+        } else if (laneValid) {
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            if (xb + v >= a.col0 && xb + v < a.col1) orow[v] = res[v];
+        }
+      }
+      ++j;
+      orow += rowStep;
     }
+    __syncwarp();  // every lane of this warp has read the stage
+    if (lane == 0) mbar_arrive(&empty[slot]);
   }
 }
 
@@ -690,15 +648,6 @@ constexpr int prefetch_depth() {
   return d >= 8 ? 8 : d >= 4 ? 4 : 2;
 }
 
-int sm_count() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
-
 // SG_STENCIL_KERNEL=reg selects the register-prefetch k_strip (kept for A/B
 // measurements); the default is the TMA-staged k_tma.
 bool use_tma() {
@@ -714,24 +663,15 @@ void launch_strip_lt(const KArgs<T>& a, dim3 grid, cudaStream_t s) {
   if (use_tma()) {
     using G = TmaGeom<T, L, L, TP, TP>;
     auto kern = k_tma<T, L, L, TP, TP, Op>;
-    static int ctasPerSm = 0;  // per instantiation
-    if (ctasPerSm == 0) {
+    static bool configured = false;  // per instantiation
+    if (!configured) {
       SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(G::smem_bytes)));
       SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctasPerSm, kern, (TMA_WARPS + 1) * 32,
-                                                            G::smem_bytes));
-      if (ctasPerSm < 1) ctasPerSm = 1;
+      configured = true;
     }
-    // One wave: gx column blocks x nseg row segments <= resident capacity
-    // (long segments: the vertical halo is read once per segment); >= 16
-    // rows per segment for small grids.
-    const int gx = (a.nx + G::CW - 1) / G::CW;
-    const int rows = a.row1 - a.row0;
-    const long long cap = 1LL * sm_count() * ctasPerSm;
-    long long nseg = std::max<long long>(1, cap / gx);
-    nseg = std::min<long long>(nseg, std::max(1, rows / 16));
-    kern<<<dim3(gx, static_cast<unsigned>(nseg)), (TMA_WARPS + 1) * 32, G::smem_bytes, s>>>(a);
+    dim3 g2((a.nx + G::CW - 1) / G::CW, grid.y);
+    kern<<<g2, (TMA_WARPS + 1) * 32, G::smem_bytes, s>>>(a);
     return;
   }
   constexpr int D = prefetch_depth<T, L>();
@@ -758,6 +698,14 @@ void launch_strip(const KArgs<T>& a, const sg_extents& e, dim3 grid, cudaStream_
   invalid("internal: no strip kernel for these extents");
 }
 
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
 
 template <typename T>
 int launch_typed(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,

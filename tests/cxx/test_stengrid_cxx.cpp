@@ -463,6 +463,44 @@ void test_ch() {  // test_cahn_hilliard.cpp:56-75, 259-318
   CHECK(worst <= 0.3 * 1e-13);
 }
 
+void test_diagnostics_and_run() {  // test_cahn_hilliard.cpp:320-366, 475-505
+  Grid2D c(64, 64, kTwoPi / 64, kTwoPi / 64);
+  c.values.setConstant(0.77);
+  CHECK(std::abs(simpson_mean(c) - 0.77) <= 0.77 * 1e-13);
+  Grid2D zero(16, 16, kTwoPi / 16, kTwoPi / 16);
+  CHECK(s_metric(zero) == 1.0);
+  Grid2D one(16, 16, kTwoPi / 16, kTwoPi / 16);
+  one.values.setConstant(1.0);
+  CHECK_THROWS_AS(s_metric(one), std::domain_error);
+  CHParams p = small_params(64, 64);
+  Grid2D cx(64, 64, p.dx(), p.dy());
+  for (int j = 0; j < 64; ++j)
+    for (int i = 0; i < 64; ++i) cx(i, j) = std::cos(i * p.dx());
+  CHECK(std::abs(k1_metric(cx) - 1.0) <= 1e-12);
+  CHECK_THROWS_AS(k1_metric(Grid2D(64, 64, p.dx(), p.dy())), std::domain_error);
+  CHParams q = small_params(16, 16);
+  q.T = q.dt;
+  q.icAmplitude = 0.0;
+  std::vector<Diagnostics> rows;
+  RunSink sink;
+  sink.diagEvery = 1;
+  sink.onDiagnostics = [&](const Diagnostics& d) { rows.push_back(d); };
+  run(q, 1, 1, sink);
+  CHECK(rows.size() == 2);
+  CHECK(rows.size() == 2 && rows[0].t == 0.0 && rows[1].t == q.dt);
+  q.T = 10.5 * q.dt;
+  int snaps = 0;
+  RunSink s2;
+  s2.diagEvery = 0;
+  s2.snapEvery = 5;
+  s2.onSnapshot = [&](const Grid2D& g, int, double) {
+    CHECK(g.nx == 16);
+    ++snaps;
+  };
+  run(q, 1, 1, s2);
+  CHECK(snaps == 3);
+}
+
 }  // namespace
 
 int main() {
@@ -476,6 +514,7 @@ int main() {
   test_acceptance_criterion_2();
   test_penta();
   test_ch();
+  test_diagnostics_and_run();
   std::printf("%d checks passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
