@@ -113,9 +113,9 @@ def reference_arm(args, rank, world):
     reference library, all host threads) on a bounded sample of the config."""
     if rank != 0:
         return
-    line = cpu_reference_sample(target_s=max(5.0, args.ref_seconds))
+    line = cpu_reference_sample(reps=args.steps, warmup=args.warmup)
     out = {"metric": METRIC, "value": line["value"], "unit": UNIT, "n_gpus": world, "steps": line["reps"],
-           "warmup": 1, "ms_per_step": line["ms_per_app_sample"], "higher_is_better": True,
+           "warmup": args.warmup, "ms_per_step": line["ms_per_app_sample"], "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": WORKLOAD, "nx": NX, "ny": NY, "sample_rows": line["rows"]},
            "impl": "reference",
@@ -125,7 +125,7 @@ def reference_arm(args, rank, world):
     print(json.dumps(out), flush=True)
 
 
-def cpu_reference_sample(target_s=12.0, rows=2048):
+def cpu_reference_sample(target_s=12.0, rows=2048, reps=None, warmup=1):
     """Reference compute() on a 32768 x `rows` periodic band, numWorkers =
     numTiles = host threads, steady_clock around compute() only
     (bench.cpp:33-40). Falls back to the C restatement (kind "port") only
@@ -139,11 +139,13 @@ def cpu_reference_sample(target_s=12.0, rows=2048):
     try:
         ref = Reference()
         kind = "reference"
-        t1 = ref.stencil_timed(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3", tiles=min(cores, rows),
-                               workers=cores, warmup=1, reps=1)
-        reps = max(1, min(200, int(target_s / max(t1, 1e-6))))
+        if reps is None:  # size the sample to ~target_s of CPU work
+            t1 = ref.stencil_timed(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3", tiles=min(cores, rows),
+                                   workers=cores, warmup=1, reps=1)
+            reps = max(1, min(200, int(target_s / max(t1, 1e-6))))
+            warmup = 0
         secs = ref.stencil_timed(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3", tiles=min(cores, rows),
-                                 workers=cores, warmup=0, reps=reps)
+                                 workers=cores, warmup=warmup, reps=reps)
     except FileNotFoundError:
         orc = Restatement()
         kind = "port"
@@ -322,7 +324,7 @@ def ours_arm(args, rank, world, local_rank):
     traffic = None
     tp = ROOT / "profiles" / "traffic_r01.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get("k_strip_fp64_3x3_bytes_per_launch")
+        traffic = json.loads(tp.read_text()).get("bytes_per_launch")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -332,7 +334,7 @@ def ours_arm(args, rank, world, local_rank):
                    "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_strip<double,1,1,1,1,OpWeighted3x3>", "kernel_ms": kms,
+                     "kernel": "k_tma<double,1,1,1,1,OpWeighted3x3>", "kernel_ms": kms,
                      "algorithmic_bytes_per_launch": alg_bytes},
         "clocks": clocks,
         "gpu_launches": int(launches),
