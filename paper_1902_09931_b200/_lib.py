@@ -10,7 +10,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libstengrid_b200.so"
+import os
+
+# SG_LIB_PATH overrides the library (A/B experiments with alternative builds).
+LIB_PATH = Path(os.environ.get("SG_LIB_PATH") or Path(__file__).resolve().parent / "libstengrid_b200.so")
 
 # sg_status
 SG_OK, SG_ERR_INVALID_ARGUMENT, SG_ERR_LOGIC, SG_ERR_PENTA_SOLVE, SG_ERR_DOMAIN, SG_ERR_CUDA, \

@@ -369,7 +369,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // CTA geometry: TMA_WARPS consumer warps side by side cover CW columns; one
 // producer warp streams rows (CW + halos) into a STAGES x RPS ring.
-constexpr int TMA_WARPS = 4;
+#ifndef SG_TMA_WARPS
+#define SG_TMA_WARPS 16
+#endif
+constexpr int TMA_WARPS = SG_TMA_WARPS;
 
 template <typename T, int L, int R, int TP, int BT>
 struct TmaGeom {
