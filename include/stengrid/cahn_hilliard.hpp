@@ -190,6 +190,9 @@ class CHStepper {
     dirty_ = true;
   }
 
+  /// Restore the step counter (exact checkpoint resume; not in the reference).
+  void set_step_index(int step) { detail::check(sg_ch_set_step(h_, step)); }
+
   int step_index() const {
     int s = 0;
     detail::check(sg_ch_status(h_, &s, nullptr));

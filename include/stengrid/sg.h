@@ -174,6 +174,9 @@ sg_status sg_ch_set_state(sg_ch_t ch, const double* curr, const double* prev, sg
 sg_status sg_ch_get_field(sg_ch_t ch, int which, double* out, sg_memory memory);
 sg_status sg_ch_device_field(sg_ch_t ch, int which, const double** dptr);
 sg_status sg_ch_status(sg_ch_t ch, int* step, double* time);
+/* Restore the step counter (time = step*dt) after set_state, for exact
+ * checkpoint resume; set_state itself resets it to 0 like the reference. */
+sg_status sg_ch_set_step(sg_ch_t ch, int step);
 sg_status sg_ch_destroy(sg_ch_t* ch);
 /* CHStepper::diagnostics (cahn_hilliard.cpp:330-340) on the device-resident
  * C^n: t, s = s_metric, k1Inv = 1/k1_metric (0 for an all-zero field).

@@ -178,6 +178,9 @@ class Reference:
                                  _dp, _dp]
         L.ref_ch_timed.argtypes = [_dp, C.POINTER(C.c_longlong), C.c_int, C.c_int, C.c_int, C.c_int, _dp]
         L.ref_ch_diagnostics.argtypes = [_dp, C.c_int, C.c_int, C.c_double, C.c_double, _dp, _dp]
+        L.ref_write_snapshot.argtypes = [_dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_char_p]
+        L.ref_read_snapshot.argtypes = [C.c_char_p, _ip, _ip, _dp, _dp, _dp, C.c_longlong]
+        L.ref_write_diagnostics_csv.argtypes = [_dp, C.c_int, C.c_char_p]
 
     def _check(self, rc):
         if rc != 0:
@@ -275,6 +278,23 @@ class Reference:
         secs = C.c_double()
         self._check(self.lib.ref_ch_timed(_d(dp), ip, tiles, workers, warmup, steps, C.byref(secs)))
         return secs.value
+
+    def write_snapshot(self, values, dx, dy, path):
+        v = _f64(values)
+        ny, nx = v.shape
+        self._check(self.lib.ref_write_snapshot(_d(v), nx, ny, dx, dy, str(path).encode()))
+
+    def read_snapshot(self, path, cap=1 << 22):
+        nx, ny = C.c_int(), C.c_int()
+        dx, dy = C.c_double(), C.c_double()
+        buf = np.empty(cap)
+        self._check(self.lib.ref_read_snapshot(str(path).encode(), C.byref(nx), C.byref(ny), C.byref(dx),
+                                               C.byref(dy), _d(buf), cap))
+        return buf[: nx.value * ny.value].reshape(ny.value, nx.value).copy(), dx.value, dy.value
+
+    def write_diagnostics_csv(self, rows, path):
+        r = _f64(np.asarray(rows, dtype=np.float64).reshape(-1, 3))
+        self._check(self.lib.ref_write_diagnostics_csv(_d(r), r.shape[0], str(path).encode()))
 
     def ch_diagnostics(self, field, dx, dy):
         f = _f64(field)

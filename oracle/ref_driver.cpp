@@ -23,6 +23,7 @@
 #include "stengrid/cahn_hilliard.hpp"
 #include "stengrid/grid.hpp"
 #include "stengrid/penta.hpp"
+#include "stengrid/snapshot.hpp"
 #include "stengrid/stencil.hpp"
 
 #include <chrono>
@@ -310,6 +311,33 @@ int ref_ch_diagnostics(const double* field, int nx, int ny, double dx, double dy
     } catch (const std::domain_error&) {
       *k1Inv = 0.0;
     }
+  });
+}
+
+int ref_write_snapshot(const double* v, int nx, int ny, double dx, double dy, const char* path) {
+  return guarded([&] {
+    Grid2D g(nx, ny, dx, dy);
+    std::memcpy(g.data(), v, sizeof(double) * static_cast<std::size_t>(g.size()));
+    write_snapshot(g, std::string(path));
+  });
+}
+
+int ref_read_snapshot(const char* path, int* nx, int* ny, double* dx, double* dy, double* out, long long cap) {
+  return guarded([&] {
+    const Grid2D g = read_snapshot(std::string(path));
+    *nx = g.nx;
+    *ny = g.ny;
+    *dx = g.dx;
+    *dy = g.dy;
+    if (out && cap >= g.size()) std::memcpy(out, g.data(), sizeof(double) * static_cast<std::size_t>(g.size()));
+  });
+}
+
+int ref_write_diagnostics_csv(const double* rows, int n, const char* path) {
+  return guarded([&] {
+    std::vector<Diagnostics> v(static_cast<std::size_t>(n));
+    for (int k = 0; k < n; ++k) v[k] = Diagnostics{rows[3 * k], rows[3 * k + 1], rows[3 * k + 2]};
+    write_diagnostics_csv(v, std::string(path));
   });
 }
 

@@ -18,7 +18,12 @@ from .penta import (Axis, PentaBatch, PentaFactor, PeriodicPentaFactor, RhsBatch
 from .cahn_hilliard import (CHParams, CHStepper, Diagnostics, RunSink, biharmonic_weights, k1_metric,
                             nonlinear_laplacian_coefficients, run, s_metric, simpson_mean)
 
+from .snapshot import (format_diagnostics_row, load_checkpoint, read_snapshot, save_checkpoint,
+                       write_diagnostics_csv, write_snapshot)
+
 __all__ = [
+    "format_diagnostics_row", "load_checkpoint", "read_snapshot", "save_checkpoint",
+    "write_diagnostics_csv", "write_snapshot",
     "Axis", "PentaBatch", "PentaFactor", "PeriodicPentaFactor", "RhsBatch",
     "build_hyperdiffusion_operator", "deinterleave", "interleave", "solve_batch",
     "solve_periodic_batch", "CHParams", "CHStepper", "Diagnostics", "biharmonic_weights",

@@ -665,6 +665,14 @@ sg_status sg_ch_diagnostics(sg_ch_t ch, double* t, double* s, double* k1Inv) {
   });
 }
 
+sg_status sg_ch_set_step(sg_ch_t ch, int step) {
+  return guard2([&] {
+    if (!ch) sg::logic("CHStepper: destroyed");
+    if (step < 0) sg::invalid("CHStepper: step must be >= 0");
+    ch->st->step = step;
+  });
+}
+
 sg_status sg_ch_destroy(sg_ch_t* ch) {
   return guard2([&] {
     if (!ch || !*ch) return;
