@@ -48,8 +48,13 @@ class DistCHStepper:
         self.cur = torch.zeros((self.own + 2 * HALO, nx), dtype=dt, device=device)
         self.prev = torch.zeros_like(self.cur)
         self.send = torch.empty(self.own * nx, dtype=dt, device=device)
-        self.ycol = torch.empty(ny * self.nxq, dtype=dt, device=device)
-        self.recv = torch.empty(self.own * nx, dtype=dt, device=device)
+        if world == 1 and transport is None:
+            # one rank: both all-to-alls are the identity, so the three
+            # buffers alias and no copy is made
+            self.ycol = self.recv = self.send
+        else:
+            self.ycol = torch.empty(ny * self.nxq, dtype=dt, device=device)
+            self.recv = torch.empty(self.own * nx, dtype=dt, device=device)
         self.steps_done = 0
         check(_lib.lib().sg_chd_init(self._h, self._p(self.cur), self._p(self.prev), self._s()))
 
@@ -72,7 +77,8 @@ class DistCHStepper:
         if self.transport is not None:
             self.transport.alltoall(self, out, inp, phase)
         elif self.world == 1:
-            out.copy_(inp)
+            if out.data_ptr() != inp.data_ptr():
+                out.copy_(inp)
         else:
             self.dist.all_to_all_single(out, inp)
 

@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -118,71 +119,101 @@ __device__ __forceinline__ int wrap_once(int i, int n) {  // i in [-n, 2n)
   return i < 0 ? i + n : (i >= n ? i - n : i);
 }
 
+// Output tile: RX = 64 columns (i) x RY = 32 rows (j); 256 threads, each
+// computes 2 columns x 4 rows. Inputs are staged with a 2-point halo
+// (68 x 36: 1.2x redundancy) through a flattened, coalesced load loop.
+constexpr int RX = 64, RY = 32;
+constexpr int RXE = RX + 2 * HALO, RYE = RY + 2 * HALO;
+
 template <bool NONLINEAR>
 __global__ void __launch_bounds__(256) k_rhs(const double* __restrict__ cc, const double* __restrict__ cp,
                                              double* __restrict__ rhsT, const RhsGeom G,
                                              const __grid_constant__ RhsParams P) {
-  __shared__ double sc[TE][TE + 1];  // C^n with a 2-point halo
-  __shared__ double sb[TE][TE + 1];  // Cbar with a 2-point halo
-  __shared__ double sp[TS][TS + 1];  // C^{n-1}, tile interior
+  extern __shared__ __align__(16) double rsm[];
+  double (*sc)[RXE + 1] = reinterpret_cast<double (*)[RXE + 1]>(rsm);              // C^n
+  double (*sb)[RXE + 1] = reinterpret_cast<double (*)[RXE + 1]>(rsm + RYE * (RXE + 1));  // Cbar
+  double (*sp)[RX + 1] = reinterpret_cast<double (*)[RX + 1]>(rsm + 2 * RYE * (RXE + 1));  // C^{n-1}
   const int nx = G.nx;
-  const int i0 = blockIdx.x * TS, j0 = blockIdx.y * TS;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int y = ty; y < TE; y += blockDim.y) {
+  const int i0 = blockIdx.x * RX, j0 = blockIdx.y * RY;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int e = tid; e < RYE * RXE; e += 256) {
+    const int y = e / RXE, x = e - y * RXE;
     int j = j0 - HALO + y + G.inShift;
-    j = G.wrapY ? (G.inRows >= TE ? wrap_once(j, G.inRows) : wrapi(j, G.inRows)) : min(max(j, 0), G.inRows - 1);
-    for (int x = tx; x < TE; x += blockDim.x) {
-      const int i = nx >= TE ? wrap_once(i0 - HALO + x, nx) : wrapi(i0 - HALO + x, nx);
-      const long long idx = static_cast<long long>(j) * nx + i;
-      const double c = __ldg(cc + idx), p = __ldg(cp + idx);
-      sc[y][x] = c;
-      sb[y][x] = 2.0 * c - p;  // cahn_hilliard.cpp:273
-      if (y >= HALO && y < HALO + TS && x >= HALO && x < HALO + TS) sp[y - HALO][x - HALO] = p;
-    }
+    j = G.wrapY ? (G.inRows >= RYE ? wrap_once(j, G.inRows) : wrapi(j, G.inRows)) : min(max(j, 0), G.inRows - 1);
+    const int i = nx >= RXE ? wrap_once(i0 - HALO + x, nx) : wrapi(i0 - HALO + x, nx);
+    const long long idx = static_cast<long long>(j) * nx + i;
+    const double c = __ldg(cc + idx), p = __ldg(cp + idx);
+    sc[y][x] = c;
+    sb[y][x] = 2.0 * c - p;  // cahn_hilliard.cpp:273
+    if (y >= HALO && y < HALO + RY && x >= HALO && x < HALO + RX) sp[y - HALO][x - HALO] = p;
   }
   __syncthreads();
   constexpr int kBihTaps[13] = SG_BIH_TAPS;
   constexpr int kNlTaps[5] = SG_NL_TAPS;
-  double res[TS / 8];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  double res[2][4];
 #pragma unroll
-  for (int k = 0; k < TS / 8; ++k) {
-    const int y = ty + 8 * k;  // output row within the tile
-    const int x = tx;
-    double bh = 0.0;
+  for (int cx = 0; cx < 2; ++cx)
 #pragma unroll
-    for (int t = 0; t < 13; ++t) {
-      const int q = kBihTaps[t] / 5, p = kBihTaps[t] % 5;
-      bh += P.bw[kBihTaps[t]] * sb[y + q][x + p];
-    }
-    const double c = sc[y + HALO][x + HALO];
-    const double pr = sp[y][x];
-    double r;
-    if constexpr (NONLINEAR) {
-      double nl = 0.0;
+    for (int k = 0; k < 4; ++k) {
+      const int y = ty + 8 * k;   // output row within the tile
+      const int x = tx + 32 * cx;  // output column within the tile
+      double bh = 0.0;
 #pragma unroll
-      for (int t = 0; t < 5; ++t) {
-        const int q = kNlTaps[t] / 3, p = kNlTaps[t] % 3;
-        const double v = sc[y + 1 + q][x + 1 + p];
-        nl += P.nl[kNlTaps[t]] * (v * v * v - v);
+      for (int t = 0; t < 13; ++t) {
+        const int q = kBihTaps[t] / 5, p = kBihTaps[t] % 5;
+        bh += P.bw[kBihTaps[t]] * sb[y + q][x + p];
       }
-      r = P.kDiff * (c - pr) - P.kBih * bh + P.kNl * nl;  // cahn_hilliard.cpp:292
-    } else {
-      r = P.kDiff * (c - pr) - P.kBih * bh;  // cahn_hilliard.cpp:294
+      const double c = sc[y + HALO][x + HALO];
+      const double pr = sp[y][x];
+      double r;
+      if constexpr (NONLINEAR) {
+        double nl = 0.0;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+          const int q = kNlTaps[t] / 3, p = kNlTaps[t] % 3;
+          const double v = sc[y + 1 + q][x + 1 + p];
+          nl += P.nl[kNlTaps[t]] * (v * v * v - v);
+        }
+        r = P.kDiff * (c - pr) - P.kBih * bh + P.kNl * nl;  // cahn_hilliard.cpp:292
+      } else {
+        r = P.kDiff * (c - pr) - P.kBih * bh;  // cahn_hilliard.cpp:294
+      }
+      res[cx][k] = r;
     }
-    res[k] = r;
-  }
   __syncthreads();
-  // stage the tile transposed in smem, then write rhsT[i*outRows + jl]
-  // coalesced in jl (the x-sweep's interleaved batch)
+  // stage transposed ([i][j], reusing sc/sb) and write rhsT[i*outRows + j],
+  // one 256 B row segment per warp instruction
+  double (*tt)[RY + 1] = reinterpret_cast<double (*)[RY + 1]>(rsm);
 #pragma unroll
-  for (int k = 0; k < TS / 8; ++k) sc[tx][ty + 8 * k] = res[k];
+  for (int cx = 0; cx < 2; ++cx)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tt[tx + 32 * cx][ty + 8 * k] = res[cx][k];
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < TS / 8; ++k) {
+  for (int k = 0; k < RX / 8; ++k) {
     const int x = ty + 8 * k;  // i within the tile
     const int i = i0 + x, j = j0 + tx;
-    if (i < nx && j < G.outRows) rhsT[static_cast<long long>(i) * G.outRows + j] = sc[x][tx];
+    if (i < nx && j < G.outRows) rhsT[static_cast<long long>(i) * G.outRows + j] = tt[x][tx];
   }
+}
+
+constexpr size_t kRhsSmem = (2 * RYE * (RXE + 1) + RY * (RX + 1)) * sizeof(double);
+
+void launch_rhs(bool nonlinear, const double* cc, const double* cp, double* rhsT, const RhsGeom& g,
+                const RhsParams& rp, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    SG_CUDA(cudaFuncSetAttribute(k_rhs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kRhsSmem)));
+    SG_CUDA(cudaFuncSetAttribute(k_rhs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kRhsSmem)));
+    configured = true;
+  }
+  dim3 tb(32, 8), tg((g.nx + RX - 1) / RX, (g.outRows + RY - 1) / RY);
+  if (nonlinear)
+    k_rhs<true><<<tg, tb, kRhsSmem, s>>>(cc, cp, rhsT, g, rp);
+  else
+    k_rhs<false><<<tg, tb, kRhsSmem, s>>>(cc, cp, rhsT, g, rp);
+  check_launch("ch rhs kernel");
 }
 
 struct CorrTables {
@@ -290,11 +321,7 @@ static void ch_phase_x(const sg_ch_params& p, const RhsParams& rp, const PentaTa
   const int nx = p.nx;
   dim3 tb(32, 8), tg((nx + TS - 1) / TS, (own + TS - 1) / TS);
   const RhsGeom geom{nx, own, own + 2 * HALO, HALO, 0};
-  if (p.nonlinearEnabled)
-    k_rhs<true><<<tg, tb, 0, s>>>(cur, prev, rhsT, geom, rp);
-  else
-    k_rhs<false><<<tg, tb, 0, s>>>(cur, prev, rhsT, geom, rp);
-  check_launch("ch slab rhs kernel");
+  launch_rhs(p.nonlinearEnabled, cur, prev, rhsT, geom, rp, s);
   penta_sweep(fx, own, nx, rhsT, y4x, true, true, s);
   CorrTables tx{{fx.W[0], fx.W[1], fx.W[2], fx.W[3]}, y4x};
   k_transpose_correct<<<tg, tb, 0, s>>>(rhsT, send, nx, own, nxq, tx);
@@ -310,6 +337,18 @@ static void ch_combine_packed(int nx, int own, int nxq, const double* cur, doubl
 namespace {
 
 bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// The fused sweeps (x-sweep writing row-major w, y-sweep correcting on load)
+// remove the transpose/correct pass but lengthen the single-warp recurrence
+// loop; measured slower on B200 at 1024^2 and 8192^2, so they
+// are opt-in: SG_CH_FUSED=1.
+bool unfused() {
+  static const bool v = [] {
+    const char* e = std::getenv("SG_CH_FUSED");
+    return !(e && e[0] == '1');
+  }();
+  return v;
+}
 
 }  // namespace
 
@@ -409,16 +448,18 @@ struct ChState {
     double* cp = field[1 - c];
     dim3 tb(32, 8), tg((nx + TS - 1) / TS, (ny + TS - 1) / TS);
     const RhsGeom geom{nx, ny, ny, 0, 1};
-    if (p.nonlinearEnabled)
-      k_rhs<true><<<tg, tb, 0, s>>>(cc, cp, rhsT, geom, rp);
-    else
-      k_rhs<false><<<tg, tb, 0, s>>>(cc, cp, rhsT, geom, rp);
-    check_launch("ch rhs kernel");
-    penta_sweep(fx.t, ny, nx, rhsT, y4x, true, true, s);
-    CorrTables tx{{fx.t.W[0], fx.t.W[1], fx.t.W[2], fx.t.W[3]}, y4x};
-    k_transpose_correct<<<tg, tb, 0, s>>>(rhsT, w, nx, ny, nx, tx);
-    check_launch("ch transpose kernel");
-    penta_sweep(fy.t, nx, ny, w, y4y, true, true, s);
+    launch_rhs(p.nonlinearEnabled, cc, cp, rhsT, geom, rp, s);
+    // x-sweep writes its (uncorrected) result straight into row-major w;
+    // the y-sweep applies the x Woodbury correction as it loads w.
+    const bool fused = !unfused() && penta_sweep_fused(fx.t, ny, nx, rhsT, y4x, nullptr, nullptr, w, s) &&
+                       penta_sweep_fused(fy.t, nx, ny, w, y4y, fx.t.W, y4x, nullptr, s);
+    if (!fused) {
+      penta_sweep(fx.t, ny, nx, rhsT, y4x, true, true, s);
+      CorrTables tx{{fx.t.W[0], fx.t.W[1], fx.t.W[2], fx.t.W[3]}, y4x};
+      k_transpose_correct<<<tg, tb, 0, s>>>(rhsT, w, nx, ny, nx, tx);
+      check_launch("ch transpose kernel");
+      penta_sweep(fy.t, nx, ny, w, y4y, true, true, s);
+    }
     CorrTables ty{{fy.t.W[0], fy.t.W[1], fy.t.W[2], fy.t.W[3]}, y4y};
     k_combine<<<dim3((nx + 255) / 256, ny), 256, 0, s>>>(cc, cp, w, nx, ny, ty);
     check_launch("ch combine kernel");

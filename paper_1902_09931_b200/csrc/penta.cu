@@ -176,6 +176,39 @@ __global__ void k_periodic_setup(PentaTables f, int B, int n, const double* __re
   for (int k = 0; k < 4; ++k) piv[b * 4 + k] = pv[k];
 }
 
+// Uniform operator: the four core solves W_k = P^{-1} e_{0,1,n-2,n-1} are
+// independent — one thread each — then thread 0 builds K (penta.cpp:204-251).
+__global__ void k_periodic_setup_uniform(PentaTables f, int n, const double* __restrict__ e,
+                                         const double* __restrict__ c, const double* __restrict__ a,
+                                         const double* __restrict__ bb, double* W0, double* W1, double* W2,
+                                         double* W3, double* cw, double* K, int* piv, int* singular) {
+  const int k = threadIdx.x;
+  double* Wk[4] = {W0, W1, W2, W3};
+  const int rowOf[4] = {0, 1, n - 2, n - 1};
+  if (k < 4) {
+    for (int r = 0; r < n; ++r) Wk[k][r] = 0.0;
+    Wk[k][rowOf[k]] = 1.0;
+    substitute(f, 1, 0, Wk[k], 1, n);
+  }
+  __syncthreads();
+  if (k != 0) return;
+  double cwl[6] = {e[0], c[0], e[1], bb[n - 2], a[n - 1], bb[n - 1]};
+  for (int q = 0; q < 6; ++q) cw[q] = cwl[q];
+  double Kl[16];
+  for (int q = 0; q < 4; ++q) {
+    const double w0 = Wk[q][0], w1 = Wk[q][1], wn2 = Wk[q][n - 2], wn1 = Wk[q][n - 1];
+    Kl[0 * 4 + q] = cwl[0] * wn2 + cwl[1] * wn1;
+    Kl[1 * 4 + q] = cwl[2] * wn1;
+    Kl[2 * 4 + q] = cwl[3] * w0;
+    Kl[3 * 4 + q] = cwl[4] * w0 + cwl[5] * w1;
+  }
+  for (int r = 0; r < 4; ++r) Kl[r * 4 + r] += 1.0;
+  int pv[4] = {0, 1, 2, 3};
+  singular[0] = lu4_factor(Kl, pv) ? 0 : 1;
+  for (int q = 0; q < 16; ++q) K[q] = Kl[q];
+  for (int q = 0; q < 4; ++q) piv[q] = pv[q];
+}
+
 }  // namespace
 
 namespace {
@@ -305,6 +338,18 @@ constexpr int SW_NSTG = 4;  // stages in flight
 struct alignas(64) SweepMaps {
   CUtensorMap z;     // 2D {B, n}, box {32, RS}
   CUtensorMap t[5];  // m1, m2, dInv, ap, bp: uniform 1D {n} box {RS}; else 2D like z
+  CUtensorMap yc[4]; // XCORR: the previous sweep's Woodbury coefficients y_k[r], 1D {n} box {RS}
+};
+
+// Fusions used by the Cahn-Hilliard step (ch.cu):
+//  XCORR: the input is another sweep's UNcorrected result; apply its
+//         Woodbury correction on load: z(b, r) -= Wc0[b] yc0[r] + ... + Wc3[b] yc3[r]
+//         (penta.cpp:279-286, same expression), streaming yc with the rows.
+//  XOUT:  write the backward results transposed, zout[b*n + r] (the grid's
+//         natural layout) instead of back into the interleaved z.
+struct SweepFuse {
+  const double* Wc[4] = {nullptr, nullptr, nullptr, nullptr};
+  double* zout = nullptr;
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) {
@@ -344,24 +389,28 @@ __device__ __forceinline__ void s_tma_1d(void* dst, const CUtensorMap* m, int x,
       : "memory");
 }
 
-template <bool UNIFORM>
+template <bool UNIFORM, bool XCORR = false>
 struct SweepSmem {
   // doubles per factor table per stage; tensor-TMA destinations must be
   // 128 B aligned, so the uniform (SW_RS-long) tables get a 16-double slot
   static constexpr int FAC = UNIFORM ? (SW_RS + 15) / 16 * 16 : SW_RS * 32;
-  static constexpr int STAGE = SW_RS * 32 + 3 * FAC;             // z + up to 3 tables
+  static constexpr int YCS = (SW_RS + 15) / 16 * 16;                // one yc table slot
+  static constexpr int STAGE = SW_RS * 32 + 3 * FAC + (XCORR ? 4 * YCS : 0);
   static constexpr int STAGE_PAD = (STAGE * 8 + 127) / 128 * 16;  // doubles, 128 B aligned stride
-  static constexpr size_t bytes = static_cast<size_t>(SW_NSTG) * STAGE_PAD * 8 + 2 * SW_NSTG * 8;
+  static constexpr int XT = 32 * (SW_RS + 1);                       // XOUT staging tile
+  static constexpr size_t bytes = static_cast<size_t>(SW_NSTG) * STAGE_PAD * 8 + XT * 8 + 2 * SW_NSTG * 8;
 };
 
-template <bool UNIFORM, bool PERIODIC, int MODE>
+template <bool UNIFORM, bool PERIODIC, int MODE, bool XCORR = false, bool XOUT = false>
 __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __grid_constant__ SweepMaps maps,
-                                                  int B, int n, double* __restrict__ z, double* __restrict__ y4) {
+                                                  int B, int n, double* __restrict__ z, double* __restrict__ y4,
+                                                  const SweepFuse fuse) {
   // Warp 0: consumer (32 systems, the dependency chain). Warp 1 lane 0:
   // producer (tensor-TMA issue), so the chain never stalls on issue code.
-  using SM = SweepSmem<UNIFORM>;
+  using SM = SweepSmem<UNIFORM, XCORR>;
   extern __shared__ __align__(128) double sw_smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(sw_smem + SW_NSTG * SM::STAGE_PAD);
+  double* xt = sw_smem + SW_NSTG * SM::STAGE_PAD;  // XOUT staging tile [32][RS+1]
+  uint64_t* full = reinterpret_cast<uint64_t*>(xt + SM::XT);
   uint64_t* empty = full + SW_NSTG;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -400,7 +449,8 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
         double* st = sw_smem + slot * SM::STAGE_PAD;
         const int r0 = pass == 0 ? gg * RS : n - (gg + 1) * RS;
         const int nt = pass == 0 ? 2 : 3;
-        s_mbar_expect_tx(&full[slot], ZB + nt * FB);
+        const bool yc = XCORR && pass == 0;
+        s_mbar_expect_tx(&full[slot], ZB + nt * FB + (yc ? 4u * RS * 8u : 0u));
         s_tma_2d(st, &maps.z, b0, r0, &full[slot]);
         for (int k = 0; k < nt; ++k) {
           const CUtensorMap* m = &maps.t[pass == 0 ? k : 2 + k];  // fwd: m1, m2; bwd: dInv, ap, bp
@@ -409,6 +459,8 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
           else
             s_tma_2d(st + RS * 32 + k * FAC, m, b0, r0, &full[slot]);
         }
+        if (yc)
+          for (int k = 0; k < 4; ++k) s_tma_1d(st + RS * 32 + 3 * FAC + k * SM::YCS, &maps.yc[k], r0, &full[slot]);
       }
     }
     return;
@@ -417,6 +469,25 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
   // -------------------------------------------------------------- consumer
   auto fac = [&](const double* st, int k, int row) -> double {
     return UNIFORM ? st[RS * 32 + k * FAC + row] : st[RS * 32 + k * FAC + row * 32 + lane];
+  };
+  double wc0 = 0.0, wc1 = 0.0, wc2 = 0.0, wc3 = 0.0;
+  if constexpr (XCORR) {
+    if (active) {
+      wc0 = fuse.Wc[0][b];
+      wc1 = fuse.Wc[1][b];
+      wc2 = fuse.Wc[2][b];
+      wc3 = fuse.Wc[3][b];
+    }
+  }
+  // z(b, r) as the recurrence sees it: raw, or corrected on load (XCORR)
+  auto zin = [&](const double* st, int k) -> double {
+    const double raw = st[k * 32 + lane];
+    if constexpr (XCORR) {
+      const double* yc = st + RS * 32 + 3 * FAC;
+      return raw - (wc0 * yc[k] + wc1 * yc[SM::YCS + k] + wc2 * yc[2 * SM::YCS + k] + wc3 * yc[3 * SM::YCS + k]);
+    } else {
+      return raw;
+    }
   };
   double* zc = z + b;
   const long long sB = B;
@@ -427,7 +498,7 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
     const double* st = sw_smem;
 #pragma unroll
     for (int k = 0; k < RS; ++k) {
-      const double zr = st[k * 32 + lane];
+      const double zr = zin(st, k);
       double yr;
       if (k >= 2)
         yr = zr - (fac(st, 0, k) * y2 + fac(st, 1, k) * y1);
@@ -435,7 +506,9 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
         yr = zr - fac(st, 1, k) * y1;  // y1 holds y[0]
       else
         yr = zr;
-      if (active && k >= 1 && k < n) zc[k * sB] = yr;
+      // row 0 is unchanged by the forward pass; with XCORR its corrected
+      // value must still reach memory for the backward pass
+      if (active && (k >= 1 || XCORR) && k < n) zc[k * sB] = yr;
       y2 = y1;
       y1 = yr;
     }
@@ -454,7 +527,7 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
     if (r0 + RS <= n) {
 #pragma unroll
       for (int k = 0; k < RS; ++k) {
-        const double yr = st[k * 32 + lane] - (fac(st, 0, k) * y2 + fac(st, 1, k) * y1);  // penta.cpp:180
+        const double yr = zin(st, k) - (fac(st, 0, k) * y2 + fac(st, 1, k) * y1);  // penta.cpp:180
         if (active) *zp = yr;
         zp += step;
         y2 = y1;
@@ -463,7 +536,7 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
     } else {
 #pragma unroll
       for (int k = 0; k < RS; ++k) {
-        const double yr = st[k * 32 + lane] - (fac(st, 0, k) * y2 + fac(st, 1, k) * y1);
+        const double yr = zin(st, k) - (fac(st, 0, k) * y2 + fac(st, 1, k) * y1);
         if (active && r0 + k < n) *zp = yr;
         zp += step;
         y2 = y1;
@@ -477,11 +550,21 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
   asm volatile("bar.sync 1, 64;" ::: "memory");
   // ---- backward (penta.cpp:183-196): stage 0 (rows n-RS..n-1) peeled
   double s1 = 0.0, s2 = 0.0, zn1 = 0.0, zn2 = 0.0, zz0 = 0.0, zz1 = 0.0;
+  constexpr int XP = RS + 1;  // XOUT tile pitch (odd: conflict-free columns)
+  // result of row r (= r0 + k): into z, or into the transposition tile
+  auto put = [&](int k, int r, double yr, double* zq) {
+    if constexpr (XOUT) {
+      xt[lane * XP + k] = yr;
+    } else {
+      if (active && r >= 0) *zq = yr;
+    }
+  };
   for (int g = nS; g < total; ++g) {
     const int slot = g % SW_NSTG;
     s_mbar_wait(&full[slot], (g / SW_NSTG) & 1);
     const double* st = sw_smem + slot * SM::STAGE_PAD;
     const int r0 = n - (g - nS + 1) * RS;
+    double* zq = zc + static_cast<long long>(r0 + RS - 1) * sB;
     if (g == nS) {
 #pragma unroll
       for (int k = RS - 1; k >= 0; --k) {
@@ -497,7 +580,8 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
         } else {
           yr = (yv - fac(st, 1, k) * s1 - fac(st, 2, k) * s2) * fac(st, 0, k);
         }
-        if (active && r >= 0) zc[r * sB] = yr;
+        put(k, r, yr, zq);
+        zq -= sB;
         if (r == 1) zz1 = yr;
         if (r == 0) zz0 = yr;
         s2 = s1;
@@ -505,11 +589,10 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
       }
     } else if (r0 >= 2) {
       // full stage above row 1: branch-free, walking pointer
-      double* zq = zc + static_cast<long long>(r0 + RS - 1) * sB;
 #pragma unroll
       for (int k = RS - 1; k >= 0; --k) {
         const double yr = (st[k * 32 + lane] - fac(st, 1, k) * s1 - fac(st, 2, k) * s2) * fac(st, 0, k);
-        if (active) *zq = yr;
+        put(k, r0 + k, yr, zq);
         zq -= sB;
         s2 = s1;
         s1 = yr;
@@ -519,7 +602,8 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
       for (int k = RS - 1; k >= 0; --k) {
         const int r = r0 + k;
         const double yr = (st[k * 32 + lane] - fac(st, 1, k) * s1 - fac(st, 2, k) * s2) * fac(st, 0, k);
-        if (active && r >= 0) zc[r * sB] = yr;
+        put(k, r, yr, zq);
+        zq -= sB;
         zz1 = r == 1 ? yr : zz1;
         zz0 = r == 0 ? yr : zz0;
         s2 = s1;
@@ -528,6 +612,19 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
     }
     __syncwarp();
     if (lane == 0) s_mbar_arrive(&empty[slot]);
+    if constexpr (XOUT) {
+      // tile [system][row] -> zout[(b0 + system) * n + r0 + k]: two systems
+      // per instruction, 16 consecutive rows (128 B) each
+      const int half = lane >> 4, k = lane & 15;
+#pragma unroll 4
+      for (int pr = 0; pr < 32; pr += 2) {
+        const int sysl = pr + half;
+        const int r = r0 + k;
+        if (k < RS && r >= 0 && b0 + sysl < B)
+          fuse.zout[static_cast<long long>(b0 + sysl) * n + r] = xt[sysl * XP + k];
+      }
+      __syncwarp();
+    }
   }
   if constexpr (PERIODIC) {
     const int sys = UNIFORM ? 0 : b;
@@ -595,18 +692,18 @@ bool sweep_maps(const PentaTables& f, int B, int n, const double* z, SweepMaps* 
   return true;
 }
 
-template <bool U, bool P, int M>
+template <bool U, bool P, int M, bool XC = false, bool XO = false>
 void launch_sweep_tma(const PentaTables& f, const SweepMaps& maps, int B, int n, double* z, double* y4,
-                      cudaStream_t s) {
-  auto kern = k_sweep_tma<U, P, M>;
+                      cudaStream_t s, const SweepFuse& fuse = SweepFuse{}) {
+  auto kern = k_sweep_tma<U, P, M, XC, XO>;
+  using SM = SweepSmem<U, XC>;
   static bool configured = false;
   if (!configured) {
-    SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(SweepSmem<U>::bytes)));
+    SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SM::bytes)));
     configured = true;
   }
   const int blocks = (B + 31) / 32;
-  kern<<<blocks, 64, SweepSmem<U>::bytes, s>>>(f, maps, B, n, z, y4);
+  kern<<<blocks, 64, SM::bytes, s>>>(f, maps, B, n, z, y4, fuse);
 }
 
 template <bool U, bool P, int M>
@@ -667,6 +764,31 @@ void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool
     else launch_sweep_t<false, true, 0>(f, B, n, z, y4, s);
   }
   check_launch("penta sweep kernel");
+}
+
+bool penta_sweep_fused(const PentaTables& f, int B, int n, double* z, double* y4, const double* const* Wc,
+                       const double* yc, double* zout, cudaStream_t s) {
+  // Uniform periodic operator only (the CH sweeps); y4 receives this sweep's
+  // Woodbury coefficients (MODE 1). Returns false when the TMA path cannot
+  // run (caller falls back to the unfused kernels).
+  if (!f.uniform) return false;
+  SweepMaps maps;
+  if (!sweep_maps(f, B, n, z, &maps)) return false;
+  SweepFuse fuse;
+  if (Wc) {
+    if (reinterpret_cast<uintptr_t>(yc) & 15) return false;
+    for (int k = 0; k < 4; ++k) {
+      fuse.Wc[k] = Wc[k];
+      if (!encode_map(&maps.yc[k], yc + static_cast<size_t>(k) * n, 1, n, 1, SW_RS, 1)) return false;
+    }
+  }
+  fuse.zout = zout;
+  if (Wc && zout) launch_sweep_tma<true, true, 1, true, true>(f, maps, B, n, z, y4, s, fuse);
+  else if (Wc) launch_sweep_tma<true, true, 1, true, false>(f, maps, B, n, z, y4, s, fuse);
+  else if (zout) launch_sweep_tma<true, true, 1, false, true>(f, maps, B, n, z, y4, s, fuse);
+  else launch_sweep_tma<true, true, 1>(f, maps, B, n, z, y4, s);
+  check_launch("penta fused sweep (TMA) kernel");
+  return true;
 }
 
 // ------------------------------------------------------------ PentaFactor
@@ -732,8 +854,11 @@ void DevicePenta::build(int B_, int n_, bool periodic_, bool uniform, const doub
   t.piv = piv;
   // For the uniform case the setup thread reads the bands of system 0 with
   // stride 1: pass the single-system bands.
-  k_periodic_setup<<<(nsys + 127) / 128, 128, 0, s>>>(t, B, n, e, c, a, b, W[0], W[1], W[2], W[3], cw, K,
-                                                    piv, dBad);
+  if (uniform)
+    k_periodic_setup_uniform<<<1, 4, 0, s>>>(t, n, e, c, a, b, W[0], W[1], W[2], W[3], cw, K, piv, dBad);
+  else
+    k_periodic_setup<<<(nsys + 127) / 128, 128, 0, s>>>(t, B, n, e, c, a, b, W[0], W[1], W[2], W[3], cw, K,
+                                                      piv, dBad);
   check_launch("penta periodic setup kernel");
   SG_CUDA(cudaMemcpyAsync(bad.data(), dBad, sizeof(int) * nsys, cudaMemcpyDeviceToHost, s));
   SG_CUDA(cudaStreamSynchronize(s));

@@ -48,6 +48,13 @@ struct DevicePenta {
 void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool periodic,
                  bool fusedCorrection, cudaStream_t s);
 
+// CH fusion (uniform periodic operator, MODE 1): Wc/yc apply a previous
+// sweep's Woodbury correction on load (Wc: 4 vectors of length B, yc: 4
+// vectors of length n); zout receives the backward results transposed
+// (zout[b*n + r]). Returns false if the fused TMA path is unavailable.
+bool penta_sweep_fused(const PentaTables& f, int B, int n, double* z, double* y4, const double* const* Wc,
+                       const double* yc, double* zout, cudaStream_t s);
+
 // lu4_solve, penta.cpp:61-70.
 __device__ __forceinline__ void lu4_solve_dev(const double* K, const int* piv, double* y) {
 #pragma unroll

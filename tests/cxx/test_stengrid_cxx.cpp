@@ -15,6 +15,7 @@
 
 #include "stengrid/cahn_hilliard.hpp"
 #include "stengrid/penta.hpp"
+#include "stengrid/snapshot.hpp"
 #include "stengrid/stencil.hpp"
 
 using namespace stengrid;
@@ -501,6 +502,27 @@ void test_diagnostics_and_run() {  // test_cahn_hilliard.cpp:320-366, 475-505
   CHECK(snaps == 3);
 }
 
+void test_snapshot_and_checkpoint() {  // test_io.cpp:26-93 + exact BDF2 resume
+  Grid2D g = random_grid(13, 7, 5);
+  const std::string path = "/tmp/stengrid_cxx_test.csg";
+  write_snapshot(g, path);
+  const Grid2D back = read_snapshot(path);
+  CHECK(grids_equal_bitwise(back, g) && back.dx == g.dx && back.dy == g.dy);
+  CHECK(format_diagnostics_row(Diagnostics{0.5, 1.25, 0.0}) == "0.5,1.25,0");
+  CHParams p = small_params(32, 16);
+  CHStepper a(p);
+  a.steps(7);
+  const std::string ck = "/tmp/stengrid_cxx_test.ck";
+  save_checkpoint(a, ck);
+  a.steps(9);
+  CHStepper b(p);
+  load_checkpoint(b, ck);
+  CHECK(b.step_index() == 7);
+  b.steps(9);
+  CHECK(grids_equal_bitwise(a.field(), b.field()));
+  CHECK(b.time() == a.time());
+}
+
 }  // namespace
 
 int main() {
@@ -515,6 +537,7 @@ int main() {
   test_penta();
   test_ch();
   test_diagnostics_and_run();
+  test_snapshot_and_checkpoint();
   std::printf("%d checks passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
