@@ -136,6 +136,13 @@ sg_status sg_stencil_launch(const sg_slab_desc* desc, sg_extents ext, sg_functio
                             const double* values, size_t count, sg_dtype dtype, const void* in,
                             void* out, void* stream);
 
+/* --------------------------------------------------------- WENO5 advection
+ * weno_advect (weno.cpp:50-94): out = -(u dphi/dx + v dphi/dy) with
+ * fifth-order WENO upwind derivatives on a periodic grid, bitwise identical
+ * to the reference. All four fields nx*ny row-major in `memory`; nx, ny >= 7. */
+sg_status sg_weno_advect(const double* phi, const double* u, const double* v, int nx, int ny, double dx,
+                         double dy, double* out, sg_memory memory, void* stream);
+
 /* ---------------------------------------------------- pentadiagonal batch
  * PentaFactor / PeriodicPentaFactor (penta.hpp:57-100, penta.cpp:93-295) on
  * the device. Bands are interleaved (r*B + b, penta.hpp:12-20), `memory`

@@ -181,6 +181,7 @@ class Reference:
         L.ref_write_snapshot.argtypes = [_dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_char_p]
         L.ref_read_snapshot.argtypes = [C.c_char_p, _ip, _ip, _dp, _dp, _dp, C.c_longlong]
         L.ref_write_diagnostics_csv.argtypes = [_dp, C.c_int, C.c_char_p]
+        L.ref_weno_advect.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _dp]
 
     def _check(self, rc):
         if rc != 0:
@@ -291,6 +292,13 @@ class Reference:
         self._check(self.lib.ref_read_snapshot(str(path).encode(), C.byref(nx), C.byref(ny), C.byref(dx),
                                                C.byref(dy), _d(buf), cap))
         return buf[: nx.value * ny.value].reshape(ny.value, nx.value).copy(), dx.value, dy.value
+
+    def weno_advect(self, phi, u, v, dx, dy, tiles=1, workers=1):
+        phi, u, v = _f64(phi), _f64(u), _f64(v)
+        ny, nx = phi.shape
+        out = np.empty_like(phi)
+        self._check(self.lib.ref_weno_advect(_d(phi), _d(u), _d(v), nx, ny, dx, dy, tiles, workers, _d(out)))
+        return out
 
     def write_diagnostics_csv(self, rows, path):
         r = _f64(np.asarray(rows, dtype=np.float64).reshape(-1, 3))

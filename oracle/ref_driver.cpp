@@ -25,6 +25,7 @@
 #include "stengrid/penta.hpp"
 #include "stengrid/snapshot.hpp"
 #include "stengrid/stencil.hpp"
+#include "stengrid/weno.hpp"
 
 #include <chrono>
 #include <cstring>
@@ -330,6 +331,19 @@ int ref_read_snapshot(const char* path, int* nx, int* ny, double* dx, double* dy
     *dx = g.dx;
     *dy = g.dy;
     if (out && cap >= g.size()) std::memcpy(out, g.data(), sizeof(double) * static_cast<std::size_t>(g.size()));
+  });
+}
+
+int ref_weno_advect(const double* phi, const double* u, const double* v, int nx, int ny, double dx, double dy,
+                    int tiles, int workers, double* out) {
+  return guarded([&] {
+    Grid2D f(nx, ny, dx, dy);
+    std::memcpy(f.data(), phi, sizeof(double) * static_cast<std::size_t>(f.size()));
+    VelocityField vel{Grid2D(nx, ny, dx, dy), Grid2D(nx, ny, dx, dy)};
+    std::memcpy(vel.u.data(), u, sizeof(double) * static_cast<std::size_t>(f.size()));
+    std::memcpy(vel.v.data(), v, sizeof(double) * static_cast<std::size_t>(f.size()));
+    const Grid2D o = weno_advect(f, vel, tiles, workers);
+    std::memcpy(out, o.data(), sizeof(double) * static_cast<std::size_t>(o.size()));
   });
 }
 

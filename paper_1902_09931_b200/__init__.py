@@ -21,7 +21,10 @@ from .cahn_hilliard import (CHParams, CHStepper, Diagnostics, RunSink, biharmoni
 from .snapshot import (format_diagnostics_row, load_checkpoint, read_snapshot, save_checkpoint,
                        write_diagnostics_csv, write_snapshot)
 
+from .weno import UpwindSide, VelocityField, upwind_side, weno_advect, weno_derivative_7
+
 __all__ = [
+    "UpwindSide", "VelocityField", "upwind_side", "weno_advect", "weno_derivative_7",
     "format_diagnostics_row", "load_checkpoint", "read_snapshot", "save_checkpoint",
     "write_diagnostics_csv", "write_snapshot",
     "Axis", "PentaBatch", "PentaFactor", "PeriodicPentaFactor", "RhsBatch",

@@ -448,6 +448,36 @@ int sg_plan_kernel_kind(sg_plan_t p) {
                                  p->buf[p->inIdx].dev, p->buf[1 - p->inIdx].dev);
 }
 
+sg_status sg_weno_advect(const double* phi, const double* u, const double* v, int nx, int ny, double dx,
+                         double dy, double* out, sg_memory memory, void* stream) {
+  return guard([&] {
+    // weno.cpp:51-53
+    if (nx < 7 || ny < 7) sg::invalid("weno_advect: need nx, ny >= 7");
+    if (!(dx > 0.0) || !(dy > 0.0)) sg::invalid("weno_advect: dx and dy must be > 0");
+    require_device();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t bytes = sizeof(double) * static_cast<size_t>(nx) * ny;
+    if (memory == SG_MEM_DEVICE) {
+      sg::launch_weno(phi, u, v, out, nx, ny, dx, dy, s);
+      if (!stream) SG_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    double* d = nullptr;
+    SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 4 * bytes, s));
+    double* dp = d;
+    double* du = d + static_cast<size_t>(nx) * ny;
+    double* dv = du + static_cast<size_t>(nx) * ny;
+    double* dout = dv + static_cast<size_t>(nx) * ny;
+    SG_CUDA(cudaMemcpyAsync(dp, phi, bytes, cudaMemcpyHostToDevice, s));
+    SG_CUDA(cudaMemcpyAsync(du, u, bytes, cudaMemcpyHostToDevice, s));
+    SG_CUDA(cudaMemcpyAsync(dv, v, bytes, cudaMemcpyHostToDevice, s));
+    sg::launch_weno(dp, du, dv, dout, nx, ny, dx, dy, s);
+    SG_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaFreeAsync(d, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 sg_status sg_stencil_launch(const sg_slab_desc* desc, sg_extents ext, sg_function fn,
                             const double* values, size_t count, sg_dtype dtype, const void* in,
                             void* out, void* stream) {

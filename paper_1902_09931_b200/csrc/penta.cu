@@ -525,9 +525,19 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
     const double* st = sw_smem + slot * SM::STAGE_PAD;
     const int r0 = g * RS;
     if (r0 + RS <= n) {
+      // all operands of the stage first (the compiler may not sink these
+      // loads into the dependency chain: shared-memory latency stays off it)
+      double zr[RS], f0[RS], f1[RS];
 #pragma unroll
       for (int k = 0; k < RS; ++k) {
-        const double yr = zin(st, k) - (fac(st, 0, k) * y2 + fac(st, 1, k) * y1);  // penta.cpp:180
+        zr[k] = zin(st, k);
+        f0[k] = fac(st, 0, k);
+        f1[k] = fac(st, 1, k);
+      }
+      asm volatile("" ::: "memory");
+#pragma unroll
+      for (int k = 0; k < RS; ++k) {
+        const double yr = zr[k] - (f0[k] * y2 + f1[k] * y1);  // penta.cpp:180
         if (active) *zp = yr;
         zp += step;
         y2 = y1;
@@ -588,10 +598,19 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
         s1 = yr;
       }
     } else if (r0 >= 2) {
-      // full stage above row 1: branch-free, walking pointer
+      // full stage above row 1: operands first, then the branch-free chain
+      double yv[RS], di[RS], ap[RS], bp[RS];
+#pragma unroll
+      for (int k = 0; k < RS; ++k) {
+        yv[k] = st[k * 32 + lane];
+        di[k] = fac(st, 0, k);
+        ap[k] = fac(st, 1, k);
+        bp[k] = fac(st, 2, k);
+      }
+      asm volatile("" ::: "memory");
 #pragma unroll
       for (int k = RS - 1; k >= 0; --k) {
-        const double yr = (st[k * 32 + lane] - fac(st, 1, k) * s1 - fac(st, 2, k) * s2) * fac(st, 0, k);
+        const double yr = (yv[k] - ap[k] * s1 - bp[k] * s2) * di[k];
         put(k, r0 + k, yr, zq);
         zq -= sB;
         s2 = s1;

@@ -47,6 +47,10 @@ int stencil_kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size
 bool function_shape(int fn, int* minW, int* minH, int* minCoe);
 const char* function_name(int fn);
 
+// WENO5 advection (weno.cu).
+void launch_weno(const double* phi, const double* u, const double* v, double* out, int nx, int ny, double dx,
+                 double dy, cudaStream_t s);
+
 // Diagnostics (diagnostics.cu).
 void device_simpson(const double* v, int nx, int ny, bool square, double* out, cudaStream_t s);
 double device_k1(const double* v, int nx, int ny, double dx, double dy, cudaStream_t s);

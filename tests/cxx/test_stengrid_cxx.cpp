@@ -17,6 +17,7 @@
 #include "stengrid/penta.hpp"
 #include "stengrid/snapshot.hpp"
 #include "stengrid/stencil.hpp"
+#include "stengrid/weno.hpp"
 
 using namespace stengrid;
 
@@ -523,6 +524,30 @@ void test_snapshot_and_checkpoint() {  // test_io.cpp:26-93 + exact BDF2 resume
   CHECK(b.time() == a.time());
 }
 
+void test_weno() {  // test_weno.cpp: constant field, shape errors
+  const int n = 64;
+  const double dx = kTwoPi / n;
+  Grid2D c(n, n, dx, dx);
+  c.values.setConstant(0.7);
+  VelocityField vel{Grid2D(n, n, dx, dx), Grid2D(n, n, dx, dx)};
+  vel.u.values.setConstant(1.0);
+  vel.v.values.setConstant(-0.5);
+  const Grid2D o = weno_advect(c, vel);
+  bool zero = true;
+  for (std::ptrdiff_t k = 0; k < o.size(); ++k) zero = zero && o.data()[k] == 0.0;
+  CHECK(zero);
+  Grid2D s(n, n, dx, dx);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) s(i, j) = std::sin(i * dx);
+  vel.v.values.setZero();
+  const Grid2D d = weno_advect(s, vel);
+  double err = 0.0;
+  for (int i = 0; i < n; ++i) err = std::max(err, std::abs(d(i, 3) + std::cos(i * dx)));
+  CHECK(err < 1e-5);
+  CHECK_THROWS_AS(weno_advect(Grid2D(6, 8, 1.0, 1.0), VelocityField{Grid2D(6, 8, 1.0, 1.0), Grid2D(6, 8, 1.0, 1.0)}),
+                  std::invalid_argument);
+}
+
 }  // namespace
 
 int main() {
@@ -538,6 +563,7 @@ int main() {
   test_ch();
   test_diagnostics_and_run();
   test_snapshot_and_checkpoint();
+  test_weno();
   std::printf("%d checks passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
