@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_sweep(const PentaTables f, in
 // (backward) dependent ops. Forward results go to z with coalesced stores
 // and come back through the same ring for the backward pass (a proxy fence
 // orders the generic stores before the async-proxy reads).
-constexpr int SW_RS = 16;   // rows per stage
+constexpr int SW_RS = 32;   // rows per stage
 constexpr int SW_NSTG = 4;  // stages in flight
 
 struct alignas(64) SweepMaps {
@@ -370,6 +370,17 @@ __device__ __forceinline__ void s_mbar_wait(uint64_t* bar, uint32_t phase) {
         : "r"(s_u32(bar)), "r"(phase)
         : "memory");
   } while (!ok);
+}
+// Non-blocking phase test: issued one stage ahead so its latency hides
+// behind the current stage's recurrence.
+__device__ __forceinline__ bool s_mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(s_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ void s_mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(bar)) : "memory");
@@ -519,9 +530,11 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
   // issue-bound: one warp per SM sub-partition, every instruction counts).
   double* zp = zc + RS * sB;
   const long long step = sB;
+  bool ready = false;  // stage g known complete (tested one stage early)
   for (int g = 1; g < nS; ++g) {
     const int slot = g % SW_NSTG;
-    s_mbar_wait(&full[slot], (g / SW_NSTG) & 1);
+    if (!ready) s_mbar_wait(&full[slot], (g / SW_NSTG) & 1);
+    ready = g + 1 < nS && s_mbar_test(&full[(g + 1) % SW_NSTG], ((g + 1) / SW_NSTG) & 1);
     const double* st = sw_smem + slot * SM::STAGE_PAD;
     const int r0 = g * RS;
     if (r0 + RS <= n) {
@@ -569,9 +582,11 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
       if (active && r >= 0) *zq = yr;
     }
   };
+  ready = false;
   for (int g = nS; g < total; ++g) {
     const int slot = g % SW_NSTG;
-    s_mbar_wait(&full[slot], (g / SW_NSTG) & 1);
+    if (!ready) s_mbar_wait(&full[slot], (g / SW_NSTG) & 1);
+    ready = g + 1 < total && s_mbar_test(&full[(g + 1) % SW_NSTG], ((g + 1) / SW_NSTG) & 1);
     const double* st = sw_smem + slot * SM::STAGE_PAD;
     const int r0 = n - (g - nS + 1) * RS;
     double* zq = zc + static_cast<long long>(r0 + RS - 1) * sB;
@@ -632,12 +647,14 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
     __syncwarp();
     if (lane == 0) s_mbar_arrive(&empty[slot]);
     if constexpr (XOUT) {
-      // tile [system][row] -> zout[(b0 + system) * n + r0 + k]: two systems
-      // per instruction, 16 consecutive rows (128 B) each
-      const int half = lane >> 4, k = lane & 15;
+      // tile [system][row] -> zout[(b0 + system) * n + r0 + k]: 32/RS
+      // systems per instruction, RS consecutive rows (8*RS bytes) each
+      static_assert(32 % RS == 0 || RS % 32 == 0, "XOUT flush layout");
+      constexpr int PER = RS >= 32 ? 1 : 32 / RS;
+      const int sub = RS >= 32 ? 0 : lane / RS, k = RS >= 32 ? lane : lane % RS;
 #pragma unroll 4
-      for (int pr = 0; pr < 32; pr += 2) {
-        const int sysl = pr + half;
+      for (int pr = 0; pr < 32; pr += PER) {
+        const int sysl = pr + sub;
         const int r = r0 + k;
         if (k < RS && r >= 0 && b0 + sysl < B)
           fuse.zout[static_cast<long long>(b0 + sysl) * n + r] = xt[sysl * XP + k];

@@ -109,6 +109,11 @@ class Grid2D:
         return g
 
 
+def _current_stream():
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
 def _dtype_code(dt) -> int:
     s = str(dt)
     if s.endswith("float64"):
@@ -159,6 +164,7 @@ class StencilPlan:
         self.ext = Extents()
         self._tiles = []
         self.num_workers = 1
+        self._device = False
 
     def valid(self) -> bool:
         return bool(self._h.value) and _lib.lib().sg_plan_valid(self._h) == 1
@@ -245,6 +251,7 @@ def create_plan(direction, mode, kind, input, output, num_tiles: int = 1, num_wo
                                     C.c_void_p(pin), C.c_void_p(pout), nxi, nyi, memory, num_tiles,
                                     num_workers, C.byref(plan._h)))
     plan._grids = [input, output]
+    plan._device = not host
     plan.direction, plan.mode, plan.ext = Direction(direction), BoundaryMode(mode), ext
     plan._tiles = make_tiles(nyi, num_tiles)
     plan.num_workers = num_workers
@@ -275,6 +282,9 @@ def compute(plan: StencilPlan, hint: Residency = Residency.Host, stream=None,
     if not plan.valid():
         raise LogicError("compute: plan was destroyed")
     s = getattr(stream, "cuda_stream", stream)
+    if s is None and plan._device:
+        # device grids (torch tensors): run in order with the caller's work
+        s = _current_stream()
     check(_lib.lib().sg_plan_compute(plan._h, int(hint), C.c_void_p(s or 0), int(bool(synchronize))))
 
 
@@ -293,6 +303,8 @@ def launch_slab(desc: dict, ext: Extents, kind, inp, out, stream=None) -> None:
     fid, vals = _kind_values(kind)
     d = SgSlabDesc(**desc)
     s = getattr(stream, "cuda_stream", stream)
+    if s is None:
+        s = _current_stream()
     vptr = vals.ctypes.data_as(C.POINTER(C.c_double)) if vals.size else None
     check(_lib.lib().sg_stencil_launch(C.byref(d), ext._c(), fid, vptr, vals.size,
                                        _dtype_code(inp.dtype), C.c_void_p(inp.data_ptr()),
