@@ -308,7 +308,7 @@ def ours_arm(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     sg._lib.check(sg._lib.lib().sg_init(local_rank))
     peak, peak_kind = measured_peak()
-    if world > 1:
+    if world > 1 or args.slab:
         from paper_1902_09931_b200 import slab
         return slab.bench_multi_gpu(args, rank, world, local_rank, METRIC, UNIT, WORKLOAD, peak, peak_kind)
 
@@ -364,6 +364,8 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-extra", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--slab", action="store_true",
+                    help="use the multi-GPU y-slab path even at N=1 (NCCL world of one)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -651,6 +651,15 @@ constexpr int prefetch_depth() {
   return d >= 8 ? 8 : d >= 4 ? 4 : 2;
 }
 
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
 // SG_STENCIL_KERNEL=reg selects the register-prefetch k_strip (kept for A/B
 // measurements); the default is the TMA-staged k_tma.
 bool use_tma() {
@@ -666,15 +675,27 @@ void launch_strip_lt(const KArgs<T>& a, dim3 grid, cudaStream_t s) {
   if (use_tma()) {
     using G = TmaGeom<T, L, L, TP, TP>;
     auto kern = k_tma<T, L, L, TP, TP, Op>;
-    static bool configured = false;  // per instantiation
-    if (!configured) {
+    static int ctasPerSm = 0;  // per instantiation
+    if (ctasPerSm == 0) {
       SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(G::smem_bytes)));
       SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      configured = true;
+      SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctasPerSm, kern, (TMA_WARPS + 1) * 32, G::smem_bytes));
+      if (ctasPerSm < 1) ctasPerSm = 1;
     }
-    dim3 g2((a.nx + G::CW - 1) / G::CW, grid.y);
-    kern<<<g2, (TMA_WARPS + 1) * 32, G::smem_bytes, s>>>(a);
+    // Row segments: one wave of CTAs when the grid is small (each CTA's
+    // pipeline start-up is then paid once), 512-row segments (several waves)
+    // when it is large.
+    const int gx = (a.nx + G::CW - 1) / G::CW;
+    const int rows = a.row1 - a.row0;
+    const long long cap = 1LL * sm_count() * ctasPerSm;
+    long long seg = (1LL * rows * gx + cap - 1) / cap;
+    seg = std::max<long long>(seg, std::min(rows, 2 * G::RPS));
+    seg = std::min<long long>(seg, 512);
+    KArgs<T> b = a;
+    b.segRows = static_cast<int>(seg);
+    dim3 g2(gx, static_cast<unsigned>((rows + seg - 1) / seg));
+    kern<<<g2, (TMA_WARPS + 1) * 32, G::smem_bytes, s>>>(b);
     return;
   }
   constexpr int D = prefetch_depth<T, L>();
@@ -701,14 +722,6 @@ void launch_strip(const KArgs<T>& a, const sg_extents& e, dim3 grid, cudaStream_
   invalid("internal: no strip kernel for these extents");
 }
 
-int sm_count() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
 
 template <typename T>
 int launch_typed(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,

@@ -214,7 +214,13 @@ def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak,
 
     from . import _lib
     from .stencil import Extents, FunctionStencil
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if not dist.is_initialized():
+        import os as _os
+        _os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        _os.environ.setdefault("MASTER_PORT", "29511")
+        _os.environ.setdefault("RANK", str(rank))
+        _os.environ.setdefault("WORLD_SIZE", str(world))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     nx = per = 32768
     ny = per * world
     slab = Slab(nx, ny, world, rank, 1, 1, True)
