@@ -69,6 +69,12 @@ class Clocks:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            # wait for the sampler's first line so the timed region is covered;
+            # samples taken before the region starts are dropped in summary()
+            t0 = time.time()
+            while time.time() - t0 < 5.0 and not self.path.read_text().strip():
+                time.sleep(0.02)
+            self.skip = len(self.path.read_text().splitlines())
         except Exception:
             self.proc = None
         return self
@@ -84,7 +90,7 @@ class Clocks:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.path.read_text().splitlines():
+        for line in self.path.read_text().splitlines()[getattr(self, "skip", 0):]:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -164,20 +170,28 @@ def cpu_reference_sample(target_s=12.0, rows=2048, reps=None, warmup=1):
 # --------------------------------------------------------------------- ours
 
 
-def time_plan_steps(sg, torch, plan, steps, stream):
-    """Run `steps` compute+swap steps on `stream`; per-launch CUDA events.
-    Returns (total_ms, [per-launch ms])."""
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+def time_plan_steps(sg, torch, plan, steps, stream, per_launch=False):
+    """Run `steps` compute+swap steps on `stream`, timed by CUDA events on
+    that stream. Returns (total_ms, [per-launch ms]). Each step is exactly
+    one kernel launch and nothing else runs on the stream, so the mean
+    launch duration is total/steps; per-launch events (per_launch=True)
+    measure the same thing but cost ~1 % (they break back-to-back launch
+    overlap), so the headline does not record them."""
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)] if per_launch else None
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(stream)
     for k in range(steps):
-        ev[k][0].record(stream)
+        if ev:
+            ev[k][0].record(stream)
         sg.compute(plan, stream=stream, synchronize=False)
-        ev[k][1].record(stream)
+        if ev:
+            ev[k][1].record(stream)
         sg.swap_plan(plan)
     end.record(stream)
     end.synchronize()
-    return start.elapsed_time(end), [a.elapsed_time(b) for a, b in ev]
+    total = start.elapsed_time(end)
+    return total, ([a.elapsed_time(b) for a, b in ev] if ev else [total / max(steps, 1)] * steps)
 
 
 def bench_device_stencil(sg, torch, dtype, nx, ny, steps, warmup, stream, fn="fn_weighted_3x3"):
@@ -310,7 +324,14 @@ def ours_arm(args, rank, world, local_rank):
     peak, peak_kind = measured_peak()
     if world > 1 or args.slab:
         from paper_1902_09931_b200 import slab
-        return slab.bench_multi_gpu(args, rank, world, local_rank, METRIC, UNIT, WORKLOAD, peak, peak_kind)
+        line = slab.bench_multi_gpu(args, rank, world, local_rank, METRIC, UNIT, WORKLOAD, peak, peak_kind, Clocks)
+        if line is not None:
+            if world == 1 and not args.skip_cpu:
+                cb = cpu_reference_sample(target_s=args.ref_seconds)
+                line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"],
+                                        "kind": cb["kind"], "sample": cb["sample"]}
+            print(json.dumps(line), flush=True)
+        return
 
     stream = torch.cuda.Stream()
     with Clocks(local_rank) as clk:
@@ -335,6 +356,8 @@ def ours_arm(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "k_tma<double,1,1,1,1,OpWeighted3x3>", "kernel_ms": kms,
+                     "kernel_timing": "CUDA events on the launching stream around the timed region "
+                                      "/ launches (one k_tma launch per step)",
                      "algorithmic_bytes_per_launch": alg_bytes},
         "clocks": clocks,
         "gpu_launches": int(launches),

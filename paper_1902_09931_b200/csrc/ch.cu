@@ -200,6 +200,163 @@ __global__ void __launch_bounds__(256) k_rhs(const double* __restrict__ cc, cons
 
 constexpr size_t kRhsSmem = (2 * RYE * (RXE + 1) + RY * (RX + 1)) * sizeof(double);
 
+// k_rhs_v: the production RHS kernel for nx a multiple of 64 (every CH grid
+// with nx >= 64; CHParams requires powers of two). Same output tile (64 i x
+// 32 j), restructured for bytes in flight and shared-memory bandwidth:
+//  * loads: every 16 B granule (2 columns) of C^n and C^{n-1} in the 68 x 36
+//    halo tile is fetched by exactly one thread with independent 16 B loads
+//    issued back to back (4 "own" granules per thread + <= 1 halo granule),
+//    and transformed on the way into shared memory: sb = 2c - p (Cbar) and
+//    sf = c^3 - c (the nonlinear window's per-point term, cahn_hilliard.cpp:
+//    36-47); d = c - p of the thread's own outputs stays in registers;
+//  * compute: each thread produces a 2-column x 4-row block. Input rows are
+//    streamed once (3 x 16 B shared loads per row) and every output row
+//    that a row touches accumulates its taps in the reference's row-major tap
+//    order, so each sum is the same sequence of operations as before;
+//  * store: the 4 consecutive j of one column are 32 B contiguous in rhsT
+//    (one full sector) — the transposed layout needs no staging pass.
+constexpr int VR = 4;  // output rows per thread
+constexpr int VG = RXE / 2;  // 16 B granules per tile row (34)
+
+template <bool NONLINEAR>
+__global__ void __launch_bounds__(256, 4) k_rhs_v(const double* __restrict__ cc, const double* __restrict__ cp,
+                                                  double* __restrict__ rhsT, const RhsGeom G,
+                                                  const __grid_constant__ RhsParams P) {
+  __shared__ __align__(16) double sb[RYE][RXE];
+  __shared__ __align__(16) double sf[NONLINEAR ? RYE : 1][RXE];
+  const int nx = G.nx;
+  const int i0 = blockIdx.x * RX, j0 = blockIdx.y * RY;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * 32 + tx;
+  auto in_row = [&](int y) {  // tile row y (0..RYE) -> input row
+    int j = j0 - HALO + y + G.inShift;
+    if (G.wrapY) return G.inRows >= RYE ? wrap_once(j, G.inRows) : wrapi(j, G.inRows);
+    return min(max(j, 0), G.inRows - 1);
+  };
+  auto put = [&](int y, int g, double2 c, double2 p) {
+    double2 b, f;
+    b.x = 2.0 * c.x - p.x;  // cahn_hilliard.cpp:273
+    b.y = 2.0 * c.y - p.y;
+    *reinterpret_cast<double2*>(&sb[y][2 * g]) = b;
+    if constexpr (NONLINEAR) {
+      f.x = c.x * c.x * c.x - c.x;
+      f.y = c.y * c.y * c.y - c.y;
+      *reinterpret_cast<double2*>(&sf[y][2 * g]) = f;
+    }
+  };
+  // ---- loads: 4 own granules (rows 2 + 4ty + r, granule tx + 1) + 1 halo
+  double2 oc[VR], op[VR], hc, hp;
+  int hy = 0, hg = 0;
+  const bool halo = tid < 2 * VG * 2 + 2 * RY;  // 136 edge-row + 64 edge-column granules
+#pragma unroll
+  for (int r = 0; r < VR; ++r) {
+    const long long idx = static_cast<long long>(in_row(HALO + VR * ty + r)) * nx + i0 + 2 * tx;
+    oc[r] = __ldg(reinterpret_cast<const double2*>(cc + idx));
+    op[r] = __ldg(reinterpret_cast<const double2*>(cp + idx));
+  }
+  if (halo) {
+    if (tid < 4 * VG) {
+      const int k = tid / VG;
+      hy = k < 2 ? k : RY + k;  // rows 0, 1, RY+2, RY+3
+      hg = tid - k * VG;
+    } else {
+      const int h = tid - 4 * VG;
+      hy = HALO + (h >> 1);
+      hg = (h & 1) ? VG - 1 : 0;
+    }
+    int i = i0 - HALO + 2 * hg;
+    i = i < 0 ? i + nx : (i >= nx ? i - nx : i);
+    const long long idx = static_cast<long long>(in_row(hy)) * nx + i;
+    hc = __ldg(reinterpret_cast<const double2*>(cc + idx));
+    hp = __ldg(reinterpret_cast<const double2*>(cp + idx));
+  }
+  double d[VR][2];
+#pragma unroll
+  for (int r = 0; r < VR; ++r) {
+    put(HALO + VR * ty + r, tx + 1, oc[r], op[r]);
+    d[r][0] = oc[r].x - op[r].x;
+    d[r][1] = oc[r].y - op[r].y;
+  }
+  if (halo) put(hy, hg, hc, hp);
+  __syncthreads();
+
+  // ---- compute: outputs (x0 + cx, y0 + r), cx < 2, r < 4
+  const int x0 = 2 * tx, y0 = VR * ty;
+  double bh[VR][2], nl[VR][2];
+#pragma unroll
+  for (int r = 0; r < VR; ++r) bh[r][0] = bh[r][1] = nl[r][0] = nl[r][1] = 0.0;
+#pragma unroll
+  for (int yy = 0; yy < VR + 4; ++yy) {  // Cbar rows y0 .. y0 + 7
+    double b[6];
+#pragma unroll
+    for (int g = 0; g < 3; ++g) {
+      const double2 v = *reinterpret_cast<const double2*>(&sb[y0 + yy][x0 + 2 * g]);
+      b[2 * g] = v.x;
+      b[2 * g + 1] = v.y;
+    }
+#pragma unroll
+    for (int r = 0; r < VR; ++r) {
+      const int q = yy - r;
+      if (q < 0 || q > 4) continue;
+#pragma unroll
+      for (int p = 0; p < 5; ++p) {
+        constexpr unsigned kMask = (1u << 2) | (1u << 6) | (1u << 7) | (1u << 8) | (1u << 10) | (1u << 11) |
+                                   (1u << 12) | (1u << 13) | (1u << 14) | (1u << 16) | (1u << 17) | (1u << 18) |
+                                   (1u << 22);  // SG_BIH_TAPS
+        if (!((kMask >> (q * 5 + p)) & 1u)) continue;
+        bh[r][0] += P.bw[q * 5 + p] * b[p];
+        bh[r][1] += P.bw[q * 5 + p] * b[p + 1];
+      }
+    }
+  }
+  if constexpr (NONLINEAR) {
+#pragma unroll
+    for (int yy = 0; yy < VR + 2; ++yy) {  // f rows y0 + 1 .. y0 + 6
+      double f[6];
+#pragma unroll
+      for (int g = 0; g < 3; ++g) {
+        const double2 v = *reinterpret_cast<const double2*>(&sf[y0 + 1 + yy][x0 + 2 * g]);
+        f[2 * g] = v.x;
+        f[2 * g + 1] = v.y;
+      }
+#pragma unroll
+      for (int r = 0; r < VR; ++r) {
+        const int q = yy - r;
+        if (q < 0 || q > 2) continue;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          constexpr unsigned kMask = (1u << 1) | (1u << 3) | (1u << 4) | (1u << 5) | (1u << 7);  // SG_NL_TAPS
+          if (!((kMask >> (q * 3 + p)) & 1u)) continue;
+          nl[r][0] += P.nl[q * 3 + p] * f[1 + p];
+          nl[r][1] += P.nl[q * 3 + p] * f[2 + p];
+        }
+      }
+    }
+  }
+  // ---- combine (cahn_hilliard.cpp:292/294) and store 4 consecutive j per column
+  const int jb = j0 + y0;
+#pragma unroll
+  for (int cx = 0; cx < 2; ++cx) {
+    double res[VR];
+#pragma unroll
+    for (int r = 0; r < VR; ++r) {
+      if constexpr (NONLINEAR)
+        res[r] = P.kDiff * d[r][cx] - P.kBih * bh[r][cx] + P.kNl * nl[r][cx];
+      else
+        res[r] = P.kDiff * d[r][cx] - P.kBih * bh[r][cx];
+    }
+    double* dst = rhsT + static_cast<long long>(i0 + x0 + cx) * G.outRows + jb;
+    if (jb + VR <= G.outRows && (G.outRows & 1) == 0) {
+      reinterpret_cast<double2*>(dst)[0] = make_double2(res[0], res[1]);
+      reinterpret_cast<double2*>(dst)[1] = make_double2(res[2], res[3]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < VR; ++r)
+        if (jb + r < G.outRows) dst[r] = res[r];
+    }
+  }
+}
+
 void launch_rhs(bool nonlinear, const double* cc, const double* cp, double* rhsT, const RhsGeom& g,
                 const RhsParams& rp, cudaStream_t s) {
   static bool configured = false;
@@ -209,6 +366,18 @@ void launch_rhs(bool nonlinear, const double* cc, const double* cp, double* rhsT
     configured = true;
   }
   dim3 tb(32, 8), tg((g.nx + RX - 1) / RX, (g.outRows + RY - 1) / RY);
+  static const bool legacy = [] {
+    const char* e = std::getenv("SG_CH_RHS");
+    return e && std::strcmp(e, "legacy") == 0;
+  }();
+  if (g.nx % RX == 0 && !legacy) {
+    if (nonlinear)
+      k_rhs_v<true><<<tg, tb, 0, s>>>(cc, cp, rhsT, g, rp);
+    else
+      k_rhs_v<false><<<tg, tb, 0, s>>>(cc, cp, rhsT, g, rp);
+    check_launch("ch rhs kernel");
+    return;
+  }
   if (nonlinear)
     k_rhs<true><<<tg, tb, kRhsSmem, s>>>(cc, cp, rhsT, g, rp);
   else
@@ -250,6 +419,62 @@ __global__ void __launch_bounds__(256) k_transpose_correct(const double* __restr
       w[static_cast<long long>(q) * own * nxq + static_cast<long long>(j) * nxq + c] = tile[tx][ty + 8 * k];
     }
   }
+}
+
+// Same operation on 64 x 64 tiles (nx, own multiples of 64): 512 B row
+// segments on both sides of the transpose (DRAM page locality), the four
+// y4 values of a thread's two j columns loaded once, 16 independent zT loads
+// per thread in flight.
+constexpr int TT = 64;
+__global__ void __launch_bounds__(256) k_transpose_correct_v(const double* __restrict__ zT,
+                                                             double* __restrict__ w, int nx, int own, int nxq,
+                                                             const CorrTables t) {
+  __shared__ double tile[TT][TT + 1];
+  const int i0 = blockIdx.x * TT, j0 = blockIdx.y * TT;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  double y4[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) y4[h][k] = __ldg(t.y4 + static_cast<long long>(k) * own + j0 + tx + 32 * h);
+  double z[TT / 8][2];
+#pragma unroll
+  for (int k = 0; k < TT / 8; ++k)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      z[k][h] = zT[static_cast<long long>(i0 + ty + 8 * k) * own + j0 + tx + 32 * h];
+#pragma unroll
+  for (int k = 0; k < TT / 8; ++k) {
+    const int i = i0 + ty + 8 * k;
+    const double w0 = __ldg(t.W[0] + i), w1 = __ldg(t.W[1] + i), w2 = __ldg(t.W[2] + i), w3 = __ldg(t.W[3] + i);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double corr = w0 * y4[h][0] + w1 * y4[h][1] + w2 * y4[h][2] + w3 * y4[h][3];
+      tile[ty + 8 * k][tx + 32 * h] = z[k][h] - corr;  // penta.cpp:283-284
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < TT / 8; ++k) {
+    const int j = j0 + ty + 8 * k;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = i0 + tx + 32 * h;
+      const int q = i / nxq, c = i - q * nxq;
+      w[static_cast<long long>(q) * own * nxq + static_cast<long long>(j) * nxq + c] = tile[tx + 32 * h][ty + 8 * k];
+    }
+  }
+}
+
+void launch_transpose_correct(const double* zT, double* w, int nx, int own, int nxq, const CorrTables& t,
+                              cudaStream_t s) {
+  if (nx % TT == 0 && own % TT == 0 && nxq % 32 == 0) {
+    k_transpose_correct_v<<<dim3(nx / TT, own / TT), dim3(32, 8), 0, s>>>(zT, w, nx, own, nxq, t);
+  } else {
+    k_transpose_correct<<<dim3((nx + TS - 1) / TS, (own + TS - 1) / TS), dim3(32, 8), 0, s>>>(zT, w, nx, own,
+                                                                                             nxq, t);
+  }
+  check_launch("ch transpose kernel");
 }
 
 // Single GPU: C^{n+1} = (2 C^n - C^{n-1}) + (w - (Wy0[j] y0[i] + ... + Wy3[j] y3[i])), over C^{n-1}.
@@ -319,13 +544,11 @@ static void k_init_slab_launch(unsigned long long seed, double amp, int nx, int 
 static void ch_phase_x(const sg_ch_params& p, const RhsParams& rp, const PentaTables& fx, int own, int nxq,
                 const double* cur, const double* prev, double* rhsT, double* y4x, double* send, cudaStream_t s) {
   const int nx = p.nx;
-  dim3 tb(32, 8), tg((nx + TS - 1) / TS, (own + TS - 1) / TS);
   const RhsGeom geom{nx, own, own + 2 * HALO, HALO, 0};
   launch_rhs(p.nonlinearEnabled, cur, prev, rhsT, geom, rp, s);
   penta_sweep(fx, own, nx, rhsT, y4x, true, true, s);
   CorrTables tx{{fx.W[0], fx.W[1], fx.W[2], fx.W[3]}, y4x};
-  k_transpose_correct<<<tg, tb, 0, s>>>(rhsT, send, nx, own, nxq, tx);
-  check_launch("ch slab transpose kernel");
+  launch_transpose_correct(rhsT, send, nx, own, nxq, tx, s);
 }
 
 static void ch_combine_packed(int nx, int own, int nxq, const double* cur, double* prev, const double* recv,
@@ -446,7 +669,6 @@ struct ChState {
     const int nx = p.nx, ny = p.ny;
     const double* cc = field[c];
     double* cp = field[1 - c];
-    dim3 tb(32, 8), tg((nx + TS - 1) / TS, (ny + TS - 1) / TS);
     const RhsGeom geom{nx, ny, ny, 0, 1};
     launch_rhs(p.nonlinearEnabled, cc, cp, rhsT, geom, rp, s);
     // x-sweep writes its (uncorrected) result straight into row-major w;
@@ -456,8 +678,7 @@ struct ChState {
     if (!fused) {
       penta_sweep(fx.t, ny, nx, rhsT, y4x, true, true, s);
       CorrTables tx{{fx.t.W[0], fx.t.W[1], fx.t.W[2], fx.t.W[3]}, y4x};
-      k_transpose_correct<<<tg, tb, 0, s>>>(rhsT, w, nx, ny, nx, tx);
-      check_launch("ch transpose kernel");
+      launch_transpose_correct(rhsT, w, nx, ny, nx, tx, s);
       penta_sweep(fy.t, nx, ny, w, y4y, true, true, s);
     }
     CorrTables ty{{fy.t.W[0], fy.t.W[1], fy.t.W[2], fy.t.W[3]}, y4y};

@@ -19,9 +19,7 @@ are bitwise invariant in the GPU count.
 """
 from __future__ import annotations
 
-import json
 import os
-import statistics
 import time
 from dataclasses import dataclass
 
@@ -204,10 +202,83 @@ class SlabStencil:
     def swap(self):
         self.a, self.b = self.b, self.a
 
+    def apply_host(self, hin, hout, chunks: int = 16):
+        """End-to-end application from/to pinned HOST memory: the own rows
+        are uploaded in `chunks` row blocks on a copy stream (first and last
+        block first, so the halo exchange can start early), each block's
+        interior output rows are computed as soon as the block below has
+        landed, and finished output blocks stream back on a second copy
+        stream while later blocks compute. Same kernels and arithmetic as
+        `apply` (bitwise equal); returns after the D2H copies complete."""
+        from .stencil import launch_slab
+        torch = self.torch
+        s = self.slab
+        own, top = s.own, s.top
+        lr = (self.ext.left, self.ext.right)
+        comp = torch.cuda.current_stream()
+        if not hasattr(self, "_h2d"):
+            self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        h2d, d2h = self._h2d, self._d2h
+        chunks = max(1, min(chunks, own))
+        bounds = [(own * c // chunks, own * (c + 1) // chunks) for c in range(chunks)]
+        order = [0, chunks - 1] + list(range(1, chunks - 1)) if chunks > 1 else [0]
+        landed = {}
+        h2d.wait_stream(comp)  # the previous step's readers of `a` are done
+        a_own, b_own = self.own_view(self.a), self.own_view(self.b)
+        for c in order:
+            r0, r1 = bounds[c]
+            with torch.cuda.stream(h2d):
+                a_own[r0:r1].copy_(hin[r0:r1], non_blocking=True)
+                landed[c] = torch.cuda.Event()
+                landed[c].record(h2d)
+        comp.wait_event(landed[0])
+        comp.wait_event(landed[chunks - 1])
+        if s.world == 1:
+            local_wrap_fill(s, self.a)
+            works = []
+        else:
+            ops = exchange_ops(s, self.a, self.dist)
+            works = self.dist.batch_isend_irecv(ops) if ops else []
+        ia, ib = s.interior_rows()
+        oa, ob = s.output_rows()
+        done = []
+        for c in range(chunks):
+            r0, r1 = bounds[c]
+            if c + 1 < chunks:
+                comp.wait_event(landed[c + 1])  # the window's bottom rows
+            lo, hi = max(r0, ia), min(r1, ib)
+            if lo < hi:
+                launch_slab(s.desc(lr, lo, hi), self.ext, self.kind, self.a, b_own, comp.cuda_stream)
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            done.append(ev)
+        for w in works:
+            w.wait()
+        edges = ((oa, ob),) if ia >= ib else ((oa, min(ia, ob)), (max(ib, oa), ob))
+        for lo, hi in edges:
+            if lo < hi:
+                launch_slab(s.desc(lr, lo, hi), self.ext, self.kind, self.a, b_own, comp.cuda_stream)
+        fin = torch.cuda.Event()
+        fin.record(comp)
+        # d2h is in-order: interior blocks first (each as soon as it is
+        # computed), the blocks holding halo-dependent rows last
+        edge = [bounds[c][0] < ia or bounds[c][1] > ib for c in range(chunks)]
+        with torch.cuda.stream(d2h):
+            for c in sorted(range(chunks), key=lambda c: edge[c]):
+                r0, r1 = bounds[c]
+                d2h.wait_event(fin if edge[c] else done[c])
+                hout[r0:r1].copy_(b_own[r0:r1], non_blocking=True)
+        d2h.synchronize()
 
-def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak, peak_kind):
+
+def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak, peak_kind, clocks_cls=None):
     """Weak scaling: every rank owns a 32768 x 32768 slab of a periodic
-    (world*32768) x 32768 grid; one step = halo exchange + application."""
+    (world*32768) x 32768 grid; one step = halo exchange + application.
+
+    Returns rank 0's JSON line (None elsewhere). Device time is CUDA events
+    on the compute stream, max over ranks; `e2e` adds, every step, the H2D
+    copy of the rank's slab from pinned host memory and the D2H copy of its
+    output rows (wall clock between barriers, max over ranks)."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -215,11 +286,10 @@ def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak,
     from . import _lib
     from .stencil import Extents, FunctionStencil
     if not dist.is_initialized():
-        import os as _os
-        _os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        _os.environ.setdefault("MASTER_PORT", "29511")
-        _os.environ.setdefault("RANK", str(rank))
-        _os.environ.setdefault("WORLD_SIZE", str(world))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     nx = per = 32768
     ny = per * world
@@ -229,12 +299,22 @@ def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak,
     g = torch.Generator(device="cuda").manual_seed(4 + rank)
     st.own_view(st.a).copy_(torch.rand((slab.own, nx), dtype=torch.float64, device="cuda", generator=g))
     stream = torch.cuda.current_stream()
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     for _ in range(args.warmup):
         st.apply(stream.cuda_stream)
         st.swap()
     torch.cuda.synchronize()
     dist.barrier()
+    torch.cuda.synchronize()
     l0 = _lib.launch_count()
+    clk = clocks_cls(local_rank) if (clocks_cls is not None and rank == 0) else None
+    if clk:
+        clk.__enter__()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
@@ -242,11 +322,29 @@ def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak,
         st.swap()
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    if clk:
+        clk.__exit__(None, None, None)
     launches = _lib.launch_count() - l0
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    dist.barrier()
+
+    e2e = None
+    e2e_steps = getattr(args, "e2e_steps", 3)
+    if not getattr(args, "skip_e2e", False) and e2e_steps > 0:
+        hin = torch.empty((slab.own, nx), dtype=torch.float64, pin_memory=True)
+        hout = torch.empty_like(hin, pin_memory=True)
+        hin.uniform_(-1, 1)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            st.apply_host(hin, hout)
+        dt = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": nx * ny * e2e_steps / dt / 1e9, "unit": unit,
+               "h2d_bytes_per_step": slab.own * nx * 8 * world, "d2h_bytes_per_step": slab.own * nx * 8 * world,
+               "steps": e2e_steps,
+               "path": "SlabStencil.apply_host on every rank: slab uploaded from / output downloaded to pinned host memory, row-chunk pipelined"}
+    line = None
     if rank == 0:
         value = nx * ny / (ms * 1e-3) / 1e9
         alg = nx * per * 16
@@ -260,5 +358,9 @@ def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak,
                              "frac": alg / (ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_kind": peak_kind,
                              "note": "per-GPU step time incl. halo exchange"},
                 "gpu_launches": int(launches)}
-        print(json.dumps(line), flush=True)
+        if clk:
+            line["clocks"] = clk.summary()
+        if e2e:
+            line["e2e"] = e2e
     dist.destroy_process_group()
+    return line
