@@ -29,6 +29,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "penta.cuh"
@@ -687,6 +688,338 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
   }
 }
 
+// ------------------------------------------------------------ k_sweep_res
+// Uniform-operator sweep with a RESIDENT TURN (the production path for the
+// CH sweeps and every uniform batch). Warp 0 runs the recurrence of 32
+// systems; warp 1 (one lane) owns ALL data movement, so the chain warp only
+// computes:
+//  * stages of RR_RS rows of z plus the five factor boxes stream in by
+//    tensor TMA into an RR_NSTG-slot ring (full mbarriers);
+//  * the consumer writes each result back into its slot (st.shared, constant
+//    offsets), fences it to the async proxy and arrives on the slot's `done`
+//    mbarrier; the producer then stores the slot with ONE tensor-TMA store
+//    (shared -> global) before it reuses the slot for a later load;
+//  * the last RR_NSTG forward stages are never stored: the backward pass
+//    starts on them straight from shared memory while the producer refetches
+//    the older stages (their stores completed: same thread, bulk wait_group),
+//    so the forward->backward round trip through memory leaves the chain;
+//  * operands are loaded RG rows ahead of the chain (software pipelined,
+//    pinned by compiler barriers), so shared-memory latency stays off it.
+// Arithmetic per row is penta.cpp:171-196 exactly, as in k_sweep_tma.
+constexpr int RR_RS = 64;    // rows per stage
+constexpr int RR_NSTG = 5;   // ring slots (= stages resident at the turn)
+constexpr int RR_FAC = RR_RS;  // doubles per uniform factor slot
+constexpr int RG = 8;        // rows per software-pipelined operand group
+constexpr int RR_STAGE = RR_RS * 32 + 5 * RR_FAC;  // doubles per slot
+static_assert((RR_STAGE * 8) % 128 == 0 && (RR_FAC * 8) % 128 == 0, "TMA destinations must be 128 B aligned");
+static_assert(RR_RS % RG == 0, "stage = whole operand groups");
+constexpr size_t RR_SMEM = static_cast<size_t>(RR_NSTG) * RR_STAGE * 8 + 2 * RR_NSTG * 8;
+
+__device__ __forceinline__ void s_tma_store_2d(const CUtensorMap* m, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(x), "r"(y), "r"(s_u32(src))
+               : "memory");
+}
+
+#ifdef SG_SWEEP_TRACE  // scripts/micro/sweep_trace.cu: per-stage clock64 of CTA 0's consumer
+__device__ long long g_sweep_trace[8192];
+#define SG_TRACE(i)                                                   \
+  do {                                                                \
+    if (blockIdx.x == 0 && lane == 0) g_sweep_trace[(i)] = clock64(); \
+  } while (0)
+#else
+#define SG_TRACE(i) \
+  do {              \
+  } while (0)
+#endif
+
+template <bool PERIODIC>
+__global__ void __launch_bounds__(64) k_sweep_res(const PentaTables f, const __grid_constant__ SweepMaps maps, int B,
+                                                  int n, double* __restrict__ y4) {
+  extern __shared__ __align__(128) double rr_smem[];
+  constexpr int RS = RR_RS, NST = RR_NSTG, FAC = RR_FAC, STG = RR_STAGE;
+  constexpr uint32_t TX = RS * 32 * 8 + 5 * RS * 8;  // bytes per stage load
+  uint64_t* full = reinterpret_cast<uint64_t*>(rr_smem + NST * STG);
+  uint64_t* done = full + NST;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b0 = blockIdx.x * 32;
+  const int nS = (n + RS - 1) / RS;
+  const int keep = nS < NST ? nS : NST;  // forward stages resident at the turn
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < NST; ++k) {
+      s_mbar_init(&full[k], 1);
+      s_mbar_init(&done[k], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  // forward uses of ring slot s. full[s] completes once per load into s;
+  // done[s] once per consumer use of s EXCEPT the resident forward stage
+  auto uses = [&](int s) { return s < nS ? (nS - s + NST - 1) / NST : 0; };
+
+  if (warp == 1) {
+    // ------------------------------------------------------------ producer
+    if (lane != 0) return;
+    auto load = [&](int s, int G) {
+      double* st = rr_smem + s * STG;
+      s_mbar_expect_tx(&full[s], TX);
+      s_tma_2d(st, &maps.z, b0, G * RS, &full[s]);
+      for (int k = 0; k < 5; ++k) s_tma_1d(st + RS * 32 + k * FAC, &maps.t[k], G * RS, &full[s]);
+    };
+    auto store = [&](int s, int G) {
+      s_tma_store_2d(&maps.z, b0, G * RS, rr_smem + s * STG);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    };
+    // forward: loading stage g reuses the slot of stage g - NST, which is
+    // stored first (it is never resident: g - NST < nS - NST)
+    for (int g = 0; g < nS; ++g) {
+      const int s = g % NST;
+      if (g >= NST) {
+        s_mbar_wait(&done[s], ((g / NST) + 1) & 1);
+        store(s, g - NST);
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      load(s, g);
+    }
+    // turn: every forward store has landed before those rows are refetched
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // backward stage h (rows of forward stage G = nS-1-h) reuses the slot of
+    // backward stage h - NST, which is stored first
+    for (int h = keep; h < nS; ++h) {
+      const int G = nS - 1 - h, s = G % NST;
+      s_mbar_wait(&done[s], (uses(s) + h / NST) & 1);
+      store(s, G + NST);
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      load(s, G);
+    }
+    // the last NST backward stages (or all, for short systems)
+    for (int h = nS - keep; h < nS; ++h) {
+      const int G = nS - 1 - h, s = G % NST;
+      s_mbar_wait(&done[s], (uses(s) + h / NST + 1) & 1);
+      store(s, G);
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    return;
+  }
+
+  // -------------------------------------------------------------- consumer
+  // Results go back with st.shared through asm WITHOUT a memory clobber (they
+  // never alias a pending operand load); `finish` makes the slot's writes
+  // visible to the async proxy and hands it to the producer.
+  auto put = [&](uint32_t base, int k, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(base + k * 256), "d"(v));
+  };
+  auto finish = [&](int s) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) s_mbar_arrive(&done[s]);
+  };
+  // ---- forward (penta.cpp:171-181)
+  double y2 = 0.0, y1 = 0.0;
+  bool ready = false;  // stage known complete (tested one stage early)
+  for (int g = 0; g < nS; ++g) {
+    const int s = g % NST;
+    SG_TRACE(3 * g);
+    if (!ready) s_mbar_wait(&full[s], (g / NST) & 1);
+    ready = g + 1 < nS && s_mbar_test(&full[(g + 1) % NST], ((g + 1) / NST) & 1);
+    SG_TRACE(3 * g + 1);
+    double* st = rr_smem + s * STG;
+    const uint32_t sb = s_u32(st) + lane * 8;
+    const double* m1 = st + RS * 32;
+    const double* m2 = m1 + FAC;
+    const int r0 = g * RS;
+    // groups of RG rows from group J0 on: the operands of group j+1 are
+    // loaded (and pinned there by the barrier) before group j's chain
+    auto groups = [&](auto j0) {
+      constexpr int J0 = decltype(j0)::value;
+      double zr[2][RG], f0[2][RG], f1[2][RG];
+#pragma unroll
+      for (int k = 0; k < RG; ++k) {
+        zr[J0 & 1][k] = st[(J0 * RG + k) * 32 + lane];
+        f0[J0 & 1][k] = m1[J0 * RG + k];
+        f1[J0 & 1][k] = m2[J0 * RG + k];
+      }
+#pragma unroll
+      for (int j = J0; j < RS / RG; ++j) {
+        const int c = j & 1;
+        if (j + 1 < RS / RG) {
+#pragma unroll
+          for (int k = 0; k < RG; ++k) {
+            const int kk = (j + 1) * RG + k;
+            zr[c ^ 1][k] = st[kk * 32 + lane];
+            f0[c ^ 1][k] = m1[kk];
+            f1[c ^ 1][k] = m2[kk];
+          }
+        }
+        asm volatile("" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < RG; ++k) {
+          const double yr = zr[c][k] - (f0[c][k] * y2 + f1[c][k] * y1);  // penta.cpp:180
+          put(sb, j * RG + k, yr);
+          y2 = y1;
+          y1 = yr;
+        }
+      }
+    };
+    if (r0 >= 2 && r0 + RS <= n) {
+      groups(std::integral_constant<int, 0>{});
+    } else if (r0 == 0 && RS <= n) {
+      // rows 0 and 1 are special (penta.cpp:173-175): first group scalar
+#pragma unroll
+      for (int k = 0; k < RG; ++k) {
+        const double zr = st[k * 32 + lane];
+        double yr;
+        if (k >= 2) yr = zr - (m1[k] * y2 + m2[k] * y1);
+        else if (k == 1) yr = zr - m2[k] * y1;  // y1 holds y[0]
+        else yr = zr;
+        put(sb, k, yr);
+        y2 = y1;
+        y1 = yr;
+      }
+      groups(std::integral_constant<int, 1>{});
+    } else {
+#pragma unroll 8
+      for (int k = 0; k < RS; ++k) {
+        const int r = r0 + k;
+        const double zr = st[k * 32 + lane];
+        double yr;
+        if (r >= 2) yr = zr - (m1[k] * y2 + m2[k] * y1);
+        else if (r == 1) yr = zr - m2[k] * y1;  // y1 holds y[0]
+        else yr = zr;
+        put(sb, k, yr);
+        y2 = y1;
+        y1 = yr;
+      }
+    }
+    SG_TRACE(3 * g + 2);
+    // resident stages (the last `keep`) stay with the consumer
+    if (g < nS - keep) finish(s);
+  }
+  __syncwarp();
+  // ---- backward (penta.cpp:183-196), resident stages first
+  double s1 = 0.0, s2 = 0.0, zn1 = 0.0, zn2 = 0.0, zz0 = 0.0, zz1 = 0.0;
+  ready = false;
+  for (int h = 0; h < nS; ++h) {
+    const int G = nS - 1 - h, s = G % NST;
+    SG_TRACE(3 * (nS + h));
+    if (h >= keep && !ready) s_mbar_wait(&full[s], (uses(s) + h / NST + 1) & 1);
+    if (h + 1 >= keep && h + 1 < nS) {
+      const int sn = (nS - 2 - h) % NST;
+      ready = s_mbar_test(&full[sn], (uses(sn) + (h + 1) / NST + 1) & 1);
+    }
+    SG_TRACE(3 * (nS + h) + 1);
+    double* st = rr_smem + s * STG;
+    const uint32_t sb = s_u32(st) + lane * 8;
+    const double* dI = st + RS * 32 + 2 * FAC;
+    const double* ap = dI + FAC;
+    const double* bp = ap + FAC;
+    const int r0 = G * RS;
+    // groups of RG rows from the top of the stage down (group J0 on),
+    // pipelined as in the forward pass
+    auto groups = [&](auto j0) {
+      constexpr int J0 = decltype(j0)::value;
+      double yv[2][RG], di[2][RG], fa[2][RG], fb[2][RG];
+#pragma unroll
+      for (int k = 0; k < RG; ++k) {
+        const int kk = RS - 1 - (J0 * RG + k);
+        yv[J0 & 1][k] = st[kk * 32 + lane];
+        di[J0 & 1][k] = dI[kk];
+        fa[J0 & 1][k] = ap[kk];
+        fb[J0 & 1][k] = bp[kk];
+      }
+#pragma unroll
+      for (int j = J0; j < RS / RG; ++j) {
+        const int c = j & 1;
+        if (j + 1 < RS / RG) {
+#pragma unroll
+          for (int k = 0; k < RG; ++k) {
+            const int kk = RS - 1 - ((j + 1) * RG + k);
+            yv[c ^ 1][k] = st[kk * 32 + lane];
+            di[c ^ 1][k] = dI[kk];
+            fa[c ^ 1][k] = ap[kk];
+            fb[c ^ 1][k] = bp[kk];
+          }
+        }
+        asm volatile("" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < RG; ++k) {
+          const double yr = (yv[c][k] - fa[c][k] * s1 - fb[c][k] * s2) * di[c][k];  // penta.cpp:193-195
+          put(sb, RS - 1 - (j * RG + k), yr);
+          s2 = s1;
+          s1 = yr;
+        }
+      }
+      if (r0 == 0) {  // rows 0 and 1 closed the chain: the Woodbury inputs
+        zz0 = s1;
+        zz1 = s2;
+      }
+    };
+    if (r0 + RS <= n - 2) {
+      groups(std::integral_constant<int, 0>{});
+    } else if (r0 + RS == n && n >= RG + 2) {
+      // rows n-1 and n-2 are special (penta.cpp:184-186): top group scalar
+#pragma unroll
+      for (int k = RS - 1; k >= RS - RG; --k) {
+        const double yv = st[k * 32 + lane];
+        double yr;
+        if (k == RS - 1) {
+          yr = yv * dI[k];
+          zn1 = yr;
+        } else if (k == RS - 2) {
+          yr = (yv - ap[k] * s1) * dI[k];
+          zn2 = yr;
+        } else {
+          yr = (yv - ap[k] * s1 - bp[k] * s2) * dI[k];
+        }
+        put(sb, k, yr);
+        s2 = s1;
+        s1 = yr;
+      }
+      groups(std::integral_constant<int, 1>{});
+    } else {
+#pragma unroll 8
+      for (int k = RS - 1; k >= 0; --k) {
+        const int r = r0 + k;
+        if (r >= n) continue;
+        const double yv = st[k * 32 + lane];
+        double yr;
+        if (r == n - 1) {
+          yr = yv * dI[k];
+          zn1 = yr;
+        } else if (r == n - 2) {
+          yr = (yv - ap[k] * s1) * dI[k];
+          zn2 = yr;
+        } else {
+          yr = (yv - ap[k] * s1 - bp[k] * s2) * dI[k];
+        }
+        if (r == 1) zz1 = yr;
+        if (r == 0) zz0 = yr;
+        put(sb, k, yr);
+        s2 = s1;
+        s1 = yr;
+      }
+    }
+    SG_TRACE(3 * (nS + h) + 2);
+    finish(s);
+  }
+  if constexpr (PERIODIC) {
+    const int b = b0 + lane;
+    if (b >= B) return;
+    const double* cw = f.cw;
+    double y[4];
+    y[0] = cw[0] * zn2 + cw[1] * zn1;
+    y[1] = cw[2] * zn1;
+    y[2] = cw[3] * zz0;
+    y[3] = cw[4] * zz0 + cw[5] * zz1;
+    lu4_solve_dev(f.K, f.piv, y);
+    const long long sB = B;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) y4[k * sB + b] = y[k];
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
@@ -713,16 +1046,16 @@ bool encode_map(CUtensorMap* m, const double* p, int rank, uint64_t d0, uint64_t
 
 // TMA path needs 16 B aligned rows (B even, aligned pointers) and a driver
 // tensor-map encoder; otherwise the register-prefetch k_sweep runs.
-bool sweep_maps(const PentaTables& f, int B, int n, const double* z, SweepMaps* maps) {
+bool sweep_maps(const PentaTables& f, int B, int n, const double* z, SweepMaps* maps, int rows = SW_RS) {
   if (B % 2 != 0 || (reinterpret_cast<uintptr_t>(z) & 15)) return false;
   if (std::getenv("SG_SWEEP_KERNEL") && std::strcmp(std::getenv("SG_SWEEP_KERNEL"), "reg") == 0) return false;
   std::memset(maps, 0, sizeof(*maps));
-  if (!encode_map(&maps->z, z, 2, B, n, 32, SW_RS)) return false;
+  if (!encode_map(&maps->z, z, 2, B, n, 32, rows)) return false;
   const double* t[5] = {f.m1, f.m2, f.dInv, f.ap, f.bp};
   for (int k = 0; k < 5; ++k) {
     if (reinterpret_cast<uintptr_t>(t[k]) & 15) return false;
-    const bool ok = f.uniform ? encode_map(&maps->t[k], t[k], 1, n, 1, SW_RS, 1)
-                              : encode_map(&maps->t[k], t[k], 2, B, n, 32, SW_RS);
+    const bool ok = f.uniform ? encode_map(&maps->t[k], t[k], 1, n, 1, rows, 1)
+                              : encode_map(&maps->t[k], t[k], 2, B, n, 32, rows);
     if (!ok) return false;
   }
   return true;
@@ -740,6 +1073,31 @@ void launch_sweep_tma(const PentaTables& f, const SweepMaps& maps, int B, int n,
   }
   const int blocks = (B + 31) / 32;
   kern<<<blocks, 64, SM::bytes, s>>>(f, maps, B, n, z, y4, fuse);
+}
+
+bool use_resident_sweep() {
+  static const bool v = [] {
+    const char* e = std::getenv("SG_SWEEP_KERNEL");
+    return !(e && std::strcmp(e, "tma") == 0);
+  }();
+  return v;
+}
+
+void launch_sweep_res(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
+                      cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    SG_CUDA(cudaFuncSetAttribute(k_sweep_res<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(RR_SMEM)));
+    SG_CUDA(cudaFuncSetAttribute(k_sweep_res<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(RR_SMEM)));
+    configured = true;
+  }
+  const int blocks = (B + 31) / 32;
+  if (periodic)
+    k_sweep_res<true><<<blocks, 64, RR_SMEM, s>>>(f, maps, B, n, y4);
+  else
+    k_sweep_res<false><<<blocks, 64, RR_SMEM, s>>>(f, maps, B, n, y4);
 }
 
 template <bool U, bool P, int M>
@@ -777,6 +1135,12 @@ void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool
     return;
   }
   SweepMaps maps;
+  if (f.uniform && (!periodic || fusedCorrection) && use_resident_sweep() &&
+      sweep_maps(f, B, n, z, &maps, RR_RS)) {
+    launch_sweep_res(periodic, f, maps, B, n, y4, s);
+    check_launch("penta sweep (TMA, resident turn) kernel");
+    return;
+  }
   if (sweep_maps(f, B, n, z, &maps)) {
     if (f.uniform) {
       if (!periodic) launch_sweep_tma<true, false, 0>(f, maps, B, n, z, y4, s);
