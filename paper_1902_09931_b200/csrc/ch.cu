@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(256) k_rhs(const double* __restrict__ cc, cons
   const int nx = G.nx;
   const int i0 = blockIdx.x * RX, j0 = blockIdx.y * RY;
   const int tid = threadIdx.y * 32 + threadIdx.x;
+  pdl_wait();
   for (int e = tid; e < RYE * RXE; e += 256) {
     const int y = e / RXE, x = e - y * RXE;
     int j = j0 - HALO + y + G.inShift;
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(256, 4) k_rhs_v(const double* __restrict__ cc,
   const int i0 = blockIdx.x * RX, j0 = blockIdx.y * RY;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
+  pdl_wait();
   auto in_row = [&](int y) {  // tile row y (0..RYE) -> input row
     int j = j0 - HALO + y + G.inShift;
     if (G.wrapY) return G.inRows >= RYE ? wrap_once(j, G.inRows) : wrapi(j, G.inRows);
@@ -358,7 +360,7 @@ __global__ void __launch_bounds__(256, 4) k_rhs_v(const double* __restrict__ cc,
 }
 
 void launch_rhs(bool nonlinear, const double* cc, const double* cp, double* rhsT, const RhsGeom& g,
-                const RhsParams& rp, cudaStream_t s) {
+                const RhsParams& rp, cudaStream_t s, bool pdl = false) {
   static bool configured = false;
   if (!configured) {
     SG_CUDA(cudaFuncSetAttribute(k_rhs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kRhsSmem)));
@@ -371,10 +373,7 @@ void launch_rhs(bool nonlinear, const double* cc, const double* cp, double* rhsT
     return e && std::strcmp(e, "legacy") == 0;
   }();
   if (g.nx % RX == 0 && !legacy) {
-    if (nonlinear)
-      k_rhs_v<true><<<tg, tb, 0, s>>>(cc, cp, rhsT, g, rp);
-    else
-      k_rhs_v<false><<<tg, tb, 0, s>>>(cc, cp, rhsT, g, rp);
+    launch_ex(nonlinear ? k_rhs_v<true> : k_rhs_v<false>, tg, tb, 0, s, pdl, cc, cp, rhsT, g, rp);
     check_launch("ch rhs kernel");
     return;
   }
@@ -399,6 +398,7 @@ __global__ void __launch_bounds__(256) k_transpose_correct(const double* __restr
   __shared__ double tile[TS][TS + 1];
   const int i0 = blockIdx.x * TS, j0 = blockIdx.y * TS;
   const int tx = threadIdx.x, ty = threadIdx.y;
+  pdl_wait();
 #pragma unroll
   for (int k = 0; k < TS / 8; ++k) {
     const int i = i0 + ty + 8 * k, j = j0 + tx;
@@ -432,6 +432,7 @@ __global__ void __launch_bounds__(256) k_transpose_correct_v(const double* __res
   __shared__ double tile[TT][TT + 1];
   const int i0 = blockIdx.x * TT, j0 = blockIdx.y * TT;
   const int tx = threadIdx.x, ty = threadIdx.y;
+  pdl_wait();
   double y4[2][4];
 #pragma unroll
   for (int h = 0; h < 2; ++h)
@@ -467,9 +468,9 @@ __global__ void __launch_bounds__(256) k_transpose_correct_v(const double* __res
 }
 
 void launch_transpose_correct(const double* zT, double* w, int nx, int own, int nxq, const CorrTables& t,
-                              cudaStream_t s) {
+                              cudaStream_t s, bool pdl = false) {
   if (nx % TT == 0 && own % TT == 0 && nxq % 32 == 0) {
-    k_transpose_correct_v<<<dim3(nx / TT, own / TT), dim3(32, 8), 0, s>>>(zT, w, nx, own, nxq, t);
+    launch_ex(k_transpose_correct_v, dim3(nx / TT, own / TT), dim3(32, 8), 0, s, pdl, zT, w, nx, own, nxq, t);
   } else {
     k_transpose_correct<<<dim3((nx + TS - 1) / TS, (own + TS - 1) / TS), dim3(32, 8), 0, s>>>(zT, w, nx, own,
                                                                                              nxq, t);
@@ -483,6 +484,7 @@ __global__ void __launch_bounds__(256) k_combine(const double* __restrict__ cc, 
                                                  const CorrTables t) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
+  pdl_wait();
   if (i >= nx) return;
   const long long idx = static_cast<long long>(j) * nx + i;
   const double v = w[idx] - (__ldg(t.W[0] + j) * __ldg(t.y4 + i) + __ldg(t.W[1] + j) * __ldg(t.y4 + nx + i) +
@@ -534,6 +536,14 @@ __global__ void k_fill_bands(double sigma, int n, double* e, double* c, double* 
 }
 
 }  // namespace
+
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("SG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 
 static void k_init_slab_launch(unsigned long long seed, double amp, int nx, int own, int r0, double* ext,
                         cudaStream_t s) {
@@ -670,19 +680,21 @@ struct ChState {
     const double* cc = field[c];
     double* cp = field[1 - c];
     const RhsGeom geom{nx, ny, ny, 0, 1};
-    launch_rhs(p.nonlinearEnabled, cc, cp, rhsT, geom, rp, s);
+    const bool pdl = pdl_enabled();
+    launch_rhs(p.nonlinearEnabled, cc, cp, rhsT, geom, rp, s, pdl);
     // x-sweep writes its (uncorrected) result straight into row-major w;
     // the y-sweep applies the x Woodbury correction as it loads w.
     const bool fused = !unfused() && penta_sweep_fused(fx.t, ny, nx, rhsT, y4x, nullptr, nullptr, w, s) &&
                        penta_sweep_fused(fy.t, nx, ny, w, y4y, fx.t.W, y4x, nullptr, s);
     if (!fused) {
-      penta_sweep(fx.t, ny, nx, rhsT, y4x, true, true, s);
+      penta_sweep(fx.t, ny, nx, rhsT, y4x, true, true, s, pdl);
       CorrTables tx{{fx.t.W[0], fx.t.W[1], fx.t.W[2], fx.t.W[3]}, y4x};
-      launch_transpose_correct(rhsT, w, nx, ny, nx, tx, s);
-      penta_sweep(fy.t, nx, ny, w, y4y, true, true, s);
+      launch_transpose_correct(rhsT, w, nx, ny, nx, tx, s, pdl);
+      penta_sweep(fy.t, nx, ny, w, y4y, true, true, s, pdl);
     }
     CorrTables ty{{fy.t.W[0], fy.t.W[1], fy.t.W[2], fy.t.W[3]}, y4y};
-    k_combine<<<dim3((nx + 255) / 256, ny), 256, 0, s>>>(cc, cp, w, nx, ny, ty);
+    launch_ex(k_combine, dim3((nx + 255) / 256, ny), dim3(256), 0, s, pdl, cc, cp, const_cast<const double*>(w), nx,
+              ny, ty);
     check_launch("ch combine kernel");
   }
 

@@ -755,6 +755,9 @@ __global__ void __launch_bounds__(64) k_sweep_res(const PentaTables f, const __g
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
+  // programmatic dependent launch: everything above touches only shared
+  // memory; z and y4 belong to the predecessor kernels
+  pdl_wait();
   // forward uses of ring slot s. full[s] completes once per load into s;
   // done[s] once per consumer use of s EXCEPT the resident forward stage
   auto uses = [&](int s) { return s < nS ? (nS - s + NST - 1) / NST : 0; };
@@ -1084,7 +1087,7 @@ bool use_resident_sweep() {
 }
 
 void launch_sweep_res(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool pdl) {
   static bool configured = false;
   if (!configured) {
     SG_CUDA(cudaFuncSetAttribute(k_sweep_res<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1094,10 +1097,8 @@ void launch_sweep_res(bool periodic, const PentaTables& f, const SweepMaps& maps
     configured = true;
   }
   const int blocks = (B + 31) / 32;
-  if (periodic)
-    k_sweep_res<true><<<blocks, 64, RR_SMEM, s>>>(f, maps, B, n, y4);
-  else
-    k_sweep_res<false><<<blocks, 64, RR_SMEM, s>>>(f, maps, B, n, y4);
+  launch_ex(periodic ? k_sweep_res<true> : k_sweep_res<false>, dim3(blocks), dim3(64), RR_SMEM, s, pdl, f, maps, B,
+            n, y4);
 }
 
 template <bool U, bool P, int M>
@@ -1126,7 +1127,7 @@ __global__ void __launch_bounds__(256) k_penta_correct(const PentaTables f, int 
 }  // namespace
 
 void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool periodic,
-                 bool fusedCorrection, cudaStream_t s) {
+                 bool fusedCorrection, cudaStream_t s, bool pdl) {
   if (periodic && !fusedCorrection && y4 != nullptr) {
     // recurrence with y handed over, then the correction as a parallel pass
     penta_sweep(f, B, n, z, y4, true, true, s);
@@ -1137,7 +1138,7 @@ void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool
   SweepMaps maps;
   if (f.uniform && (!periodic || fusedCorrection) && use_resident_sweep() &&
       sweep_maps(f, B, n, z, &maps, RR_RS)) {
-    launch_sweep_res(periodic, f, maps, B, n, y4, s);
+    launch_sweep_res(periodic, f, maps, B, n, y4, s, pdl);
     check_launch("penta sweep (TMA, resident turn) kernel");
     return;
   }

@@ -45,8 +45,10 @@ struct DevicePenta {
 
 // Forward/back substitution (+ periodic correction) of B interleaved systems
 // in z. fusedCorrection: skip z -= W y and write y (y4[k*B + b]) instead.
+// pdl: launch the resident-turn sweep as a programmatic dependent of the
+// previous kernel on `s` (the kernel waits before touching global memory).
 void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool periodic,
-                 bool fusedCorrection, cudaStream_t s);
+                 bool fusedCorrection, cudaStream_t s, bool pdl = false);
 
 // CH fusion (uniform periodic operator, MODE 1): Wc/yc apply a previous
 // sweep's Woodbury correction on load (Wc: 4 vectors of length B, yc: 4

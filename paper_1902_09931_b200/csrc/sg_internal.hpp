@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "stengrid/sg.h"
 
@@ -34,6 +35,36 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 inline void check_launch(const char* what) {
   count_launch();
   cuda_check(cudaGetLastError(), what);
+}
+
+// Programmatic dependent launch (PDL). A kernel launched with launch_ex(...,
+// pdl = true) may be scheduled before its stream predecessor has finished;
+// it must call pdl_wait() before its first global-memory access (read OR
+// write) — only shared-memory/mbarrier setup and kernel-parameter reads may
+// precede it. Kernels never trigger early (griddepcontrol.launch_dependents):
+// measured on B200 that made the CH step slower (the next kernel's waiting
+// CTAs crowd the running one) and, chained over five kernels, broke bitwise
+// parity; the implicit trigger at exit still hides the launch latency.
+// Without a programmatic dependency pdl_wait() is a no-op.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// SG_PDL=0 disables programmatic dependent launch (A/B measurements).
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+void launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+               Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cuda_check(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), "cudaLaunchKernelEx");
 }
 
 // Stencil launch (stencil.cu). `values` are the weights (fn == SG_FN_NONE) or
