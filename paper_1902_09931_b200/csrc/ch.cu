@@ -33,6 +33,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -216,13 +217,28 @@ constexpr size_t kRhsSmem = (2 * RYE * (RXE + 1) + RY * (RX + 1)) * sizeof(doubl
 //    order, so each sum is the same sequence of operations as before;
 //  * store: the 4 consecutive j of one column are 32 B contiguous in rhsT
 //    (one full sector) — the transposed layout needs no staging pass.
+struct CorrTables {
+  const double* W[4];
+  const double* y4;  // y4[k*B + b]
+};
+
 constexpr int VR = 4;  // output rows per thread
 constexpr int VG = RXE / 2;  // 16 B granules per tile row (34)
 
-template <bool NONLINEAR>
-__global__ void __launch_bounds__(256, 4) k_rhs_v(const double* __restrict__ cc, const double* __restrict__ cp,
-                                                  double* __restrict__ rhsT, const RhsGeom G,
-                                                  const __grid_constant__ RhsParams P) {
+//
+// FUSE (k_rhs_v<NL, true>, the steady-state single-GPU step): the PREVIOUS
+// step's combine is folded into the load. Inputs are C^n (cc), C^{n-1} (cp),
+// that step's y-sweep output w and its Woodbury coefficients (ty); every
+// loaded point first becomes C^{n+1} = (2C^n - C^{n-1}) + (w - W·y) — k_combine's
+// expression, term for term — which is written to cnew (own points only)
+// and then plays C^n's role in this step's RHS, with C^n as C^{n-1}.
+// 40 B/pt instead of k_combine's 32 + k_rhs_v's 24.
+template <bool NONLINEAR, bool FUSE>
+__global__ void __launch_bounds__(256, FUSE ? 2 : 4) k_rhs_v(const double* __restrict__ cc, const double* __restrict__ cp,
+                                                              double* __restrict__ rhsT, const RhsGeom G,
+                                                              const __grid_constant__ RhsParams P,
+                                                              const double* __restrict__ wv, const CorrTables cy,
+                                                              double* __restrict__ cnew) {
   __shared__ __align__(16) double sb[RYE][RXE];
   __shared__ __align__(16) double sf[NONLINEAR ? RYE : 1][RXE];
   const int nx = G.nx;
@@ -247,14 +263,16 @@ __global__ void __launch_bounds__(256, 4) k_rhs_v(const double* __restrict__ cc,
     }
   };
   // ---- loads: 4 own granules (rows 2 + 4ty + r, granule tx + 1) + 1 halo
-  double2 oc[VR], op[VR], hc, hp;
-  int hy = 0, hg = 0;
+  double2 oc[VR], op[VR], ow[VR], hc, hp, hw;
+  int hy = 0, hg = 0, hi = 0;
   const bool halo = tid < 2 * VG * 2 + 2 * RY;  // 136 edge-row + 64 edge-column granules
+  long long oidx[VR];
 #pragma unroll
   for (int r = 0; r < VR; ++r) {
-    const long long idx = static_cast<long long>(in_row(HALO + VR * ty + r)) * nx + i0 + 2 * tx;
-    oc[r] = __ldg(reinterpret_cast<const double2*>(cc + idx));
-    op[r] = __ldg(reinterpret_cast<const double2*>(cp + idx));
+    oidx[r] = static_cast<long long>(in_row(HALO + VR * ty + r)) * nx + i0 + 2 * tx;
+    oc[r] = __ldg(reinterpret_cast<const double2*>(cc + oidx[r]));
+    op[r] = __ldg(reinterpret_cast<const double2*>(cp + oidx[r]));
+    if constexpr (FUSE) ow[r] = __ldg(reinterpret_cast<const double2*>(wv + oidx[r]));
   }
   if (halo) {
     if (tid < 4 * VG) {
@@ -266,11 +284,40 @@ __global__ void __launch_bounds__(256, 4) k_rhs_v(const double* __restrict__ cc,
       hy = HALO + (h >> 1);
       hg = (h & 1) ? VG - 1 : 0;
     }
-    int i = i0 - HALO + 2 * hg;
-    i = i < 0 ? i + nx : (i >= nx ? i - nx : i);
-    const long long idx = static_cast<long long>(in_row(hy)) * nx + i;
+    hi = i0 - HALO + 2 * hg;
+    hi = hi < 0 ? hi + nx : (hi >= nx ? hi - nx : hi);
+    const long long idx = static_cast<long long>(in_row(hy)) * nx + hi;
     hc = __ldg(reinterpret_cast<const double2*>(cc + idx));
     hp = __ldg(reinterpret_cast<const double2*>(cp + idx));
+    if constexpr (FUSE) hw = __ldg(reinterpret_cast<const double2*>(wv + idx));
+  }
+  if constexpr (FUSE) {
+    // C^{n+1} at granule (row, columns i, i+1): k_combine's arithmetic
+    // (penta.cpp:283-284 correction, cahn_hilliard.cpp:273,320)
+    auto advance = [&](int row, int i, double2 c, double2 p, double2 w) {
+      const double W0 = __ldg(cy.W[0] + row), W1 = __ldg(cy.W[1] + row), W2 = __ldg(cy.W[2] + row),
+                   W3 = __ldg(cy.W[3] + row);
+      const double2 y0 = __ldg(reinterpret_cast<const double2*>(cy.y4 + i));
+      const double2 y1 = __ldg(reinterpret_cast<const double2*>(cy.y4 + nx + i));
+      const double2 y2 = __ldg(reinterpret_cast<const double2*>(cy.y4 + 2LL * nx + i));
+      const double2 y3 = __ldg(reinterpret_cast<const double2*>(cy.y4 + 3LL * nx + i));
+      double2 r;
+      r.x = (2.0 * c.x - p.x) + (w.x - (W0 * y0.x + W1 * y1.x + W2 * y2.x + W3 * y3.x));
+      r.y = (2.0 * c.y - p.y) + (w.y - (W0 * y0.y + W1 * y1.y + W2 * y2.y + W3 * y3.y));
+      return r;
+    };
+#pragma unroll
+    for (int r = 0; r < VR; ++r) {
+      const double2 cn = advance(in_row(HALO + VR * ty + r), i0 + 2 * tx, oc[r], op[r], ow[r]);
+      if (j0 + VR * ty + r < G.outRows) *reinterpret_cast<double2*>(cnew + oidx[r]) = cn;
+      op[r] = oc[r];  // this step's C^{n-1} is the loaded C^n
+      oc[r] = cn;
+    }
+    if (halo) {
+      const double2 cn = advance(in_row(hy), hi, hc, hp, hw);
+      hp = hc;
+      hc = cn;
+    }
   }
   double d[VR][2];
 #pragma unroll
@@ -359,6 +406,28 @@ __global__ void __launch_bounds__(256, 4) k_rhs_v(const double* __restrict__ cc,
   }
 }
 
+// SG_CH_RHS=legacy selects the scalar-load k_rhs (A/B); default k_rhs_v.
+// (A persistent cp.async-pipelined variant with one 117 KB CTA per SM was
+// measured 1.55x slower than k_rhs_v's two register-staged CTAs per SM at
+// 8192^2 and is not kept.)
+int rhs_kind() {
+  static const int v = [] {
+    const char* e = std::getenv("SG_CH_RHS");
+    return e && std::strcmp(e, "legacy") == 0 ? 0 : 1;
+  }();
+  return v;
+}
+
+// The steady-state step's first kernel: previous combine + this RHS (k_rhs_v
+// FUSE). Single GPU (full periodic grid), nx a multiple of 64.
+void launch_rhs_fused(bool nonlinear, const double* cc, const double* cp, const double* w, const CorrTables& ty,
+                      double* cnew, double* rhsT, const RhsGeom& g, const RhsParams& rp, cudaStream_t s, bool pdl) {
+  dim3 tb(32, 8), tg(g.nx / RX, (g.outRows + RY - 1) / RY);
+  launch_ex(nonlinear ? k_rhs_v<true, true> : k_rhs_v<false, true>, tg, tb, 0, s, pdl, cc, cp, rhsT, g, rp, w, ty,
+            cnew);
+  check_launch("ch fused combine+rhs kernel");
+}
+
 void launch_rhs(bool nonlinear, const double* cc, const double* cp, double* rhsT, const RhsGeom& g,
                 const RhsParams& rp, cudaStream_t s, bool pdl = false) {
   static bool configured = false;
@@ -368,12 +437,10 @@ void launch_rhs(bool nonlinear, const double* cc, const double* cp, double* rhsT
     configured = true;
   }
   dim3 tb(32, 8), tg((g.nx + RX - 1) / RX, (g.outRows + RY - 1) / RY);
-  static const bool legacy = [] {
-    const char* e = std::getenv("SG_CH_RHS");
-    return e && std::strcmp(e, "legacy") == 0;
-  }();
+  const bool legacy = rhs_kind() == 0;
   if (g.nx % RX == 0 && !legacy) {
-    launch_ex(nonlinear ? k_rhs_v<true> : k_rhs_v<false>, tg, tb, 0, s, pdl, cc, cp, rhsT, g, rp);
+    launch_ex(nonlinear ? k_rhs_v<true, false> : k_rhs_v<false, false>, tg, tb, 0, s, pdl, cc, cp, rhsT, g, rp,
+              static_cast<const double*>(nullptr), CorrTables{}, static_cast<double*>(nullptr));
     check_launch("ch rhs kernel");
     return;
   }
@@ -383,11 +450,6 @@ void launch_rhs(bool nonlinear, const double* cc, const double* cp, double* rhsT
     k_rhs<false><<<tg, tb, kRhsSmem, s>>>(cc, cp, rhsT, g, rp);
   check_launch("ch rhs kernel");
 }
-
-struct CorrTables {
-  const double* W[4];
-  const double* y4;  // y4[k*B + b]
-};
 
 // w(i,jl) = zT[i*own + jl] - (Wx0[i] y0[jl] + Wx1[i] y1[jl] + Wx2[i] y2[jl] + Wx3[i] y3[jl]),
 // stored PACKED for the all-to-all: block q = i / nxq holds own x nxq
@@ -600,12 +662,19 @@ struct ChState {
   sg_ch_params p{};
   int device = 0;
   cudaStream_t stream = nullptr;
-  double* field[2] = {nullptr, nullptr};  // ping-pong time levels
-  int curr = 0;                           // field[curr] = C^n, field[1-curr] = C^{n-1}
+  // Three time-level buffers: field[ic] = C^n, field[ip] = C^{n-1}, the third
+  // receives C^{n+1} in the fused steady-state step (its RHS kernel reads a
+  // halo around every point, so C^{n+1} cannot overwrite C^{n-1} in place).
+  double* field[3] = {nullptr, nullptr, nullptr};
+  int ic = 0, ip = 1;
   double *rhsT = nullptr, *w = nullptr, *y4x = nullptr, *y4y = nullptr;
   DevicePenta fx, fy;
   RhsParams rp{};
-  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  // CUDA graphs keyed by (kind, ic, ip): kind 0 = full step, 1 = head (step
+  // without its combine), 2 = steady (previous combine fused into this
+  // step's RHS), 3 = three steady steps (the buffer rotation closes), 4 =
+  // tail (the pending combine alone).
+  std::map<int, cudaGraphExec_t> graphs;
   int step = 0;
   std::vector<void*> allocs;
 
@@ -619,11 +688,14 @@ struct ChState {
   ~ChState() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    for (auto& g : graph)
-      if (g) cudaGraphExecDestroy(g);
+    for (auto& g : graphs) cudaGraphExecDestroy(g.second);
     for (void* q : allocs) cudaFree(q);
     if (stream) cudaStreamDestroy(stream);
   }
+
+  double* cur() const { return field[ic]; }
+  double* prev() const { return field[ip]; }
+  int spare() const { return 3 - ic - ip; }
 
   void build_factor(DevicePenta& f, double sigma, int n) {
     double* bands = dalloc(5 * static_cast<size_t>(n));
@@ -638,8 +710,7 @@ struct ChState {
     SG_CUDA(cudaGetDevice(&device));
     SG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     const size_t cnt = static_cast<size_t>(p.nx) * p.ny;
-    field[0] = dalloc(cnt);
-    field[1] = dalloc(cnt);
+    for (auto& f : field) f = dalloc(cnt);
     rhsT = dalloc(cnt);
     w = dalloc(cnt);
     y4x = dalloc(4 * static_cast<size_t>(p.ny));
@@ -669,19 +740,35 @@ struct ChState {
     k_init<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(p.seed, p.icAmplitude, n, field[0]);
     check_launch("ch init kernel");
     SG_CUDA(cudaMemcpyAsync(field[1], field[0], cnt * sizeof(double), cudaMemcpyDeviceToDevice, stream));
-    curr = 0;
+    ic = 0;
+    ip = 1;
     step = 0;
     SG_CUDA(cudaStreamSynchronize(stream));
   }
 
-  // One step with time levels (field[c], field[1-c]).
-  void enqueue_step(int c, cudaStream_t s) {
+  // The fused steady-state step needs the vectorised RHS kernel (nx a
+  // multiple of 64); SG_CH_STEADY=0 disables it (A/B measurements).
+  bool steady_ok() const {
+    static const bool off = [] {
+      const char* e = std::getenv("SG_CH_STEADY");
+      return e && e[0] == '0';
+    }();
+    return !off && p.nx % RX == 0 && rhs_kind() != 0 && unfused();
+  }
+
+  // RHS (or, steady, the fused previous combine + RHS writing C^{n+1} into
+  // field[in]), the two sweeps and the transpose/correct between them.
+  // Leaves the step's combine pending: C^{n+1} = 2C^n - C^{n-1} + (w - W·y4y).
+  void enqueue_solve(int c, int q, int in, cudaStream_t s) {
     const int nx = p.nx, ny = p.ny;
-    const double* cc = field[c];
-    double* cp = field[1 - c];
     const RhsGeom geom{nx, ny, ny, 0, 1};
     const bool pdl = pdl_enabled();
-    launch_rhs(p.nonlinearEnabled, cc, cp, rhsT, geom, rp, s, pdl);
+    if (in >= 0) {
+      CorrTables ty{{fy.t.W[0], fy.t.W[1], fy.t.W[2], fy.t.W[3]}, y4y};
+      launch_rhs_fused(p.nonlinearEnabled, field[c], field[q], w, ty, field[in], rhsT, geom, rp, s, pdl);
+    } else {
+      launch_rhs(p.nonlinearEnabled, field[c], field[q], rhsT, geom, rp, s, pdl);
+    }
     // x-sweep writes its (uncorrected) result straight into row-major w;
     // the y-sweep applies the x Woodbury correction as it loads w.
     const bool fused = !unfused() && penta_sweep_fused(fx.t, ny, nx, rhsT, y4x, nullptr, nullptr, w, s) &&
@@ -692,33 +779,90 @@ struct ChState {
       launch_transpose_correct(rhsT, w, nx, ny, nx, tx, s, pdl);
       penta_sweep(fy.t, nx, ny, w, y4y, true, true, s, pdl);
     }
+  }
+
+  // The pending combine: C^{n+1} written over C^{n-1} (field[q]) in place.
+  void enqueue_combine(int c, int q, cudaStream_t s) {
+    const int nx = p.nx, ny = p.ny;
     CorrTables ty{{fy.t.W[0], fy.t.W[1], fy.t.W[2], fy.t.W[3]}, y4y};
-    launch_ex(k_combine, dim3((nx + 255) / 256, ny), dim3(256), 0, s, pdl, cc, cp, const_cast<const double*>(w), nx,
-              ny, ty);
+    launch_ex(k_combine, dim3((nx + 255) / 256, ny), dim3(256), 0, s, pdl_enabled(),
+              static_cast<const double*>(field[c]), field[q], static_cast<const double*>(w), nx, ny, ty);
     check_launch("ch combine kernel");
   }
 
-  void capture() {
-    for (int c = 0; c < 2; ++c) {
-      cudaGraph_t g;
-      SG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-      const uint64_t before = g_launches.load();
-      enqueue_step(c, stream);
-      g_launches.store(before);  // captured, not launched
-      SG_CUDA(cudaStreamEndCapture(stream, &g));
-      SG_CUDA(cudaGraphInstantiate(&graph[c], g, 0));
-      SG_CUDA(cudaGraphDestroy(g));
+  cudaGraphExec_t graph(int kind, int c, int q) {
+    const int key = kind * 16 + c * 4 + q;
+    auto it = graphs.find(key);
+    if (it != graphs.end()) return it->second;
+    cudaGraph_t g;
+    SG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    const uint64_t before = g_launches.load();
+    switch (kind) {
+      case 0:
+        enqueue_solve(c, q, -1, stream);
+        enqueue_combine(c, q, stream);
+        break;
+      case 1:
+        enqueue_solve(c, q, -1, stream);
+        break;
+      case 2:
+        enqueue_solve(c, q, 3 - c - q, stream);
+        break;
+      case 3:
+        for (int k = 0, a = c, b = q; k < 3; ++k) {
+          const int n = 3 - a - b;
+          enqueue_solve(a, b, n, stream);
+          b = a;
+          a = n;
+        }
+        break;
+      default:
+        enqueue_combine(c, q, stream);
     }
+    g_launches.store(before);  // captured, not launched
+    SG_CUDA(cudaStreamEndCapture(stream, &g));
+    cudaGraphExec_t e;
+    SG_CUDA(cudaGraphInstantiate(&e, g, 0));
+    SG_CUDA(cudaGraphDestroy(g));
+    graphs[key] = e;
+    return e;
   }
 
+  void launch(int kind, int kernels) {
+    SG_CUDA(cudaGraphLaunch(graph(kind, ic, ip), stream));
+    count_launch(kernels);
+  }
+
+  // `steps` steps; the state (field[ic], field[ip]) is complete on return.
+  // Steady state (nx % 64 == 0, steps >= 2): head, then steps-1 fused
+  // steps (each applies the previous combine inside its RHS kernel), then
+  // the last combine alone — one kernel fewer per step.
   void run(int steps) {
-    if (!graph[0]) capture();
-    for (int k = 0; k < steps; ++k) {
-      SG_CUDA(cudaGraphLaunch(graph[curr], stream));
-      count_launch(5);
-      curr = 1 - curr;  // C^{n+1} was written over C^{n-1}
-      ++step;
+    if (steps <= 0) return;
+    const int solveK = unfused() ? 4 : 3;
+    if (steps == 1 || !steady_ok()) {
+      for (int k = 0; k < steps; ++k) {
+        launch(0, solveK + 1);
+        std::swap(ic, ip);  // C^{n+1} was written over C^{n-1}
+        ++step;
+      }
+      return;
     }
+    launch(1, solveK);
+    int left = steps - 1;
+    while (left >= 3) {
+      launch(3, 3 * solveK);
+      left -= 3;  // three rotations of (ic, ip, spare) restore it
+    }
+    for (; left > 0; --left) {
+      launch(2, solveK);
+      const int n = spare();
+      ip = ic;
+      ic = n;
+    }
+    launch(4, 1);
+    std::swap(ic, ip);
+    step += steps;
   }
 };
 
@@ -877,7 +1021,8 @@ sg_status sg_ch_set_state(sg_ch_t ch, const double* curr, const double* prev, sg
     SG_CUDA(cudaSetDevice(s.device));
     const size_t bytes = static_cast<size_t>(s.p.nx) * s.p.ny * sizeof(double);
     const cudaMemcpyKind k = memory == SG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    s.curr = 0;
+    s.ic = 0;
+    s.ip = 1;
     SG_CUDA(cudaMemcpyAsync(s.field[0], curr, bytes, k, s.stream));
     SG_CUDA(cudaMemcpyAsync(s.field[1], prev, bytes, k, s.stream));
     SG_CUDA(cudaStreamSynchronize(s.stream));
@@ -891,7 +1036,7 @@ sg_status sg_ch_get_field(sg_ch_t ch, int which, double* out, sg_memory memory) 
     auto& s = *ch->st;
     SG_CUDA(cudaSetDevice(s.device));
     const size_t bytes = static_cast<size_t>(s.p.nx) * s.p.ny * sizeof(double);
-    const double* src = s.field[which == 0 ? s.curr : 1 - s.curr];
+    const double* src = which == 0 ? s.cur() : s.prev();
     SG_CUDA(cudaMemcpyAsync(out, src, bytes, memory == SG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                             s.stream));
     SG_CUDA(cudaStreamSynchronize(s.stream));
@@ -903,7 +1048,7 @@ sg_status sg_ch_device_field(sg_ch_t ch, int which, const double** dptr) {
     if (!ch) sg::logic("CHStepper: destroyed");
     auto& s = *ch->st;
     SG_CUDA(cudaStreamSynchronize(s.stream));
-    *dptr = s.field[which == 0 ? s.curr : 1 - s.curr];
+    *dptr = which == 0 ? s.cur() : s.prev();
   });
 }
 
@@ -921,7 +1066,7 @@ sg_status sg_ch_diagnostics(sg_ch_t ch, double* t, double* s, double* k1Inv) {
     auto& st = *ch->st;
     SG_CUDA(cudaSetDevice(st.device));
     SG_CUDA(cudaStreamSynchronize(st.stream));
-    const double* f = st.field[st.curr];
+    const double* f = st.cur();
     const double dx = st.p.lx / st.p.nx, dy = st.p.ly / st.p.ny;
     if (t) *t = static_cast<double>(st.step) * st.p.dt;
     double m2 = 0.0;

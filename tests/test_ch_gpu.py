@@ -175,3 +175,21 @@ def test_fused_sweep_variant_bitwise(orc):
     c0 = orc.ch_initial_condition(64, 128)
     want, _ = orc.ch_run(p, 12, c0, c0)
     assert bits_equal(got, want)
+
+
+@pytest.mark.parametrize("nx,ny,nonlinear", [(64, 64, True), (128, 64, True), (64, 256, False)])
+def test_steady_state_step_many_bitwise(sg, orc, nx, ny, nonlinear):
+    """step_many(k) runs the steady-state schedule (head, fused combine+RHS
+    steps in threes and singles, tail combine) for nx % 64 == 0; every split
+    of the same step count must give the reference's bits, both time levels."""
+    p = params(sg, nx, ny, seed=5, nonlinearEnabled=nonlinear)
+    c0 = orc.ch_initial_condition(nx, ny, seed=5)
+    st = sg.CHStepper(p)
+    done = 0
+    for k in (1, 2, 3, 4, 5, 7):
+        st.step_many(k)
+        done += k
+        want_c, want_p = orc.ch_run(oracle_dict(p), done, c0, c0)
+        assert bits_equal(st.field().values, want_c), (k, done)
+        assert bits_equal(st.previous_field().values, want_p), (k, done)
+        assert st.step_index() == done
