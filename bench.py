@@ -205,6 +205,7 @@ def bench_device_stencil(sg, torch, dtype, nx, ny, steps, warmup, stream, fn="fn
     w = list(np.random.default_rng(4).uniform(-1, 1, 9))
     plan = sg.create_plan(sg.Direction.XY, sg.BoundaryMode.Periodic,
                           sg.FunctionStencil(sg.Extents(1, 1, 1, 1), fn, w), a, b, 1, 1)
+    stream.wait_stream(torch.cuda.current_stream())  # the input is generated there
     with torch.cuda.stream(stream):
         time_plan_steps(sg, torch, plan, warmup, stream)
         torch.cuda.synchronize()
@@ -301,6 +302,7 @@ def extras(sg, torch, stream, peak):
     plan = sg.create_plan(sg.Direction.X, sg.BoundaryMode.NonPeriodic,
                           sg.WeightStencil(sg.Extents(2, 2, 0, 0), [s4, -4 * s4, 6 * s4, -4 * s4, s4]), a, b, 1, 1)
     ts = []
+    stream.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(stream):
         for k in range(23):
             flush.zero_()
@@ -357,7 +359,31 @@ def bench_ch(sg, torch, n=1024, steps=1000):
     st.synchronize()
     dt = time.perf_counter() - t0
     out = {"cfg3_ch_1024sq_steps_s": steps / dt, "cfg3_ch_1024sq_1000steps_s": dt}
+    # end to end through the public API: host initial state uploaded
+    # (set_state), 1000 steps, field read back to the host
+    import numpy as np
+    from paper_1902_09931_b200.stencil import Grid2D
+    c0 = Grid2D.from_array(np.random.default_rng(1).uniform(-0.1, 0.1, (n, n)))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st.set_state(c0, c0)
+    st.step_many(steps)
+    host = st.field().values
+    e2e = time.perf_counter() - t0
+    out["cfg3_ch_1024sq_e2e_1000steps_s"] = e2e
+    out["cfg3_ch_1024sq_e2e_bytes"] = {"h2d": 2 * n * n * 8, "d2h": int(host.nbytes)}
     del st
+    # the reference CHStepper (oracle/_ref) on this host's cores, 5 timed steps
+    try:
+        from oracle.oracle import Reference
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        pr = dict(D=p.D, gamma=p.gamma, lx=p.lx, ly=p.ly, dt=p.dt, T=p.T, nx=n, ny=n, seed=1, amp=0.1,
+                  nonlinear=True)
+        secs = Reference().ch_timed(pr, 5, warmup=1, tiles=cores, workers=cores)
+        out["cfg3_ch_1024sq_reference_steps_s"] = {"value": 5 / secs, "cores": cores,
+                                                   "kind": "reference (oracle/_ref CHStepper::step)"}
+    except Exception as e:  # reported context only
+        out["cfg3_ch_1024sq_reference_steps_s"] = {"error": repr(e)}
     # Config 5's grid (8192^2) on ONE GPU: the single-device stepper, 40 steps.
     p = sg.CHParams(nx=8192, ny=8192)
     p.dt = 0.1 * p.dx()

@@ -97,8 +97,10 @@ sg_status sg_plan_create(sg_direction dir, sg_boundary mode, sg_extents ext, sg_
  * authoritative — the input is uploaded, the output downloaded. DEVICE
  * residency: the input is uploaded only if its device copy is stale, the
  * output stays on the device until sg_plan_sync_to_host. `stream` is a
- * cudaStream_t (NULL = the plan's own stream); `synchronize` != 0 blocks
- * until the result is complete (the reference's compute is synchronous). */
+ * cudaStream_t (NULL = the plan's own stream, a blocking stream: it is
+ * ordered after work queued on the legacy default stream, so device inputs
+ * produced there are complete); `synchronize` != 0 blocks until the result
+ * is complete (the reference's compute is synchronous). */
 sg_status sg_plan_compute(sg_plan_t plan, sg_residency residency, void* stream, int synchronize);
 /* swap_plan (stencil.cpp:197-200): exchange input and output bindings. */
 sg_status sg_plan_swap(sg_plan_t plan);

@@ -220,7 +220,9 @@ sg_status sg_plan_create(sg_direction dir, sg_boundary mode, sg_extents ext, sg_
     p->tiles = std::move(tiles);
     try {
       SG_CUDA(cudaGetDevice(&p->device));
-      SG_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+      // a BLOCKING stream: ordered after work the caller queued on the legacy
+      // default stream (e.g. torch kernels producing device inputs)
+      SG_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamDefault));
       void* ptrs[2] = {in, out};
       for (int k = 0; k < 2; ++k) {
         auto& b = p->buf[k];

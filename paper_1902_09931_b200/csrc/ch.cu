@@ -708,7 +708,9 @@ struct ChState {
 
   void init() {
     SG_CUDA(cudaGetDevice(&device));
-    SG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    // a BLOCKING stream: ordered after work the caller queued on the legacy
+    // default stream (e.g. torch kernels producing device inputs)
+    SG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamDefault));
     const size_t cnt = static_cast<size_t>(p.nx) * p.ny;
     for (auto& f : field) f = dalloc(cnt);
     rhsT = dalloc(cnt);
@@ -904,7 +906,9 @@ struct ChDist {
   }
   void init() {
     SG_CUDA(cudaGetDevice(&device));
-    SG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    // a BLOCKING stream: ordered after work the caller queued on the legacy
+    // default stream (e.g. torch kernels producing device inputs)
+    SG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamDefault));
     own = p.ny / world;
     nxq = p.nx / world;
     r0 = rank * own;
@@ -1113,7 +1117,9 @@ sg_status sg_penta_create(int batchCount, int n, int periodic, const double* e, 
     require_device2();
     auto h = std::make_unique<sg_penta_s>();
     SG_CUDA(cudaGetDevice(&h->device));
-    SG_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    // a BLOCKING stream: ordered after work the caller queued on the legacy
+    // default stream (e.g. torch kernels producing device inputs)
+    SG_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamDefault));
     h->f = std::make_unique<sg::DevicePenta>();
     const size_t len = static_cast<size_t>(batchCount) * n;
     const double* bands[5] = {e, c, d, a, b};

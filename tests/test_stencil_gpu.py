@@ -459,3 +459,55 @@ def test_large_grid_checksum_and_shift_property(sg, orc):
     sg.compute(p1)
     sg.compute(p2)
     assert torch.equal(torch.roll(o1, shifts=(123, -777), dims=(0, 1)), o2)
+
+
+def test_config4_full_size_sampled_rows_bitwise(sg, orc):
+    """BASELINE config 4 at its full size (32768^2 FP64, 8 GiB per field):
+    sampled rows — the wrap rows 0 and ny-1, and random interior rows — are
+    bitwise equal to the oracle."""
+    import torch
+    n = 32768
+    rng = np.random.default_rng(44)
+    w = list(rng.uniform(-1, 1, 9))
+    g = torch.Generator(device="cuda").manual_seed(44)
+    a = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g).mul_(2).sub_(1)
+    b = torch.empty_like(a)
+    kind = sg.FunctionStencil(sg.Extents(1, 1, 1, 1), "fn_weighted_3x3", w)
+    plan = sg.create_plan(sg.Direction.XY, sg.BoundaryMode.Periodic, kind, a, b, 1, 1)
+    sg.compute(plan)
+    rows = [0, 1, 511, 512, n // 2, n - 2, n - 1] + list(rng.integers(0, n, 5))
+    idx = sorted({(j + d) % n for j in rows for d in (-1, 0, 1)})
+    host = {j: a[j].cpu().numpy() for j in idx}
+    for j in rows:
+        band = np.stack([host[(j - 1) % n], host[j], host[(j + 1) % n]])
+        want = orc.stencil(band, (1, 1, 1, 1), w, fn="fn_weighted_3x3")[1]
+        assert bits_equal(b[j].cpu().numpy(), want), j
+    sg.destroy_plan(plan)
+    del a, b
+    torch.cuda.empty_cache()
+
+
+def test_beyond_int32_element_count_fp32(sg, orc):
+    """More than 2^31 points in one grid (32768 x 65600 FP32, 8.6 GB per
+    field): 64-bit indexing — rows past element 2^31 match the FP64 oracle
+    on the float inputs within the FP32 bar (1e-5 relative)."""
+    import torch
+    nx, ny = 32768, 65600
+    assert nx * ny > 2 ** 31
+    rng = np.random.default_rng(45)
+    w = list(rng.uniform(-1, 1, 9))
+    g = torch.Generator(device="cuda").manual_seed(45)
+    a = torch.rand((ny, nx), dtype=torch.float32, device="cuda", generator=g).mul_(2).sub_(1)
+    b = torch.empty_like(a)
+    plan = sg.create_plan(sg.Direction.XY, sg.BoundaryMode.Periodic,
+                          sg.WeightStencil(sg.Extents(1, 1, 1, 1), w), a, b, 1, 1)
+    sg.compute(plan)
+    rows = [0, 65535, 65536, ny - 2, ny - 1]
+    for j in rows:
+        band = np.stack([a[(j + d) % ny].cpu().numpy().astype(np.float64) for d in (-1, 0, 1)])
+        want = orc.stencil(band, (1, 1, 1, 1), w)[1]
+        got = b[j].cpu().numpy().astype(np.float64)
+        assert np.max(np.abs(got - want)) <= 1e-5 * np.max(np.abs(want)), j
+    sg.destroy_plan(plan)
+    del a, b
+    torch.cuda.empty_cache()
