@@ -98,6 +98,9 @@ def _field_ptr(g):
     if isinstance(g, Grid2D):
         v = np.ascontiguousarray(g.values, dtype=np.float64)
         return v, C.c_void_p(v.ctypes.data), 0, g.nx, g.ny, g.dx, g.dy
+    # a CUDA tensor: its producer may still run on the caller's torch stream
+    import torch
+    torch.cuda.current_stream(g.device).synchronize()
     return g, C.c_void_p(g.data_ptr()), 1, int(g.shape[1]), int(g.shape[0]), 1.0, 1.0
 
 

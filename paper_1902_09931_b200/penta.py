@@ -81,7 +81,10 @@ class _DeviceFactor:
         else:
             if tuple(rhs.shape) != (self.n_, self.B) or not rhs.is_contiguous():
                 raise InvalidArgument("solve_in_place: rhs shape does not match the operator")
-            check(_lib.lib().sg_penta_solve(self._h, C.c_void_p(rhs.data_ptr()), 1, None, 1))
+            # in order with the caller's torch stream
+            import torch
+            stream = torch.cuda.current_stream(rhs.device).cuda_stream
+            check(_lib.lib().sg_penta_solve(self._h, C.c_void_p(rhs.data_ptr()), 1, C.c_void_p(stream or 0), 1))
 
     def __del__(self):
         try:
