@@ -706,14 +706,24 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
 //  * operands are loaded RG rows ahead of the chain (software pipelined,
 //    pinned by compiler barriers), so shared-memory latency stays off it.
 // Arithmetic per row is penta.cpp:171-196 exactly, as in k_sweep_tma.
-constexpr int RR_RS = 64;    // rows per stage
+// Stage height RS: 64 rows (two 95 KB CTAs per SM: large batches) or 128
+// rows (one 190 KB CTA per SM: batches of at most one CTA per SM, where
+// halving the number of stage hand-offs shortens the chain's critical path:
+// CH 1024^2 97.8 -> 92.4 us/step; 256-row stages (three slots) measured
+// slower, 95.3 us — the backward group loop slows down).
+constexpr int RR_RS = 64;    // rows per stage (default geometry)
+constexpr int RR_RS_WIDE = 128;
 constexpr int RR_NSTG = 5;   // ring slots (= stages resident at the turn)
-constexpr int RR_FAC = RR_RS;  // doubles per uniform factor slot
 constexpr int RG = 8;        // rows per software-pipelined operand group
-constexpr int RR_STAGE = RR_RS * 32 + 5 * RR_FAC;  // doubles per slot
-static_assert((RR_STAGE * 8) % 128 == 0 && (RR_FAC * 8) % 128 == 0, "TMA destinations must be 128 B aligned");
-static_assert(RR_RS % RG == 0, "stage = whole operand groups");
-constexpr size_t RR_SMEM = static_cast<size_t>(RR_NSTG) * RR_STAGE * 8 + 2 * RR_NSTG * 8;
+template <int RS>
+struct RRGeom {
+  static constexpr int FAC = RS;  // doubles per uniform factor slot
+  static constexpr int STAGE = RS * 32 + 5 * FAC;  // doubles per slot
+  static_assert((STAGE * 8) % 128 == 0 && (FAC * 8) % 128 == 0, "TMA destinations must be 128 B aligned");
+  static_assert(RS % RG == 0, "stage = whole operand groups");
+  static constexpr int NST = RR_NSTG;
+  static constexpr size_t SMEM = static_cast<size_t>(NST) * STAGE * 8 + 2 * NST * 8;
+};
 
 __device__ __forceinline__ void s_tma_store_2d(const CUtensorMap* m, int x, int y, const void* src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
@@ -734,11 +744,11 @@ __device__ long long g_sweep_trace[8192];
   } while (0)
 #endif
 
-template <bool PERIODIC>
+template <bool PERIODIC, int RS>
 __global__ void __launch_bounds__(64) k_sweep_res(const PentaTables f, const __grid_constant__ SweepMaps maps, int B,
                                                   int n, double* __restrict__ y4) {
   extern __shared__ __align__(128) double rr_smem[];
-  constexpr int RS = RR_RS, NST = RR_NSTG, FAC = RR_FAC, STG = RR_STAGE;
+  constexpr int NST = RRGeom<RS>::NST, FAC = RRGeom<RS>::FAC, STG = RRGeom<RS>::STAGE;
   constexpr uint32_t TX = RS * 32 * 8 + 5 * RS * 8;  // bytes per stage load
   uint64_t* full = reinterpret_cast<uint64_t*>(rr_smem + NST * STG);
   uint64_t* done = full + NST;
@@ -1086,19 +1096,39 @@ bool use_resident_sweep() {
   return v;
 }
 
-void launch_sweep_res(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
-                      cudaStream_t s, bool pdl) {
+// Stage height for a batch of B systems (one CTA per 32 systems).
+int sweep_res_rows(int B) {
+  static const int sms = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  const char* e = std::getenv("SG_SWEEP_RS");
+  if (e) return std::atoi(e) == RR_RS_WIDE ? RR_RS_WIDE : RR_RS;
+  return (B + 31) / 32 <= sms ? RR_RS_WIDE : RR_RS;
+}
+
+template <int RS>
+void launch_sweep_res_t(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
+                        cudaStream_t s, bool pdl) {
+  constexpr size_t smem = RRGeom<RS>::SMEM;
   static bool configured = false;
   if (!configured) {
-    SG_CUDA(cudaFuncSetAttribute(k_sweep_res<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(RR_SMEM)));
-    SG_CUDA(cudaFuncSetAttribute(k_sweep_res<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(RR_SMEM)));
+    SG_CUDA(cudaFuncSetAttribute(k_sweep_res<true, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    SG_CUDA(cudaFuncSetAttribute(k_sweep_res<false, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
     configured = true;
   }
   const int blocks = (B + 31) / 32;
-  launch_ex(periodic ? k_sweep_res<true> : k_sweep_res<false>, dim3(blocks), dim3(64), RR_SMEM, s, pdl, f, maps, B,
-            n, y4);
+  launch_ex(periodic ? k_sweep_res<true, RS> : k_sweep_res<false, RS>, dim3(blocks), dim3(64), smem, s, pdl, f, maps,
+            B, n, y4);
+}
+
+void launch_sweep_res(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
+                      cudaStream_t s, bool pdl, int rs) {
+  if (rs == RR_RS_WIDE) launch_sweep_res_t<RR_RS_WIDE>(periodic, f, maps, B, n, y4, s, pdl);
+  else launch_sweep_res_t<RR_RS>(periodic, f, maps, B, n, y4, s, pdl);
 }
 
 template <bool U, bool P, int M>
@@ -1136,9 +1166,9 @@ void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool
     return;
   }
   SweepMaps maps;
-  if (f.uniform && (!periodic || fusedCorrection) && use_resident_sweep() &&
-      sweep_maps(f, B, n, z, &maps, RR_RS)) {
-    launch_sweep_res(periodic, f, maps, B, n, y4, s, pdl);
+  const int rs = sweep_res_rows(B);
+  if (f.uniform && (!periodic || fusedCorrection) && use_resident_sweep() && sweep_maps(f, B, n, z, &maps, rs)) {
+    launch_sweep_res(periodic, f, maps, B, n, y4, s, pdl, rs);
     check_launch("penta sweep (TMA, resident turn) kernel");
     return;
   }

@@ -39,7 +39,8 @@ int main(int argc, char** argv) {
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     if (rep < 2) continue;
-    const int nS = (n + sg::RR_RS - 1) / sg::RR_RS;
+    const int rs = sg::sweep_res_rows(B);
+    const int nS = (n + rs - 1) / rs;
     std::vector<long long> t(6 * nS);
     cudaMemcpyFromSymbol(t.data(), sg::g_sweep_trace, 8 * t.size());
     printf("n=%d B=%d sweep %.1f us, trace span %lld cycles\n", n, B, ms * 1e3, t[6 * nS - 1] - t[0]);
