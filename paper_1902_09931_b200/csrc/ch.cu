@@ -407,9 +407,10 @@ __global__ void __launch_bounds__(256, FUSE ? 2 : 4) k_rhs_v(const double* __res
 }
 
 // SG_CH_RHS=legacy selects the scalar-load k_rhs (A/B); default k_rhs_v.
-// (A persistent cp.async-pipelined variant with one 117 KB CTA per SM was
-// measured 1.55x slower than k_rhs_v's two register-staged CTAs per SM at
-// 8192^2 and is not kept.)
+// (Measured and not kept, 8192^2 fused: a persistent cp.async-pipelined
+// variant with one 117 KB CTA per SM, 1.55x slower; a non-persistent
+// cp.async-staged variant at 80 registers / three CTAs per SM, 1.4 % slower
+// than k_rhs_v's two 128-register CTAs per SM.)
 int rhs_kind() {
   static const int v = [] {
     const char* e = std::getenv("SG_CH_RHS");
