@@ -676,6 +676,7 @@ struct ChState {
   // step's RHS), 3 = three steady steps (the buffer rotation closes), 4 =
   // tail (the pending combine alone).
   std::map<int, cudaGraphExec_t> graphs;
+  int solveK = -1;  // kernels one solve launches (counted once, by capture)
   int step = 0;
   std::vector<void*> allocs;
 
@@ -778,10 +779,23 @@ struct ChState {
                        penta_sweep_fused(fy.t, nx, ny, w, y4y, fx.t.W, y4x, nullptr, s);
     if (!fused) {
       penta_sweep(fx.t, ny, nx, rhsT, y4x, true, true, s, pdl);
-      CorrTables tx{{fx.t.W[0], fx.t.W[1], fx.t.W[2], fx.t.W[3]}, y4x};
-      launch_transpose_correct(rhsT, w, nx, ny, nx, tx, s, pdl);
-      penta_sweep(fy.t, nx, ny, w, y4y, true, true, s, pdl);
+      // y-sweep reading the x-sweep output transposed + corrected on load
+      // (penta_sweep_xin); else the separate transpose/correct pass
+      if (!(xin_ok() && penta_sweep_xin(fy.t, nx, ny, w, rhsT, fx.t.W, y4x, y4y, s, pdl))) {
+        CorrTables tx{{fx.t.W[0], fx.t.W[1], fx.t.W[2], fx.t.W[3]}, y4x};
+        launch_transpose_correct(rhsT, w, nx, ny, nx, tx, s, pdl);
+        penta_sweep(fy.t, nx, ny, w, y4y, true, true, s, pdl);
+      }
     }
+  }
+
+  // SG_CH_XIN=0 keeps the separate transpose/correct kernel (A/B).
+  static bool xin_ok() {
+    static const bool v = [] {
+      const char* e = std::getenv("SG_CH_XIN");
+      return !(e && e[0] == '0');
+    }();
+    return v;
   }
 
   // The pending combine: C^{n+1} written over C^{n-1} (field[q]) in place.
@@ -842,7 +856,19 @@ struct ChState {
   // the last combine alone — one kernel fewer per step.
   void run(int steps) {
     if (steps <= 0) return;
-    const int solveK = unfused() ? 4 : 3;
+    // kernels per solve: RHS + x-sweep + y-sweep (+ transpose/correct when
+    // the y-sweep cannot read the x output transposed). Captured launches
+    // are not counted, so count what one graph replays.
+    if (solveK < 0) {
+      const uint64_t before = g_launches.load();
+      cudaGraph_t g;
+      SG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      enqueue_solve(ic, ip, -1, stream);
+      SG_CUDA(cudaStreamEndCapture(stream, &g));
+      SG_CUDA(cudaGraphDestroy(g));
+      solveK = static_cast<int>(g_launches.load() - before);
+      g_launches.store(before);
+    }
     if (steps == 1 || !steady_ok()) {
       for (int k = 0; k < steps; ++k) {
         launch(0, solveK + 1);

@@ -340,6 +340,8 @@ struct alignas(64) SweepMaps {
   CUtensorMap z;     // 2D {B, n}, box {32, RS}
   CUtensorMap t[5];  // m1, m2, dInv, ap, bp: uniform 1D {n} box {RS}; else 2D like z
   CUtensorMap yc[4]; // XCORR: the previous sweep's Woodbury coefficients y_k[r], 1D {n} box {RS}
+  CUtensorMap zt;    // XIN (k_sweep_res): the input read TRANSPOSED from zT[b*n + r],
+                     // 2D {n, B} box {16, 32}, 128 B swizzle
 };
 
 // Fusions used by the Cahn-Hilliard step (ch.cu):
@@ -351,6 +353,7 @@ struct alignas(64) SweepMaps {
 struct SweepFuse {
   const double* Wc[4] = {nullptr, nullptr, nullptr, nullptr};
   double* zout = nullptr;
+  const double* yc = nullptr;  // XIN: yc[k*n + r], the previous sweep's y_k
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) {
@@ -715,14 +718,27 @@ constexpr int RR_RS = 64;    // rows per stage (default geometry)
 constexpr int RR_RS_WIDE = 128;
 constexpr int RR_NSTG = 5;   // ring slots (= stages resident at the turn)
 constexpr int RG = 8;        // rows per software-pipelined operand group
-template <int RS>
+// XIN (the CH y-sweep): the forward input is the x-sweep's output zT in
+// ITS layout (zT[b*n + r]: system-major), fetched as 128 B-swizzled 16 x 32
+// tensor boxes into two raw buffers; warp 1's 32 lanes transpose each stage
+// into the slot while applying the x Woodbury correction — the separate
+// transpose/correct pass (16 B/pt of traffic and a launch) disappears. Four
+// ring slots instead of five pay for the raw buffers.
+constexpr int XIN_TW = 3;  // transform warps (1-3) of the XIN sweep
+
+template <int RS, bool XIN = false>
 struct RRGeom {
   static constexpr int FAC = RS;  // doubles per uniform factor slot
   static constexpr int STAGE = RS * 32 + 5 * FAC;  // doubles per slot
   static_assert((STAGE * 8) % 128 == 0 && (FAC * 8) % 128 == 0, "TMA destinations must be 128 B aligned");
-  static_assert(RS % RG == 0, "stage = whole operand groups");
-  static constexpr int NST = RR_NSTG;
-  static constexpr size_t SMEM = static_cast<size_t>(NST) * STAGE * 8 + 2 * NST * 8;
+  static_assert(RS % RG == 0 && RS % 16 == 0, "stage = whole operand groups / swizzle boxes");
+  static constexpr int NST = XIN ? 4 : RR_NSTG;
+  // doubles per raw buffer: RS/16 swizzled zT boxes of 4 KB, then the
+  // stage's four y_k row vectors (1D TMA)
+  static constexpr int RAW = XIN ? RS * 32 + 4 * RS : 0;
+  static constexpr size_t RAW_OFF = static_cast<size_t>(NST) * STAGE * 8;  // bytes, before alignment
+  static constexpr size_t SMEM =
+      RAW_OFF + (XIN ? 2 * RAW * 8 + 1024 : 0) + (2 * NST + 2) * 8;
 };
 
 __device__ __forceinline__ void s_tma_store_2d(const CUtensorMap* m, int x, int y, const void* src) {
@@ -744,22 +760,41 @@ __device__ long long g_sweep_trace[8192];
   } while (0)
 #endif
 
-template <bool PERIODIC, int RS>
-__global__ void __launch_bounds__(64) k_sweep_res(const PentaTables f, const __grid_constant__ SweepMaps maps, int B,
-                                                  int n, double* __restrict__ y4) {
+template <bool PERIODIC, int RS, bool XIN>
+__global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(const PentaTables f, const __grid_constant__ SweepMaps maps, int B,
+                                                  int n, double* __restrict__ y4, const SweepFuse fuse) {
   extern __shared__ __align__(128) double rr_smem[];
-  constexpr int NST = RRGeom<RS>::NST, FAC = RRGeom<RS>::FAC, STG = RRGeom<RS>::STAGE;
+  using GEO = RRGeom<RS, XIN>;
+  constexpr int NST = GEO::NST, FAC = GEO::FAC, STG = GEO::STAGE;
   constexpr uint32_t TX = RS * 32 * 8 + 5 * RS * 8;  // bytes per stage load
-  uint64_t* full = reinterpret_cast<uint64_t*>(rr_smem + NST * STG);
+  constexpr uint32_t FTX = 5 * RS * 8;               // factor boxes only (XIN forward)
+  // XIN raw buffers: 1024 B aligned (the 128 B swizzle pattern is a function
+  // of the shared-memory address bits 4-9)
+  double* raw = nullptr;
+  uint64_t* full;
+  if constexpr (XIN) {
+    const uint32_t a = s_u32(rr_smem) + static_cast<uint32_t>(GEO::RAW_OFF);
+    raw = rr_smem + (GEO::RAW_OFF + ((1024u - (a & 1023u)) & 1023u)) / 8;
+    full = reinterpret_cast<uint64_t*>(rr_smem + (GEO::RAW_OFF + 1024 + 2 * GEO::RAW * 8) / 8);
+  } else {
+    full = reinterpret_cast<uint64_t*>(rr_smem + NST * STG);
+  }
   uint64_t* done = full + NST;
+  uint64_t* rawfull = done + NST;  // XIN only
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b0 = blockIdx.x * 32;
   const int nS = (n + RS - 1) / RS;
   const int keep = nS < NST ? nS : NST;  // forward stages resident at the turn
   if (threadIdx.x == 0) {
     for (int k = 0; k < NST; ++k) {
-      s_mbar_init(&full[k], 1);
+      // XIN: every load of a slot completes on the TMA bytes AND a plain
+      // arrival (the transform in the forward pass, immediate in backward)
+      s_mbar_init(&full[k], XIN ? 1 + XIN_TW : 1);
       s_mbar_init(&done[k], 1);
+    }
+    if constexpr (XIN) {
+      s_mbar_init(&rawfull[0], 1);
+      s_mbar_init(&rawfull[1], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -772,29 +807,107 @@ __global__ void __launch_bounds__(64) k_sweep_res(const PentaTables f, const __g
   // done[s] once per consumer use of s EXCEPT the resident forward stage
   auto uses = [&](int s) { return s < nS ? (nS - s + NST - 1) / NST : 0; };
 
-  if (warp == 1) {
+  if (warp >= 1) {
     // ------------------------------------------------------------ producer
-    if (lane != 0) return;
+    // (warp 1; with XIN warps 1-3 share the forward transform)
     auto load = [&](int s, int G) {
       double* st = rr_smem + s * STG;
       s_mbar_expect_tx(&full[s], TX);
       s_tma_2d(st, &maps.z, b0, G * RS, &full[s]);
       for (int k = 0; k < 5; ++k) s_tma_1d(st + RS * 32 + k * FAC, &maps.t[k], G * RS, &full[s]);
+      if constexpr (XIN)  // no transform on refetched rows: the transform arrivals now
+        for (int k = 0; k < XIN_TW; ++k) s_mbar_arrive(&full[s]);
     };
     auto store = [&](int s, int G) {
       s_tma_store_2d(&maps.z, b0, G * RS, rr_smem + s * STG);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     };
-    // forward: loading stage g reuses the slot of stage g - NST, which is
-    // stored first (it is never resident: g - NST < nS - NST)
-    for (int g = 0; g < nS; ++g) {
-      const int s = g % NST;
-      if (g >= NST) {
-        s_mbar_wait(&done[s], ((g / NST) + 1) & 1);
-        store(s, g - NST);
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if constexpr (XIN) {
+      // forward stages: warp 1 lane 0 issues the TMA traffic; warps 1-3
+      // (three SMSPs: the transform's FP64 work is ~2x the consumer's per
+      // row) transpose + correct the raw zT boxes of stage g into slot
+      // g % NST (k_transpose_correct's expression: z - (W0 y0 + W1 y1 + W2 y2
+      // + W3 y3), penta.cpp:283-284)
+      const int tw = warp - 1;  // transform warp 0..XIN_TW-1
+      const bool issuer = tw == 0 && lane == 0;
+      const int bl = b0 + lane;
+      double Wb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) Wb[k] = bl < B ? __ldg(fuse.Wc[k] + bl) : 0.0;
+      auto load_raw = [&](int g) {
+        double* rb = raw + (g & 1) * GEO::RAW;
+        s_mbar_expect_tx(&rawfull[g & 1], (RS * 32 + 4 * RS) * 8);
+        for (int x = 0; x < RS / 16; ++x) s_tma_2d(rb + x * 512, &maps.zt, g * RS + x * 16, b0, &rawfull[g & 1]);
+        for (int k = 0; k < 4; ++k) s_tma_1d(rb + RS * 32 + k * RS, &maps.yc[k], g * RS, &rawfull[g & 1]);
+      };
+      if (issuer) load_raw(0);
+      for (int g = 0; g < nS; ++g) {
+        const int s = g % NST;
+        if (issuer && g >= NST) {
+          s_mbar_wait(&done[s], ((g / NST) + 1) & 1);
+          store(s, g - NST);
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        // slot s is free (its store has read it) and every transform warp has
+        // finished stage g-1 (so its raw buffer can be refilled)
+        asm volatile("bar.sync 1, %0;" ::"n"(XIN_TW * 32) : "memory");
+        if (issuer) {
+          double* st = rr_smem + s * STG;
+          s_mbar_expect_tx(&full[s], FTX);
+          for (int k = 0; k < 5; ++k) s_tma_1d(st + RS * 32 + k * FAC, &maps.t[k], g * RS, &full[s]);
+          if (g + 1 < nS) load_raw(g + 1);
+        }
+        s_mbar_wait(&rawfull[g & 1], (g >> 1) & 1);
+        const double* rb = raw + (g & 1) * GEO::RAW;
+        double* zs = rr_smem + s * STG;
+        // batches of TB row pairs, dealt round-robin to the transform warps:
+        // all loads first, then the arithmetic (independent chains
+        // interleave), then the stores
+        constexpr int TB = 4;
+        for (int jb = tw * TB; jb < RS / 2; jb += XIN_TW * TB) {
+          double2 v[TB], y[TB][4];
+#pragma unroll
+          for (int t = 0; t < TB; ++t) {
+            const int jp = jb + t;
+            // rows 2jp, 2jp+1 of system bl: box jp/8, 16 B chunk jp%8 of
+            // smem row `lane`, XOR-swizzled by lane % 8
+            v[t] = *reinterpret_cast<const double2*>(rb + (jp >> 3) * 512 + lane * 16 +
+                                                     (((jp & 7) ^ (lane & 7)) << 1));
+#pragma unroll
+            for (int k = 0; k < 4; ++k)  // broadcast: every lane reads the same pair
+              y[t][k] = *reinterpret_cast<const double2*>(rb + RS * 32 + k * RS + 2 * jp);
+          }
+          double o[TB][2];
+#pragma unroll
+          for (int t = 0; t < TB; ++t) {
+            const double c0 = Wb[0] * y[t][0].x + Wb[1] * y[t][1].x + Wb[2] * y[t][2].x + Wb[3] * y[t][3].x;
+            const double c1 = Wb[0] * y[t][0].y + Wb[1] * y[t][1].y + Wb[2] * y[t][2].y + Wb[3] * y[t][3].y;
+            o[t][0] = v[t].x - c0;
+            o[t][1] = v[t].y - c1;
+          }
+#pragma unroll
+          for (int t = 0; t < TB; ++t) {
+            zs[(2 * (jb + t)) * 32 + lane] = o[t][0];
+            zs[(2 * (jb + t) + 1) * 32 + lane] = o[t][1];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) s_mbar_arrive(&full[s]);
       }
-      load(s, g);
+      if (!issuer) return;
+    } else {
+      if (lane != 0) return;
+      // forward: loading stage g reuses the slot of stage g - NST, which is
+      // stored first (it is never resident: g - NST < nS - NST)
+      for (int g = 0; g < nS; ++g) {
+        const int s = g % NST;
+        if (g >= NST) {
+          s_mbar_wait(&done[s], ((g / NST) + 1) & 1);
+          store(s, g - NST);
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        load(s, g);
+      }
     }
     // turn: every forward store has landed before those rows are refetched
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1045,7 +1158,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
   return encode;
 }
 
-bool encode_map(CUtensorMap* m, const double* p, int rank, uint64_t d0, uint64_t d1, uint32_t b0, uint32_t b1) {
+bool encode_map(CUtensorMap* m, const double* p, int rank, uint64_t d0, uint64_t d1, uint32_t b0, uint32_t b1,
+                bool swizzle128 = false) {
   auto enc = tensor_encoder();
   if (!enc) return false;
   const cuuint64_t dims[2] = {d0, d1};
@@ -1053,7 +1167,8 @@ bool encode_map(CUtensorMap* m, const double* p, int rank, uint64_t d0, uint64_t
   const cuuint32_t box[2] = {b0, b1};
   const cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(p), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1108,27 +1223,32 @@ int sweep_res_rows(int B) {
   return (B + 31) / 32 <= sms ? RR_RS_WIDE : RR_RS;
 }
 
-template <int RS>
+template <int RS, bool XIN>
 void launch_sweep_res_t(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
-                        cudaStream_t s, bool pdl) {
-  constexpr size_t smem = RRGeom<RS>::SMEM;
+                        cudaStream_t s, bool pdl, const SweepFuse& fuse) {
+  constexpr size_t smem = RRGeom<RS, XIN>::SMEM;
   static bool configured = false;
   if (!configured) {
-    SG_CUDA(cudaFuncSetAttribute(k_sweep_res<true, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SG_CUDA(cudaFuncSetAttribute(k_sweep_res<true, RS, XIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-    SG_CUDA(cudaFuncSetAttribute(k_sweep_res<false, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SG_CUDA(cudaFuncSetAttribute(k_sweep_res<false, RS, XIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     configured = true;
   }
   const int blocks = (B + 31) / 32;
-  launch_ex(periodic ? k_sweep_res<true, RS> : k_sweep_res<false, RS>, dim3(blocks), dim3(64), smem, s, pdl, f, maps,
-            B, n, y4);
+  launch_ex(periodic ? k_sweep_res<true, RS, XIN> : k_sweep_res<false, RS, XIN>, dim3(blocks),
+            dim3(XIN ? 32 * (1 + XIN_TW) : 64), smem, s, pdl, f, maps, B, n, y4, fuse);
 }
 
 void launch_sweep_res(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
-                      cudaStream_t s, bool pdl, int rs) {
-  if (rs == RR_RS_WIDE) launch_sweep_res_t<RR_RS_WIDE>(periodic, f, maps, B, n, y4, s, pdl);
-  else launch_sweep_res_t<RR_RS>(periodic, f, maps, B, n, y4, s, pdl);
+                      cudaStream_t s, bool pdl, int rs, bool xin = false, const SweepFuse& fuse = SweepFuse{}) {
+  if (xin) {
+    if (rs == RR_RS_WIDE) launch_sweep_res_t<RR_RS_WIDE, true>(periodic, f, maps, B, n, y4, s, pdl, fuse);
+    else launch_sweep_res_t<RR_RS, true>(periodic, f, maps, B, n, y4, s, pdl, fuse);
+    return;
+  }
+  if (rs == RR_RS_WIDE) launch_sweep_res_t<RR_RS_WIDE, false>(periodic, f, maps, B, n, y4, s, pdl, fuse);
+  else launch_sweep_res_t<RR_RS, false>(periodic, f, maps, B, n, y4, s, pdl, fuse);
 }
 
 template <bool U, bool P, int M>
@@ -1195,6 +1315,26 @@ void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool
     else launch_sweep_t<false, true, 0>(f, B, n, z, y4, s);
   }
   check_launch("penta sweep kernel");
+}
+
+bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double* zT, const double* const* Wc,
+                     const double* yc, double* y4, cudaStream_t s, bool pdl) {
+  // Uniform periodic operator, resident-turn sweep only (the CH y-sweep).
+  if (!f.uniform || !use_resident_sweep()) return false;
+  if ((reinterpret_cast<uintptr_t>(zT) & 15) || (reinterpret_cast<uintptr_t>(yc) & 15) || (n & 1)) return false;
+  const int rs = sweep_res_rows(B);
+  SweepMaps maps;
+  if (!sweep_maps(f, B, n, z, &maps, rs)) return false;
+  // zT[b*n + r]: dims {n (inner), B}, box {16 rows, 32 systems}, 128 B swizzle
+  if (!encode_map(&maps.zt, zT, 2, n, B, 16, 32, true)) return false;
+  for (int k = 0; k < 4; ++k)
+    if (!encode_map(&maps.yc[k], yc + static_cast<size_t>(k) * n, 1, n, 1, rs, 1)) return false;
+  SweepFuse fuse;
+  for (int k = 0; k < 4; ++k) fuse.Wc[k] = Wc[k];
+  fuse.yc = yc;
+  launch_sweep_res(true, f, maps, B, n, y4, s, pdl, rs, true, fuse);
+  check_launch("penta sweep (TMA, resident turn, transposed corrected input) kernel");
+  return true;
 }
 
 bool penta_sweep_fused(const PentaTables& f, int B, int n, double* z, double* y4, const double* const* Wc,

@@ -331,8 +331,18 @@ def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak,
     e2e = None
     e2e_steps = getattr(args, "e2e_steps", 3)
     if not getattr(args, "skip_e2e", False) and e2e_steps > 0:
-        hin = torch.empty((slab.own, nx), dtype=torch.float64, pin_memory=True)
-        hout = torch.empty_like(hin, pin_memory=True)
+        try:  # 2 x 8.6 GB of pinned host memory per rank
+            hin = torch.empty((slab.own, nx), dtype=torch.float64, pin_memory=True)
+            hout = torch.empty_like(hin, pin_memory=True)
+            ok = 1.0
+        except RuntimeError:
+            ok = 0.0
+        t_ok = torch.tensor([ok], device="cuda")
+        dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+        if t_ok.item() < 1.0:
+            e2e_steps = 0
+            e2e = {"error": "pinned host buffers (2 x 8.6 GB per rank) could not be allocated"}
+    if not getattr(args, "skip_e2e", False) and e2e_steps > 0:
         hin.uniform_(-1, 1)
         torch.cuda.synchronize()
         dist.barrier()
