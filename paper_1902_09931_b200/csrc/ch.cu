@@ -114,6 +114,9 @@ __device__ __forceinline__ int wrapi(int i, int n) {
 // and below: inShift 2, wrapY 0). Columns always wrap (periodic in x).
 struct RhsGeom {
   int nx, outRows, inRows, inShift, wrapY;
+  // k_rhs_v only: write the RHS row-major (rhs[j*nx + i]) instead of
+  // transposed — the single-GPU step, whose x-sweep reads it transposed
+  int rowOut = 0;
 };
 
 __device__ __forceinline__ int wrap_once(int i, int n) {  // i in [-n, 2n)
@@ -384,6 +387,24 @@ __global__ void __launch_bounds__(256, FUSE ? 2 : 4) k_rhs_v(const double* __res
   }
   // ---- combine (cahn_hilliard.cpp:292/294) and store 4 consecutive j per column
   const int jb = j0 + y0;
+  if (G.rowOut) {  // row-major: 16 B per lane, 512 B per warp and row
+    double res[2][VR];
+#pragma unroll
+    for (int cx = 0; cx < 2; ++cx)
+#pragma unroll
+      for (int r = 0; r < VR; ++r) {
+        if constexpr (NONLINEAR)
+          res[cx][r] = P.kDiff * d[r][cx] - P.kBih * bh[r][cx] + P.kNl * nl[r][cx];
+        else
+          res[cx][r] = P.kDiff * d[r][cx] - P.kBih * bh[r][cx];
+      }
+#pragma unroll
+    for (int r = 0; r < VR; ++r)
+      if (jb + r < G.outRows)
+        *reinterpret_cast<double2*>(rhsT + static_cast<long long>(jb + r) * nx + i0 + x0) =
+            make_double2(res[0][r], res[1][r]);
+    return;
+  }
 #pragma unroll
   for (int cx = 0; cx < 2; ++cx) {
     double res[VR];
@@ -669,6 +690,11 @@ struct ChState {
   double* field[3] = {nullptr, nullptr, nullptr};
   int ic = 0, ip = 1;
   double *rhsT = nullptr, *w = nullptr, *y4x = nullptr, *y4y = nullptr;
+  // xpipe: the RHS is written row-major into rhsT, the x-sweep reads it
+  // transposed and writes its interleaved result to xT, the y-sweep reads xT
+  // transposed with the x Woodbury correction (no transpose kernel)
+  double* xT = nullptr;
+  bool xpipe = false;
   DevicePenta fx, fy;
   RhsParams rp{};
   // CUDA graphs keyed by (kind, ic, ip): kind 0 = full step, 1 = head (step
@@ -739,6 +765,12 @@ struct ChState {
     for (int t : kBihTaps) keep[t] = true;
     for (int k = 0; k < 25; ++k)
       if (!keep[k] && rp.bw[k] != 0.0) throw Error(SG_ERR_CUDA, "internal: biharmonic zero pattern");
+    // the transposed-input sweep pipeline (see xpipe)
+    if (xin_ok() && unfused() && rhs_kind() == 1 && p.nx % RX == 0) {
+      xT = dalloc(cnt);
+      xpipe = penta_sweep_xin(fx.t, p.ny, p.nx, xT, rhsT, nullptr, nullptr, y4x, stream, false, false) &&
+              penta_sweep_xin(fy.t, p.nx, p.ny, w, xT, fx.t.W, y4x, y4y, stream, false, false);
+    }
     // initial_condition (cahn_hilliard.cpp:68-76); C^{n-1} := C^n (:218)
     const long long n = static_cast<long long>(cnt);
     k_init<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(p.seed, p.icAmplitude, n, field[0]);
@@ -765,7 +797,7 @@ struct ChState {
   // Leaves the step's combine pending: C^{n+1} = 2C^n - C^{n-1} + (w - W·y4y).
   void enqueue_solve(int c, int q, int in, cudaStream_t s) {
     const int nx = p.nx, ny = p.ny;
-    const RhsGeom geom{nx, ny, ny, 0, 1};
+    const RhsGeom geom{nx, ny, ny, 0, 1, xpipe ? 1 : 0};
     const bool pdl = pdl_enabled();
     if (in >= 0) {
       CorrTables ty{{fy.t.W[0], fy.t.W[1], fy.t.W[2], fy.t.W[3]}, y4y};
@@ -777,16 +809,19 @@ struct ChState {
     // the y-sweep applies the x Woodbury correction as it loads w.
     const bool fused = !unfused() && penta_sweep_fused(fx.t, ny, nx, rhsT, y4x, nullptr, nullptr, w, s) &&
                        penta_sweep_fused(fy.t, nx, ny, w, y4y, fx.t.W, y4x, nullptr, s);
-    if (!fused) {
-      penta_sweep(fx.t, ny, nx, rhsT, y4x, true, true, s, pdl);
-      // y-sweep reading the x-sweep output transposed + corrected on load
-      // (penta_sweep_xin); else the separate transpose/correct pass
-      if (!(xin_ok() && penta_sweep_xin(fy.t, nx, ny, w, rhsT, fx.t.W, y4x, y4y, s, pdl))) {
-        CorrTables tx{{fx.t.W[0], fx.t.W[1], fx.t.W[2], fx.t.W[3]}, y4x};
-        launch_transpose_correct(rhsT, w, nx, ny, nx, tx, s, pdl);
-        penta_sweep(fy.t, nx, ny, w, y4y, true, true, s, pdl);
-      }
+    if (fused) return;
+    if (xpipe) {
+      // x-sweep: rhs (row-major) read transposed -> xT (interleaved);
+      // y-sweep: xT read transposed + x-corrected -> w (row-major)
+      if (!penta_sweep_xin(fx.t, ny, nx, xT, rhsT, nullptr, nullptr, y4x, s, pdl) ||
+          !penta_sweep_xin(fy.t, nx, ny, w, xT, fx.t.W, y4x, y4y, s, pdl))
+        throw Error(SG_ERR_CUDA, "internal: transposed-input sweep unavailable");
+      return;
     }
+    penta_sweep(fx.t, ny, nx, rhsT, y4x, true, true, s, pdl);
+    CorrTables tx{{fx.t.W[0], fx.t.W[1], fx.t.W[2], fx.t.W[3]}, y4x};
+    launch_transpose_correct(rhsT, w, nx, ny, nx, tx, s, pdl);
+    penta_sweep(fy.t, nx, ny, w, y4y, true, true, s, pdl);
   }
 
   // SG_CH_XIN=0 keeps the separate transpose/correct kernel (A/B).

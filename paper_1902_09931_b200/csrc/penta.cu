@@ -718,15 +718,17 @@ constexpr int RR_RS = 64;    // rows per stage (default geometry)
 constexpr int RR_RS_WIDE = 128;
 constexpr int RR_NSTG = 5;   // ring slots (= stages resident at the turn)
 constexpr int RG = 8;        // rows per software-pipelined operand group
-// XIN (the CH y-sweep): the forward input is the x-sweep's output zT in
+// XIN 1 (the CH y-sweep): the forward input is the x-sweep's output zT in
 // ITS layout (zT[b*n + r]: system-major), fetched as 128 B-swizzled 16 x 32
 // tensor boxes into two raw buffers; warp 1's 32 lanes transpose each stage
 // into the slot while applying the x Woodbury correction — the separate
-// transpose/correct pass (16 B/pt of traffic and a launch) disappears. Four
-// ring slots instead of five pay for the raw buffers.
+// transpose/correct pass (16 B/pt of traffic and a launch) disappears.
+// XIN 2 (the CH x-sweep): the same transposed read with no correction — the
+// RHS kernel then writes its output row-major (coalesced) instead of
+// transposed. Four ring slots instead of five pay for the raw buffers.
 constexpr int XIN_TW = 3;  // transform warps (1-3) of the XIN sweep
 
-template <int RS, bool XIN = false>
+template <int RS, int XIN = 0>
 struct RRGeom {
   static constexpr int FAC = RS;  // doubles per uniform factor slot
   static constexpr int STAGE = RS * 32 + 5 * FAC;  // doubles per slot
@@ -760,7 +762,7 @@ __device__ long long g_sweep_trace[8192];
   } while (0)
 #endif
 
-template <bool PERIODIC, int RS, bool XIN>
+template <bool PERIODIC, int RS, int XIN>
 __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(const PentaTables f, const __grid_constant__ SweepMaps maps, int B,
                                                   int n, double* __restrict__ y4, const SweepFuse fuse) {
   extern __shared__ __align__(128) double rr_smem[];
@@ -831,14 +833,17 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
       const int tw = warp - 1;  // transform warp 0..XIN_TW-1
       const bool issuer = tw == 0 && lane == 0;
       const int bl = b0 + lane;
-      double Wb[4];
+      double Wb[4] = {0.0, 0.0, 0.0, 0.0};
+      if constexpr (XIN == 1) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) Wb[k] = bl < B ? __ldg(fuse.Wc[k] + bl) : 0.0;
+        for (int k = 0; k < 4; ++k) Wb[k] = bl < B ? __ldg(fuse.Wc[k] + bl) : 0.0;
+      }
       auto load_raw = [&](int g) {
         double* rb = raw + (g & 1) * GEO::RAW;
-        s_mbar_expect_tx(&rawfull[g & 1], (RS * 32 + 4 * RS) * 8);
+        s_mbar_expect_tx(&rawfull[g & 1], (RS * 32 + (XIN == 1 ? 4 * RS : 0)) * 8);
         for (int x = 0; x < RS / 16; ++x) s_tma_2d(rb + x * 512, &maps.zt, g * RS + x * 16, b0, &rawfull[g & 1]);
-        for (int k = 0; k < 4; ++k) s_tma_1d(rb + RS * 32 + k * RS, &maps.yc[k], g * RS, &rawfull[g & 1]);
+        if constexpr (XIN == 1)
+          for (int k = 0; k < 4; ++k) s_tma_1d(rb + RS * 32 + k * RS, &maps.yc[k], g * RS, &rawfull[g & 1]);
       };
       if (issuer) load_raw(0);
       for (int g = 0; g < nS; ++g) {
@@ -873,17 +878,24 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
             // smem row `lane`, XOR-swizzled by lane % 8
             v[t] = *reinterpret_cast<const double2*>(rb + (jp >> 3) * 512 + lane * 16 +
                                                      (((jp & 7) ^ (lane & 7)) << 1));
+            if constexpr (XIN == 1) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)  // broadcast: every lane reads the same pair
-              y[t][k] = *reinterpret_cast<const double2*>(rb + RS * 32 + k * RS + 2 * jp);
+              for (int k = 0; k < 4; ++k)  // broadcast: every lane reads the same pair
+                y[t][k] = *reinterpret_cast<const double2*>(rb + RS * 32 + k * RS + 2 * jp);
+            }
           }
           double o[TB][2];
 #pragma unroll
           for (int t = 0; t < TB; ++t) {
-            const double c0 = Wb[0] * y[t][0].x + Wb[1] * y[t][1].x + Wb[2] * y[t][2].x + Wb[3] * y[t][3].x;
-            const double c1 = Wb[0] * y[t][0].y + Wb[1] * y[t][1].y + Wb[2] * y[t][2].y + Wb[3] * y[t][3].y;
-            o[t][0] = v[t].x - c0;
-            o[t][1] = v[t].y - c1;
+            if constexpr (XIN == 1) {
+              const double c0 = Wb[0] * y[t][0].x + Wb[1] * y[t][1].x + Wb[2] * y[t][2].x + Wb[3] * y[t][3].x;
+              const double c1 = Wb[0] * y[t][0].y + Wb[1] * y[t][1].y + Wb[2] * y[t][2].y + Wb[3] * y[t][3].y;
+              o[t][0] = v[t].x - c0;
+              o[t][1] = v[t].y - c1;
+            } else {
+              o[t][0] = v[t].x;
+              o[t][1] = v[t].y;
+            }
           }
 #pragma unroll
           for (int t = 0; t < TB; ++t) {
@@ -1223,7 +1235,7 @@ int sweep_res_rows(int B) {
   return (B + 31) / 32 <= sms ? RR_RS_WIDE : RR_RS;
 }
 
-template <int RS, bool XIN>
+template <int RS, int XIN>
 void launch_sweep_res_t(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
                         cudaStream_t s, bool pdl, const SweepFuse& fuse) {
   constexpr size_t smem = RRGeom<RS, XIN>::SMEM;
@@ -1241,14 +1253,18 @@ void launch_sweep_res_t(bool periodic, const PentaTables& f, const SweepMaps& ma
 }
 
 void launch_sweep_res(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
-                      cudaStream_t s, bool pdl, int rs, bool xin = false, const SweepFuse& fuse = SweepFuse{}) {
-  if (xin) {
-    if (rs == RR_RS_WIDE) launch_sweep_res_t<RR_RS_WIDE, true>(periodic, f, maps, B, n, y4, s, pdl, fuse);
-    else launch_sweep_res_t<RR_RS, true>(periodic, f, maps, B, n, y4, s, pdl, fuse);
-    return;
+                      cudaStream_t s, bool pdl, int rs, int xin = 0, const SweepFuse& fuse = SweepFuse{}) {
+  const bool wide = rs == RR_RS_WIDE;
+  if (xin == 1) {
+    if (wide) launch_sweep_res_t<RR_RS_WIDE, 1>(periodic, f, maps, B, n, y4, s, pdl, fuse);
+    else launch_sweep_res_t<RR_RS, 1>(periodic, f, maps, B, n, y4, s, pdl, fuse);
+  } else if (xin == 2) {
+    if (wide) launch_sweep_res_t<RR_RS_WIDE, 2>(periodic, f, maps, B, n, y4, s, pdl, fuse);
+    else launch_sweep_res_t<RR_RS, 2>(periodic, f, maps, B, n, y4, s, pdl, fuse);
+  } else {
+    if (wide) launch_sweep_res_t<RR_RS_WIDE, 0>(periodic, f, maps, B, n, y4, s, pdl, fuse);
+    else launch_sweep_res_t<RR_RS, 0>(periodic, f, maps, B, n, y4, s, pdl, fuse);
   }
-  if (rs == RR_RS_WIDE) launch_sweep_res_t<RR_RS_WIDE, false>(periodic, f, maps, B, n, y4, s, pdl, fuse);
-  else launch_sweep_res_t<RR_RS, false>(periodic, f, maps, B, n, y4, s, pdl, fuse);
 }
 
 template <bool U, bool P, int M>
@@ -1318,22 +1334,26 @@ void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool
 }
 
 bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double* zT, const double* const* Wc,
-                     const double* yc, double* y4, cudaStream_t s, bool pdl) {
-  // Uniform periodic operator, resident-turn sweep only (the CH y-sweep).
+                     const double* yc, double* y4, cudaStream_t s, bool pdl, bool launch) {
+  // Uniform periodic operator, resident-turn sweep only (the CH sweeps).
   if (!f.uniform || !use_resident_sweep()) return false;
-  if ((reinterpret_cast<uintptr_t>(zT) & 15) || (reinterpret_cast<uintptr_t>(yc) & 15) || (n & 1)) return false;
+  if ((reinterpret_cast<uintptr_t>(zT) & 15) || (n & 1)) return false;
+  if (Wc && (reinterpret_cast<uintptr_t>(yc) & 15)) return false;
   const int rs = sweep_res_rows(B);
   SweepMaps maps;
   if (!sweep_maps(f, B, n, z, &maps, rs)) return false;
   // zT[b*n + r]: dims {n (inner), B}, box {16 rows, 32 systems}, 128 B swizzle
   if (!encode_map(&maps.zt, zT, 2, n, B, 16, 32, true)) return false;
-  for (int k = 0; k < 4; ++k)
-    if (!encode_map(&maps.yc[k], yc + static_cast<size_t>(k) * n, 1, n, 1, rs, 1)) return false;
   SweepFuse fuse;
-  for (int k = 0; k < 4; ++k) fuse.Wc[k] = Wc[k];
-  fuse.yc = yc;
-  launch_sweep_res(true, f, maps, B, n, y4, s, pdl, rs, true, fuse);
-  check_launch("penta sweep (TMA, resident turn, transposed corrected input) kernel");
+  if (Wc) {
+    for (int k = 0; k < 4; ++k)
+      if (!encode_map(&maps.yc[k], yc + static_cast<size_t>(k) * n, 1, n, 1, rs, 1)) return false;
+    for (int k = 0; k < 4; ++k) fuse.Wc[k] = Wc[k];
+    fuse.yc = yc;
+  }
+  if (!launch) return true;
+  launch_sweep_res(true, f, maps, B, n, y4, s, pdl, rs, Wc ? 1 : 2, fuse);
+  check_launch("penta sweep (TMA, resident turn, transposed input) kernel");
   return true;
 }
 

@@ -57,13 +57,15 @@ void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool
 bool penta_sweep_fused(const PentaTables& f, int B, int n, double* z, double* y4, const double* const* Wc,
                        const double* yc, double* zout, cudaStream_t s);
 
-// CH y-sweep with the x-sweep's transpose + Woodbury correction fused into
-// its loads: the input is zT[b*n + r] (the x-sweep output, system-major for
-// THIS batch) corrected by zT - (Wc0[b] yc0[r] + ... + Wc3[b] yc3[r])
-// (yc[k*n + r]); results (uncorrected, y -> y4) go to the interleaved z.
-// Returns false if the path is unavailable (caller runs the unfused pair).
+// Uniform periodic sweep reading its input TRANSPOSED: zT[b*n + r] (system-
+// major for this batch), e.g. the other sweep's output or a row-major RHS.
+// With Wc (the CH y-sweep) the previous sweep's Woodbury correction is
+// applied on load: zT - (Wc0[b] yc0[r] + ... + Wc3[b] yc3[r]) (yc[k*n + r]);
+// Wc = nullptr reads zT as is (the CH x-sweep). Results (uncorrected,
+// y -> y4) go to the interleaved z. launch = false only checks
+// availability. Returns false if the path is unavailable.
 bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double* zT, const double* const* Wc,
-                     const double* yc, double* y4, cudaStream_t s, bool pdl);
+                     const double* yc, double* y4, cudaStream_t s, bool pdl, bool launch = true);
 
 // lu4_solve, penta.cpp:61-70.
 __device__ __forceinline__ void lu4_solve_dev(const double* K, const int* piv, double* y) {
