@@ -40,6 +40,9 @@ METRIC = "2D stencil Gpts/s (XY periodic 9-point user-function, FP64)"
 UNIT = "Gpts/s"
 NX = NY = 32768
 BYTES_PER_PT = {"f64": 16, "f32": 8}  # read once + write once
+# nominal FP64 (non-tensor) instruction rate: 148 SMs x 64 lanes x 1.965 GHz
+# (DADD/DMUL/DFMA one each) — the bound of the tall-window stencils
+FP64_PEAK_OPS = 148 * 64 * 1.965e9
 WORKLOAD = "2D xy periodic 9-point user-function stencil (fn_weighted_3x3), 32768x32768"
 
 
@@ -342,9 +345,54 @@ def extras(sg, torch, stream, peak):
         best = min(best, time.perf_counter() - t0)
     sg.destroy_plan(plan)
     out["cfg1_512sq_10apps_ms"] = best * 1e3
+    out["stencil_variants_16384sq_fp64"] = bench_variants(sg, torch, stream, peak)
     if hasattr(sg, "CHStepper"):
         out.update(bench_ch(sg, torch))
     return out
+
+
+def bench_variants(sg, torch, stream, peak, n=16384, launches=20):
+    """HBM roofline fraction of the fast path across the API surface
+    (directions, boundary modes, window sizes, weights vs functions) on a
+    16384^2 FP64 grid (2 GiB per field >> L2)."""
+    import numpy as np
+    rng = np.random.default_rng(9)
+    cases = [
+        ("x_nonperiodic_5pt_weights", sg.Direction.X, sg.BoundaryMode.NonPeriodic, sg.Extents(2, 2, 0, 0), None, 5),
+        ("y_periodic_5pt_weights", sg.Direction.Y, sg.BoundaryMode.Periodic, sg.Extents(0, 0, 2, 2), None, 5),
+        ("xy_periodic_3x3_weights", sg.Direction.XY, sg.BoundaryMode.Periodic, sg.Extents(1, 1, 1, 1), None, 9),
+        ("xy_periodic_5x5_weights", sg.Direction.XY, sg.BoundaryMode.Periodic, sg.Extents(2, 2, 2, 2), None, 25),
+        ("xy_periodic_9x9_weights", sg.Direction.XY, sg.BoundaryMode.Periodic, sg.Extents(4, 4, 4, 4), None, 81),
+        ("xy_nonperiodic_3x3_weights", sg.Direction.XY, sg.BoundaryMode.NonPeriodic, sg.Extents(1, 1, 1, 1), None, 9),
+        ("xy_periodic_ch_nonlinear_window", sg.Direction.XY, sg.BoundaryMode.Periodic, sg.Extents(1, 1, 1, 1),
+         "ch_nonlinear_window", 9),
+    ]
+    a = torch.rand((n, n), dtype=torch.float64, device="cuda")
+    b = torch.zeros_like(a)
+    stream.wait_stream(torch.cuda.current_stream())
+    res = {}
+    for name, d, mode, ext, fn, nv in cases:
+        vals = list(rng.uniform(-1, 1, nv))
+        kind = sg.WeightStencil(ext, vals) if fn is None else sg.FunctionStencil(ext, fn, vals)
+        plan = sg.create_plan(d, mode, kind, a, b, 1, 1)
+        with torch.cuda.stream(stream):
+            time_plan_steps(sg, torch, plan, 3, stream)
+            tot, _ = time_plan_steps(sg, torch, plan, launches, stream)
+        sg.destroy_plan(plan)
+        ms = tot / launches
+        rows = n - (ext.top + ext.bottom if mode == sg.BoundaryMode.NonPeriodic else 0)
+        cols = n - (ext.left + ext.right if mode == sg.BoundaryMode.NonPeriodic else 0)
+        alg = 8 * (n * n + rows * cols)
+        # FP64 instructions per output point (no FMA contraction: a multiply
+        # and an add per tap; the CH window adds c^3 - c per tap)
+        ops = 5 * nv if fn == "ch_nonlinear_window" else 2 * nv
+        rate = ops * rows * cols / (ms * 1e-3)
+        res[name] = {"gpts_s": rows * cols / (ms * 1e-3) / 1e9, "kernel_ms": ms,
+                     "hbm_frac": alg / (ms * 1e-3) / 1e9 / peak,
+                     "fp64_ops_per_pt": ops, "fp64_frac": rate / FP64_PEAK_OPS}
+    del a, b
+    torch.cuda.empty_cache()
+    return res
 
 
 def bench_ch(sg, torch, n=1024, steps=1000):

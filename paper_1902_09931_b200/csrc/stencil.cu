@@ -479,7 +479,15 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32) k_tma(const __grid_const
   // ---------------- consumers
   const int xb = cx0 + warp * SW + lane * V;
   const bool laneValid = xb < nx;
-  T win[H][E];  // ring: input row t lives in win[t % H]
+  // Weight stencils with tall windows (H >= 5) keep H PENDING OUTPUT
+  // accumulators instead of H input rows: each arriving input row adds its
+  // tap row to every output that needs it. Output o still accumulates its
+  // taps row by row (q ascending, then p) — the reference's order — since
+  // rows arrive top to bottom. Registers: H*V + E instead of H*E (a 9x9
+  // window would otherwise spill).
+  constexpr bool ACC = std::is_same_v<Op, OpWeights> && H >= 5;
+  T win[ACC ? 1 : H][E];  // ring: input row t lives in win[t % H]
+  T pend[ACC ? H : 1][V];  // ACC: output started at local input row u lives in pend[u % H]
   T* __restrict__ orow = a.out + static_cast<long long>(ra - (H - 1)) * nx + xb;
   const bool vecStore = laneValid && xb >= a.col0 && xb + V <= a.col1;
   const long long rowStep = nx;
@@ -491,7 +499,7 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32) k_tma(const __grid_const
 #pragma unroll
     for (int k = 0; k < RPS; ++k) {
       const T* srow = sbase + k * ROW;
-      T* e = win[k % H];
+      T* e = win[ACC ? 0 : k % H];
       const VT c = *reinterpret_cast<const VT*>(srow);
       if constexpr (V == 2) {
         e[L] = c.x;
@@ -509,6 +517,22 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32) k_tma(const __grid_const
       // Output row j uses input rows j-TP .. j+BT = the H most recent rows,
       // oldest in slot (k + 1) % H.
       T res[V];
+      if constexpr (ACC) {
+        // this row is tap row q of the output started q rows ago (slot
+        // (k - q) mod H; RPS is a multiple of H, so slots are compile-time)
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+          T* acc = pend[((k - q) % H + H) % H];
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if (q == 0) acc[v] = T(0);
+#pragma unroll
+            for (int p = 0; p < W; ++p) acc[v] += a.v[q * W + p] * e[v + p];
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) res[v] = pend[(k + 1) % H][v];  // completed (q = H-1 just added)
+      } else {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         if constexpr (std::is_same_v<Op, OpWeights>) {
@@ -526,6 +550,7 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32) k_tma(const __grid_const
             for (int p = 0; p < W; ++p) w[q * W + p] = win[(k + 1 + q) % H][v + p];
           res[v] = Op::template apply<T>(w, a.v, W);
         }
+      }
       }
       if (j >= ra && j < rb) {  // warp-uniform
         if (vecStore) {
