@@ -717,7 +717,17 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
 constexpr int RR_RS = 64;    // rows per stage (default geometry)
 constexpr int RR_RS_WIDE = 128;
 constexpr int RR_NSTG = 5;   // ring slots (= stages resident at the turn)
-constexpr int RG = 8;        // rows per software-pipelined operand group
+// Rows per software-pipelined operand group (>= 2: the first group of a
+// system holds its special rows 0 and 1). Measured (sweep_trace, 1024
+// rows): RG 8 -> 27.3 / 36.3 cycles per row forward / backward, RG 4 ->
+// 26.5 / 34.8, RG 2 -> 25.7 / 34.9 (chain floor 24.6 / 32.8); in the CH
+// step (transposed-input sweeps) RG 4 is fastest: 88.4 us/step at 1024^2
+// against 92.3 (RG 2) and 90.5 (RG 8).
+#ifndef SG_SWEEP_RG
+#define SG_SWEEP_RG 4
+#endif
+constexpr int RG = SG_SWEEP_RG;
+static_assert(RG >= 2, "the first operand group must cover rows 0 and 1");
 // XIN 1 (the CH y-sweep): the forward input is the x-sweep's output zT in
 // ITS layout (zT[b*n + r]: system-major), fetched as 128 B-swizzled 16 x 32
 // tensor boxes into two raw buffers; warp 1's 32 lanes transpose each stage
