@@ -224,6 +224,33 @@ sg_status sg_chd_phase_y(sg_chd_t h, double* ycol, void* stream);
 sg_status sg_chd_combine(sg_chd_t h, const double* currExt, double* prevExt, const double* recv, void* stream);
 sg_status sg_chd_destroy(sg_chd_t* h);
 
+/* P2P form of the same step: the two all-to-alls are fused into the sweeps.
+ * Each sweep kernel TMA-stores every finished stage of its backward pass
+ * straight into the buffer of the rank that consumes it (peer memory over
+ * NVLink: IPC-mapped device pointers, sg_ipc_*), and writes its Woodbury
+ * coefficients to every rank, so the exchange overlaps the recurrence; the
+ * receiving sweep reads its input transposed with the x correction on load,
+ * and the combine applies the y correction. Per step:
+ *   halo exchange; sg_chd_phase_x_p2p; barrier (all ranks);
+ *   sg_chd_phase_y_p2p; barrier; sg_chd_combine_p2p.
+ * The barriers order the peers' writes (e.g. a one-element NCCL all-reduce
+ * on the compute stream). Bitwise identical to the single-GPU stepper.
+ * sg_chd_p2p_buffers returns this rank's receive buffers (to export);
+ * sg_chd_set_peers takes every rank's, in rank order, and reports whether
+ * the path can run (needs nx % 64 == 0, own and nx/world multiples of the
+ * sweep stage height, world <= 8). */
+sg_status sg_chd_p2p_buffers(sg_chd_t h, double** recvX, double** recvY, double** y4xAll, double** y4yAll);
+sg_status sg_chd_set_peers(sg_chd_t h, double* const* recvX, double* const* recvY, double* const* y4xAll,
+                           double* const* y4yAll, int* enabled);
+sg_status sg_chd_phase_x_p2p(sg_chd_t h, const double* currExt, const double* prevExt, void* stream);
+sg_status sg_chd_phase_y_p2p(sg_chd_t h, void* stream);
+sg_status sg_chd_combine_p2p(sg_chd_t h, const double* currExt, double* prevExt, void* stream);
+
+/* CUDA IPC (peer device memory across processes): a handle is 64 bytes. */
+sg_status sg_ipc_get_handle(const void* devPtr, void* handle64);
+sg_status sg_ipc_open_handle(const void* handle64, void** devPtr);
+sg_status sg_ipc_close(void* devPtr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -38,7 +38,8 @@ EXPORTED = [
     "sg_ch_default_params", "sg_ch_validate", "sg_ch_create", "sg_ch_step", "sg_ch_set_state",
     "sg_ch_get_field", "sg_ch_device_field", "sg_ch_status", "sg_ch_destroy", "sg_chd_create",
     "sg_chd_geometry", "sg_chd_init", "sg_chd_phase_x", "sg_chd_phase_y", "sg_chd_combine",
-    "sg_chd_destroy", "sg_ch_diagnostics", "sg_simpson_mean", "sg_s_metric", "sg_k1_metric", "sg_ch_set_step", "sg_weno_advect",
+    "sg_chd_destroy", "sg_chd_p2p_buffers", "sg_chd_set_peers", "sg_chd_phase_x_p2p", "sg_chd_phase_y_p2p",
+    "sg_chd_combine_p2p", "sg_ipc_get_handle", "sg_ipc_open_handle", "sg_ipc_close", "sg_ch_diagnostics", "sg_simpson_mean", "sg_s_metric", "sg_k1_metric", "sg_ch_set_step", "sg_weno_advect",
 ]
 
 
@@ -142,6 +143,14 @@ def lib():
         "sg_chd_phase_y": (C.c_int, [vp, vp, vp]),
         "sg_chd_combine": (C.c_int, [vp, vp, vp, vp, vp]),
         "sg_chd_destroy": (C.c_int, [C.POINTER(vp)]),
+        "sg_chd_p2p_buffers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+        "sg_chd_set_peers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), ip]),
+        "sg_chd_phase_x_p2p": (C.c_int, [vp, vp, vp, vp]),
+        "sg_chd_phase_y_p2p": (C.c_int, [vp, vp]),
+        "sg_chd_combine_p2p": (C.c_int, [vp, vp, vp, vp]),
+        "sg_ipc_get_handle": (C.c_int, [vp, vp]),
+        "sg_ipc_open_handle": (C.c_int, [vp, C.POINTER(vp)]),
+        "sg_ipc_close": (C.c_int, [vp]),
         "sg_ch_diagnostics": (C.c_int, [vp, dp, dp, dp]),
         "sg_ch_set_step": (C.c_int, [vp, C.c_int]),
         "sg_weno_advect": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_double, C.c_double, vp, C.c_int, vp]),

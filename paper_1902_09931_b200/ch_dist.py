@@ -17,6 +17,14 @@ step (cahn_hilliard.cpp:260-328 across GPUs):
 
 Every arithmetic operation is the single-GPU step's, so C^n is bitwise
 identical for every G (tests/test_ch_dist_gpu.py, tests/test_ch_dist.py).
+
+mode="p2p" fuses both all-to-alls into the sweeps (sg_chd_*_p2p): every
+finished backward stage of a sweep is TMA-stored straight into the buffer of
+the rank that consumes it (CUDA IPC-mapped peer memory over NVLink), so the
+exchange overlaps the recurrence, and the Woodbury corrections move to the
+consumers (the y-sweep's load, the combine). Steps 3 and 5 become
+barriers (a one-element NCCL all-reduce on the compute stream). Falls back
+to mode "nccl" when the geometry does not allow it (sg_chd_set_peers).
 """
 from __future__ import annotations
 
@@ -30,7 +38,8 @@ HALO = 2
 
 
 class DistCHStepper:
-    def __init__(self, params, world: int = 1, rank: int = 0, dist=None, device="cuda", transport=None):
+    def __init__(self, params, world: int = 1, rank: int = 0, dist=None, device="cuda", transport=None,
+                 mode: str = "nccl"):
         import torch
         self.torch = torch
         self.p, self.world, self.rank, self.dist = params, world, rank, dist
@@ -57,6 +66,62 @@ class DistCHStepper:
             self.recv = torch.empty(self.own * nx, dtype=dt, device=device)
         self.steps_done = 0
         check(_lib.lib().sg_chd_init(self._h, self._p(self.cur), self._p(self.prev), self._s()))
+        self.mode = "nccl"
+        if mode == "p2p":
+            bufs = [C.c_void_p() for _ in range(4)]
+            check(_lib.lib().sg_chd_p2p_buffers(self._h, *[C.byref(b) for b in bufs]))
+            self.p2p_buffers = [b.value for b in bufs]  # recvX, recvY, y4xAll, y4yAll
+            if transport is not None:
+                transport.register(self)  # peers are wired once every rank exists
+            elif world == 1:
+                self.set_peers([[b] for b in self.p2p_buffers])
+            else:
+                self._ipc_peers()
+
+    # -- P2P wiring
+    def set_peers(self, tables):
+        """tables: for each of (recvX, recvY, y4xAll, y4yAll) the device
+        pointers of every rank, in rank order."""
+        arrs = [(C.c_void_p * self.world)(*t) for t in tables]
+        ok = C.c_int()
+        check(_lib.lib().sg_chd_set_peers(self._h, *arrs, C.byref(ok)))
+        self.mode = "p2p" if ok.value else "nccl"
+        return self.mode == "p2p"
+
+    def _ipc_peers(self):
+        """Exchange CUDA IPC handles of the four receive buffers (all_gather
+        over the process group) and map the peers' buffers."""
+        handles = []
+        for ptr in self.p2p_buffers:
+            h = (C.c_char * 64)()
+            check(_lib.lib().sg_ipc_get_handle(C.c_void_p(ptr), h))
+            handles.append(bytes(h))
+        gathered = [None] * self.world
+        self.dist.all_gather_object(gathered, handles)
+        self._opened = []
+        tables = [[0] * self.world for _ in range(4)]
+        for r in range(self.world):
+            for k in range(4):
+                if r == self.rank:
+                    tables[k][r] = self.p2p_buffers[k]
+                else:
+                    ptr = C.c_void_p()
+                    h = (C.c_char * 64).from_buffer_copy(gathered[r][k])
+                    check(_lib.lib().sg_ipc_open_handle(h, C.byref(ptr)))
+                    self._opened.append(ptr.value)
+                    tables[k][r] = ptr.value
+        ok = self.set_peers(tables)
+        flags = self.torch.tensor([1.0 if ok else 0.0], device=self.cur.device)
+        self.dist.all_reduce(flags, op=self.dist.ReduceOp.MIN)
+        if flags.item() < 1.0:  # every rank must take the same path
+            self.mode = "nccl"
+        self._flag = self.torch.zeros(1, device=self.cur.device)
+
+    def _barrier(self):
+        """Orders the peers' P2P writes before this rank reads them: each
+        rank's all-reduce contribution is queued after its sweep kernel."""
+        if self.transport is None and self.world > 1:
+            self.dist.all_reduce(self._flag)
 
     @staticmethod
     def _p(t):
@@ -85,15 +150,27 @@ class DistCHStepper:
     # -- the split step
     def phase_x(self):
         self._halos()
+        if self.mode == "p2p":
+            check(_lib.lib().sg_chd_phase_x_p2p(self._h, self._p(self.cur), self._p(self.prev), self._s()))
+            return
         check(_lib.lib().sg_chd_phase_x(self._h, self._p(self.cur), self._p(self.prev), self._p(self.send), self._s()))
 
     def phase_y(self):
+        if self.mode == "p2p":
+            self._barrier()
+            check(_lib.lib().sg_chd_phase_y_p2p(self._h, self._s()))
+            return
         self._alltoall(self.ycol, self.send, 0)
         check(_lib.lib().sg_chd_phase_y(self._h, self._p(self.ycol), self._s()))
 
     def phase_combine(self):
-        self._alltoall(self.recv, self.ycol, 1)
-        check(_lib.lib().sg_chd_combine(self._h, self._p(self.cur), self._p(self.prev), self._p(self.recv), self._s()))
+        if self.mode == "p2p":
+            self._barrier()
+            check(_lib.lib().sg_chd_combine_p2p(self._h, self._p(self.cur), self._p(self.prev), self._s()))
+        else:
+            self._alltoall(self.recv, self.ycol, 1)
+            check(_lib.lib().sg_chd_combine(self._h, self._p(self.cur), self._p(self.prev), self._p(self.recv),
+                                            self._s()))
         self.cur, self.prev = self.prev, self.cur
         self.steps_done += 1
 
@@ -109,6 +186,8 @@ class DistCHStepper:
 
     def __del__(self):
         try:
+            for ptr in getattr(self, "_opened", []):
+                _lib.lib().sg_ipc_close(C.c_void_p(ptr))
             if self._h.value:
                 _lib.lib().sg_chd_destroy(C.byref(self._h))
         except Exception:
@@ -123,6 +202,17 @@ class LocalTransport:
     def __init__(self, ranks):
         self.ranks = ranks  # list of DistCHStepper, index = rank
         self.pending = {}
+        self.p2p = []
+
+    def register(self, st):
+        """P2P mode: once all G ranks exist, give each every rank's receive
+        buffers (the simulated 'peer memory' is the other ranks' buffers on
+        the same device)."""
+        self.p2p.append(st)
+        if len(self.p2p) == st.world:
+            tables = [[r.p2p_buffers[k] for r in sorted(self.p2p, key=lambda x: x.rank)] for k in range(4)]
+            for r in self.p2p:
+                r.set_peers(tables)
 
     def halos(self, st):
         # fill st's halos from the neighbours' own rows (periodic ring)

@@ -593,6 +593,28 @@ __global__ void __launch_bounds__(256) k_combine_packed(const double* __restrict
   cpExt[idx] = cb + vv;  // cahn_hilliard.cpp:320
 }
 
+// y-slab, P2P path: the y-sweep results arrive UNcorrected (packed blocks
+// [q][jl][i_local], each straight from rank q's sweep) with every rank's y
+// coefficients in y4All[k*nx + i]; the correction and the update are
+// k_combine's expression (penta.cpp:283-284, cahn_hilliard.cpp:273,320).
+__global__ void __launch_bounds__(256) k_combine_packed_corr(const double* __restrict__ ccExt,
+                                                             double* __restrict__ cpExt,
+                                                             const double* __restrict__ v, int nx, int own, int nxq,
+                                                             int r0, const CorrTables t) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jl = blockIdx.y;
+  pdl_wait();
+  if (i >= nx) return;
+  const int j = r0 + jl;
+  const long long idx = static_cast<long long>(jl + HALO) * nx + i;
+  const int q = i / nxq, c = i - q * nxq;
+  const double w = v[static_cast<long long>(q) * own * nxq + static_cast<long long>(jl) * nxq + c];
+  const double vv = w - (__ldg(t.W[0] + j) * __ldg(t.y4 + i) + __ldg(t.W[1] + j) * __ldg(t.y4 + nx + i) +
+                         __ldg(t.W[2] + j) * __ldg(t.y4 + 2LL * nx + i) + __ldg(t.W[3] + j) * __ldg(t.y4 + 3LL * nx + i));
+  const double cb = 2.0 * ccExt[idx] - cpExt[idx];
+  cpExt[idx] = cb + vv;  // cahn_hilliard.cpp:320
+}
+
 // initial_condition on a slab: global element index k = (r0 + jl)*nx + i.
 __global__ void k_init_slab(unsigned long long seed, double amp, int nx, int own, int r0, double* __restrict__ ext) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -944,8 +966,72 @@ struct ChDist {
   DevicePenta fx, fy;
   RhsParams rp{};
   double *rhsT = nullptr, *y4x = nullptr, *ybuf = nullptr;
+  // P2P path (the all-to-alls fused into the sweeps' final stores): local
+  // scratch + the four buffers the peers write into
+  double *xloc = nullptr, *ycol = nullptr, *recvX = nullptr, *recvY = nullptr, *y4xAll = nullptr,
+         *y4yAll = nullptr;
+  SweepPeers px, py;  // destinations of the x- and y-sweep results
+  bool p2p = false;
   std::vector<void*> allocs;
   cudaStream_t stream = nullptr;
+
+  void alloc_p2p() {
+    if (recvX) return;
+    const size_t slab = static_cast<size_t>(own) * p.nx;
+    xloc = dalloc(slab);
+    ycol = dalloc(static_cast<size_t>(p.ny) * nxq);
+    recvX = dalloc(slab);
+    recvY = dalloc(slab);
+    y4xAll = dalloc(4 * static_cast<size_t>(p.ny));
+    y4yAll = dalloc(4 * static_cast<size_t>(p.nx));
+  }
+
+  // Peer buffers in rank order (device pointers valid in this process:
+  // IPC-mapped peer memory, or other simulated ranks' buffers). Returns
+  // whether the P2P path can run (tile/box divisibility, alignment, TMA).
+  bool set_peers(double* const* rx, double* const* ry, double* const* y4xa, double* const* y4ya) {
+    if (world > 8 || p.nx % 64) return false;
+    px = SweepPeers{};
+    py = SweepPeers{};
+    px.npeer = py.npeer = world;
+    px.prow = nxq;  // x-sweep unknowns i -> the rank owning column block i / nxq
+    py.prow = own;  // y-sweep unknowns j -> the rank owning row block j / own
+    for (int d = 0; d < world; ++d) {
+      px.dst[d] = rx[d] + static_cast<size_t>(rank) * nxq * own;  // my block [i_local][jl]
+      px.y4[d] = y4xa[d];
+      py.dst[d] = ry[d] + static_cast<size_t>(rank) * own * nxq;  // my block [jl][i_local]
+      py.y4[d] = y4ya[d];
+    }
+    px.y4Stride = p.ny;
+    px.y4Off = rank * own;
+    py.y4Stride = p.nx;
+    py.y4Off = rank * nxq;
+    const double* wx[4];
+    for (int k = 0; k < 4; ++k) wx[k] = fx.t.W[k] + static_cast<size_t>(rank) * nxq;
+    p2p = penta_sweep_xin(fx.t, own, p.nx, xloc, rhsT, nullptr, nullptr, y4x, stream, false, false, 0, &px) &&
+          penta_sweep_xin(fy.t, nxq, p.ny, ycol, recvX, wx, y4xAll, ybuf, stream, false, false, own, &py);
+    return p2p;
+  }
+
+  void phase_x_p2p(const double* cur, const double* prev, cudaStream_t s) {
+    const RhsGeom geom{p.nx, own, own + 2 * HALO, HALO, 0, 1};  // row-major RHS
+    launch_rhs(p.nonlinearEnabled, cur, prev, rhsT, geom, rp, s);
+    if (!penta_sweep_xin(fx.t, own, p.nx, xloc, rhsT, nullptr, nullptr, y4x, s, false, true, 0, &px))
+      throw Error(SG_ERR_CUDA, "internal: P2P x-sweep unavailable");
+  }
+
+  void phase_y_p2p(cudaStream_t s) {
+    const double* wx[4];
+    for (int k = 0; k < 4; ++k) wx[k] = fx.t.W[k] + static_cast<size_t>(rank) * nxq;
+    if (!penta_sweep_xin(fy.t, nxq, p.ny, ycol, recvX, wx, y4xAll, ybuf, s, false, true, own, &py))
+      throw Error(SG_ERR_CUDA, "internal: P2P y-sweep unavailable");
+  }
+
+  void combine_p2p(const double* cur, double* prev, cudaStream_t s) {
+    CorrTables ty{{fy.t.W[0], fy.t.W[1], fy.t.W[2], fy.t.W[3]}, y4yAll};
+    k_combine_packed_corr<<<dim3((p.nx + 255) / 256, own), 256, 0, s>>>(cur, prev, recvY, p.nx, own, nxq, r0, ty);
+    check_launch("ch slab combine (P2P) kernel");
+  }
 
   double* dalloc(size_t n) {
     void* q = nullptr;
@@ -1336,6 +1422,93 @@ sg_status sg_chd_combine(sg_chd_t h, const double* currExt, double* prevExt, con
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
     sg::ch_combine_packed(d.p.nx, d.own, d.nxq, currExt, prevExt, recv, s);
     if (!stream) SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+sg_status sg_chd_p2p_buffers(sg_chd_t h, double** recvX, double** recvY, double** y4xAll, double** y4yAll) {
+  return guard2([&] {
+    if (!h) sg::logic("CH slab: destroyed");
+    auto& d = *h->d;
+    SG_CUDA(cudaSetDevice(d.device));
+    d.alloc_p2p();
+    if (recvX) *recvX = d.recvX;
+    if (recvY) *recvY = d.recvY;
+    if (y4xAll) *y4xAll = d.y4xAll;
+    if (y4yAll) *y4yAll = d.y4yAll;
+  });
+}
+
+sg_status sg_chd_set_peers(sg_chd_t h, double* const* recvX, double* const* recvY, double* const* y4xAll,
+                           double* const* y4yAll, int* enabled) {
+  return guard2([&] {
+    if (!h) sg::logic("CH slab: destroyed");
+    if (!recvX || !recvY || !y4xAll || !y4yAll) sg::invalid("CH slab: null peer table");
+    auto& d = *h->d;
+    SG_CUDA(cudaSetDevice(d.device));
+    d.alloc_p2p();
+    const bool ok = sg::rhs_kind() != 0 && d.set_peers(recvX, recvY, y4xAll, y4yAll);
+    if (enabled) *enabled = ok ? 1 : 0;
+  });
+}
+
+sg_status sg_chd_phase_x_p2p(sg_chd_t h, const double* currExt, const double* prevExt, void* stream) {
+  return guard2([&] {
+    if (!h) sg::logic("CH slab: destroyed");
+    auto& d = *h->d;
+    if (!d.p2p) sg::logic("CH slab: P2P path not enabled (sg_chd_set_peers)");
+    SG_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    d.phase_x_p2p(currExt, prevExt, s);
+    if (!stream) SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+sg_status sg_chd_phase_y_p2p(sg_chd_t h, void* stream) {
+  return guard2([&] {
+    if (!h) sg::logic("CH slab: destroyed");
+    auto& d = *h->d;
+    if (!d.p2p) sg::logic("CH slab: P2P path not enabled (sg_chd_set_peers)");
+    SG_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    d.phase_y_p2p(s);
+    if (!stream) SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+sg_status sg_chd_combine_p2p(sg_chd_t h, const double* currExt, double* prevExt, void* stream) {
+  return guard2([&] {
+    if (!h) sg::logic("CH slab: destroyed");
+    auto& d = *h->d;
+    if (!d.p2p) sg::logic("CH slab: P2P path not enabled (sg_chd_set_peers)");
+    SG_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    d.combine_p2p(currExt, prevExt, s);
+    if (!stream) SG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+sg_status sg_ipc_get_handle(const void* devPtr, void* handle64) {
+  return guard2([&] {
+    if (!devPtr || !handle64) sg::invalid("ipc: null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t hd;
+    SG_CUDA(cudaIpcGetMemHandle(&hd, const_cast<void*>(devPtr)));
+    std::memcpy(handle64, &hd, sizeof hd);
+  });
+}
+
+sg_status sg_ipc_open_handle(const void* handle64, void** devPtr) {
+  return guard2([&] {
+    if (!devPtr || !handle64) sg::invalid("ipc: null argument");
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle64, sizeof hd);
+    SG_CUDA(cudaIpcOpenMemHandle(devPtr, hd, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+sg_status sg_ipc_close(void* devPtr) {
+  return guard2([&] {
+    if (devPtr) SG_CUDA(cudaIpcCloseMemHandle(devPtr));
   });
 }
 

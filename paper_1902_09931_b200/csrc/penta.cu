@@ -340,8 +340,15 @@ struct alignas(64) SweepMaps {
   CUtensorMap z;     // 2D {B, n}, box {32, RS}
   CUtensorMap t[5];  // m1, m2, dInv, ap, bp: uniform 1D {n} box {RS}; else 2D like z
   CUtensorMap yc[4]; // XCORR: the previous sweep's Woodbury coefficients y_k[r], 1D {n} box {RS}
-  CUtensorMap zt;    // XIN (k_sweep_res): the input read TRANSPOSED from zT[b*n + r],
-                     // 2D {n, B} box {16, 32}, 128 B swizzle
+  CUtensorMap zt;    // XIN (k_sweep_res): the input read TRANSPOSED, system-major:
+                     // 3D {ztInner, B, n / ztInner} box {16, 32, 1}, 128 B swizzle —
+                     // unknown r of system b at ((r % ztInner), b, r / ztInner): one
+                     // block per source rank on the distributed y-sweep, else one
+  CUtensorMap pz[8]; // P2P: the final (backward) results of unknowns [d*prow, (d+1)*prow)
+                     // go to destination d's buffer (box {32, RS}, at (b, r - d*prow))
+  int ztInner = 0;
+  int npeer = 0;     // 0: final results stay in z
+  int prow = 0;
 };
 
 // Fusions used by the Cahn-Hilliard step (ch.cu):
@@ -354,6 +361,10 @@ struct SweepFuse {
   const double* Wc[4] = {nullptr, nullptr, nullptr, nullptr};
   double* zout = nullptr;
   const double* yc = nullptr;  // XIN: yc[k*n + r], the previous sweep's y_k
+  // P2P: y (this sweep's Woodbury coefficients) also written to every
+  // destination: py4[d][k*y4Stride + y4Off + b]
+  double* py4[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int y4Stride = 0, y4Off = 0;
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) {
@@ -394,6 +405,13 @@ __device__ __forceinline__ void s_tma_2d(void* dst, const CUtensorMap* m, int x,
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           s_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(s_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void s_tma_3d(void* dst, const CUtensorMap* m, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(s_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(z), "r"(s_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void s_tma_1d(void* dst, const CUtensorMap* m, int x, uint64_t* bar) {
@@ -851,7 +869,10 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
       auto load_raw = [&](int g) {
         double* rb = raw + (g & 1) * GEO::RAW;
         s_mbar_expect_tx(&rawfull[g & 1], (RS * 32 + (XIN == 1 ? 4 * RS : 0)) * 8);
-        for (int x = 0; x < RS / 16; ++x) s_tma_2d(rb + x * 512, &maps.zt, g * RS + x * 16, b0, &rawfull[g & 1]);
+        for (int x = 0; x < RS / 16; ++x) {
+          const int r = g * RS + x * 16;
+          s_tma_3d(rb + x * 512, &maps.zt, r % maps.ztInner, b0, r / maps.ztInner, &rawfull[g & 1]);
+        }
         if constexpr (XIN == 1)
           for (int k = 0; k < 4; ++k) s_tma_1d(rb + RS * 32 + k * RS, &maps.yc[k], g * RS, &rawfull[g & 1]);
       };
@@ -933,12 +954,24 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
     }
     // turn: every forward store has landed before those rows are refetched
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // final (backward) results: into z, or (P2P) straight into the buffer of
+    // the destination owning those unknowns — the distributed CH's
+    // all-to-all, overlapped with the recurrence stage by stage
+    auto fstore = [&](int s, int G) {
+      if (maps.npeer == 0) {
+        store(s, G);
+        return;
+      }
+      const int r = G * RS, d = r / maps.prow;
+      s_tma_store_2d(&maps.pz[d], b0, r - d * maps.prow, rr_smem + s * STG);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    };
     // backward stage h (rows of forward stage G = nS-1-h) reuses the slot of
     // backward stage h - NST, which is stored first
     for (int h = keep; h < nS; ++h) {
       const int G = nS - 1 - h, s = G % NST;
       s_mbar_wait(&done[s], (uses(s) + h / NST) & 1);
-      store(s, G + NST);
+      fstore(s, G + NST);
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       load(s, G);
     }
@@ -946,7 +979,7 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
     for (int h = nS - keep; h < nS; ++h) {
       const int G = nS - 1 - h, s = G % NST;
       s_mbar_wait(&done[s], (uses(s) + h / NST + 1) & 1);
-      store(s, G);
+      fstore(s, G);
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     return;
@@ -1165,6 +1198,10 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
     const long long sB = B;
 #pragma unroll
     for (int k = 0; k < 4; ++k) y4[k * sB + b] = y[k];
+    for (int d = 0; d < maps.npeer; ++d)
+      if (fuse.py4[d])
+#pragma unroll
+        for (int k = 0; k < 4; ++k) fuse.py4[d][static_cast<long long>(k) * fuse.y4Stride + fuse.y4Off + b] = y[k];
   }
 }
 
@@ -1192,6 +1229,19 @@ bool encode_map(CUtensorMap* m, const double* p, int rank, uint64_t d0, uint64_t
              CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool encode_map3(CUtensorMap* m, const double* p, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
+                 uint32_t b2, bool swizzle128) {
+  auto enc = tensor_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {d0 * 8, d0 * d1 * 8};
+  const cuuint32_t box[3] = {b0, b1, b2};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // TMA path needs 16 B aligned rows (B even, aligned pointers) and a driver
@@ -1344,17 +1394,35 @@ void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool
 }
 
 bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double* zT, const double* const* Wc,
-                     const double* yc, double* y4, cudaStream_t s, bool pdl, bool launch) {
+                     const double* yc, double* y4, cudaStream_t s, bool pdl, bool launch, int ztInner,
+                     const SweepPeers* peers) {
   // Uniform periodic operator, resident-turn sweep only (the CH sweeps).
   if (!f.uniform || !use_resident_sweep()) return false;
-  if ((reinterpret_cast<uintptr_t>(zT) & 15) || (n & 1)) return false;
+  if (ztInner <= 0) ztInner = n;
+  if ((reinterpret_cast<uintptr_t>(zT) & 15) || (n & 1) || n % ztInner || ztInner % 16) return false;
   if (Wc && (reinterpret_cast<uintptr_t>(yc) & 15)) return false;
   const int rs = sweep_res_rows(B);
   SweepMaps maps;
   if (!sweep_maps(f, B, n, z, &maps, rs)) return false;
-  // zT[b*n + r]: dims {n (inner), B}, box {16 rows, 32 systems}, 128 B swizzle
-  if (!encode_map(&maps.zt, zT, 2, n, B, 16, 32, true)) return false;
+  // zT: unknown r of system b at ((r % ztInner), b, r / ztInner) — dims
+  // {ztInner, B, n / ztInner}, box {16 unknowns, 32 systems, 1}, 128 B swizzle
+  if (!encode_map3(&maps.zt, zT, ztInner, B, n / ztInner, 16, 32, 1, true)) return false;
+  maps.ztInner = ztInner;
+  if (peers && peers->npeer > 0) {
+    if (peers->npeer > 8 || peers->prow % rs || n != peers->npeer * peers->prow) return false;
+    for (int d = 0; d < peers->npeer; ++d) {
+      if (reinterpret_cast<uintptr_t>(peers->dst[d]) & 15) return false;
+      if (!encode_map(&maps.pz[d], peers->dst[d], 2, B, peers->prow, 32, rs)) return false;
+    }
+    maps.npeer = peers->npeer;
+    maps.prow = peers->prow;
+  }
   SweepFuse fuse;
+  if (peers && peers->npeer > 0) {
+    for (int d = 0; d < peers->npeer; ++d) fuse.py4[d] = peers->y4[d];
+    fuse.y4Stride = peers->y4Stride;
+    fuse.y4Off = peers->y4Off;
+  }
   if (Wc) {
     for (int k = 0; k < 4; ++k)
       if (!encode_map(&maps.yc[k], yc + static_cast<size_t>(k) * n, 1, n, 1, rs, 1)) return false;

@@ -64,8 +64,25 @@ bool penta_sweep_fused(const PentaTables& f, int B, int n, double* z, double* y4
 // Wc = nullptr reads zT as is (the CH x-sweep). Results (uncorrected,
 // y -> y4) go to the interleaved z. launch = false only checks
 // availability. Returns false if the path is unavailable.
+// P2P destinations of the final results (the distributed CH sweeps): the
+// unknowns [d*prow, (d+1)*prow) of all B systems go to dst[d] laid out
+// [unknown - d*prow][system] (row length B) — peer memory over NVLink in
+// production; y (the Woodbury coefficients) also goes to
+// y4[d][k*y4Stride + y4Off + b].
+struct SweepPeers {
+  int npeer = 0;
+  int prow = 0;
+  double* dst[8] = {};
+  double* y4[8] = {};
+  int y4Stride = 0, y4Off = 0;
+};
+
+// ztInner: the input's unknowns are stored in blocks of ztInner per system
+// (zT[(r / ztInner)*(B*ztInner) + b*ztInner + r % ztInner]; 0 = n: plain
+// system-major) — the distributed y-sweep reads one block per source rank.
 bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double* zT, const double* const* Wc,
-                     const double* yc, double* y4, cudaStream_t s, bool pdl, bool launch = true);
+                     const double* yc, double* y4, cudaStream_t s, bool pdl, bool launch = true, int ztInner = 0,
+                     const SweepPeers* peers = nullptr);
 
 // lu4_solve, penta.cpp:61-70.
 __device__ __forceinline__ void lu4_solve_dev(const double* K, const int* piv, double* y) {
