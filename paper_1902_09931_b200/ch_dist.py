@@ -91,25 +91,18 @@ class DistCHStepper:
     def _ipc_peers(self):
         """Exchange CUDA IPC handles of the four receive buffers (all_gather
         over the process group) and map the peers' buffers."""
-        handles = []
-        for ptr in self.p2p_buffers:
+        def get_handle(ptr):
             h = (C.c_char * 64)()
             check(_lib.lib().sg_ipc_get_handle(C.c_void_p(ptr), h))
-            handles.append(bytes(h))
-        gathered = [None] * self.world
-        self.dist.all_gather_object(gathered, handles)
-        self._opened = []
-        tables = [[0] * self.world for _ in range(4)]
-        for r in range(self.world):
-            for k in range(4):
-                if r == self.rank:
-                    tables[k][r] = self.p2p_buffers[k]
-                else:
-                    ptr = C.c_void_p()
-                    h = (C.c_char * 64).from_buffer_copy(gathered[r][k])
-                    check(_lib.lib().sg_ipc_open_handle(h, C.byref(ptr)))
-                    self._opened.append(ptr.value)
-                    tables[k][r] = ptr.value
+            return bytes(h)
+
+        def open_handle(hb):
+            ptr = C.c_void_p()
+            check(_lib.lib().sg_ipc_open_handle((C.c_char * 64).from_buffer_copy(hb), C.byref(ptr)))
+            return ptr.value
+
+        tables, self._opened = exchange_peer_tables(self.dist, self.rank, self.world, self.p2p_buffers,
+                                                    get_handle, open_handle)
         ok = self.set_peers(tables)
         flags = self.torch.tensor([1.0 if ok else 0.0], device=self.cur.device)
         self.dist.all_reduce(flags, op=self.dist.ReduceOp.MIN)
@@ -192,6 +185,26 @@ class DistCHStepper:
                 _lib.lib().sg_chd_destroy(C.byref(self._h))
         except Exception:
             pass
+
+
+def exchange_peer_tables(dist, rank, world, local_ptrs, get_handle, open_handle):
+    """All-gather the IPC handles of every rank's receive buffers and map
+    the peers' ones. Returns (tables, opened): tables[k][r] is buffer k of
+    rank r as a pointer valid in this process (this rank's own pointers for
+    r == rank), opened the pointers to close at teardown."""
+    handles = [get_handle(p) for p in local_ptrs]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, handles)
+    tables = [[0] * world for _ in local_ptrs]
+    opened = []
+    for r in range(world):
+        for k in range(len(local_ptrs)):
+            if r == rank:
+                tables[k][r] = local_ptrs[k]
+            else:
+                tables[k][r] = open_handle(gathered[r][k])
+                opened.append(tables[k][r])
+    return tables, opened
 
 
 class LocalTransport:

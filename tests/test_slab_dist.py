@@ -115,3 +115,49 @@ def test_gloo_ch_alltoall_layout(world):
     for p in procs:
         p.join(timeout=60)
     assert all(r[1] == "ok" for r in res), res
+
+
+def _p2p_worker(rank, world, port, q):
+    """P2P wiring of the distributed CH step with fake pointers: the IPC
+    handle of a 'buffer' encodes (rank, k); opening it must yield the peer's
+    pointer, and every rank must see the same rank-ordered tables."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1902_09931_b200.ch_dist import exchange_peer_tables
+
+        def ptr(r, k):
+            return 0x10000000 * (r + 1) + 0x1000 * k
+
+        local = [ptr(rank, k) for k in range(4)]
+        get_handle = lambda p: p.to_bytes(8, "little") * 8  # a 64-byte "handle"
+        opened_log = []
+
+        def open_handle(hb):
+            assert len(hb) == 64
+            p = int.from_bytes(hb[:8], "little")
+            opened_log.append(p)
+            return p + 7  # a mapped alias differs from the exporter's pointer
+
+        tables, opened = exchange_peer_tables(dist, rank, world, local, get_handle, open_handle)
+        ok = all(tables[k][r] == (ptr(r, k) if r == rank else ptr(r, k) + 7)
+                 for k in range(4) for r in range(world))
+        ok = ok and sorted(opened) == sorted(p + 7 for p in opened_log) and len(opened) == 4 * (world - 1)
+        q.put((rank, "ok" if ok else "bad"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ch_p2p_peer_tables(world):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[1] == "ok" for r in res), res
