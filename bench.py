@@ -346,9 +346,40 @@ def extras(sg, torch, stream, peak):
     sg.destroy_plan(plan)
     out["cfg1_512sq_10apps_ms"] = best * 1e3
     out["stencil_variants_16384sq_fp64"] = bench_variants(sg, torch, stream, peak)
+    out["penta_general_periodic"] = bench_penta_general(sg, torch, peak)
     if hasattr(sg, "CHStepper"):
         out.update(bench_ch(sg, torch))
     return out
+
+
+def bench_penta_general(sg, torch, peak, B=65536, n=1024, reps=10):
+    """PeriodicPentaFactor::solve_in_place on a batch of B NON-uniform
+    periodic systems (per-system factor tables, penta.cpp:160-295), rhs
+    device-resident. Bytes per solve: 9 factor tables read + z read and
+    written twice (forward/backward) + the Woodbury correction pass."""
+    import numpy as np
+    rng = np.random.default_rng(3)
+    m = sg.PentaBatch(B, n, True)
+    for band in m.bands():
+        band[:] = rng.uniform(-1, 1, (n, B))
+    m.diag += 6.0
+    f = sg.PeriodicPentaFactor(m)
+    rhs = torch.rand((n, B), dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        f.solve_in_place(rhs)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        f.solve_in_place(rhs)
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    alg = (9 + 4 + 2) * B * n * 8  # tables + sweep z traffic + correction (read+write)
+    del f, rhs
+    torch.cuda.empty_cache()
+    return {"batch": B, "n": n, "solve_ms": ms, "unknowns_per_s": B * n / (ms * 1e-3),
+            "hbm_frac": alg / (ms * 1e-3) / 1e9 / peak}
 
 
 def bench_variants(sg, torch, stream, peak, n=16384, launches=20):

@@ -1091,6 +1091,14 @@ struct sg_penta_s {
   std::unique_ptr<sg::DevicePenta> f;
   int device = 0;
   cudaStream_t stream = nullptr;
+  // solve scratch, allocated once (per-call stream-ordered allocations cost
+  // milliseconds once the pool has released them)
+  double* y4 = nullptr;   // periodic: y = K^{-1} V^T z, 4 x B
+  double* tmp = nullptr;  // host-memory solves: device copy of the rhs
+  ~sg_penta_s() {
+    if (y4) cudaFree(y4);
+    if (tmp) cudaFree(tmp);
+  }
 };
 
 // Reuse the error plumbing of capi.cu through these two helpers.
@@ -1314,19 +1322,15 @@ sg_status sg_penta_solve(sg_penta_t f, double* rhs, sg_memory memory, void* stre
     const int B = f->f->B, n = f->f->n;
     const size_t bytes = static_cast<size_t>(B) * n * sizeof(double);
     double* z = rhs;
-    double* tmp = nullptr;
     if (memory == SG_MEM_HOST) {
-      SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), bytes, s));
-      SG_CUDA(cudaMemcpyAsync(tmp, rhs, bytes, cudaMemcpyHostToDevice, s));
-      z = tmp;
+      if (!f->tmp) SG_CUDA(cudaMalloc(reinterpret_cast<void**>(&f->tmp), bytes));
+      SG_CUDA(cudaMemcpyAsync(f->tmp, rhs, bytes, cudaMemcpyHostToDevice, s));
+      z = f->tmp;
     }
-    double* y4 = nullptr;
-    if (f->f->periodic) SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&y4), 4 * sizeof(double) * B, s));
-    sg::penta_sweep(f->f->t, B, n, z, y4, f->f->periodic, false, s);
-    if (y4) SG_CUDA(cudaFreeAsync(y4, s));
+    if (f->f->periodic && !f->y4) SG_CUDA(cudaMalloc(reinterpret_cast<void**>(&f->y4), 4 * sizeof(double) * B));
+    sg::penta_sweep(f->f->t, B, n, z, f->f->periodic ? f->y4 : nullptr, f->f->periodic, false, s);
     if (memory == SG_MEM_HOST) {
-      SG_CUDA(cudaMemcpyAsync(rhs, tmp, bytes, cudaMemcpyDeviceToHost, s));
-      SG_CUDA(cudaFreeAsync(tmp, s));
+      SG_CUDA(cudaMemcpyAsync(rhs, f->tmp, bytes, cudaMemcpyDeviceToHost, s));
       synchronize = 1;
     }
     if (synchronize) SG_CUDA(cudaStreamSynchronize(s));

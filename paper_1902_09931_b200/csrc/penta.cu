@@ -145,6 +145,23 @@ __device__ bool lu4_factor(double* K, int* piv) {
 }
 
 // penta.cpp:204-251, one thread per system (uniform: a single thread).
+// The four core solves W_k = P^{-1} e_{0,1,n-2,n-1} of every system
+// (penta.cpp:219-227) are independent: blockIdx.y = k, one thread per
+// system and k (4x the parallelism of one thread per system).
+__global__ void k_periodic_core(PentaTables f, int B, int n, double* W0, double* W1, double* W2, double* W3) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int k = blockIdx.y;
+  const long long s = B;
+  double* Wk = (k == 0 ? W0 : k == 1 ? W1 : k == 2 ? W2 : W3) + b;
+  const int row = k == 0 ? 0 : k == 1 ? 1 : k == 2 ? n - 2 : n - 1;
+  for (int r = 0; r < n; ++r) Wk[r * s] = 0.0;
+  Wk[row * s] = 1.0;
+  substitute(f, B, b, Wk, s, n);
+}
+
+// Corner coefficients, capacitance K = I + V^T W and its 4x4 LU
+// (penta.cpp:210-217, 229-250) from the W_k of k_periodic_core.
 __global__ void k_periodic_setup(PentaTables f, int B, int n, const double* __restrict__ e,
                                  const double* __restrict__ c, const double* __restrict__ a,
                                  const double* __restrict__ bb, double* W0, double* W1, double* W2,
@@ -154,12 +171,6 @@ __global__ void k_periodic_setup(PentaTables f, int B, int n, const double* __re
   if (b >= nsys) return;
   const long long s = f.uniform ? 1 : B;
   double* Wk[4] = {W0 + b, W1 + b, W2 + b, W3 + b};
-  const int rowOf[4] = {0, 1, n - 2, n - 1};
-  for (int k = 0; k < 4; ++k) {
-    for (int r = 0; r < n; ++r) Wk[k][r * s] = 0.0;
-    Wk[k][rowOf[k] * s] = 1.0;
-    substitute(f, B, b, Wk[k], s, n);
-  }
   double cwl[6] = {e[b], c[b], e[s + b], bb[(n - 2) * s + b], a[(n - 1) * s + b], bb[(n - 1) * s + b]};
   for (int k = 0; k < 6; ++k) cw[b * 6 + k] = cwl[k];
   double Kl[16];
@@ -1525,9 +1536,12 @@ void DevicePenta::build(int B_, int n_, bool periodic_, bool uniform, const doub
   // stride 1: pass the single-system bands.
   if (uniform)
     k_periodic_setup_uniform<<<1, 4, 0, s>>>(t, n, e, c, a, b, W[0], W[1], W[2], W[3], cw, K, piv, dBad);
-  else
+  else {
+    k_periodic_core<<<dim3((nsys + 127) / 128, 4), 128, 0, s>>>(t, B, n, W[0], W[1], W[2], W[3]);
+    check_launch("penta periodic core-solve kernel");
     k_periodic_setup<<<(nsys + 127) / 128, 128, 0, s>>>(t, B, n, e, c, a, b, W[0], W[1], W[2], W[3], cw, K,
                                                       piv, dBad);
+  }
   check_launch("penta periodic setup kernel");
   SG_CUDA(cudaMemcpyAsync(bad.data(), dBad, sizeof(int) * nsys, cudaMemcpyDeviceToHost, s));
   SG_CUDA(cudaStreamSynchronize(s));
