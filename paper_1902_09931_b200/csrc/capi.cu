@@ -465,6 +465,7 @@ sg_status sg_weno_advect(const double* phi, const double* u, const double* v, in
       return;
     }
     double* d = nullptr;
+    sg::retain_async_pool();
     SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 4 * bytes, s));
     double* dp = d;
     double* du = d + static_cast<size_t>(nx) * ny;

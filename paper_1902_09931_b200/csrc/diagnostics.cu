@@ -17,6 +17,9 @@
 #include <cuda_runtime.h>
 #include <cufft.h>
 
+#include <map>
+#include <tuple>
+
 #include <cmath>
 #include <string>
 
@@ -120,6 +123,7 @@ __global__ void k_k1_final(const double* __restrict__ part, int nb, double* out)
 void device_simpson(const double* v, int nx, int ny, bool square, double* out, cudaStream_t s) {
   if (nx % 2 != 0 || ny % 2 != 0) invalid("simpson_mean: nx and ny must be even");
   double* buf = nullptr;
+  retain_async_pool();
   SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(double) * (ny + 1), s));
   if (square)
     k_simpson_rows<true><<<(ny + DT - 1) / DT, DT, 0, s>>>(v, nx, ny, buf);
@@ -133,24 +137,46 @@ void device_simpson(const double* v, int nx, int ny, bool square, double* out, c
   SG_CUDA(cudaStreamSynchronize(s));
 }
 
+// cuFFT plans are created once per (thread, device, grid) and kept
+// (creating one costs more than the transform at the diagnostics cadence).
+// Per thread: a plan's work area must not be shared by concurrent calls.
+cufftHandle cached_plan(int nx, int ny) {
+  struct Cache {
+    std::map<std::tuple<int, int, int>, cufftHandle> plans;
+    ~Cache() {
+      for (auto& kv : plans) cufftDestroy(kv.second);
+    }
+  };
+  thread_local Cache cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, nx, ny);
+  auto it = cache.plans.find(key);
+  if (it != cache.plans.end()) return it->second;
+  cufftHandle plan;
+  if (cufftPlan2d(&plan, ny, nx, CUFFT_Z2Z) != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftPlan2d failed");
+  cache.plans[key] = plan;
+  return plan;
+}
+
 // k1 = num/den over the FFT spectrum; throws domain_error-class on den == 0.
 double device_k1(const double* v, int nx, int ny, double dx, double dy, cudaStream_t s) {
   if (nx < 1 || ny < 1 || (nx & (nx - 1)) || (ny & (ny - 1)))
     invalid("fft_2d: grid dimensions must be powers of two");
   const long long n = static_cast<long long>(nx) * ny;
   cufftDoubleComplex* c = nullptr;
+  retain_async_pool();
   SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(cufftDoubleComplex) * n, s));
   k_to_complex<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(v, n, c);
   check_launch("k1 complex kernel");
-  cufftHandle plan;
-  if (cufftPlan2d(&plan, ny, nx, CUFFT_Z2Z) != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftPlan2d failed");
+  const cufftHandle plan = cached_plan(nx, ny);
   cufftSetStream(plan, s);
   const cufftResult fr = cufftExecZ2Z(plan, c, c, CUFFT_FORWARD);
   count_launch();
-  cufftDestroy(plan);
   if (fr != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftExecZ2Z failed");
   const int nb = 296;
   double* part = nullptr;
+  retain_async_pool();
   SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * (2 * nb + 2), s));
   const double kxScale = 2.0 * 3.14159265358979323846 / (dx * nx);
   const double kyScale = 2.0 * 3.14159265358979323846 / (dy * ny);
@@ -197,6 +223,7 @@ struct DevField {
       p = f;
       return;
     }
+    sg::retain_async_pool();
     SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double) * n, s));
     SG_CUDA(cudaMemcpyAsync(tmp, f, sizeof(double) * n, cudaMemcpyHostToDevice, s));
     p = tmp;

@@ -29,6 +29,24 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 #define SG_CUDA(x) ::sg::cuda_check((x), #x)
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the device's default
+// memory pool; with the pool's default release threshold (0) every
+// synchronisation hands the memory back and the next allocation costs
+// milliseconds. Keep it (once per device) so per-call scratch is cheap.
+inline void retain_async_pool() {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return;
+  const uint64_t bit = 1ull << dev;
+  if (done.load() & bit) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done.fetch_or(bit);
+}
+
 // Number of kernels launched by this library (reported as gpu_launches).
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }

@@ -802,6 +802,7 @@ int launch_typed(const sg_slab_desc& d, const sg_extents& e, int fn, const doubl
 
   T* wtmp = nullptr;
   if (fn == SG_FN_NONE && count > static_cast<size_t>(VMAX)) {
+    retain_async_pool();
     SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wtmp), count * sizeof(T), s));
     T* hw = new T[count];
     for (size_t k = 0; k < count; ++k) hw[k] = static_cast<T>(values[k]);
