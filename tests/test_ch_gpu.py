@@ -193,3 +193,36 @@ def test_steady_state_step_many_bitwise(sg, orc, nx, ny, nonlinear):
         assert bits_equal(st.field().values, want_c), (k, done)
         assert bits_equal(st.previous_field().values, want_p), (k, done)
         assert st.step_index() == done
+
+
+@pytest.mark.parametrize("env,nx,ny", [
+    ({"SG_SWEEP_RS": "64"}, 128, 128),     # 64-row stages (large batches' geometry), XIN modes 1/2
+    ({"SG_SWEEP_RS": "64"}, 256, 64),
+    ({"SG_CH_XIN": "0"}, 128, 64),          # separate transpose/correct kernel
+    ({"SG_PDL": "0"}, 128, 128),            # plain stream-ordered launches
+    ({"SG_CH_STEADY": "0"}, 128, 128),      # combine not folded into the next RHS
+])
+def test_step_variants_bitwise(orc, env, nx, ny):
+    """Every selectable CH pipeline variant gives the reference's bits
+    (each runs in a fresh process: the selections are read once)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.');"
+        "import paper_1902_09931_b200 as sg;"
+        f"p = sg.CHParams(nx={nx}, ny={ny}); p.dt = 0.1 * p.dx(); p.T = 1.0;"
+        "st = sg.CHStepper(p); st.step_many(9);"
+        "np.save(sys.argv[1], np.stack([st.field().values, st.previous_field().values]))")
+    root = Path(__file__).resolve().parents[1]
+    out = f"/tmp/ch_variant_{os.getpid()}.npy"
+    r = subprocess.run([sys.executable, "-c", code, out], cwd=root, env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = np.load(out)
+    p = dict(D=1.0, gamma=0.01, lx=2 * math.pi, ly=2 * math.pi, dt=0.1 * (2 * math.pi / nx), nx=nx, ny=ny)
+    c0 = orc.ch_initial_condition(nx, ny)
+    want_c, want_p = orc.ch_run(p, 9, c0, c0)
+    assert bits_equal(got[0], want_c)
+    assert bits_equal(got[1], want_p)

@@ -125,3 +125,18 @@ def test_device_resident_rhs(sg, orc):
     t = torch.from_numpy(rhs.copy()).cuda()
     f.solve_in_place(t)
     assert bits_equal(t.cpu().numpy(), orc.penta_solve(True, m.bands(), rhs))
+
+
+@pytest.mark.parametrize("periodic", [False, True])
+def test_uniform_large_batch_bitwise(sg, orc, periodic):
+    """A uniform operator over more systems than one CTA per SM (B = 8192:
+    the resident-turn sweep's 64-row-stage geometry, two CTAs per SM),
+    device-resident rhs, bitwise vs the oracle."""
+    import torch
+    B, n = 8192, 96
+    m = sg.build_hyperdiffusion_operator(2.5, n, B, periodic)
+    rhs = np.random.default_rng(8).uniform(-1, 1, (n, B))
+    f = sg.PeriodicPentaFactor(m) if periodic else sg.PentaFactor(m)
+    t = torch.from_numpy(rhs.copy()).cuda()
+    f.solve_in_place(t)
+    assert bits_equal(t.cpu().numpy(), orc.penta_solve(periodic, m.bands(), rhs))
