@@ -226,3 +226,37 @@ def test_step_variants_bitwise(orc, env, nx, ny):
     want_c, want_p = orc.ch_run(p, 9, c0, c0)
     assert bits_equal(got[0], want_c)
     assert bits_equal(got[1], want_p)
+
+
+def test_config3_1000_steps_bitwise_vs_reference(sg, ref):
+    """BASELINE config 3 in full: 1024^2, 1000 steps, against the UNMODIFIED
+    reference CHStepper (oracle/_ref) run on this host's cores — every bit of
+    both time levels (north-star bar: 1e-9 relative L2)."""
+    import os
+    n, steps = 1024, 1000
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    p = params(sg, n)
+    st = sg.CHStepper(p)
+    st.step_many(steps)
+    rp = dict(D=p.D, gamma=p.gamma, lx=p.lx, ly=p.ly, dt=p.dt, T=p.T, nx=n, ny=n, seed=1, amp=0.1, nonlinear=True)
+    want_c, want_p = ref.ch_run(rp, steps, tiles=cores, workers=cores)
+    got = st.field().values
+    rel = np.linalg.norm(got - want_c) / np.linalg.norm(want_c)
+    assert rel <= 1e-9
+    assert bits_equal(got, want_c)
+    assert bits_equal(st.previous_field().values, want_p)
+
+
+def test_config5_grid_steps_bitwise_vs_reference(sg, ref):
+    """Config 5's grid (8192^2) on one GPU — the 64-row-stage sweeps, the
+    steady-state step — against the reference CHStepper, 3 steps, bitwise."""
+    import os
+    n, steps = 8192, 3
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    p = params(sg, n)
+    st = sg.CHStepper(p)
+    st.step_many(steps)
+    rp = dict(D=p.D, gamma=p.gamma, lx=p.lx, ly=p.ly, dt=p.dt, T=p.T, nx=n, ny=n, seed=1, amp=0.1, nonlinear=True)
+    want_c, want_p = ref.ch_run(rp, steps, tiles=cores, workers=cores)
+    assert bits_equal(st.field().values, want_c)
+    assert bits_equal(st.previous_field().values, want_p)
