@@ -587,3 +587,27 @@ def test_config4_full_bitwise_vs_reference(sg, ref):
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     want = ref.stencil(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3", tiles=cores, workers=cores)
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_config4_full_fp32_within_1e5_of_reference(sg, ref):
+    """BASELINE config 4, FP32 half: 32768^2 XY periodic fn_weighted_3x3 in
+    FP32 against the reference (FP64) on the float-rounded input, normwise
+    max |err| <= 1e-5 max |ref| over all 2^30 points (north-star bar)."""
+    import os
+    import torch
+    n = 32768
+    w = list(np.random.default_rng(40).uniform(-1, 1, 9))
+    g = torch.Generator(device="cuda").manual_seed(40)
+    a = torch.rand((n, n), dtype=torch.float32, device="cuda", generator=g).mul_(2).sub_(1)
+    b = torch.empty_like(a)
+    plan = sg.create_plan(sg.Direction.XY, sg.BoundaryMode.Periodic,
+                          sg.FunctionStencil(sg.Extents(1, 1, 1, 1), "fn_weighted_3x3", w), a, b, 1, 1)
+    sg.compute(plan)
+    inp = a.cpu().numpy().astype(np.float64)
+    got = b.cpu().numpy()
+    del a, b
+    torch.cuda.empty_cache()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    want = ref.stencil(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3", tiles=cores, workers=cores)
+    err = float(np.max(np.abs(got.astype(np.float64) - want)))
+    assert err <= 1e-5 * float(np.max(np.abs(want)))
