@@ -554,6 +554,10 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--slab", action="store_true",
                     help="use the multi-GPU y-slab path even at N=1 (NCCL world of one)")
+    ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
+                    help="multi-GPU halo exchange: p2p = fused into the stencil kernel (the boundary rows are "
+                         "stored into the neighbours' buffers over NVLink, CUDA IPC), falling back to nccl "
+                         "(torch.distributed P2P overlapped with the interior rows) if peer mapping fails")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -137,6 +137,15 @@ typedef struct sg_slab_desc {
 sg_status sg_stencil_launch(const sg_slab_desc* desc, sg_extents ext, sg_function fn,
                             const double* values, size_t count, sg_dtype dtype, const void* in,
                             void* out, void* stream);
+/* Same launch, fused with the halo exchange of the NEXT application: output
+ * rows j < upRows are also stored to peerUp + j*nx (the up neighbour's
+ * bottom halo rows, in its output buffer), rows j >= dnRow0 to
+ * peerDn + (j - dnRow0)*nx (the down neighbour's top halo) — peer device
+ * memory over NVLink (sg_ipc_*). NULL peers are skipped. The caller orders
+ * the peers' writes with a barrier between applications. */
+sg_status sg_stencil_launch_p2p(const sg_slab_desc* desc, sg_extents ext, sg_function fn, const double* values,
+                                size_t count, sg_dtype dtype, const void* in, void* out, void* peerUp, int upRows,
+                                void* peerDn, int dnRow0, void* stream);
 
 /* --------------------------------------------------------- WENO5 advection
  * weno_advect (weno.cpp:50-94): out = -(u dphi/dx + v dphi/dy) with
@@ -246,8 +255,10 @@ sg_status sg_chd_phase_x_p2p(sg_chd_t h, const double* currExt, const double* pr
 sg_status sg_chd_phase_y_p2p(sg_chd_t h, void* stream);
 sg_status sg_chd_combine_p2p(sg_chd_t h, const double* currExt, double* prevExt, void* stream);
 
-/* CUDA IPC (peer device memory across processes): a handle is 64 bytes. */
-sg_status sg_ipc_get_handle(const void* devPtr, void* handle64);
+/* CUDA IPC (peer device memory across processes): a handle is 64 bytes and
+ * names the allocation containing devPtr; *offset is devPtr's byte offset in
+ * it (add it to the pointer sg_ipc_open_handle returns). */
+sg_status sg_ipc_get_handle(const void* devPtr, void* handle64, size_t* offset);
 sg_status sg_ipc_open_handle(const void* handle64, void** devPtr);
 sg_status sg_ipc_close(void* devPtr);
 

@@ -34,7 +34,7 @@ EXPORTED = [
     "sg_function_min_coe", "sg_function_name", "sg_wrap", "sg_make_tiles", "sg_plan_create",
     "sg_plan_compute", "sg_plan_swap", "sg_plan_destroy", "sg_plan_sync_to_host",
     "sg_plan_mark_host_dirty", "sg_plan_binding", "sg_plan_valid", "sg_plan_kernel_kind",
-    "sg_stencil_launch", "sg_penta_create", "sg_penta_solve", "sg_penta_destroy",
+    "sg_stencil_launch", "sg_stencil_launch_p2p", "sg_penta_create", "sg_penta_solve", "sg_penta_destroy",
     "sg_ch_default_params", "sg_ch_validate", "sg_ch_create", "sg_ch_step", "sg_ch_set_state",
     "sg_ch_get_field", "sg_ch_device_field", "sg_ch_status", "sg_ch_destroy", "sg_chd_create",
     "sg_chd_geometry", "sg_chd_init", "sg_chd_phase_x", "sg_chd_phase_y", "sg_chd_combine",
@@ -123,6 +123,8 @@ def lib():
         "sg_plan_kernel_kind": (C.c_int, [vp]),
         "sg_stencil_launch": (C.c_int, [C.POINTER(SgSlabDesc), SgExtents, C.c_int, dp, C.c_size_t,
                                         C.c_int, vp, vp, vp]),
+        "sg_stencil_launch_p2p": (C.c_int, [C.POINTER(SgSlabDesc), SgExtents, C.c_int, dp, C.c_size_t,
+                                            C.c_int, vp, vp, vp, C.c_int, vp, C.c_int, vp]),
         "sg_penta_create": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_int,
                                       C.POINTER(vp)]),
         "sg_penta_solve": (C.c_int, [vp, vp, C.c_int, vp, C.c_int]),
@@ -148,7 +150,7 @@ def lib():
         "sg_chd_phase_x_p2p": (C.c_int, [vp, vp, vp, vp]),
         "sg_chd_phase_y_p2p": (C.c_int, [vp, vp]),
         "sg_chd_combine_p2p": (C.c_int, [vp, vp, vp, vp]),
-        "sg_ipc_get_handle": (C.c_int, [vp, vp]),
+        "sg_ipc_get_handle": (C.c_int, [vp, vp, C.POINTER(C.c_size_t)]),
         "sg_ipc_open_handle": (C.c_int, [vp, C.POINTER(vp)]),
         "sg_ipc_close": (C.c_int, [vp]),
         "sg_ch_diagnostics": (C.c_int, [vp, dp, dp, dp]),

@@ -91,17 +91,8 @@ class DistCHStepper:
     def _ipc_peers(self):
         """Exchange CUDA IPC handles of the four receive buffers (all_gather
         over the process group) and map the peers' buffers."""
-        def get_handle(ptr):
-            h = (C.c_char * 64)()
-            check(_lib.lib().sg_ipc_get_handle(C.c_void_p(ptr), h))
-            return bytes(h)
-
-        def open_handle(hb):
-            ptr = C.c_void_p()
-            check(_lib.lib().sg_ipc_open_handle((C.c_char * 64).from_buffer_copy(hb), C.byref(ptr)))
-            return ptr.value
-
-        tables, self._opened = exchange_peer_tables(self.dist, self.rank, self.world, self.p2p_buffers,
+        get_handle, open_handle, self._opened = ipc_handle_functions()
+        tables, _ = exchange_peer_tables(self.dist, self.rank, self.world, self.p2p_buffers,
                                                     get_handle, open_handle)
         ok = self.set_peers(tables)
         flags = self.torch.tensor([1.0 if ok else 0.0], device=self.cur.device)
@@ -185,6 +176,28 @@ class DistCHStepper:
                 _lib.lib().sg_chd_destroy(C.byref(self._h))
         except Exception:
             pass
+
+
+def ipc_handle_functions():
+    """(get_handle, open_handle, bases) over the C ABI's CUDA IPC calls. A
+    handle is the 64-byte IPC handle of the allocation plus the pointer's
+    offset in it; opening maps the peer's allocation (its base is appended
+    to `bases`, for sg_ipc_close) and re-applies the offset."""
+    bases = []
+
+    def get_handle(ptr):
+        h = (C.c_char * 64)()
+        off = C.c_size_t()
+        check(_lib.lib().sg_ipc_get_handle(C.c_void_p(ptr), h, C.byref(off)))
+        return bytes(h) + off.value.to_bytes(8, "little")
+
+    def open_handle(hb):
+        ptr = C.c_void_p()
+        check(_lib.lib().sg_ipc_open_handle((C.c_char * 64).from_buffer_copy(hb[:64]), C.byref(ptr)))
+        bases.append(ptr.value)
+        return ptr.value + int.from_bytes(hb[64:72], "little")
+
+    return get_handle, open_handle, bases
 
 
 def exchange_peer_tables(dist, rank, world, local_ptrs, get_handle, open_handle):

@@ -498,4 +498,27 @@ sg_status sg_stencil_launch(const sg_slab_desc* desc, sg_extents ext, sg_functio
   });
 }
 
+sg_status sg_stencil_launch_p2p(const sg_slab_desc* desc, sg_extents ext, sg_function fn, const double* values,
+                                size_t count, sg_dtype dtype, const void* in, void* out, void* peerUp, int upRows,
+                                void* peerDn, int dnRow0, void* stream) {
+  return guard([&] {
+    if (!desc) sg::invalid("stencil_launch: null descriptor");
+    const sg_slab_desc& d = *desc;
+    if (d.nx < 1 || d.inRows < 1) sg::invalid("stencil_launch: empty input");
+    if (d.col0 < 0 || d.col1 > d.nx || d.row0 < 0) sg::invalid("stencil_launch: bad output window");
+    if (!d.wrapY && d.row1 > d.row0 &&
+        (d.row0 + d.inShift - ext.top < 0 || d.row1 - 1 + d.inShift + ext.bottom >= d.inRows))
+      sg::invalid("stencil_launch: rows outside the input slab (missing halo)");
+    if (in == out) sg::invalid("stencil_launch: input and output must be distinct buffers");
+    if (upRows < 0 || dnRow0 < 0) sg::invalid("stencil_launch: bad P2P row range");
+    require_device();
+    sg::PeerRows pr;
+    pr.up = peerUp;
+    pr.dn = peerDn;
+    pr.upRows = upRows;
+    pr.dnRow0 = dnRow0;
+    sg::launch_stencil(d, ext, fn, values, count, dtype, in, out, static_cast<cudaStream_t>(stream), pr);
+  });
+}
+
 }  // extern "C"

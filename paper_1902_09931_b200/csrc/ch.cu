@@ -28,6 +28,7 @@
 // whose weight is exactly 0.0 (4 of the 9 nonlinear coefficients, 12 of the
 // 25 biharmonic weights — verified at construction) are skipped; for finite
 // fields acc + 0*x == acc exactly (acc starts at +0 and is never -0).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -1491,13 +1492,30 @@ sg_status sg_chd_combine_p2p(sg_chd_t h, const double* currExt, double* prevExt,
   });
 }
 
-sg_status sg_ipc_get_handle(const void* devPtr, void* handle64) {
+sg_status sg_ipc_get_handle(const void* devPtr, void* handle64, size_t* offset) {
   return guard2([&] {
-    if (!devPtr || !handle64) sg::invalid("ipc: null argument");
+    if (!devPtr || !handle64 || !offset) sg::invalid("ipc: null argument");
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    // the handle names the whole allocation (e.g. a caching allocator's
+    // segment): report where devPtr lies inside it
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange get_range = [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        fn = nullptr;
+      return reinterpret_cast<GetRange>(fn);
+    }();
+    if (!get_range) throw sg::Error(SG_ERR_CUDA, "ipc: cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(devPtr)) != CUDA_SUCCESS)
+      throw sg::Error(SG_ERR_CUDA, "ipc: cuMemGetAddressRange failed");
     cudaIpcMemHandle_t hd;
-    SG_CUDA(cudaIpcGetMemHandle(&hd, const_cast<void*>(devPtr)));
+    SG_CUDA(cudaIpcGetMemHandle(&hd, reinterpret_cast<void*>(base)));
     std::memcpy(handle64, &hd, sizeof hd);
+    *offset = static_cast<size_t>(reinterpret_cast<CUdeviceptr>(devPtr) - base);
   });
 }
 

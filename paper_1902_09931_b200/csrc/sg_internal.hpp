@@ -85,10 +85,18 @@ void launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   cuda_check(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), "cudaLaunchKernelEx");
 }
 
+// P2P halo forwarding of a slab launch (see KArgs in stencil.cu).
+struct PeerRows {
+  void* up = nullptr;
+  void* dn = nullptr;
+  int upRows = 0, dnRow0 = 0;
+};
+
 // Stencil launch (stencil.cu). `values` are the weights (fn == SG_FN_NONE) or
 // the function coefficients; returns the kernel kind used (1 fast, 0 generic).
 int launch_stencil(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,
-                   size_t count, sg_dtype dtype, const void* in, void* out, cudaStream_t stream);
+                   size_t count, sg_dtype dtype, const void* in, void* out, cudaStream_t stream,
+                   const PeerRows& peers = PeerRows{});
 // Which kernel launch_stencil would pick, without launching.
 int stencil_kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size_t count,
                         sg_dtype dtype, const void* in, const void* out);

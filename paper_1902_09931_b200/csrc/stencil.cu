@@ -54,8 +54,23 @@ struct KArgs {
   int left, right, top, bottom;
   int segRows;
   int count;
+  // P2P halo forwarding (multi-GPU y-slabs): output rows j < upRows are
+  // also stored to peerUp + j*nx (the up neighbour's bottom halo), rows
+  // j >= dnRow0 to peerDn + (j - dnRow0)*nx (the down neighbour's top
+  // halo) — peer memory over NVLink; null = none
+  T* peerUp;
+  T* peerDn;
+  int upRows, dnRow0;
   T v[VMAX];
 };
+
+// Store one output value (and its P2P halo copies).
+template <typename T>
+__device__ __forceinline__ void put_out(const KArgs<T>& a, long long j, long long i, T v) {
+  a.out[j * a.nx + i] = v;
+  if (a.peerUp && j < a.upRows) a.peerUp[j * a.nx + i] = v;
+  if (a.peerDn && j >= a.dnRow0) a.peerDn[(j - a.dnRow0) * a.nx + i] = v;
+}
 
 // ----------------------------------------------------------- window ops
 // Device twins of the reference's window functions. Same expression trees,
@@ -570,10 +585,14 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32) k_tma(const __grid_const
             o.w = res[3];
           }
           *reinterpret_cast<VT*>(orow) = o;
+          if (a.peerUp && j < a.upRows)  // warp-uniform
+            *reinterpret_cast<VT*>(a.peerUp + static_cast<long long>(j) * nx + xb) = o;
+          if (a.peerDn && j >= a.dnRow0)
+            *reinterpret_cast<VT*>(a.peerDn + static_cast<long long>(j - a.dnRow0) * nx + xb) = o;
         } else if (laneValid) {
 #pragma unroll
           for (int v = 0; v < V; ++v)
-            if (xb + v >= a.col0 && xb + v < a.col1) orow[v] = res[v];
+            if (xb + v >= a.col0 && xb + v < a.col1) put_out(a, j, xb + v, res[v]);
         }
       }
       ++j;
@@ -606,7 +625,7 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T
         acc += wt[q * W + p] * rowp[c];
       }
     }
-    a.out[static_cast<long long>(j) * a.nx + i] = acc;
+    put_out(a, j, i, acc);
   } else {
     T w[GENERIC_FN_MAX];
     for (int q = 0; q < H; ++q) {
@@ -619,7 +638,7 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T
         w[q * W + p] = rowp[c];
       }
     }
-    a.out[static_cast<long long>(j) * a.nx + i] = Op::template apply<T>(w, a.v, W);
+    put_out(a, j, i, Op::template apply<T>(w, a.v, W));
   }
 }
 
@@ -755,7 +774,7 @@ void launch_strip(const KArgs<T>& a, const sg_extents& e, dim3 grid, cudaStream_
 
 template <typename T>
 int launch_typed(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,
-                 size_t count, const void* in, void* out, cudaStream_t s) {
+                 size_t count, const void* in, void* out, cudaStream_t s, const PeerRows& peers) {
   const int rows = d.row1 - d.row0;
   const int cols = d.col1 - d.col0;
   if (rows <= 0 || cols <= 0) return strip_eligible<T>(d, e, fn, count, in, out) ? 1 : 0;
@@ -778,6 +797,12 @@ int launch_typed(const sg_slab_desc& d, const sg_extents& e, int fn, const doubl
   a.top = e.top;
   a.bottom = e.bottom;
   a.count = static_cast<int>(count);
+  a.peerUp = static_cast<T*>(peers.up);
+  a.peerDn = static_cast<T*>(peers.dn);
+  a.upRows = peers.upRows;
+  a.dnRow0 = peers.dnRow0;
+  if ((a.peerUp || a.peerDn) && !use_tma() && strip_eligible<T>(d, e, fn, count, in, out))
+    invalid("stencil: P2P halo forwarding needs the TMA kernel (SG_STENCIL_KERNEL=reg)");
   const size_t nv = std::min(count, static_cast<size_t>(VMAX));
   for (size_t k = 0; k < nv; ++k) a.v[k] = static_cast<T>(values[k]);
 
@@ -841,12 +866,13 @@ int stencil_kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size
 }
 
 int launch_stencil(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,
-                   size_t count, sg_dtype dtype, const void* in, void* out, cudaStream_t stream) {
+                   size_t count, sg_dtype dtype, const void* in, void* out, cudaStream_t stream,
+                   const PeerRows& peers) {
   if (fn != SG_FN_NONE && (e.left + e.right + 1) * (e.top + e.bottom + 1) > GENERIC_FN_MAX &&
       !strip_supported(e, fn))
     invalid("create_plan: device function windows are limited to 256 taps");
-  if (dtype == SG_F64) return launch_typed<double>(d, e, fn, values, count, in, out, stream);
-  if (dtype == SG_F32) return launch_typed<float>(d, e, fn, values, count, in, out, stream);
+  if (dtype == SG_F64) return launch_typed<double>(d, e, fn, values, count, in, out, stream, peers);
+  if (dtype == SG_F32) return launch_typed<float>(d, e, fn, values, count, in, out, stream, peers);
   invalid("unknown dtype");
 }
 

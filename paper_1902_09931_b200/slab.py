@@ -168,6 +168,57 @@ class SlabStencil:
         self.a = torch.zeros((slab.ext_rows, slab.nx), dtype=dtype, device=device)
         self.b = torch.zeros_like(self.a)
         self.torch = torch
+        self.mode = "nccl"
+        self._out = 1  # index of the output buffer in (a, b); swap() toggles it
+        self._tables = None
+
+    # -- P2P mode: the halo exchange fused into the stencil launch --------
+    def p2p_buffers(self):
+        """This rank's (a, b) ext buffers, to be exported to the neighbours."""
+        return [self.a.data_ptr(), self.b.data_ptr()]
+
+    def enable_p2p(self, tables, barrier=None):
+        """tables[k][r]: rank r's buffer k (0 = a, 1 = b at construction) as
+        a pointer valid in this process (IPC-mapped peer memory, or another
+        simulated rank's buffer). From now on every apply() also stores the
+        rows its neighbours need as halos straight into their output buffer
+        (sg_stencil_launch_p2p), so no exchange precedes the next apply; the
+        `barrier` (default: a one-element all-reduce on the compute stream
+        when world > 1) orders those writes between applications. The
+        caller fills the input's halos once before the first apply
+        (exchange_halos)."""
+        self._tables = tables
+        self._barrier = barrier
+        self.mode = "p2p"
+
+    def _peers(self):
+        s = self.slab
+        esz = self.a.element_size()
+        nx = s.nx
+        up_ptr = dn_ptr = 0
+        up_rows = dn_row0 = 0
+        if s.up is not None and s.bottom:
+            up = Slab(nx, s.ny, s.world, s.up, s.top, s.bottom, s.periodic)
+            up_ptr = self._tables[self._out][s.up] + esz * (s.top + up.own) * nx  # its bottom halo
+            up_rows = s.bottom  # my first `bottom` rows
+        if s.down is not None and s.top:
+            dn_ptr = self._tables[self._out][s.down]  # its top halo (ext rows 0..top)
+            dn_row0 = s.own - s.top  # my last `top` rows
+        return up_ptr, up_rows, dn_ptr, dn_row0
+
+    def _apply_p2p(self, stream=None):
+        from .stencil import launch_slab
+        s = self.slab
+        oa, ob = s.output_rows()
+        if oa < ob:
+            launch_slab(s.desc((self.ext.left, self.ext.right), oa, ob), self.ext, self.kind, self.a,
+                        self.own_view(self.b), stream, peers=self._peers())
+        if self._barrier is not None:
+            self._barrier()
+        elif s.world > 1:
+            if not hasattr(self, "_flag"):
+                self._flag = self.torch.zeros(1, device=self.a.device)
+            self.dist.all_reduce(self._flag)
 
     def own_view(self, buf):
         t = self.slab.top
@@ -176,6 +227,8 @@ class SlabStencil:
     def apply(self, stream=None):
         """out(own rows of b) = stencil(a); returns after enqueueing."""
         from .stencil import launch_slab
+        if self.mode == "p2p":
+            return self._apply_p2p(stream)
         s = self.slab
         lr = (self.ext.left, self.ext.right)
         out_own = self.own_view(self.b)
@@ -201,6 +254,7 @@ class SlabStencil:
 
     def swap(self):
         self.a, self.b = self.b, self.a
+        self._out ^= 1
 
     def apply_host(self, hin, hout, chunks: int = 16):
         """End-to-end application from/to pinned HOST memory: the own rows
@@ -299,6 +353,11 @@ def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak,
     g = torch.Generator(device="cuda").manual_seed(4 + rank)
     st.own_view(st.a).copy_(torch.rand((slab.own, nx), dtype=torch.float64, device="cuda", generator=g))
     stream = torch.cuda.current_stream()
+    halo = "NCCL halo exchange"
+    if getattr(args, "halo", "nccl") == "p2p":
+        torch.cuda.synchronize()
+        if enable_p2p_ipc(st, dist):
+            halo = "halo rows stored into the neighbours' buffers by the stencil kernel (P2P over NVLink)"
 
     def max_over_ranks(x):
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
@@ -362,7 +421,7 @@ def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload + f", weak scaling: 32768x32768 y-slab per GPU ({nx}x{ny} total)",
-                           "nx": nx, "ny": ny, "parallelism": f"y-slab x{world}, NCCL halo exchange",
+                           "nx": nx, "ny": ny, "parallelism": f"y-slab x{world}, {halo}",
                            "l2": "input 8 GiB per GPU >> L2"},
                 "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                              "frac": alg / (ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_kind": peak_kind,
@@ -374,3 +433,29 @@ def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak,
             line["e2e"] = e2e
     dist.destroy_process_group()
     return line
+
+
+def enable_p2p_ipc(st: SlabStencil, dist) -> bool:
+    """Production wiring of SlabStencil's P2P mode: exchange CUDA IPC
+    handles of every rank's (a, b) buffers over the process group, map the
+    peers' buffers, fill both buffers' halos once, and switch to the fused
+    launch. Returns False (and stays in NCCL mode) if any rank cannot."""
+    from .ch_dist import exchange_peer_tables, ipc_handle_functions
+
+    get_handle, open_handle, st._opened = ipc_handle_functions()
+
+    torch = st.torch
+    ok = 1.0
+    try:
+        tables, _ = exchange_peer_tables(dist, st.slab.rank, st.slab.world, st.p2p_buffers(), get_handle,
+                                         open_handle)
+    except Exception:
+        ok = 0.0
+    flag = torch.tensor([ok], device=st.a.device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if flag.item() < 1.0:
+        return False
+    exchange_halos(st.slab, st.a, dist)
+    exchange_halos(st.slab, st.b, dist)
+    st.enable_p2p(tables)
+    return True

@@ -296,16 +296,26 @@ def mark_host_dirty(plan: StencilPlan, which: int) -> None:
     check(_lib.lib().sg_plan_mark_host_dirty(plan._h, which))
 
 
-def launch_slab(desc: dict, ext: Extents, kind, inp, out, stream=None) -> None:
+def launch_slab(desc: dict, ext: Extents, kind, inp, out, stream=None, peers=None) -> None:
     """Stateless device launch over a y-slab (sg_stencil_launch): computes
     output rows [row0,row1) × cols [col0,col1); input row for output row j,
-    tap q is j + inShift - top + q (wrapped modulo inRows iff wrapY)."""
+    tap q is j + inShift - top + q (wrapped modulo inRows iff wrapY).
+    peers = (up_ptr, up_rows, down_ptr, down_row0): the launch also forwards
+    its boundary output rows into the neighbours' halo rows
+    (sg_stencil_launch_p2p; 0 pointers are skipped)."""
     fid, vals = _kind_values(kind)
     d = SgSlabDesc(**desc)
     s = getattr(stream, "cuda_stream", stream)
     if s is None:
         s = _current_stream()
     vptr = vals.ctypes.data_as(C.POINTER(C.c_double)) if vals.size else None
-    check(_lib.lib().sg_stencil_launch(C.byref(d), ext._c(), fid, vptr, vals.size,
-                                       _dtype_code(inp.dtype), C.c_void_p(inp.data_ptr()),
-                                       C.c_void_p(out.data_ptr()), C.c_void_p(s or 0)))
+    if peers is None:
+        check(_lib.lib().sg_stencil_launch(C.byref(d), ext._c(), fid, vptr, vals.size,
+                                           _dtype_code(inp.dtype), C.c_void_p(inp.data_ptr()),
+                                           C.c_void_p(out.data_ptr()), C.c_void_p(s or 0)))
+        return
+    up, up_rows, dn, dn_row0 = peers
+    check(_lib.lib().sg_stencil_launch_p2p(C.byref(d), ext._c(), fid, vptr, vals.size, _dtype_code(inp.dtype),
+                                           C.c_void_p(inp.data_ptr()), C.c_void_p(out.data_ptr()),
+                                           C.c_void_p(up or 0), up_rows, C.c_void_p(dn or 0), dn_row0,
+                                           C.c_void_p(s or 0)))

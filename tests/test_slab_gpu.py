@@ -101,3 +101,50 @@ def test_apply_host_pipeline_equals_oracle(sg, orc, ext, periodic, chunks):
         st.apply_host(hin, hout, chunks=chunks)
         want = orc.stencil(g, ext, w, periodic=periodic, out=np.full_like(g, sentinel))
         assert np.array_equal(hout.numpy().view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4])
+@pytest.mark.parametrize("ext,periodic,fn", [((1, 1, 1, 1), True, "fn_weighted_3x3"),
+                                             ((2, 2, 2, 2), True, "weights"),
+                                             ((1, 1, 1, 1), False, "weights"),
+                                             ((0, 0, 1, 2), False, "weights")])
+def test_p2p_fused_halo_steps_equal_full_grid(sg, orc, G, ext, periodic, fn):
+    """P2P mode: each application also stores the rows the neighbours need
+    straight into their output buffers' halo rows (sg_stencil_launch_p2p) —
+    no exchange between applications. Simulated ranks on one device (the
+    'peer memory' is the other ranks' buffers); 3 applications with swaps
+    equal the full-grid oracle BITWISE for every G, frames included."""
+    import torch
+    from paper_1902_09931_b200.slab import Slab, SlabStencil
+    rng = np.random.default_rng(G * 11 + ext[2])
+    nx, ny = 128, 48
+    g = rng.uniform(-1, 1, (ny, nx))
+    W = (ext[0] + ext[1] + 1) * (ext[2] + ext[3] + 1)
+    w = list(rng.uniform(-2, 2, 9 if fn != "weights" else W))
+    e = sg.Extents(*ext)
+    kind = sg.WeightStencil(e, w) if fn == "weights" else sg.FunctionStencil(e, fn, w)
+    sentinel = -12345.678
+    A, B = g.copy(), np.full_like(g, sentinel)
+    for _ in range(3):
+        B = orc.stencil(A, ext, w, periodic=periodic, fn=fn, out=B)
+        A, B = B, A
+    ranks = []
+    for r in range(G):
+        slab = Slab(nx, ny, G, r, ext[2], ext[3], periodic)
+        st = SlabStencil(slab, e, kind, torch.float64, "cuda")
+        for buf, src in ((st.a, g), (st.b, np.full_like(g, sentinel))):
+            for k, gr in enumerate(slab.global_rows_of_ext()):  # own rows + initial halos
+                if gr is not None:
+                    buf[k] = torch.from_numpy(src[gr])
+        ranks.append(st)
+    tables = [[st.p2p_buffers()[k] for st in ranks] for k in range(2)]
+    for st in ranks:
+        st.enable_p2p(tables, barrier=lambda: None)
+    for _ in range(3):
+        for st in ranks:  # one stream: every rank's writes land before the next application
+            st.apply()
+        for st in ranks:
+            st.swap()
+    torch.cuda.synchronize()
+    got = np.concatenate([st.own_view(st.a).cpu().numpy() for st in ranks], axis=0)
+    assert np.array_equal(got.view(np.uint64), A.view(np.uint64))
