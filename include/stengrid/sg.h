@@ -253,7 +253,12 @@ sg_status sg_chd_set_peers(sg_chd_t h, double* const* recvX, double* const* recv
                            double* const* y4yAll, int* enabled);
 sg_status sg_chd_phase_x_p2p(sg_chd_t h, const double* currExt, const double* prevExt, void* stream);
 sg_status sg_chd_phase_y_p2p(sg_chd_t h, void* stream);
-sg_status sg_chd_combine_p2p(sg_chd_t h, const double* currExt, double* prevExt, void* stream);
+/* peerUpPrev / peerDnPrev (may be NULL): the up / down neighbours' ext slab
+ * of the time level being written (their prevExt). The first 2 rows of
+ * C^{n+1} also go into the up neighbour's bottom halo, the last 2 into the
+ * down neighbour's top halo — the next step needs no halo exchange. */
+sg_status sg_chd_combine_p2p(sg_chd_t h, const double* currExt, double* prevExt, double* peerUpPrev,
+                             double* peerDnPrev, void* stream);
 
 /* CUDA IPC (peer device memory across processes): a handle is 64 bytes and
  * names the allocation containing devPtr; *offset is devPtr's byte offset in

@@ -149,7 +149,7 @@ def lib():
         "sg_chd_set_peers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), ip]),
         "sg_chd_phase_x_p2p": (C.c_int, [vp, vp, vp, vp]),
         "sg_chd_phase_y_p2p": (C.c_int, [vp, vp]),
-        "sg_chd_combine_p2p": (C.c_int, [vp, vp, vp, vp]),
+        "sg_chd_combine_p2p": (C.c_int, [vp, vp, vp, vp, vp, vp]),
         "sg_ipc_get_handle": (C.c_int, [vp, vp, C.POINTER(C.c_size_t)]),
         "sg_ipc_open_handle": (C.c_int, [vp, C.POINTER(vp)]),
         "sg_ipc_close": (C.c_int, [vp]),

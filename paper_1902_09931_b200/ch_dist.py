@@ -18,13 +18,15 @@ step (cahn_hilliard.cpp:260-328 across GPUs):
 Every arithmetic operation is the single-GPU step's, so C^n is bitwise
 identical for every G (tests/test_ch_dist_gpu.py, tests/test_ch_dist.py).
 
-mode="p2p" fuses both all-to-alls into the sweeps (sg_chd_*_p2p): every
+mode="p2p" fuses every exchange into a kernel (sg_chd_*_p2p): every
 finished backward stage of a sweep is TMA-stored straight into the buffer of
 the rank that consumes it (CUDA IPC-mapped peer memory over NVLink), so the
-exchange overlaps the recurrence, and the Woodbury corrections move to the
-consumers (the y-sweep's load, the combine). Steps 3 and 5 become
-barriers (a one-element NCCL all-reduce on the compute stream). Falls back
-to mode "nccl" when the geometry does not allow it (sg_chd_set_peers).
+all-to-alls overlap the recurrence; the Woodbury corrections move to the
+consumers (the y-sweep's load, the combine); the combine also stores the
+halo rows of C^{n+1} into the neighbours' slabs. Steps 1, 3 and 5 become
+barriers (a one-element NCCL all-reduce on the compute stream); only the
+first step exchanges halos. Falls back to mode "nccl" when the geometry
+does not allow it (sg_chd_set_peers).
 """
 from __future__ import annotations
 
@@ -70,19 +72,26 @@ class DistCHStepper:
         if mode == "p2p":
             bufs = [C.c_void_p() for _ in range(4)]
             check(_lib.lib().sg_chd_p2p_buffers(self._h, *[C.byref(b) for b in bufs]))
-            self.p2p_buffers = [b.value for b in bufs]  # recvX, recvY, y4xAll, y4yAll
+            # recvX, recvY, y4xAll, y4yAll, then the two time-level ext slabs
+            # (cur, prev at construction), whose halo rows the neighbours'
+            # combines write
+            self.p2p_buffers = [b.value for b in bufs] + [self.cur.data_ptr(), self.prev.data_ptr()]
+            self._prev_idx = 1  # construction index of the buffer holding C^{n-1}
+            self._halos_valid = False
             if transport is not None:
                 transport.register(self)  # peers are wired once every rank exists
             elif world == 1:
                 self.set_peers([[b] for b in self.p2p_buffers])
+                self._flag = None
             else:
                 self._ipc_peers()
 
     # -- P2P wiring
     def set_peers(self, tables):
-        """tables: for each of (recvX, recvY, y4xAll, y4yAll) the device
-        pointers of every rank, in rank order."""
-        arrs = [(C.c_void_p * self.world)(*t) for t in tables]
+        """tables: for each of (recvX, recvY, y4xAll, y4yAll, ext0, ext1) the
+        device pointers of every rank, in rank order."""
+        self._ext_tables = tables[4:6]
+        arrs = [(C.c_void_p * self.world)(*t) for t in tables[:4]]
         ok = C.c_int()
         check(_lib.lib().sg_chd_set_peers(self._h, *arrs, C.byref(ok)))
         self.mode = "p2p" if ok.value else "nccl"
@@ -133,10 +142,15 @@ class DistCHStepper:
 
     # -- the split step
     def phase_x(self):
-        self._halos()
         if self.mode == "p2p":
+            if self._halos_valid:
+                self._barrier()  # the neighbours' combines forwarded this step's halos
+            else:
+                self._halos()  # once: later halos arrive with the combine
+                self._halos_valid = True
             check(_lib.lib().sg_chd_phase_x_p2p(self._h, self._p(self.cur), self._p(self.prev), self._s()))
             return
+        self._halos()
         check(_lib.lib().sg_chd_phase_x(self._h, self._p(self.cur), self._p(self.prev), self._p(self.send), self._s()))
 
     def phase_y(self):
@@ -150,7 +164,11 @@ class DistCHStepper:
     def phase_combine(self):
         if self.mode == "p2p":
             self._barrier()
-            check(_lib.lib().sg_chd_combine_p2p(self._h, self._p(self.cur), self._p(self.prev), self._s()))
+            up, dn = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+            ext = self._ext_tables[self._prev_idx]
+            check(_lib.lib().sg_chd_combine_p2p(self._h, self._p(self.cur), self._p(self.prev), C.c_void_p(ext[up]),
+                                                C.c_void_p(ext[dn]), self._s()))
+            self._prev_idx ^= 1
         else:
             self._alltoall(self.recv, self.ycol, 1)
             check(_lib.lib().sg_chd_combine(self._h, self._p(self.cur), self._p(self.prev), self._p(self.recv),
@@ -159,9 +177,44 @@ class DistCHStepper:
         self.steps_done += 1
 
     def step(self):
+        """One step. In P2P mode with graphs enabled (default at world = 1;
+        opt-in via use_graphs for world > 1, where the barriers are NCCL
+        all-reduces inside the capture) every step after the first replays
+        a CUDA graph of the whole step — one per buffer parity, captured on
+        first use — so the host issues one launch per step."""
+        if self.mode == "p2p" and self._halos_valid and self._graphs_on():
+            key = self._prev_idx
+            g = self._graphs.get(key)
+            if g is None:
+                g = self.torch.cuda.CUDAGraph()
+                with self.torch.cuda.graph(g):
+                    self._step_body()  # records; the Python state advances as one step
+                self._graphs[key] = g
+            else:
+                self._advance()
+            g.replay()
+            return
+        self._step_body()
+
+    def _step_body(self):
         self.phase_x()
         self.phase_y()
         self.phase_combine()
+
+    def _advance(self):
+        # the bookkeeping _step_body does (a replayed graph skips it)
+        self.cur, self.prev = self.prev, self.cur
+        self._prev_idx ^= 1
+        self.steps_done += 1
+
+    use_graphs = None  # None: on at world == 1 without a test transport
+
+    def _graphs_on(self):
+        if not hasattr(self, "_graphs"):
+            self._graphs = {}
+        if self.use_graphs is None:
+            return self.world == 1 and self.transport is None
+        return bool(self.use_graphs)
 
     def own_rows(self, which=0):
         """View of this rank's rows of C^n (which=0) or C^{n-1} (which=1)."""
@@ -236,7 +289,7 @@ class LocalTransport:
         the same device)."""
         self.p2p.append(st)
         if len(self.p2p) == st.world:
-            tables = [[r.p2p_buffers[k] for r in sorted(self.p2p, key=lambda x: x.rank)] for k in range(4)]
+            tables = [[r.p2p_buffers[k] for r in sorted(self.p2p, key=lambda x: x.rank)] for k in range(6)]
             for r in self.p2p:
                 r.set_peers(tables)
 

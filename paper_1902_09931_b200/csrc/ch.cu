@@ -598,10 +598,15 @@ __global__ void __launch_bounds__(256) k_combine_packed(const double* __restrict
 // [q][jl][i_local], each straight from rank q's sweep) with every rank's y
 // coefficients in y4All[k*nx + i]; the correction and the update are
 // k_combine's expression (penta.cpp:283-284, cahn_hilliard.cpp:273,320).
+// peerUp / peerDn (optional): the neighbours' ext slabs of the same time
+// level — the first HALO rows of C^{n+1} are also stored into the up
+// neighbour's bottom halo, the last HALO rows into the down neighbour's top
+// halo (peer memory over NVLink), so no halo exchange precedes the next step.
 __global__ void __launch_bounds__(256) k_combine_packed_corr(const double* __restrict__ ccExt,
                                                              double* __restrict__ cpExt,
                                                              const double* __restrict__ v, int nx, int own, int nxq,
-                                                             int r0, const CorrTables t) {
+                                                             int r0, const CorrTables t, double* peerUp,
+                                                             double* peerDn) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int jl = blockIdx.y;
   pdl_wait();
@@ -613,7 +618,10 @@ __global__ void __launch_bounds__(256) k_combine_packed_corr(const double* __res
   const double vv = w - (__ldg(t.W[0] + j) * __ldg(t.y4 + i) + __ldg(t.W[1] + j) * __ldg(t.y4 + nx + i) +
                          __ldg(t.W[2] + j) * __ldg(t.y4 + 2LL * nx + i) + __ldg(t.W[3] + j) * __ldg(t.y4 + 3LL * nx + i));
   const double cb = 2.0 * ccExt[idx] - cpExt[idx];
-  cpExt[idx] = cb + vv;  // cahn_hilliard.cpp:320
+  const double cn = cb + vv;  // cahn_hilliard.cpp:320
+  cpExt[idx] = cn;
+  if (peerUp && jl < HALO) peerUp[static_cast<long long>(HALO + own + jl) * nx + i] = cn;
+  if (peerDn && jl >= own - HALO) peerDn[static_cast<long long>(jl - (own - HALO)) * nx + i] = cn;
 }
 
 // initial_condition on a slab: global element index k = (r0 + jl)*nx + i.
@@ -1028,9 +1036,10 @@ struct ChDist {
       throw Error(SG_ERR_CUDA, "internal: P2P y-sweep unavailable");
   }
 
-  void combine_p2p(const double* cur, double* prev, cudaStream_t s) {
+  void combine_p2p(const double* cur, double* prev, double* peerUp, double* peerDn, cudaStream_t s) {
     CorrTables ty{{fy.t.W[0], fy.t.W[1], fy.t.W[2], fy.t.W[3]}, y4yAll};
-    k_combine_packed_corr<<<dim3((p.nx + 255) / 256, own), 256, 0, s>>>(cur, prev, recvY, p.nx, own, nxq, r0, ty);
+    k_combine_packed_corr<<<dim3((p.nx + 255) / 256, own), 256, 0, s>>>(cur, prev, recvY, p.nx, own, nxq, r0, ty,
+                                                                        peerUp, peerDn);
     check_launch("ch slab combine (P2P) kernel");
   }
 
@@ -1480,14 +1489,15 @@ sg_status sg_chd_phase_y_p2p(sg_chd_t h, void* stream) {
   });
 }
 
-sg_status sg_chd_combine_p2p(sg_chd_t h, const double* currExt, double* prevExt, void* stream) {
+sg_status sg_chd_combine_p2p(sg_chd_t h, const double* currExt, double* prevExt, double* peerUpPrev,
+                             double* peerDnPrev, void* stream) {
   return guard2([&] {
     if (!h) sg::logic("CH slab: destroyed");
     auto& d = *h->d;
     if (!d.p2p) sg::logic("CH slab: P2P path not enabled (sg_chd_set_peers)");
     SG_CUDA(cudaSetDevice(d.device));
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
-    d.combine_p2p(currExt, prevExt, s);
+    d.combine_p2p(currExt, prevExt, peerUpPrev, peerDnPrev, s);
     if (!stream) SG_CUDA(cudaStreamSynchronize(s));
   });
 }

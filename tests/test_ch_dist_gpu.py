@@ -103,3 +103,23 @@ def test_distributed_ch_p2p_falls_back_when_tiles_do_not_fit(sg):
     for r in range(2):
         ranks.append(DistCHStepper(p, 2, r, transport=tr, mode="p2p"))
     assert all(st.mode == "nccl" for st in ranks)
+
+
+def test_distributed_ch_p2p_graph_replay_world1(sg):
+    """World 1, P2P mode: steps after the first replay per-parity CUDA graphs
+    of the whole step (halo forwarding included) — bitwise equal to the
+    single-GPU stepper, both time levels, odd and even step counts."""
+    import torch
+    from paper_1902_09931_b200.ch_dist import DistCHStepper
+    p = params(sg, 256, 256, seed=13)
+    st = DistCHStepper(p, 1, 0, mode="p2p")
+    assert st.mode == "p2p"
+    single = sg.CHStepper(p)
+    for steps in (1, 2, 5):
+        for _ in range(steps):
+            st.step()
+        single.step_many(steps)
+        torch.cuda.synchronize()
+        assert bits_equal(st.own_rows(0).cpu().numpy(), single.field().values)
+        assert bits_equal(st.own_rows(1).cpu().numpy(), single.previous_field().values)
+    assert len(st._graphs) == 2
