@@ -411,6 +411,9 @@ __device__ __forceinline__ bool s_mbar_test(uint64_t* bar, uint32_t phase) {
 __device__ __forceinline__ void s_mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void s_mbar_arrive_cnt(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(bar)), "r"(count) : "memory");
+}
 __device__ __forceinline__ void s_tma_2d(void* dst, const CUtensorMap* m, int x, int y, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -484,7 +487,9 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
       if (g == nS) {
         // backward stages read the forward results: wait until the consumer
         // has stored them all and fenced them to the async proxy
-        asm volatile("bar.sync 1, 64;" ::: "memory");
+        // non-.aligned form: lane 0 ran the issue code (independent thread
+        // scheduling); every one of the 64 threads arrives individually
+        asm volatile("barrier.sync 1, 64;" ::: "memory");
       }
       if (lane == 0) {
         if (g >= SW_NSTG) s_mbar_wait(&empty[slot], ((g / SW_NSTG) + 1) & 1);
@@ -603,7 +608,7 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
     if (lane == 0) s_mbar_arrive(&empty[slot]);
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");
-  asm volatile("bar.sync 1, 64;" ::: "memory");
+  asm volatile("barrier.sync 1, 64;" ::: "memory");  // non-.aligned: see the producer side
   // ---- backward (penta.cpp:183-196): stage 0 (rows n-RS..n-1) peeled
   double s1 = 0.0, s2 = 0.0, zn1 = 0.0, zn2 = 0.0, zz0 = 0.0, zz1 = 0.0;
   constexpr int XP = RS + 1;  // XOUT tile pitch (odd: conflict-free columns)
@@ -830,7 +835,7 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
     for (int k = 0; k < NST; ++k) {
       // XIN: every load of a slot completes on the TMA bytes AND a plain
       // arrival (the transform in the forward pass, immediate in backward)
-      s_mbar_init(&full[k], XIN ? 1 + XIN_TW : 1);
+      s_mbar_init(&full[k], XIN ? 1 + 32 * XIN_TW : 1);  // XIN: every transform thread arrives
       s_mbar_init(&done[k], 1);
     }
     if constexpr (XIN) {
@@ -857,7 +862,7 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
       s_tma_2d(st, &maps.z, b0, G * RS, &full[s]);
       for (int k = 0; k < 5; ++k) s_tma_1d(st + RS * 32 + k * FAC, &maps.t[k], G * RS, &full[s]);
       if constexpr (XIN)  // no transform on refetched rows: the transform arrivals now
-        for (int k = 0; k < XIN_TW; ++k) s_mbar_arrive(&full[s]);
+        s_mbar_arrive_cnt(&full[s], 32 * XIN_TW);
     };
     auto store = [&](int s, int G) {
       s_tma_store_2d(&maps.z, b0, G * RS, rr_smem + s * STG);
@@ -897,6 +902,7 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
         }
         // slot s is free (its store has read it) and every transform warp has
         // finished stage g-1 (so its raw buffer can be refilled)
+        __syncwarp();  // the issuer lane diverged: reconverge before the aligned barrier
         asm volatile("bar.sync 1, %0;" ::"n"(XIN_TW * 32) : "memory");
         if (issuer) {
           double* st = rr_smem + s * STG;
@@ -945,8 +951,7 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
             zs[(2 * (jb + t) + 1) * 32 + lane] = o[t][1];
           }
         }
-        __syncwarp();
-        if (lane == 0) s_mbar_arrive(&full[s]);
+        s_mbar_arrive(&full[s]);  // each thread releases its own slot writes
       }
       if (!issuer) return;
     } else {

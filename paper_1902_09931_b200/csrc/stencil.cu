@@ -388,6 +388,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #define SG_TMA_WARPS 16
 #endif
 constexpr int TMA_WARPS = SG_TMA_WARPS;
+// Release of a ring stage by the consumers: every thread arrives on the
+// "empty" mbarrier (1), or each warp's lane 0 after __syncwarp (0).
+#ifndef SG_EMPTY_ALL_LANES
+#define SG_EMPTY_ALL_LANES 1
+#endif
 
 template <typename T, int L, int R, int TP, int BT>
 struct TmaGeom {
@@ -432,7 +437,7 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32) k_tma(const __grid_const
   if (threadIdx.x == 0) {
     for (int k = 0; k < STAGES; ++k) {
       mbar_init(&full[k], 2);  // expect_tx arrival + cp.async (halo) arrival
-      mbar_init(&empty[k], TMA_WARPS);
+      mbar_init(&empty[k], SG_EMPTY_ALL_LANES ? TMA_WARPS * 32 : TMA_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -598,8 +603,13 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32) k_tma(const __grid_const
       ++j;
       orow += rowStep;
     }
-    __syncwarp();  // every lane of this warp has read the stage
-    if (lane == 0) mbar_arrive(&empty[slot]);
+    // every lane of this warp has read the stage
+    if constexpr (SG_EMPTY_ALL_LANES) {
+      mbar_arrive(&empty[slot]);  // each thread releases its own reads of the slot
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
   }
 }
 
