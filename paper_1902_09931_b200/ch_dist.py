@@ -104,7 +104,8 @@ class DistCHStepper:
         tables, _ = exchange_peer_tables(self.dist, self.rank, self.world, self.p2p_buffers,
                                                     get_handle, open_handle)
         ok = self.set_peers(tables)
-        flags = self.torch.tensor([1.0 if ok else 0.0], device=self.cur.device)
+        flags = self.torch.tensor([1.0 if ok else 0.0],
+                                  device=self.cur.device if self.dist.get_backend() == "nccl" else "cpu")
         self.dist.all_reduce(flags, op=self.dist.ReduceOp.MIN)
         if flags.item() < 1.0:  # every rank must take the same path
             self.mode = "nccl"

@@ -435,7 +435,7 @@ def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak,
     return line
 
 
-def enable_p2p_ipc(st: SlabStencil, dist) -> bool:
+def enable_p2p_ipc(st: SlabStencil, dist, fill_halos: bool = True) -> bool:
     """Production wiring of SlabStencil's P2P mode: exchange CUDA IPC
     handles of every rank's (a, b) buffers over the process group, map the
     peers' buffers, fill both buffers' halos once, and switch to the fused
@@ -451,11 +451,12 @@ def enable_p2p_ipc(st: SlabStencil, dist) -> bool:
                                          open_handle)
     except Exception:
         ok = 0.0
-    flag = torch.tensor([ok], device=st.a.device)
+    flag = torch.tensor([ok], device=st.a.device if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     if flag.item() < 1.0:
         return False
-    exchange_halos(st.slab, st.a, dist)
-    exchange_halos(st.slab, st.b, dist)
+    if fill_halos:
+        exchange_halos(st.slab, st.a, dist)
+        exchange_halos(st.slab, st.b, dist)
     st.enable_p2p(tables)
     return True
