@@ -275,6 +275,8 @@ class Reference:
         return c, pr
 
     def ch_timed(self, p, steps, warmup=1, tiles=1, workers=1):
+        """Seconds PER STEP of the reference CHStepper::step over `steps`
+        timed steps (after `warmup`)."""
         dp, ip = self._ch_params(p)
         secs = C.c_double()
         self._check(self.lib.ref_ch_timed(_d(dp), ip, tiles, workers, warmup, steps, C.byref(secs)))
