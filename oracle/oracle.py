@@ -213,6 +213,7 @@ class Reference:
 
     def stencil_timed(self, inp, ext, weights, *, direction=2, periodic=True, fn="weights",
                       tiles=1, workers=1, warmup=1, reps=1):
+        """Seconds PER compute() of the reference (mean over `reps`)."""
         inp = _f64(inp)
         ny, nx = inp.shape
         e = (C.c_int * 4)(*ext)
