@@ -731,7 +731,7 @@ struct ChState {
   // CUDA graphs keyed by (kind, ic, ip): kind 0 = full step, 1 = head (step
   // without its combine), 2 = steady (previous combine fused into this
   // step's RHS), 3 = three steady steps (the buffer rotation closes), 4 =
-  // tail (the pending combine alone).
+  // tail (the pending combine alone), 5 = twelve steady steps.
   std::map<int, cudaGraphExec_t> graphs;
   int solveK = -1;  // kernels one solve launches (counted once, by capture)
   int step = 0;
@@ -892,7 +892,8 @@ struct ChState {
         enqueue_solve(c, q, 3 - c - q, stream);
         break;
       case 3:
-        for (int k = 0, a = c, b = q; k < 3; ++k) {
+      case 5:  // 3 or 12 steady steps (the rotation closes every 3)
+        for (int k = 0, a = c, b = q; k < (kind == 3 ? 3 : 12); ++k) {
           const int n = 3 - a - b;
           enqueue_solve(a, b, n, stream);
           b = a;
@@ -945,6 +946,10 @@ struct ChState {
     }
     launch(1, solveK);
     int left = steps - 1;
+    while (left >= 12) {  // one graph launch per 12 steps
+      launch(5, 12 * solveK);
+      left -= 12;
+    }
     while (left >= 3) {
       launch(3, 3 * solveK);
       left -= 3;  // three rotations of (ic, ip, spare) restore it
