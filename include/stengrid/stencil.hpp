@@ -260,7 +260,11 @@ inline void swap_plan(StencilPlan& plan) {
   std::swap(plan.boundIn_, plan.boundOut_);
 }
 
-/// stencil.cpp:202-235 — runs on the GPU; synchronous.
+/// stencil.cpp:202-235 — runs on the GPU. Residency::Host (the default) is
+/// synchronous like the reference; Residency::Device returns once the kernel
+/// is queued (the output stays on the device — sync_to_host or a Host compute
+/// completes it), so chains of Device-residency applications do not wait on
+/// the host between launches.
 inline void compute(StencilPlan& plan, Residency hint = Residency::Host) {
   if (!plan.valid()) throw std::logic_error("compute: plan was destroyed");
   Grid2D& in = *plan.input_;
@@ -268,8 +272,8 @@ inline void compute(StencilPlan& plan, Residency hint = Residency::Host) {
   if (!in.same_shape(out)) throw std::invalid_argument("compute: bound grids changed shape");
   if (in.data() == out.data()) throw std::invalid_argument("compute: bound grids alias");
   if (in.data() != plan.boundIn_ || out.data() != plan.boundOut_) plan.bind();  // storage moved
-  detail::check(sg_plan_compute(plan.h_, hint == Residency::Host ? SG_RESIDENCY_HOST : SG_RESIDENCY_DEVICE,
-                                nullptr, 1));
+  const bool host = hint == Residency::Host;
+  detail::check(sg_plan_compute(plan.h_, host ? SG_RESIDENCY_HOST : SG_RESIDENCY_DEVICE, nullptr, host ? 1 : 0));
 }
 
 /// Bring Device-resident results back into the bound host grids.

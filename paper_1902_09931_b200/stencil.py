@@ -272,13 +272,17 @@ def swap_plan(plan: StencilPlan) -> None:
 
 
 def compute(plan: StencilPlan, hint: Residency = Residency.Host, stream=None,
-            synchronize: bool = True) -> None:
+            synchronize=None) -> None:
     """stencil.cpp:202-235 — apply the stencil on the GPU.
 
     Host-bound plans: ``Residency.Host`` leaves the host output valid on
     return; ``Residency.Device`` keeps it on the device until
     :func:`sync_to_host`. ``stream`` is a ``torch.cuda.Stream`` / raw
-    cudaStream_t or None (the plan's own stream)."""
+    cudaStream_t or None (the plan's own stream). ``synchronize`` defaults to
+    ``hint == Residency.Host``: Device-residency applications return once
+    queued."""
+    if synchronize is None:
+        synchronize = hint == Residency.Host
     if not plan.valid():
         raise LogicError("compute: plan was destroyed")
     s = getattr(stream, "cuda_stream", stream)
