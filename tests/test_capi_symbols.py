@@ -67,3 +67,40 @@ def test_validation_errors_precede_device_checks():
         with pytest.raises(sg.NoDeviceError):
             sg.create_plan(sg.Direction.X, sg.BoundaryMode.Periodic,
                            sg.WeightStencil(sg.Extents(1, 1), [1.0, -2.0, 1.0]), a, b, 1, 1)
+
+
+def test_plain_c_client_compiles_links_and_fails_loudly_without_gpu(tmp_path):
+    """The C ABI is usable from C99 (INTEGRATION.md's example): it compiles
+    with gcc against include/stengrid/sg.h, links libstengrid_b200.so, and on
+    a machine without a GPU reports SG_ERR_NO_DEVICE instead of computing on
+    the CPU."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check")
+    src = tmp_path / "client.c"
+    src.write_text(r'''
+#include "stengrid/sg.h"
+#include <stdio.h>
+int main(void) {
+  enum { nx = 64, ny = 32 };
+  static double in_host[nx * ny], out_host[nx * ny];
+  sg_plan_t plan;
+  sg_extents e = {1, 1, 1, 1};
+  double coe[9] = {0, 1, 0, 1, -4, 1, 0, 1, 0};
+  sg_status st = sg_plan_create(SG_DIR_XY, SG_PERIODIC, e, SG_FN_WEIGHTED_3X3, coe, 9, SG_F64, in_host,
+                                out_host, nx, ny, SG_MEM_HOST, 1, 1, &plan);
+  printf("%d %s\n", (int)st, st == SG_OK ? "" : sg_last_error());
+  return st == SG_ERR_NO_DEVICE ? 0 : 1;
+}
+''')
+    lib = ROOT / "paper_1902_09931_b200"
+    exe = tmp_path / "client"
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", f"-I{ROOT / 'include'}", str(src), f"-L{lib}",
+                    "-lstengrid_b200", f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "no CUDA device" in r.stdout
