@@ -140,3 +140,97 @@ def test_uniform_large_batch_bitwise(sg, orc, periodic):
     t = torch.from_numpy(rhs.copy()).cuda()
     f.solve_in_place(t)
     assert bits_equal(t.cpu().numpy(), orc.penta_solve(periodic, m.bands(), rhs))
+
+
+def _solve(sg, m, rhs):
+    """Device solve of a copy of rhs (n, B) with a fresh factor of m."""
+    import torch
+    f = sg.PeriodicPentaFactor(m) if m.periodic else sg.PentaFactor(m)
+    t = torch.from_numpy(np.ascontiguousarray(rhs, dtype=np.float64).copy()).cuda()
+    f.solve_in_place(t)
+    return t.cpu().numpy()
+
+
+def _zero_corners(m):
+    """penta.hpp:15-20: the cyclic wrap slots."""
+    n = m.n
+    m.secondSub[0, :] = m.secondSub[1, :] = m.sub[0, :] = 0.0
+    m.secondSuper[n - 2, :] = m.super[n - 1, :] = m.secondSuper[n - 1, :] = 0.0
+
+
+def test_zero_corner_periodic_equals_nonperiodic(sg):
+    """test_penta.cpp:161-174: a periodic batch whose wrap couplings are zero
+    solves to the same bits as the non-periodic batch."""
+    m = random_batch(sg, 24, 40, True, 21)
+    _zero_corners(m)
+    rhs = np.random.default_rng(22).uniform(-1, 1, (40, 24))
+    mn = sg.PentaBatch(24, 40, False)
+    for a, b in zip(mn.bands(), m.bands()):
+        a[:] = b
+    assert bits_equal(_solve(sg, m, rhs), _solve(sg, mn, rhs))
+
+
+@pytest.mark.parametrize("periodic", [False, True])
+def test_system_permutation_bitwise(sg, periodic):
+    """test_penta.cpp:225-247: permuting the systems of a batch permutes the
+    solutions, bit for bit (systems are independent)."""
+    B, n = 37, 29
+    m = random_batch(sg, B, n, periodic, 31)
+    rhs = np.random.default_rng(32).uniform(-1, 1, (n, B))
+    perm = np.random.default_rng(33).permutation(B)
+    mp = sg.PentaBatch(B, n, periodic)
+    for a, b in zip(mp.bands(), m.bands()):
+        a[:] = b[:, perm]
+    assert bits_equal(_solve(sg, mp, rhs[:, perm]), _solve(sg, m, rhs)[:, perm])
+
+
+@pytest.mark.parametrize("periodic", [False, True])
+def test_batch_equals_single_system_solves(sg, periodic):
+    """test_penta.cpp:306-316 (parallel == serial): the batched device solve
+    equals solving every system as a batch of one, bitwise."""
+    B, n = 9, 33
+    m = random_batch(sg, B, n, periodic, 41)
+    rhs = np.random.default_rng(42).uniform(-1, 1, (n, B))
+    got = _solve(sg, m, rhs)
+    for b in range(B):
+        m1 = sg.PentaBatch(1, n, periodic)
+        for a, band in zip(m1.bands(), m.bands()):
+            a[:, 0] = band[:, b]
+        assert bits_equal(_solve(sg, m1, rhs[:, b:b + 1])[:, 0], got[:, b])
+
+
+def test_amortized_factor_equals_fresh(sg):
+    """test_penta.cpp:294-304: one factor reused for several right-hand
+    sides gives the same bits as a fresh factor per solve."""
+    import torch
+    m = random_batch(sg, 16, 48, True, 51)
+    f = sg.PeriodicPentaFactor(m)
+    rng = np.random.default_rng(52)
+    for _ in range(4):
+        rhs = rng.uniform(-1, 1, (48, 16))
+        t = torch.from_numpy(rhs.copy()).cuda()
+        f.solve_in_place(t)
+        assert bits_equal(t.cpu().numpy(), _solve(sg, m, rhs))
+
+
+def test_linearity(sg):
+    """test_penta.cpp:249-263: solve(a x + b y) = a solve(x) + b solve(y)
+    within 1e-12 (relative, normwise)."""
+    m = random_batch(sg, 12, 50, True, 61)
+    rng = np.random.default_rng(62)
+    x, y = rng.uniform(-1, 1, (50, 12)), rng.uniform(-1, 1, (50, 12))
+    a, b = 0.75, -1.25
+    lhs = _solve(sg, m, a * x + b * y)
+    rhs = a * _solve(sg, m, x) + b * _solve(sg, m, y)
+    assert np.max(np.abs(lhs - rhs)) <= 1e-12 * np.max(np.abs(rhs))
+
+
+def test_hyperdiffusion_preserves_the_mean(sg):
+    """test_penta.cpp:278-292: rows of the periodic hyperdiffusion operator
+    sum to 1 and it is circulant, so the solution keeps the mean of the
+    right-hand side (1e-13)."""
+    n, B = 64, 8
+    m = sg.build_hyperdiffusion_operator(3.5, n, B, True)
+    rhs = np.random.default_rng(71).uniform(-1, 1, (n, B))
+    got = _solve(sg, m, rhs)
+    assert np.max(np.abs(got.mean(axis=0) - rhs.mean(axis=0))) <= 1e-13
