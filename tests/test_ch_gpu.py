@@ -260,3 +260,103 @@ def test_config5_grid_steps_bitwise_vs_reference(sg, ref):
     want_c, want_p = ref.ch_run(rp, steps, tiles=cores, workers=cores)
     assert bits_equal(st.field().values, want_c)
     assert bits_equal(st.previous_field().values, want_p)
+
+
+# ------------------------- test_cahn_hilliard.cpp operator / stepping cases
+
+
+def _sine_grid(sg, nx, ny, amp=1.0, k=1):
+    dx, dy = 2 * math.pi / nx, 2 * math.pi / ny
+    x = np.arange(nx) * dx
+    g = sg.Grid2D(nx, ny, dx, dy)
+    g.values[:] = amp * np.sin(k * x)[None, :]
+    return g
+
+
+def _apply(sg, kind, g):
+    out = sg.Grid2D(g.nx, g.ny, g.dx, g.dy)
+    plan = sg.create_plan(sg.Direction.XY, sg.BoundaryMode.Periodic, kind, g, out, 1, 1)
+    sg.compute(plan)
+    return out.values
+
+
+def test_nonlinear_window_equals_cube_then_laplacian_weights(sg):
+    """The CH nonlinear window function equals c^3 - c followed by the
+    nonlinear Laplacian as a weight stencil, bitwise."""
+    p = params(sg, 16, 8)
+    st = sg.CHStepper(p)
+    c = st.field()
+    coe = sg.nonlinear_laplacian_coefficients(c.dx, c.dy)
+    via_fn = _apply(sg, sg.FunctionStencil(sg.Extents(1, 1, 1, 1), "ch_nonlinear_window", coe), c)
+    cubed = sg.Grid2D(c.nx, c.ny, c.dx, c.dy)
+    v = c.values
+    cubed.values[:] = v * v * v - v
+    via_w = _apply(sg, sg.WeightStencil(sg.Extents(1, 1, 1, 1), coe), cubed)
+    assert bits_equal(via_fn, via_w)
+
+
+def test_nonlinear_window_fourier_symbol(sg):
+    """On eps*sin(x): c^3 - c = (3eps^3/4 - eps) sin x - (eps^3/4) sin 3x, each
+    mode scaled by the discrete Laplacian symbol (1e-11)."""
+    nx, ny, eps = 64, 8, 0.1
+    c = _sine_grid(sg, nx, ny, eps)
+    coe = sg.nonlinear_laplacian_coefficients(c.dx, c.dy)
+    out = _apply(sg, sg.FunctionStencil(sg.Extents(1, 1, 1, 1), "ch_nonlinear_window", coe), c)
+    lam = lambda k: (2.0 * math.cos(k * c.dx) - 2.0) / (c.dx * c.dx)
+    x = np.arange(nx) * c.dx
+    want = (3 * eps ** 3 / 4 - eps) * lam(1) * np.sin(x) - (eps ** 3 / 4) * lam(3) * np.sin(3 * x)
+    assert np.max(np.abs(out - want[None, :])) <= 1e-11 * max(1.0, np.max(np.abs(want)))
+
+
+def test_biharmonic_symbol_and_constants(sg):
+    """The 5x5 biharmonic weights: sin(x) is scaled by
+    (6 - 8 cos h + 2 cos 2h)/h^4 (1e-9); constants map to ~0 (1e-9)."""
+    nx, ny = 64, 8
+    c = _sine_grid(sg, nx, ny)
+    bw = sg.biharmonic_weights(c.dx, c.dy)
+    kind = sg.WeightStencil(sg.Extents(2, 2, 2, 2), bw)
+    h = c.dx
+    symbol = (6.0 - 8.0 * math.cos(h) + 2.0 * math.cos(2.0 * h)) / h ** 4
+    out = _apply(sg, kind, c)
+    want = symbol * np.sin(np.arange(nx) * h)[None, :]
+    assert np.max(np.abs(out - want)) <= 1e-9 * max(1.0, np.max(np.abs(want)))
+    k = sg.Grid2D(64, 64, 2 * math.pi / 64, 2 * math.pi / 64)
+    k.values[:] = 0.7
+    bw64 = sg.biharmonic_weights(k.dx, k.dy)
+    assert np.max(np.abs(_apply(sg, sg.WeightStencil(sg.Extents(2, 2, 2, 2), bw64), k))) <= 1e-9
+
+
+def test_linear_stepping_bounded_at_large_dt(sg):
+    """Linear CH (nonlinear term off) at dt = 10 dx for 1000 steps stays
+    bounded by 0.2 (initial amplitude 0.1; hyperdiffusion only damps)."""
+    p = params(sg, 64, 64, dt_factor=10.0, nonlinearEnabled=False, seed=9)
+    st = sg.CHStepper(p)
+    peak = 0.0
+    for _ in range(10):
+        st.step_many(100)
+        peak = max(peak, float(np.max(np.abs(st.field().values))))
+    assert peak <= 0.2
+
+
+def test_temporal_self_convergence_order(sg):
+    """BDF2-ADI is second order in time: on a stiff hyperdiffusion-dominated
+    mode (cos 50x + cos 50y, n = 128, T = 6.4e-4) the self-convergence order
+    log2(|f(dt) - f(dt/2)| / |f(dt/2) - f(dt/4)|) is at least 1.8."""
+    n = 128
+
+    def final(dt):
+        p = sg.CHParams(nx=n, ny=n)
+        p.dt = dt
+        p.T = 6.4e-4
+        st = sg.CHStepper(p)
+        ic = sg.Grid2D(n, n, p.dx(), p.dy())
+        x = np.arange(n) * p.dx()
+        ic.values[:] = 1e-3 * (np.cos(50.0 * x)[None, :] + np.cos(50.0 * x)[:, None])
+        st.set_state(ic, ic)
+        st.step_many(int(round(p.T / dt)))
+        return st.field().values
+
+    dt0 = 8e-5
+    f1, f2, f4 = final(dt0), final(dt0 / 2), final(dt0 / 4)
+    e1, e2 = np.max(np.abs(f1 - f2)), np.max(np.abs(f2 - f4))
+    assert math.log2(e1 / e2) >= 1.8
