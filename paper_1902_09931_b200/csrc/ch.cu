@@ -686,17 +686,10 @@ namespace {
 
 bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
-// The fused sweeps (x-sweep writing row-major w, y-sweep correcting on load)
-// remove the transpose/correct pass but lengthen the single-warp recurrence
-// loop; measured slower on B200 at 1024^2 and 8192^2, so they
-// are opt-in: SG_CH_FUSED=1.
-bool unfused() {
-  static const bool v = [] {
-    const char* e = std::getenv("SG_CH_FUSED");
-    return !(e && e[0] == '1');
-  }();
-  return v;
-}
+// (An earlier design applied the x correction inside the y-sweep's chain
+// warp and wrote the x results transposed from the chain warp: measured
+// slower than the separate pass at 1024^2 and 8192^2 and removed; the XIN
+// sweeps move that work to three transform warps instead.)
 
 }  // namespace
 
@@ -797,7 +790,7 @@ struct ChState {
     for (int k = 0; k < 25; ++k)
       if (!keep[k] && rp.bw[k] != 0.0) throw Error(SG_ERR_CUDA, "internal: biharmonic zero pattern");
     // the transposed-input sweep pipeline (see xpipe)
-    if (xin_ok() && unfused() && rhs_kind() == 1 && p.nx % RX == 0) {
+    if (xin_ok() && rhs_kind() == 1 && p.nx % RX == 0) {
       xT = dalloc(cnt);
       xpipe = penta_sweep_xin(fx.t, p.ny, p.nx, xT, rhsT, nullptr, nullptr, y4x, stream, false, false) &&
               penta_sweep_xin(fy.t, p.nx, p.ny, w, xT, fx.t.W, y4x, y4y, stream, false, false);
@@ -820,7 +813,7 @@ struct ChState {
       const char* e = std::getenv("SG_CH_STEADY");
       return e && e[0] == '0';
     }();
-    return !off && p.nx % RX == 0 && rhs_kind() != 0 && unfused();
+    return !off && p.nx % RX == 0 && rhs_kind() != 0;
   }
 
   // RHS (or, steady, the fused previous combine + RHS writing C^{n+1} into
@@ -836,11 +829,6 @@ struct ChState {
     } else {
       launch_rhs(p.nonlinearEnabled, field[c], field[q], rhsT, geom, rp, s, pdl);
     }
-    // x-sweep writes its (uncorrected) result straight into row-major w;
-    // the y-sweep applies the x Woodbury correction as it loads w.
-    const bool fused = !unfused() && penta_sweep_fused(fx.t, ny, nx, rhsT, y4x, nullptr, nullptr, w, s) &&
-                       penta_sweep_fused(fy.t, nx, ny, w, y4y, fx.t.W, y4x, nullptr, s);
-    if (fused) return;
     if (xpipe) {
       // x-sweep: rhs (row-major) read transposed -> xT (interleaved);
       // y-sweep: xT read transposed + x-corrected -> w (row-major)

@@ -350,7 +350,7 @@ constexpr int SW_NSTG = 4;  // stages in flight
 struct alignas(64) SweepMaps {
   CUtensorMap z;     // 2D {B, n}, box {32, RS}
   CUtensorMap t[5];  // m1, m2, dInv, ap, bp: uniform 1D {n} box {RS}; else 2D like z
-  CUtensorMap yc[4]; // XCORR: the previous sweep's Woodbury coefficients y_k[r], 1D {n} box {RS}
+  CUtensorMap yc[4]; // XIN 1: the previous sweep's Woodbury coefficients y_k[r], 1D {n} box {RS}
   CUtensorMap zt;    // XIN (k_sweep_res): the input read TRANSPOSED, system-major:
                      // 3D {ztInner, B, n / ztInner} box {16, 32, 1}, 128 B swizzle —
                      // unknown r of system b at ((r % ztInner), b, r / ztInner): one
@@ -362,15 +362,12 @@ struct alignas(64) SweepMaps {
   int prow = 0;
 };
 
-// Fusions used by the Cahn-Hilliard step (ch.cu):
-//  XCORR: the input is another sweep's UNcorrected result; apply its
-//         Woodbury correction on load: z(b, r) -= Wc0[b] yc0[r] + ... + Wc3[b] yc3[r]
-//         (penta.cpp:279-286, same expression), streaming yc with the rows.
-//  XOUT:  write the backward results transposed, zout[b*n + r] (the grid's
-//         natural layout) instead of back into the interleaved z.
+// Fusions of the transposed-input sweep (k_sweep_res XIN, the CH step):
+//  Wc/yc (XIN 1): the input is another sweep's UNcorrected result; its
+//         Woodbury correction is applied on load: z(b, r) -= Wc0[b] yc0[r] +
+//         ... + Wc3[b] yc3[r] (penta.cpp:279-286, same expression).
 struct SweepFuse {
   const double* Wc[4] = {nullptr, nullptr, nullptr, nullptr};
-  double* zout = nullptr;
   const double* yc = nullptr;  // XIN: yc[k*n + r], the previous sweep's y_k
   // P2P: y (this sweep's Woodbury coefficients) also written to every
   // destination: py4[d][k*y4Stride + y4Off + b]
@@ -436,28 +433,24 @@ __device__ __forceinline__ void s_tma_1d(void* dst, const CUtensorMap* m, int x,
       : "memory");
 }
 
-template <bool UNIFORM, bool XCORR = false>
+template <bool UNIFORM>
 struct SweepSmem {
   // doubles per factor table per stage; tensor-TMA destinations must be
   // 128 B aligned, so the uniform (SW_RS-long) tables get a 16-double slot
   static constexpr int FAC = UNIFORM ? (SW_RS + 15) / 16 * 16 : SW_RS * 32;
-  static constexpr int YCS = (SW_RS + 15) / 16 * 16;                // one yc table slot
-  static constexpr int STAGE = SW_RS * 32 + 3 * FAC + (XCORR ? 4 * YCS : 0);
+  static constexpr int STAGE = SW_RS * 32 + 3 * FAC;
   static constexpr int STAGE_PAD = (STAGE * 8 + 127) / 128 * 16;  // doubles, 128 B aligned stride
-  static constexpr int XT = 32 * (SW_RS + 1);                       // XOUT staging tile
-  static constexpr size_t bytes = static_cast<size_t>(SW_NSTG) * STAGE_PAD * 8 + XT * 8 + 2 * SW_NSTG * 8;
+  static constexpr size_t bytes = static_cast<size_t>(SW_NSTG) * STAGE_PAD * 8 + 2 * SW_NSTG * 8;
 };
 
-template <bool UNIFORM, bool PERIODIC, int MODE, bool XCORR = false, bool XOUT = false>
+template <bool UNIFORM, bool PERIODIC, int MODE>
 __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __grid_constant__ SweepMaps maps,
-                                                  int B, int n, double* __restrict__ z, double* __restrict__ y4,
-                                                  const SweepFuse fuse) {
+                                                  int B, int n, double* __restrict__ z, double* __restrict__ y4) {
   // Warp 0: consumer (32 systems, the dependency chain). Warp 1 lane 0:
   // producer (tensor-TMA issue), so the chain never stalls on issue code.
-  using SM = SweepSmem<UNIFORM, XCORR>;
+  using SM = SweepSmem<UNIFORM>;
   extern __shared__ __align__(128) double sw_smem[];
-  double* xt = sw_smem + SW_NSTG * SM::STAGE_PAD;  // XOUT staging tile [32][RS+1]
-  uint64_t* full = reinterpret_cast<uint64_t*>(xt + SM::XT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sw_smem + SW_NSTG * SM::STAGE_PAD);
   uint64_t* empty = full + SW_NSTG;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -498,8 +491,7 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
         double* st = sw_smem + slot * SM::STAGE_PAD;
         const int r0 = pass == 0 ? gg * RS : n - (gg + 1) * RS;
         const int nt = pass == 0 ? 2 : 3;
-        const bool yc = XCORR && pass == 0;
-        s_mbar_expect_tx(&full[slot], ZB + nt * FB + (yc ? 4u * RS * 8u : 0u));
+        s_mbar_expect_tx(&full[slot], ZB + nt * FB);
         s_tma_2d(st, &maps.z, b0, r0, &full[slot]);
         for (int k = 0; k < nt; ++k) {
           const CUtensorMap* m = &maps.t[pass == 0 ? k : 2 + k];  // fwd: m1, m2; bwd: dInv, ap, bp
@@ -508,8 +500,6 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
           else
             s_tma_2d(st + RS * 32 + k * FAC, m, b0, r0, &full[slot]);
         }
-        if (yc)
-          for (int k = 0; k < 4; ++k) s_tma_1d(st + RS * 32 + 3 * FAC + k * SM::YCS, &maps.yc[k], r0, &full[slot]);
       }
     }
     return;
@@ -519,25 +509,7 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
   auto fac = [&](const double* st, int k, int row) -> double {
     return UNIFORM ? st[RS * 32 + k * FAC + row] : st[RS * 32 + k * FAC + row * 32 + lane];
   };
-  double wc0 = 0.0, wc1 = 0.0, wc2 = 0.0, wc3 = 0.0;
-  if constexpr (XCORR) {
-    if (active) {
-      wc0 = fuse.Wc[0][b];
-      wc1 = fuse.Wc[1][b];
-      wc2 = fuse.Wc[2][b];
-      wc3 = fuse.Wc[3][b];
-    }
-  }
-  // z(b, r) as the recurrence sees it: raw, or corrected on load (XCORR)
-  auto zin = [&](const double* st, int k) -> double {
-    const double raw = st[k * 32 + lane];
-    if constexpr (XCORR) {
-      const double* yc = st + RS * 32 + 3 * FAC;
-      return raw - (wc0 * yc[k] + wc1 * yc[SM::YCS + k] + wc2 * yc[2 * SM::YCS + k] + wc3 * yc[3 * SM::YCS + k]);
-    } else {
-      return raw;
-    }
-  };
+  auto zin = [&](const double* st, int k) -> double { return st[k * 32 + lane]; };
   double* zc = z + b;
   const long long sB = B;
   // ---- forward (penta.cpp:171-181): stage 0 peeled (rows 0, 1 special)
@@ -555,9 +527,7 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
         yr = zr - fac(st, 1, k) * y1;  // y1 holds y[0]
       else
         yr = zr;
-      // row 0 is unchanged by the forward pass; with XCORR its corrected
-      // value must still reach memory for the backward pass
-      if (active && (k >= 1 || XCORR) && k < n) zc[k * sB] = yr;
+      if (active && k >= 1 && k < n) zc[k * sB] = yr;  // row 0 is unchanged by the forward pass
       y2 = y1;
       y1 = yr;
     }
@@ -611,14 +581,8 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
   asm volatile("barrier.sync 1, 64;" ::: "memory");  // non-.aligned: see the producer side
   // ---- backward (penta.cpp:183-196): stage 0 (rows n-RS..n-1) peeled
   double s1 = 0.0, s2 = 0.0, zn1 = 0.0, zn2 = 0.0, zz0 = 0.0, zz1 = 0.0;
-  constexpr int XP = RS + 1;  // XOUT tile pitch (odd: conflict-free columns)
-  // result of row r (= r0 + k): into z, or into the transposition tile
-  auto put = [&](int k, int r, double yr, double* zq) {
-    if constexpr (XOUT) {
-      xt[lane * XP + k] = yr;
-    } else {
-      if (active && r >= 0) *zq = yr;
-    }
+  auto put = [&](int, int r, double yr, double* zq) {
+    if (active && r >= 0) *zq = yr;
   };
   ready = false;
   for (int g = nS; g < total; ++g) {
@@ -684,21 +648,6 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
     }
     __syncwarp();
     if (lane == 0) s_mbar_arrive(&empty[slot]);
-    if constexpr (XOUT) {
-      // tile [system][row] -> zout[(b0 + system) * n + r0 + k]: 32/RS
-      // systems per instruction, RS consecutive rows (8*RS bytes) each
-      static_assert(32 % RS == 0 || RS % 32 == 0, "XOUT flush layout");
-      constexpr int PER = RS >= 32 ? 1 : 32 / RS;
-      const int sub = RS >= 32 ? 0 : lane / RS, k = RS >= 32 ? lane : lane % RS;
-#pragma unroll 4
-      for (int pr = 0; pr < 32; pr += PER) {
-        const int sysl = pr + sub;
-        const int r = r0 + k;
-        if (k < RS && r >= 0 && b0 + sysl < B)
-          fuse.zout[static_cast<long long>(b0 + sysl) * n + r] = xt[sysl * XP + k];
-      }
-      __syncwarp();
-    }
   }
   if constexpr (PERIODIC) {
     const int sys = UNIFORM ? 0 : b;
@@ -1277,18 +1226,18 @@ bool sweep_maps(const PentaTables& f, int B, int n, const double* z, SweepMaps* 
   return true;
 }
 
-template <bool U, bool P, int M, bool XC = false, bool XO = false>
+template <bool U, bool P, int M>
 void launch_sweep_tma(const PentaTables& f, const SweepMaps& maps, int B, int n, double* z, double* y4,
-                      cudaStream_t s, const SweepFuse& fuse = SweepFuse{}) {
-  auto kern = k_sweep_tma<U, P, M, XC, XO>;
-  using SM = SweepSmem<U, XC>;
+                      cudaStream_t s) {
+  auto kern = k_sweep_tma<U, P, M>;
+  using SM = SweepSmem<U>;
   static bool configured = false;
   if (!configured) {
     SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SM::bytes)));
     configured = true;
   }
   const int blocks = (B + 31) / 32;
-  kern<<<blocks, 64, SM::bytes, s>>>(f, maps, B, n, z, y4, fuse);
+  kern<<<blocks, 64, SM::bytes, s>>>(f, maps, B, n, z, y4);
 }
 
 bool use_resident_sweep() {
@@ -1451,30 +1400,6 @@ bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double
   return true;
 }
 
-bool penta_sweep_fused(const PentaTables& f, int B, int n, double* z, double* y4, const double* const* Wc,
-                       const double* yc, double* zout, cudaStream_t s) {
-  // Uniform periodic operator only (the CH sweeps); y4 receives this sweep's
-  // Woodbury coefficients (MODE 1). Returns false when the TMA path cannot
-  // run (caller falls back to the unfused kernels).
-  if (!f.uniform) return false;
-  SweepMaps maps;
-  if (!sweep_maps(f, B, n, z, &maps)) return false;
-  SweepFuse fuse;
-  if (Wc) {
-    if (reinterpret_cast<uintptr_t>(yc) & 15) return false;
-    for (int k = 0; k < 4; ++k) {
-      fuse.Wc[k] = Wc[k];
-      if (!encode_map(&maps.yc[k], yc + static_cast<size_t>(k) * n, 1, n, 1, SW_RS, 1)) return false;
-    }
-  }
-  fuse.zout = zout;
-  if (Wc && zout) launch_sweep_tma<true, true, 1, true, true>(f, maps, B, n, z, y4, s, fuse);
-  else if (Wc) launch_sweep_tma<true, true, 1, true, false>(f, maps, B, n, z, y4, s, fuse);
-  else if (zout) launch_sweep_tma<true, true, 1, false, true>(f, maps, B, n, z, y4, s, fuse);
-  else launch_sweep_tma<true, true, 1>(f, maps, B, n, z, y4, s);
-  check_launch("penta fused sweep (TMA) kernel");
-  return true;
-}
 
 // ------------------------------------------------------------ PentaFactor
 

@@ -50,13 +50,6 @@ struct DevicePenta {
 void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool periodic,
                  bool fusedCorrection, cudaStream_t s, bool pdl = false);
 
-// CH fusion (uniform periodic operator, MODE 1): Wc/yc apply a previous
-// sweep's Woodbury correction on load (Wc: 4 vectors of length B, yc: 4
-// vectors of length n); zout receives the backward results transposed
-// (zout[b*n + r]). Returns false if the fused TMA path is unavailable.
-bool penta_sweep_fused(const PentaTables& f, int B, int n, double* z, double* y4, const double* const* Wc,
-                       const double* yc, double* zout, cudaStream_t s);
-
 // Uniform periodic sweep reading its input TRANSPOSED: zT[b*n + r] (system-
 // major for this batch), e.g. the other sweep's output or a row-major RHS.
 // With Wc (the CH y-sweep) the previous sweep's Woodbury correction is
