@@ -31,12 +31,16 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "penta.cuh"
@@ -441,10 +445,352 @@ int rhs_kind() {
   return v;
 }
 
+// ------------------------------------------------------------ k_rhs_tp
+// k_rhs_tp<NL>: the steady-state fused combine + RHS (k_rhs_v<NL, true>'s
+// arithmetic, term for term) as a persistent tile pipeline. k_rhs_v holds
+// its loads in registers (128 per thread, two CTAs per SM) and a CTA
+// alternates between a load phase and an FP64 phase, so DRAM idles while
+// both CTAs of an SM compute (4.7 TB/s at 8192^2). Here one CTA per SM
+// walks the 64 x 32 output tiles round-robin:
+//  * one producer thread streams each tile's 68 x 36 halo windows of C^n,
+//    C^{n-1} and w, the window's 36 rows of the four y Woodbury vectors and
+//    its 68 columns of y4 into a 3-stage shared-memory ring: five 2D tensor
+//    TMA boxes per tile, completion on a per-stage mbarrier. (One bulk copy
+//    per window row — 116 per tile — measured 2x slower than k_rhs_v: small
+//    copies serialise in the TMA unit.) Boxes reaching past the grid edge
+//    read zeros there; the consumers of such a tile (2 % at 8192^2) patch
+//    the periodic wrap from global memory before the transform;
+//  * two consumer groups of eight warps take alternate tiles: the
+//    transform (C^{n+1}, Cbar = 2C^{n+1} - C^n, c^3 - c) is done in place in
+//    the stage (Cbar over the C^{n-1} window, c^3 - c over the w window),
+//    then the 13-tap biharmonic and 5-tap nonlinear sums run as in k_rhs_v;
+//    the stage is released through an "empty" mbarrier.
+// No registers hold loads, so the ring keeps ~60-120 KB per SM in flight
+// through the FP64 phase.
+constexpr int TP_NST = 3;  // ring stages
+constexpr int TP_NG = 2;   // consumer groups (8 warps each)
+constexpr int TP_THREADS = 32 * (8 * TP_NG + 1);
+
+struct TpStage {
+  double c[RYE][RXE];  // C^n window, then (in place) nothing
+  double p[RYE][RXE];  // C^{n-1} window, then Cbar
+  double w[RYE][RXE];  // w window, then c^3 - c
+  double W[4][RYE];    // y Woodbury vectors, the window's rows
+  double y[4][RXE];    // y4, the window's columns
+};
+constexpr uint32_t kTpStageBytes = sizeof(TpStage);
+struct TpMaps {
+  CUtensorMap c, p, w;  // (nx, ny) fields, box (RXE, RYE)
+  CUtensorMap W;        // y Woodbury vectors (ny, 4), box (RYE, 4)
+  CUtensorMap y;        // y4 (nx, 4), box (RXE, 4)
+};
+constexpr size_t kTpSmem = TP_NST * sizeof(TpStage) + 2 * TP_NST * sizeof(uint64_t);
+static_assert(sizeof(TpStage) % 16 == 0 && offsetof(TpStage, W) % 16 == 0 && offsetof(TpStage, y) % 16 == 0,
+              "bulk-copy destinations must be 16 B aligned");
+
+__device__ __forceinline__ uint32_t ch_s32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void ch_mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(ch_s32(bar)), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void ch_tma_2d(void* dst, const CUtensorMap* m, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          ch_s32(dst)),
+      "l"(m), "r"(x), "r"(y), "r"(ch_s32(bar))
+      : "memory");
+}
+
+template <bool NONLINEAR>
+__global__ void __launch_bounds__(TP_THREADS, 1) k_rhs_tp(const double* __restrict__ cc, const double* __restrict__ cp,
+                                                         const double* __restrict__ wv, const CorrTables cy,
+                                                         double* __restrict__ cnew, double* __restrict__ rhs,
+                                                         int nx, int ny, const __grid_constant__ RhsParams P,
+                                                         const __grid_constant__ TpMaps M) {
+  extern __shared__ __align__(128) unsigned char tp_raw[];
+  TpStage* st = reinterpret_cast<TpStage*>(tp_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tp_raw + TP_NST * sizeof(TpStage));
+  uint64_t* empty = full + TP_NST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tilesX = nx / RX, nTiles = tilesX * (ny / RY);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TP_NST; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ch_s32(full + s)) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 256;" ::"r"(ch_s32(empty + s)) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  const int myTiles = blockIdx.x < nTiles ? (nTiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp == 8 * TP_NG) {  // ---- producer (one thread)
+    if (lane != 0) return;
+    for (int k = 0; k < myTiles; ++k) {
+      const int s = k % TP_NST;
+      if (k >= TP_NST) ch_mbar_wait(empty + s, ((k / TP_NST) - 1) & 1);
+      const int tile = blockIdx.x + k * gridDim.x;
+      const int i0 = (tile % tilesX) * RX, j0 = (tile / tilesX) * RY;
+      TpStage& S = st[s];
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ch_s32(full + s)),
+                   "r"(kTpStageBytes)
+                   : "memory");
+      ch_tma_2d(S.c, &M.c, i0 - HALO, j0 - HALO, full + s);
+      ch_tma_2d(S.p, &M.p, i0 - HALO, j0 - HALO, full + s);
+      ch_tma_2d(S.w, &M.w, i0 - HALO, j0 - HALO, full + s);
+      ch_tma_2d(S.W, &M.W, j0 - HALO, 0, full + s);
+      ch_tma_2d(S.y, &M.y, i0 - HALO, 0, full + s);
+    }
+    return;
+  }
+
+  // ---- consumers: group g takes tiles g, g + NG, ...
+  const int g = warp >> 3, ty = warp & 7, tx = lane, tid = ty * 32 + tx;
+  const int x0 = 2 * tx, y0 = VR * ty;
+  // halo granule of this thread (k_rhs_v's assignment): rows 0, 1, RY+2,
+  // RY+3 (34 granules each), then the two edge granules of rows 2..RY+1
+  const bool halo = tid < 2 * VG * 2 + 2 * RY;
+  int hy = 0, hg = 0;
+  if (tid < 4 * VG) {
+    const int k = tid / VG;
+    hy = k < 2 ? k : RY + k;
+    hg = tid - k * VG;
+  } else {
+    const int h = tid - 4 * VG;
+    hy = HALO + (h >> 1);
+    hg = (h & 1) ? VG - 1 : 0;
+  }
+  for (int k = g; k < myTiles; k += TP_NG) {
+    const int s = k % TP_NST;
+    // Consecutive uses of a stage alternate between the groups, so this
+    // group may reach tile k while the stage's previous tile (k - NST, the
+    // other group's) is not even loaded: a parity wait on `full` alone would
+    // then match that older phase. Waiting for the release of tile k - NST
+    // first pins the phase (tile k - 2 NST was this group's own release).
+    if (k >= TP_NST) ch_mbar_wait(empty + s, ((k / TP_NST) - 1) & 1);
+    ch_mbar_wait(full + s, (k / TP_NST) & 1);
+    const int tile = blockIdx.x + k * gridDim.x;
+    const int i0 = (tile % tilesX) * RX, j0 = (tile / tilesX) * RY;
+    TpStage& S = st[s];
+    const bool ex = i0 == 0 || i0 + RX == nx, ey = j0 == 0 || j0 + RY == ny;
+    if (ex || ey) {  // periodic wrap of the boxes' out-of-grid parts
+      for (int e = tid; e < RYE * RXE; e += 256) {
+        const int y = e / RXE, x = e - y * RXE;
+        const int j = j0 - HALO + y, i = i0 - HALO + x;
+        if (j >= 0 && j < ny && i >= 0 && i < nx) continue;
+        const long long idx = static_cast<long long>(wrap_once(j, ny)) * nx + wrap_once(i, nx);
+        S.c[y][x] = __ldg(cc + idx);
+        S.p[y][x] = __ldg(cp + idx);
+        S.w[y][x] = __ldg(wv + idx);
+      }
+      if (ey)
+        for (int e = tid; e < 4 * RYE; e += 256) {
+          const int q = e / RYE, y = e - q * RYE, j = j0 - HALO + y;
+          if (j < 0 || j >= ny) S.W[q][y] = __ldg(cy.W[0] + static_cast<long long>(q) * ny + wrap_once(j, ny));
+        }
+      if (ex)
+        for (int e = tid; e < 4 * RXE; e += 256) {
+          const int q = e / RXE, x = e - q * RXE, i = i0 - HALO + x;
+          if (i < 0 || i >= nx) S.y[q][x] = __ldg(cy.y4 + static_cast<long long>(q) * nx + wrap_once(i, nx));
+        }
+      asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
+    }
+    // C^{n+1} at window granule (y, gc): k_combine's arithmetic
+    // (penta.cpp:283-284 correction, cahn_hilliard.cpp:273,320), then
+    // Cbar and c^3 - c in place; returns C^{n+1}, leaves C^n in cOld
+    auto advance = [&](int y, int gc, double2& cOld) {
+      const double2 c = *reinterpret_cast<const double2*>(&S.c[y][2 * gc]);
+      const double2 p = *reinterpret_cast<const double2*>(&S.p[y][2 * gc]);
+      const double2 w = *reinterpret_cast<const double2*>(&S.w[y][2 * gc]);
+      const double W0 = S.W[0][y], W1 = S.W[1][y], W2 = S.W[2][y], W3 = S.W[3][y];
+      const double2 y0v = *reinterpret_cast<const double2*>(&S.y[0][2 * gc]);
+      const double2 y1v = *reinterpret_cast<const double2*>(&S.y[1][2 * gc]);
+      const double2 y2v = *reinterpret_cast<const double2*>(&S.y[2][2 * gc]);
+      const double2 y3v = *reinterpret_cast<const double2*>(&S.y[3][2 * gc]);
+      double2 r;
+      r.x = (2.0 * c.x - p.x) + (w.x - (W0 * y0v.x + W1 * y1v.x + W2 * y2v.x + W3 * y3v.x));
+      r.y = (2.0 * c.y - p.y) + (w.y - (W0 * y0v.y + W1 * y1v.y + W2 * y2v.y + W3 * y3v.y));
+      double2 b;
+      b.x = 2.0 * r.x - c.x;  // cahn_hilliard.cpp:273 (this step's Cbar)
+      b.y = 2.0 * r.y - c.y;
+      *reinterpret_cast<double2*>(&S.p[y][2 * gc]) = b;
+      if constexpr (NONLINEAR) {
+        double2 f;
+        f.x = r.x * r.x * r.x - r.x;
+        f.y = r.y * r.y * r.y - r.y;
+        *reinterpret_cast<double2*>(&S.w[y][2 * gc]) = f;
+      }
+      cOld = c;
+      return r;
+    };
+    double d[VR][2];
+#pragma unroll
+    for (int r = 0; r < VR; ++r) {
+      double2 c;
+      const double2 cn = advance(HALO + y0 + r, tx + 1, c);
+      *reinterpret_cast<double2*>(cnew + static_cast<long long>(j0 + y0 + r) * nx + i0 + x0) = cn;
+      d[r][0] = cn.x - c.x;
+      d[r][1] = cn.y - c.y;
+    }
+    if (halo) {
+      double2 c;
+      advance(hy, hg, c);
+    }
+    asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory");
+
+    double bh[VR][2], nl[VR][2];
+#pragma unroll
+    for (int r = 0; r < VR; ++r) bh[r][0] = bh[r][1] = nl[r][0] = nl[r][1] = 0.0;
+#pragma unroll
+    for (int yy = 0; yy < VR + 4; ++yy) {  // Cbar rows y0 .. y0 + 7
+      double b[6];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const double2 v = *reinterpret_cast<const double2*>(&S.p[y0 + yy][x0 + 2 * q]);
+        b[2 * q] = v.x;
+        b[2 * q + 1] = v.y;
+      }
+#pragma unroll
+      for (int r = 0; r < VR; ++r) {
+        const int q = yy - r;
+        if (q < 0 || q > 4) continue;
+#pragma unroll
+        for (int p = 0; p < 5; ++p) {
+          constexpr unsigned kMask = (1u << 2) | (1u << 6) | (1u << 7) | (1u << 8) | (1u << 10) | (1u << 11) |
+                                     (1u << 12) | (1u << 13) | (1u << 14) | (1u << 16) | (1u << 17) | (1u << 18) |
+                                     (1u << 22);  // SG_BIH_TAPS
+          if (!((kMask >> (q * 5 + p)) & 1u)) continue;
+          bh[r][0] += P.bw[q * 5 + p] * b[p];
+          bh[r][1] += P.bw[q * 5 + p] * b[p + 1];
+        }
+      }
+    }
+    if constexpr (NONLINEAR) {
+#pragma unroll
+      for (int yy = 0; yy < VR + 2; ++yy) {  // c^3 - c rows y0 + 1 .. y0 + 6
+        double f[6];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double2 v = *reinterpret_cast<const double2*>(&S.w[y0 + 1 + yy][x0 + 2 * q]);
+          f[2 * q] = v.x;
+          f[2 * q + 1] = v.y;
+        }
+#pragma unroll
+        for (int r = 0; r < VR; ++r) {
+          const int q = yy - r;
+          if (q < 0 || q > 2) continue;
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            constexpr unsigned kMask = (1u << 1) | (1u << 3) | (1u << 4) | (1u << 5) | (1u << 7);  // SG_NL_TAPS
+            if (!((kMask >> (q * 3 + p)) & 1u)) continue;
+            nl[r][0] += P.nl[q * 3 + p] * f[1 + p];
+            nl[r][1] += P.nl[q * 3 + p] * f[2 + p];
+          }
+        }
+      }
+    }
+    // this thread's last shared-memory access of the stage: release it
+    // (generic-proxy writes above precede the next bulk copy into it)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ch_s32(empty + s)) : "memory");
+#pragma unroll
+    for (int r = 0; r < VR; ++r) {
+      double2 o;
+      if constexpr (NONLINEAR) {  // cahn_hilliard.cpp:292
+        o.x = P.kDiff * d[r][0] - P.kBih * bh[r][0] + P.kNl * nl[r][0];
+        o.y = P.kDiff * d[r][1] - P.kBih * bh[r][1] + P.kNl * nl[r][1];
+      } else {  // cahn_hilliard.cpp:294
+        o.x = P.kDiff * d[r][0] - P.kBih * bh[r][0];
+        o.y = P.kDiff * d[r][1] - P.kBih * bh[r][1];
+      }
+      *reinterpret_cast<double2*>(rhs + static_cast<long long>(j0 + y0 + r) * nx + i0 + x0) = o;
+    }
+  }
+}
+
+int ch_sm_count() {
+  static const int v = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return v;
+}
+
+// Tensor maps of the pipeline, cached by (pointer, shape): the CH buffers
+// are long-lived and a map only encodes the address and the shape.
+bool tp_map(CUtensorMap* m, const double* p, int d0, int d1, int b0, int b1) {
+  static std::mutex mu;
+  static std::map<std::tuple<const double*, int, int, int, int>, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(p, d0, d1, b0, b1);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    CUtensorMap enc;
+    if (!encode_tile_map(&enc, p, d0, d1, b0, b1)) return false;
+    it = cache.emplace(key, enc).first;
+  }
+  *m = it->second;
+  return true;
+}
+
+// SG_CH_RHS_TP=0 keeps k_rhs_v<NL, true> for the steady-state step (A/B);
+// =2 uses the pipeline on every eligible grid, however few tiles (tests).
+int rhs_tp_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("SG_CH_RHS_TP");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+// SG_CH_RHS_TP_CTAS=n caps the pipeline's grid (tests: many tiles per CTA,
+// so the ring wraps on small grids).
+int rhs_tp_ctas() {
+  static const int v = [] {
+    const char* e = std::getenv("SG_CH_RHS_TP_CTAS");
+    const int n = e ? std::atoi(e) : 0;
+    return n > 0 ? std::min(n, ch_sm_count()) : ch_sm_count();
+  }();
+  return v;
+}
+
 // The steady-state step's first kernel: previous combine + this RHS (k_rhs_v
 // FUSE). Single GPU (full periodic grid), nx a multiple of 64.
 void launch_rhs_fused(bool nonlinear, const double* cc, const double* cp, const double* w, const CorrTables& ty,
                       double* cnew, double* rhsT, const RhsGeom& g, const RhsParams& rp, cudaStream_t s, bool pdl) {
+  // the pipeline needs the y Woodbury vectors contiguous ([4][ny], ChState's
+  // wyCat copy) and boxes no larger than the grid
+  const bool wcat = ty.W[1] == ty.W[0] + g.outRows && ty.W[2] == ty.W[1] + g.outRows && ty.W[3] == ty.W[2] + g.outRows;
+  TpMaps maps;
+  // (below ~4 tiles per SM the ring never fills: 1024^2 measured 1 % slower)
+  const long long tiles = static_cast<long long>(g.nx / RX) * (g.outRows / RY);
+  const int mode = rhs_tp_mode();
+  if (mode != 0 && wcat && g.rowOut && g.outRows % RY == 0 && g.nx % RX == 0 && g.nx >= 2 * RX &&
+      g.outRows >= 2 * RY && (mode == 2 || tiles >= 4LL * ch_sm_count()) && tp_map(&maps.c, cc, g.nx, g.outRows, RXE, RYE) &&
+      tp_map(&maps.p, cp, g.nx, g.outRows, RXE, RYE) && tp_map(&maps.w, w, g.nx, g.outRows, RXE, RYE) &&
+      tp_map(&maps.W, ty.W[0], g.outRows, 4, RYE, 4) && tp_map(&maps.y, ty.y4, g.nx, 4, RXE, 4)) {
+    static bool configured = false;
+    if (!configured) {
+      SG_CUDA(cudaFuncSetAttribute(k_rhs_tp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(kTpSmem)));
+      SG_CUDA(cudaFuncSetAttribute(k_rhs_tp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(kTpSmem)));
+      configured = true;
+    }
+    const int grid = static_cast<int>(std::min<long long>(tiles, rhs_tp_ctas()));
+    launch_ex(nonlinear ? k_rhs_tp<true> : k_rhs_tp<false>, dim3(grid), dim3(TP_THREADS), kTpSmem, s, pdl, cc, cp,
+              w, ty, cnew, rhsT, g.nx, g.outRows, rp, maps);
+    check_launch("ch fused combine+rhs pipeline kernel");
+    return;
+  }
   dim3 tb(32, 8), tg(g.nx / RX, (g.outRows + RY - 1) / RY);
   launch_ex(nonlinear ? k_rhs_v<true, true> : k_rhs_v<false, true>, tg, tb, 0, s, pdl, cc, cp, rhsT, g, rp, w, ty,
             cnew);
@@ -714,6 +1060,9 @@ struct ChState {
   double* field[3] = {nullptr, nullptr, nullptr};
   int ic = 0, ip = 1;
   double *rhsT = nullptr, *w = nullptr, *y4x = nullptr, *y4y = nullptr;
+  // the y factor's four Woodbury vectors copied contiguously ([4][ny]): one
+  // tensor map for the steady-state RHS pipeline (k_rhs_tp)
+  double* wyCat = nullptr;
   // xpipe: the RHS is written row-major into rhsT, the x-sweep reads it
   // transposed and writes its interleaved result to xT, the y-sweep reads xT
   // transposed with the x Woodbury correction (no transpose kernel)
@@ -775,6 +1124,10 @@ struct ChState {
     const double sy = kTwoThirds * p.D * p.gamma * p.dt / pow4(dy);
     build_factor(fx, sx, p.nx);
     build_factor(fy, sy, p.ny);
+    wyCat = dalloc(4 * static_cast<size_t>(p.ny));
+    for (int k = 0; k < 4; ++k)
+      SG_CUDA(cudaMemcpyAsync(wyCat + static_cast<size_t>(k) * p.ny, fy.t.W[k], p.ny * sizeof(double),
+                              cudaMemcpyDeviceToDevice, stream));
     rp.kDiff = -kTwoThirds;
     rp.kBih = kTwoThirds * p.D * p.gamma * p.dt;
     rp.kNl = kTwoThirds * p.D * p.dt;
@@ -824,7 +1177,7 @@ struct ChState {
     const RhsGeom geom{nx, ny, ny, 0, 1, xpipe ? 1 : 0};
     const bool pdl = pdl_enabled();
     if (in >= 0) {
-      CorrTables ty{{fy.t.W[0], fy.t.W[1], fy.t.W[2], fy.t.W[3]}, y4y};
+      CorrTables ty{{wyCat, wyCat + ny, wyCat + 2LL * ny, wyCat + 3LL * ny}, y4y};
       launch_rhs_fused(p.nonlinearEnabled, field[c], field[q], w, ty, field[in], rhsT, geom, rp, s, pdl);
     } else {
       launch_rhs(p.nonlinearEnabled, field[c], field[q], rhsT, geom, rp, s, pdl);

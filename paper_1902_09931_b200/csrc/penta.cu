@@ -1300,6 +1300,11 @@ void launch_sweep_t(const PentaTables& f, int B, int n, double* z, double* y4, c
 
 }  // namespace
 
+// 2D FP64 tile map (no swizzle, zero OOB fill) for other kernels (ch.cu).
+bool encode_tile_map(void* m, const double* p, uint64_t d0, uint64_t d1, uint32_t b0, uint32_t b1) {
+  return encode_map(static_cast<CUtensorMap*>(m), p, 2, d0, d1, b0, b1);
+}
+
 namespace {
 // z[r*B + b] -= W0[r] y0[b] + W1[r] y1[b] + W2[r] y2[b] + W3[r] y3[b]
 // (penta.cpp:279-286) as one fully parallel pass: the recurrence kernels

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include <vector>
 
 namespace sg {
@@ -22,6 +24,10 @@ struct PentaTables {
   const int* piv = nullptr;
   int uniform = 0;
 };
+
+// Encodes a 2D FP64 tensor map (CUtensorMap*, dims d0 x d1, box b0 x b1,
+// no swizzle, OOB elements read as zero); false without a driver encoder.
+bool encode_tile_map(void* m, const double* p, uint64_t d0, uint64_t d1, uint32_t b0, uint32_t b1);
 
 // Owns the device factor of one (periodic or not) batch.
 struct DevicePenta {

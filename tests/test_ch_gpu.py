@@ -178,6 +178,12 @@ def test_steady_state_step_many_bitwise(sg, orc, nx, ny, nonlinear):
     ({"SG_CH_XIN": "0"}, 128, 64),          # separate transpose/correct kernel
     ({"SG_PDL": "0"}, 128, 128),            # plain stream-ordered launches
     ({"SG_CH_STEADY": "0"}, 128, 128),      # combine not folded into the next RHS
+    ({"SG_CH_RHS_TP": "0"}, 2048, 256),     # steady RHS without the tile pipeline
+    # the steady RHS tile pipeline on small grids, few CTAs: the 3-stage ring
+    # wraps many times, every tile touches the periodic edge on 128 x 64
+    ({"SG_CH_RHS_TP": "2", "SG_CH_RHS_TP_CTAS": "3"}, 128, 64),
+    ({"SG_CH_RHS_TP": "2", "SG_CH_RHS_TP_CTAS": "5"}, 512, 256),
+    ({"SG_CH_RHS_TP": "2", "SG_CH_RHS_TP_CTAS": "5", "_linear": "1"}, 256, 128),
 ])
 def test_step_variants_bitwise(orc, env, nx, ny):
     """Every selectable CH pipeline variant gives the reference's bits
@@ -186,10 +192,12 @@ def test_step_variants_bitwise(orc, env, nx, ny):
     import subprocess
     import sys
     from pathlib import Path
+    linear = env.get("_linear") == "1"
     code = (
         "import sys, numpy as np; sys.path.insert(0, '.');"
         "import paper_1902_09931_b200 as sg;"
         f"p = sg.CHParams(nx={nx}, ny={ny}); p.dt = 0.1 * p.dx(); p.T = 1.0;"
+        f"p.nonlinearEnabled = {not linear};"
         "st = sg.CHStepper(p); st.step_many(9);"
         "np.save(sys.argv[1], np.stack([st.field().values, st.previous_field().values]))")
     root = Path(__file__).resolve().parents[1]
@@ -198,7 +206,8 @@ def test_step_variants_bitwise(orc, env, nx, ny):
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     got = np.load(out)
-    p = dict(D=1.0, gamma=0.01, lx=2 * math.pi, ly=2 * math.pi, dt=0.1 * (2 * math.pi / nx), nx=nx, ny=ny)
+    p = dict(D=1.0, gamma=0.01, lx=2 * math.pi, ly=2 * math.pi, dt=0.1 * (2 * math.pi / nx), nx=nx, ny=ny,
+             nonlinear=not linear)
     c0 = orc.ch_initial_condition(nx, ny)
     want_c, want_p = orc.ch_run(p, 9, c0, c0)
     assert bits_equal(got[0], want_c)
