@@ -509,11 +509,25 @@ __device__ __forceinline__ void ch_tma_2d(void* dst, const CUtensorMap* m, int x
       : "memory");
 }
 
+// Tile t's origin: row-major over tiles (band 0), or bands of `band` tile
+// rows walked column by column (vertical neighbours run in the same wave).
+__device__ __forceinline__ void tp_tile_origin(int t, int tilesX, int band, int& i0, int& j0) {
+  if (band <= 0) {
+    i0 = (t % tilesX) * RX;
+    j0 = (t / tilesX) * RY;
+    return;
+  }
+  const int per = tilesX * band, b = t / per, r = t - b * per;
+  i0 = (r / band) * RX;
+  j0 = (b * band + r % band) * RY;
+}
+
 template <bool NONLINEAR>
 __global__ void __launch_bounds__(TP_THREADS, 1) k_rhs_tp(const double* __restrict__ cc, const double* __restrict__ cp,
                                                          const double* __restrict__ wv, const CorrTables cy,
                                                          double* __restrict__ cnew, double* __restrict__ rhs,
-                                                         int nx, int ny, const __grid_constant__ RhsParams P,
+                                                         int nx, int ny, int band,
+                                                         const __grid_constant__ RhsParams P,
                                                          const __grid_constant__ TpMaps M) {
   extern __shared__ __align__(128) unsigned char tp_raw[];
   TpStage* st = reinterpret_cast<TpStage*>(tp_raw);
@@ -538,7 +552,8 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_rhs_tp(const double* __restri
       const int s = k % TP_NST;
       if (k >= TP_NST) ch_mbar_wait(empty + s, ((k / TP_NST) - 1) & 1);
       const int tile = blockIdx.x + k * gridDim.x;
-      const int i0 = (tile % tilesX) * RX, j0 = (tile / tilesX) * RY;
+      int i0, j0;
+      tp_tile_origin(tile, tilesX, band, i0, j0);
       TpStage& S = st[s];
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ch_s32(full + s)),
                    "r"(kTpStageBytes)
@@ -578,7 +593,8 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_rhs_tp(const double* __restri
     if (k >= TP_NST) ch_mbar_wait(empty + s, ((k / TP_NST) - 1) & 1);
     ch_mbar_wait(full + s, (k / TP_NST) & 1);
     const int tile = blockIdx.x + k * gridDim.x;
-    const int i0 = (tile % tilesX) * RX, j0 = (tile / tilesX) * RY;
+    int i0, j0;
+    tp_tile_origin(tile, tilesX, band, i0, j0);
     TpStage& S = st[s];
     const bool ex = i0 == 0 || i0 + RX == nx, ey = j0 == 0 || j0 + RY == ny;
     if (ex || ey) {  // periodic wrap of the boxes' out-of-grid parts
@@ -786,8 +802,15 @@ void launch_rhs_fused(bool nonlinear, const double* cc, const double* cp, const 
       configured = true;
     }
     const int grid = static_cast<int>(std::min<long long>(tiles, rhs_tp_ctas()));
+    // tiles walked in bands of two tile rows, column by column: 8192^2
+    // 796 -> 835 steps/s against row-major order (SG_CH_RHS_TP_BAND=1;
+    // bands of 4 / 8: 830 / 828), 4096^2 and 2048^2 within 1 %
+    static const int band = [] {
+      const char* e = std::getenv("SG_CH_RHS_TP_BAND");
+      return e ? std::atoi(e) : 2;
+    }();
     launch_ex(nonlinear ? k_rhs_tp<true> : k_rhs_tp<false>, dim3(grid), dim3(TP_THREADS), kTpSmem, s, pdl, cc, cp,
-              w, ty, cnew, rhsT, g.nx, g.outRows, rp, maps);
+              w, ty, cnew, rhsT, g.nx, g.outRows, band > 0 && (g.outRows / RY) % band == 0 ? band : 0, rp, maps);
     check_launch("ch fused combine+rhs pipeline kernel");
     return;
   }

@@ -184,6 +184,8 @@ def test_steady_state_step_many_bitwise(sg, orc, nx, ny, nonlinear):
     ({"SG_CH_RHS_TP": "2", "SG_CH_RHS_TP_CTAS": "3"}, 128, 64),
     ({"SG_CH_RHS_TP": "2", "SG_CH_RHS_TP_CTAS": "5"}, 512, 256),
     ({"SG_CH_RHS_TP": "2", "SG_CH_RHS_TP_CTAS": "5", "_linear": "1"}, 256, 128),
+    ({"SG_CH_RHS_TP": "2", "SG_CH_RHS_TP_CTAS": "4", "SG_CH_RHS_TP_BAND": "1"}, 256, 128),  # row-major tiles
+    ({"SG_CH_RHS_TP": "2", "SG_CH_RHS_TP_CTAS": "7", "SG_CH_RHS_TP_BAND": "4"}, 512, 256),
 ])
 def test_step_variants_bitwise(orc, env, nx, ny):
     """Every selectable CH pipeline variant gives the reference's bits
