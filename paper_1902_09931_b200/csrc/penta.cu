@@ -350,7 +350,7 @@ constexpr int SW_NSTG = 4;  // stages in flight
 struct alignas(64) SweepMaps {
   CUtensorMap z;     // 2D {B, n}, box {32, RS}
   CUtensorMap t[5];  // m1, m2, dInv, ap, bp: uniform 1D {n} box {RS}; else 2D like z
-  CUtensorMap yc[4]; // XIN 1: the previous sweep's Woodbury coefficients y_k[r], 1D {n} box {RS}
+  CUtensorMap yc[1]; // XIN 1: the previous sweep's Woodbury coefficients y_k[r], 2D {n, 4} box {RS, 4}
   CUtensorMap zt;    // XIN (k_sweep_res): the input read TRANSPOSED, system-major:
                      // 3D {ztInner, B, n / ztInner} box {16, 32, 1}, 128 B swizzle —
                      // unknown r of system b at ((r % ztInner), b, r / ztInner): one
@@ -358,6 +358,7 @@ struct alignas(64) SweepMaps {
   CUtensorMap pz[8]; // P2P: the final (backward) results of unknowns [d*prow, (d+1)*prow)
                      // go to destination d's buffer (box {32, RS}, at (b, r - d*prow))
   int ztInner = 0;
+  int ztBox = 0;     // 1: zt is the 4D view {16, B, ztInner / 16, n / ztInner}, box {16, 32, RS/16, 1}
   int npeer = 0;     // 0: final results stay in z
   int prow = 0;
 };
@@ -423,6 +424,13 @@ __device__ __forceinline__ void s_tma_3d(void* dst, const CUtensorMap* m, int x,
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
       "[%5];" ::"r"(s_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(z), "r"(s_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void s_tma_4d(void* dst, const CUtensorMap* m, int x, int y, int z, int w, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(s_u32(dst)),
+      "l"(m), "r"(x), "r"(y), "r"(z), "r"(w), "r"(s_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void s_tma_1d(void* dst, const CUtensorMap* m, int x, uint64_t* bar) {
@@ -718,8 +726,16 @@ static_assert(RG >= 2, "the first operand group must cover rows 0 and 1");
 // transpose/correct pass (16 B/pt of traffic and a launch) disappears.
 // XIN 2 (the CH x-sweep): the same transposed read with no correction — the
 // RHS kernel then writes its output row-major (coalesced) instead of
-// transposed. Four ring slots instead of five pay for the raw buffers.
+// transposed. Four ring slots instead of five pay for the raw buffers; the
+// TMA traffic moves to a fifth warp (the transform warps only transform).
 constexpr int XIN_TW = 3;  // transform warps (1-3) of the XIN sweep
+// Raw zT buffers of the XIN sweep (ring slots: 4 with two raw buffers, 3
+// with three). With the TMA producer in its own warp, two suffice:
+// sweep_trace at 8192^2 y / x-sweep 375 / 352 us (two) against 379 / 362
+// (three), at 1024^2 70.5 k / 68.7 k cycles against 71.3 k / 69.7 k.
+#ifndef SG_XIN_NRAW
+#define SG_XIN_NRAW 2
+#endif
 
 template <int RS, int XIN = 0>
 struct RRGeom {
@@ -727,13 +743,16 @@ struct RRGeom {
   static constexpr int STAGE = RS * 32 + 5 * FAC;  // doubles per slot
   static_assert((STAGE * 8) % 128 == 0 && (FAC * 8) % 128 == 0, "TMA destinations must be 128 B aligned");
   static_assert(RS % RG == 0 && RS % 16 == 0, "stage = whole operand groups / swizzle boxes");
-  static constexpr int NST = XIN ? 4 : RR_NSTG;
+  // XIN: NRAW raw buffers (NRAW - 1 stages of zT in flight ahead of the
+  // transform) and NST ring slots, within the two-CTAs-per-SM budget
+  static constexpr int NRAW = XIN ? SG_XIN_NRAW : 0;
+  static constexpr int NST = XIN ? (NRAW > 2 ? 3 : 4) : RR_NSTG;
   // doubles per raw buffer: RS/16 swizzled zT boxes of 4 KB, then the
   // stage's four y_k row vectors (1D TMA)
   static constexpr int RAW = XIN ? RS * 32 + 4 * RS : 0;
   static constexpr size_t RAW_OFF = static_cast<size_t>(NST) * STAGE * 8;  // bytes, before alignment
   static constexpr size_t SMEM =
-      RAW_OFF + (XIN ? 2 * RAW * 8 + 1024 : 0) + (2 * NST + 2) * 8;
+      RAW_OFF + (XIN ? NRAW * RAW * 8 + 1024 : 0) + (XIN ? 3 * NST + 2 * NRAW : 2 * NST) * 8;
 };
 
 __device__ __forceinline__ void s_tma_store_2d(const CUtensorMap* m, int x, int y, const void* src) {
@@ -749,14 +768,21 @@ __device__ long long g_sweep_trace[8192];
   do {                                                                \
     if (blockIdx.x == 0 && lane == 0) g_sweep_trace[(i)] = clock64(); \
   } while (0)
+#define SG_TRACE_X(i)                                                                  \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && warp == 1 && lane == 0) g_sweep_trace[4096 + (i)] = clock64(); \
+  } while (0)
 #else
+#define SG_TRACE_X(i) \
+  do {                \
+  } while (0)
 #define SG_TRACE(i) \
   do {              \
   } while (0)
 #endif
 
 template <bool PERIODIC, int RS, int XIN>
-__global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(const PentaTables f, const __grid_constant__ SweepMaps maps, int B,
+__global__ void __launch_bounds__(XIN ? 32 * (2 + XIN_TW) : 64) k_sweep_res(const PentaTables f, const __grid_constant__ SweepMaps maps, int B,
                                                   int n, double* __restrict__ y4, const SweepFuse fuse) {
   extern __shared__ __align__(128) double rr_smem[];
   using GEO = RRGeom<RS, XIN>;
@@ -770,12 +796,14 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
   if constexpr (XIN) {
     const uint32_t a = s_u32(rr_smem) + static_cast<uint32_t>(GEO::RAW_OFF);
     raw = rr_smem + (GEO::RAW_OFF + ((1024u - (a & 1023u)) & 1023u)) / 8;
-    full = reinterpret_cast<uint64_t*>(rr_smem + (GEO::RAW_OFF + 1024 + 2 * GEO::RAW * 8) / 8);
+    full = reinterpret_cast<uint64_t*>(rr_smem + (GEO::RAW_OFF + 1024 + GEO::NRAW * GEO::RAW * 8) / 8);
   } else {
     full = reinterpret_cast<uint64_t*>(rr_smem + NST * STG);
   }
   uint64_t* done = full + NST;
-  uint64_t* rawfull = done + NST;  // XIN only
+  uint64_t* rawfull = done + NST;             // XIN only: raw buffer loaded
+  uint64_t* rawfree = rawfull + GEO::NRAW;     // XIN: raw buffer read by the transform
+  uint64_t* slotfree = rawfree + GEO::NRAW;    // XIN: forward slot stored, writable
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b0 = blockIdx.x * 32;
   const int nS = (n + RS - 1) / RS;
@@ -788,8 +816,11 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
       s_mbar_init(&done[k], 1);
     }
     if constexpr (XIN) {
-      s_mbar_init(&rawfull[0], 1);
-      s_mbar_init(&rawfull[1], 1);
+      for (int k = 0; k < GEO::NRAW; ++k) {
+        s_mbar_init(&rawfull[k], 1);
+        s_mbar_init(&rawfree[k], 32 * XIN_TW);
+      }
+      for (int k = 0; k < NST; ++k) s_mbar_init(&slotfree[k], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -804,7 +835,8 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
 
   if (warp >= 1) {
     // ------------------------------------------------------------ producer
-    // (warp 1; with XIN warps 1-3 share the forward transform)
+    // (warp 1 lane 0; with XIN, warp XIN_TW + 1 lane 0, while warps 1-3
+    // run the forward transform)
     auto load = [&](int s, int G) {
       double* st = rr_smem + s * STG;
       s_mbar_expect_tx(&full[s], TX);
@@ -818,91 +850,111 @@ __global__ void __launch_bounds__(XIN ? 32 * (1 + XIN_TW) : 64) k_sweep_res(cons
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     };
     if constexpr (XIN) {
-      // forward stages: warp 1 lane 0 issues the TMA traffic; warps 1-3
-      // (three SMSPs: the transform's FP64 work is ~2x the consumer's per
-      // row) transpose + correct the raw zT boxes of stage g into slot
-      // g % NST (k_transpose_correct's expression: z - (W0 y0 + W1 y1 + W2 y2
-      // + W3 y3), penta.cpp:283-284)
-      const int tw = warp - 1;  // transform warp 0..XIN_TW-1
-      const bool issuer = tw == 0 && lane == 0;
-      const int bl = b0 + lane;
-      double Wb[4] = {0.0, 0.0, 0.0, 0.0};
-      if constexpr (XIN == 1) {
+      constexpr int NR = GEO::NRAW;
+      if (warp <= XIN_TW) {
+        // forward stages, transform warps 1-3 (three SMSPs: the transform's
+        // FP64 work is ~2x the consumer's per row): transpose (+ correct) the
+        // raw zT boxes of stage g into slot g % NST (k_transpose_correct's
+        // expression: z - (W0 y0 + W1 y1 + W2 y2 + W3 y3), penta.cpp:283-284)
+        const int tw = warp - 1;  // transform warp 0..XIN_TW-1
+        const int bl = b0 + lane;
+        double Wb[4] = {0.0, 0.0, 0.0, 0.0};
+        if constexpr (XIN == 1) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) Wb[k] = bl < B ? __ldg(fuse.Wc[k] + bl) : 0.0;
-      }
-      auto load_raw = [&](int g) {
-        double* rb = raw + (g & 1) * GEO::RAW;
-        s_mbar_expect_tx(&rawfull[g & 1], (RS * 32 + (XIN == 1 ? 4 * RS : 0)) * 8);
-        for (int x = 0; x < RS / 16; ++x) {
-          const int r = g * RS + x * 16;
-          s_tma_3d(rb + x * 512, &maps.zt, r % maps.ztInner, b0, r / maps.ztInner, &rawfull[g & 1]);
+          for (int k = 0; k < 4; ++k) Wb[k] = bl < B ? __ldg(fuse.Wc[k] + bl) : 0.0;
         }
-        if constexpr (XIN == 1)
-          for (int k = 0; k < 4; ++k) s_tma_1d(rb + RS * 32 + k * RS, &maps.yc[k], g * RS, &rawfull[g & 1]);
+        for (int g = 0; g < nS; ++g) {
+          const int s = g % NST;
+          SG_TRACE_X(4 * g);
+          // the slot's previous stage has been stored (read out by the TMA)
+          if (g >= NST) s_mbar_wait(&slotfree[s], ((g / NST) - 1) & 1);
+          SG_TRACE_X(4 * g + 1);
+          s_mbar_wait(&rawfull[g % NR], (g / NR) & 1);
+          SG_TRACE_X(4 * g + 2);
+          const double* rb = raw + (g % NR) * GEO::RAW;
+          double* zs = rr_smem + s * STG;
+          // batches of TB row pairs, dealt round-robin to the transform warps:
+          // all loads first, then the arithmetic (independent chains
+          // interleave), then the stores
+          constexpr int TB = 4;
+          for (int jb = tw * TB; jb < RS / 2; jb += XIN_TW * TB) {
+            double2 v[TB], y[TB][4];
+#pragma unroll
+            for (int t = 0; t < TB; ++t) {
+              const int jp = jb + t;
+              // rows 2jp, 2jp+1 of system bl: box jp/8, 16 B chunk jp%8 of
+              // smem row `lane`, XOR-swizzled by lane % 8
+              v[t] = *reinterpret_cast<const double2*>(rb + (jp >> 3) * 512 + lane * 16 +
+                                                       (((jp & 7) ^ (lane & 7)) << 1));
+              if constexpr (XIN == 1) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)  // broadcast: every lane reads the same pair
+                  y[t][k] = *reinterpret_cast<const double2*>(rb + RS * 32 + k * RS + 2 * jp);
+              }
+            }
+            double o[TB][2];
+#pragma unroll
+            for (int t = 0; t < TB; ++t) {
+              if constexpr (XIN == 1) {
+                const double c0 = Wb[0] * y[t][0].x + Wb[1] * y[t][1].x + Wb[2] * y[t][2].x + Wb[3] * y[t][3].x;
+                const double c1 = Wb[0] * y[t][0].y + Wb[1] * y[t][1].y + Wb[2] * y[t][2].y + Wb[3] * y[t][3].y;
+                o[t][0] = v[t].x - c0;
+                o[t][1] = v[t].y - c1;
+              } else {
+                o[t][0] = v[t].x;
+                o[t][1] = v[t].y;
+              }
+            }
+#pragma unroll
+            for (int t = 0; t < TB; ++t) {
+              zs[(2 * (jb + t)) * 32 + lane] = o[t][0];
+              zs[(2 * (jb + t) + 1) * 32 + lane] = o[t][1];
+            }
+          }
+          s_mbar_arrive(&full[s]);         // each thread releases its own slot writes
+          s_mbar_arrive(&rawfree[g % NR]);  // ... and its reads of the raw buffer
+          SG_TRACE_X(4 * g + 3);
+        }
+        return;
+      }
+      // warp XIN_TW + 1, lane 0: every TMA operation of the CTA. Forward
+      // stage g: store slot g % NST (stage g - NST, once the consumer is
+      // done with it) and hand it to the transform; the stage's factor rows;
+      // the raw zT (+ y_k) rows of stage g + NR - 1 into the buffer that
+      // stage g - 1's transform has released. (Issuing from a transform warp
+      // serialised ~100 cycles per TMA operation and the store's smem read
+      // into the transform loop: the chain waited 20 % of the 8192^2 y-sweep.)
+      if (lane != 0) return;
+      auto load_raw = [&](int g) {
+        double* rb = raw + (g % NR) * GEO::RAW;
+        s_mbar_expect_tx(&rawfull[g % NR], (RS * 32 + (XIN == 1 ? 4 * RS : 0)) * 8);
+        if (maps.ztBox) {  // one 4D box: RS/16 chunks of 16 unknowns x 32 systems
+          const int r = g * RS;
+          s_tma_4d(rb, &maps.zt, 0, b0, (r % maps.ztInner) / 16, r / maps.ztInner, &rawfull[g % NR]);
+        } else {
+          for (int x = 0; x < RS / 16; ++x) {
+            const int r = g * RS + x * 16;
+            s_tma_3d(rb + x * 512, &maps.zt, r % maps.ztInner, b0, r / maps.ztInner, &rawfull[g % NR]);
+          }
+        }
+        if constexpr (XIN == 1) s_tma_2d(rb + RS * 32, &maps.yc[0], g * RS, 0, &rawfull[g % NR]);
       };
-      if (issuer) load_raw(0);
+      for (int g = 0; g < NR - 1 && g < nS; ++g) load_raw(g);
       for (int g = 0; g < nS; ++g) {
         const int s = g % NST;
-        if (issuer && g >= NST) {
+        if (g >= NST) {
           s_mbar_wait(&done[s], ((g / NST) + 1) & 1);
           store(s, g - NST);
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          s_mbar_arrive(&slotfree[s]);
         }
-        // slot s is free (its store has read it) and every transform warp has
-        // finished stage g-1 (so its raw buffer can be refilled)
-        __syncwarp();  // the issuer lane diverged: reconverge before the aligned barrier
-        asm volatile("bar.sync 1, %0;" ::"n"(XIN_TW * 32) : "memory");
-        if (issuer) {
-          double* st = rr_smem + s * STG;
-          s_mbar_expect_tx(&full[s], FTX);
-          for (int k = 0; k < 5; ++k) s_tma_1d(st + RS * 32 + k * FAC, &maps.t[k], g * RS, &full[s]);
-          if (g + 1 < nS) load_raw(g + 1);
+        s_mbar_expect_tx(&full[s], FTX);
+        for (int k = 0; k < 5; ++k) s_tma_1d(rr_smem + s * STG + RS * 32 + k * FAC, &maps.t[k], g * RS, &full[s]);
+        if (g + NR - 1 < nS) {
+          if (g >= 1) s_mbar_wait(&rawfree[(g - 1) % NR], ((g - 1) / NR) & 1);
+          load_raw(g + NR - 1);
         }
-        s_mbar_wait(&rawfull[g & 1], (g >> 1) & 1);
-        const double* rb = raw + (g & 1) * GEO::RAW;
-        double* zs = rr_smem + s * STG;
-        // batches of TB row pairs, dealt round-robin to the transform warps:
-        // all loads first, then the arithmetic (independent chains
-        // interleave), then the stores
-        constexpr int TB = 4;
-        for (int jb = tw * TB; jb < RS / 2; jb += XIN_TW * TB) {
-          double2 v[TB], y[TB][4];
-#pragma unroll
-          for (int t = 0; t < TB; ++t) {
-            const int jp = jb + t;
-            // rows 2jp, 2jp+1 of system bl: box jp/8, 16 B chunk jp%8 of
-            // smem row `lane`, XOR-swizzled by lane % 8
-            v[t] = *reinterpret_cast<const double2*>(rb + (jp >> 3) * 512 + lane * 16 +
-                                                     (((jp & 7) ^ (lane & 7)) << 1));
-            if constexpr (XIN == 1) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k)  // broadcast: every lane reads the same pair
-                y[t][k] = *reinterpret_cast<const double2*>(rb + RS * 32 + k * RS + 2 * jp);
-            }
-          }
-          double o[TB][2];
-#pragma unroll
-          for (int t = 0; t < TB; ++t) {
-            if constexpr (XIN == 1) {
-              const double c0 = Wb[0] * y[t][0].x + Wb[1] * y[t][1].x + Wb[2] * y[t][2].x + Wb[3] * y[t][3].x;
-              const double c1 = Wb[0] * y[t][0].y + Wb[1] * y[t][1].y + Wb[2] * y[t][2].y + Wb[3] * y[t][3].y;
-              o[t][0] = v[t].x - c0;
-              o[t][1] = v[t].y - c1;
-            } else {
-              o[t][0] = v[t].x;
-              o[t][1] = v[t].y;
-            }
-          }
-#pragma unroll
-          for (int t = 0; t < TB; ++t) {
-            zs[(2 * (jb + t)) * 32 + lane] = o[t][0];
-            zs[(2 * (jb + t) + 1) * 32 + lane] = o[t][1];
-          }
-        }
-        s_mbar_arrive(&full[s]);  // each thread releases its own slot writes
       }
-      if (!issuer) return;
     } else {
       if (lane != 0) return;
       // forward: loading stage g reuses the slot of stage g - NST, which is
@@ -1196,6 +1248,23 @@ bool encode_map(CUtensorMap* m, const double* p, int rank, uint64_t d0, uint64_t
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// zT (system-major, blocks of ztInner unknowns per system) as 4D {16, B,
+// ztInner / 16, n / ztInner}, box {16, 32, rs / 16, 1}, 128 B swizzle: the
+// box lands as rs/16 consecutive 4 KB [32 systems][16 unknowns] chunks.
+bool encode_map4_zt(CUtensorMap* m, const double* p, int ztInner, int B, int n, int rs) {
+  auto enc = tensor_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {16, static_cast<cuuint64_t>(B), static_cast<cuuint64_t>(ztInner / 16),
+                              static_cast<cuuint64_t>(n / ztInner)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(ztInner) * 8, 128,
+                                 static_cast<cuuint64_t>(B) * ztInner * 8};
+  const cuuint32_t box[4] = {16, 32, static_cast<cuuint32_t>(rs / 16), 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool encode_map3(CUtensorMap* m, const double* p, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
                  uint32_t b2, bool swizzle128) {
   auto enc = tensor_encoder();
@@ -1274,7 +1343,7 @@ void launch_sweep_res_t(bool periodic, const PentaTables& f, const SweepMaps& ma
   }
   const int blocks = (B + 31) / 32;
   launch_ex(periodic ? k_sweep_res<true, RS, XIN> : k_sweep_res<false, RS, XIN>, dim3(blocks),
-            dim3(XIN ? 32 * (1 + XIN_TW) : 64), smem, s, pdl, f, maps, B, n, y4, fuse);
+            dim3(XIN ? 32 * (2 + XIN_TW) : 64), smem, s, pdl, f, maps, B, n, y4, fuse);
 }
 
 void launch_sweep_res(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
@@ -1376,7 +1445,11 @@ bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double
   if (!sweep_maps(f, B, n, z, &maps, rs)) return false;
   // zT: unknown r of system b at ((r % ztInner), b, r / ztInner) — dims
   // {ztInner, B, n / ztInner}, box {16 unknowns, 32 systems, 1}, 128 B swizzle
-  if (!encode_map3(&maps.zt, zT, ztInner, B, n / ztInner, 16, 32, 1, true)) return false;
+  // One 4D box per stage where the stage's rows lie in one block: the view
+  // {16 unknowns, B systems, ztInner / 16 chunks, n / ztInner blocks}
+  // (strides 8 B, ztInner * 8, 128 B, B * ztInner * 8). Else RS/16 3D boxes.
+  maps.ztBox = ztInner % rs == 0 && encode_map4_zt(&maps.zt, zT, ztInner, B, n, rs) ? 1 : 0;
+  if (!maps.ztBox && !encode_map3(&maps.zt, zT, ztInner, B, n / ztInner, 16, 32, 1, true)) return false;
   maps.ztInner = ztInner;
   if (peers && peers->npeer > 0) {
     if (peers->npeer > 8 || peers->prow % rs || n != peers->npeer * peers->prow) return false;
@@ -1394,8 +1467,7 @@ bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double
     fuse.y4Off = peers->y4Off;
   }
   if (Wc) {
-    for (int k = 0; k < 4; ++k)
-      if (!encode_map(&maps.yc[k], yc + static_cast<size_t>(k) * n, 1, n, 1, rs, 1)) return false;
+    if (!encode_map(&maps.yc[0], yc, 2, n, 4, rs, 4)) return false;
     for (int k = 0; k < 4; ++k) fuse.Wc[k] = Wc[k];
     fuse.yc = yc;
   }

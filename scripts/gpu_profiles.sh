@@ -9,4 +9,4 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ncu --set full --clock-control none --import-source on -k regex:k_tma -s 2 -c 1 -o gpurun_out/p_k_tma_f64 -f python scripts/profile_stencil.py --reps 3 > /dev/null 2>&1; echo ncu1=$?
 ncu --set full --clock-control none --import-source on -k regex:k_sweep_res -s 4 -c 2 -o gpurun_out/p_k_sweep_res_1024 -f python scripts/profile_ch.py --n 1024 --steps 4 > /dev/null 2>&1; echo ncu2=$?
 ncu --set full --clock-control none --import-source on -k regex:k_sweep_res -s 2 -c 2 -o gpurun_out/p_k_sweep_res_8192 -f python scripts/profile_ch.py --n 8192 --steps 3 > /dev/null 2>&1; echo ncu3=$?
-ncu --set full --clock-control none --import-source on -k regex:k_rhs_v -s 1 -c 1 -o gpurun_out/p_k_rhs_fused_8192 -f python scripts/profile_ch.py --n 8192 --steps 3 > /dev/null 2>&1; echo ncu4=$?
+ncu --set full --clock-control none --import-source on -k regex:k_rhs_tp -s 1 -c 1 -o gpurun_out/p_k_rhs_tp_8192 -f python scripts/profile_ch.py --n 8192 --steps 3 > /dev/null 2>&1; echo ncu4=$?
