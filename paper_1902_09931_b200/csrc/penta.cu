@@ -72,14 +72,27 @@ __global__ void k_factor(int B, int n, const double* __restrict__ e, const doubl
   ap[r1] = ap1;
   bp[r1] = bp1;
   dInv[r1] = 1.0 / dp1;
+  // the next row's bands are loaded one row ahead: the chain (two dependent
+  // divisions per row) then never waits on a global load
+  double ne = 0.0, nc = 0.0, nd = 0.0, na = 0.0, nb = 0.0;
+  if (n > 2) {
+    const long long r2 = 2LL * B + b;
+    ne = e[r2], nc = c[r2], nd = d[r2], na = a[r2], nb = bb[r2];
+  }
+#pragma unroll 2
   for (int r = 2; r < n; ++r) {
     const long long cur = static_cast<long long>(r) * B + b;
-    const double mm1 = e[cur] / dp2;
-    const double cbar = c[cur] - mm1 * ap2;
+    const double ec = ne, cc = nc, dc = nd, ac = na, bc = nb;
+    if (r + 1 < n) {
+      const long long nx = cur + B;
+      ne = e[nx], nc = c[nx], nd = d[nx], na = a[nx], nb = bb[nx];
+    }
+    const double mm1 = ec / dp2;
+    const double cbar = cc - mm1 * ap2;
     const double mm2 = cbar / dp1;
-    const double dpc = d[cur] - mm1 * bp2 - mm2 * ap1;
-    const double apc = a[cur] - mm2 * bp1;
-    const double bpc = bb[cur];
+    const double dpc = dc - mm1 * bp2 - mm2 * ap1;
+    const double apc = ac - mm2 * bp1;
+    const double bpc = bc;
     m1[cur] = mm1;
     m2[cur] = mm2;
     ap[cur] = apc;
@@ -101,17 +114,34 @@ __device__ __forceinline__ double tab(const double* __restrict__ t, int r, int b
   return uniform ? __ldg(t + r) : __ldg(t + static_cast<long long>(r) * B + b);
 }
 
-// One substitution pass pair on a strided vector (used for setup only).
+// One substitution pass pair on a strided vector (used for setup only): the
+// same expressions as the sweeps (penta.cpp:171-196), the two previous
+// unknowns carried in registers (re-reading them from global memory put a
+// load round trip on every row: 2.25 ms for the n = 8192 setup).
 __device__ void substitute(const PentaTables& f, int B, int b, double* y, long long s, int n) {
   const bool u = f.uniform;
-  y[s] -= tab(f.m2, 1, b, B, u) * y[0];
-  for (int r = 2; r < n; ++r)
-    y[r * s] -= tab(f.m1, r, b, B, u) * y[(r - 2) * s] + tab(f.m2, r, b, B, u) * y[(r - 1) * s];
-  y[(n - 1) * s] *= tab(f.dInv, n - 1, b, B, u);
-  y[(n - 2) * s] = (y[(n - 2) * s] - tab(f.ap, n - 2, b, B, u) * y[(n - 1) * s]) * tab(f.dInv, n - 2, b, B, u);
-  for (int r = n - 3; r >= 0; --r)
-    y[r * s] = (y[r * s] - tab(f.ap, r, b, B, u) * y[(r + 1) * s] - tab(f.bp, r, b, B, u) * y[(r + 2) * s]) *
-               tab(f.dInv, r, b, B, u);
+  double y2 = y[0];
+  double y1 = y[s] - tab(f.m2, 1, b, B, u) * y2;
+  y[s] = y1;
+#pragma unroll 4
+  for (int r = 2; r < n; ++r) {
+    const double yr = y[r * s] - (tab(f.m1, r, b, B, u) * y2 + tab(f.m2, r, b, B, u) * y1);
+    y[r * s] = yr;
+    y2 = y1;
+    y1 = yr;
+  }
+  double s1 = y1 * tab(f.dInv, n - 1, b, B, u);
+  y[(n - 1) * s] = s1;
+  double s2 = s1;
+  s1 = (y[(n - 2) * s] - tab(f.ap, n - 2, b, B, u) * s2) * tab(f.dInv, n - 2, b, B, u);
+  y[(n - 2) * s] = s1;
+#pragma unroll 4
+  for (int r = n - 3; r >= 0; --r) {
+    const double yr = (y[r * s] - tab(f.ap, r, b, B, u) * s1 - tab(f.bp, r, b, B, u) * s2) * tab(f.dInv, r, b, B, u);
+    y[r * s] = yr;
+    s2 = s1;
+    s1 = yr;
+  }
 }
 
 // lu4_factor, penta.cpp:37-59. Returns false if singular.
