@@ -31,39 +31,88 @@ namespace {
 constexpr int DT = 32;
 
 // rowAcc[j] = sum_i (i odd ? 4 : 2) * f(v_ij), f = identity or square,
-// accumulated left to right (cahn_hilliard.cpp:166-172, 179-185).
+// accumulated left to right (cahn_hilliard.cpp:166-172, 179-185). One warp
+// per 32 rows; each 32-column chunk is loaded coalesced (one 256 B row
+// segment per load), transposed through shared memory, and the chunks two
+// ahead are already in flight in registers, so the per-row dependent add
+// chain (the bitwise order admits no other) never waits on memory. (Loading
+// each chunk only when it was needed: 112 us for 1024^2.)
 template <bool SQUARE>
 __global__ void __launch_bounds__(DT) k_simpson_rows(const double* __restrict__ v, int nx, int ny,
                                                       double* __restrict__ rowAcc) {
   __shared__ double tile[DT][DT + 1];
   const int j0 = blockIdx.x * DT;
   const int lane = threadIdx.x;
-  double acc = 0.0;
-  for (int i0 = 0; i0 < nx; i0 += DT) {
+  const int nChunks = (nx + DT - 1) / DT;
+  double pre[2][DT];  // chunks k+1 and k+2, element (row r, column lane)
+  auto fetch = [&](double* dst, int c) {
+    const int i = c * DT + lane;
+#pragma unroll
     for (int r = 0; r < DT; ++r) {
-      const int j = j0 + r, i = i0 + lane;
-      tile[r][lane] = (j < ny && i < nx) ? v[static_cast<long long>(j) * nx + i] : 0.0;
+      const int j = j0 + r;
+      dst[r] = (c < nChunks && j < ny && i < nx) ? __ldg(v + static_cast<long long>(j) * nx + i) : 0.0;
     }
-    __syncwarp();
-    const int lim = min(DT, nx - i0);
-    for (int c = 0; c < lim; ++c) {
-      const int i = i0 + c;
-      const double wx = (i % 2 == 1) ? 4.0 : 2.0;
-      const double x = tile[lane][c];
-      acc += wx * (SQUARE ? x * x : x);
+  };
+  fetch(pre[0], 0);
+  fetch(pre[1], 1);
+  double acc = 0.0;
+  for (int c = 0; c < nChunks; c += 2) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // chunk c + h, from pre[h]
+      const int cc = c + h;
+      if (cc >= nChunks) break;
+#pragma unroll
+      for (int r = 0; r < DT; ++r) tile[r][lane] = pre[h][r];
+      __syncwarp();
+      fetch(pre[h], cc + 2);
+      const int i0 = cc * DT, lim = min(DT, nx - i0);
+      if (lim == DT) {  // unrolled: the loads and products run ahead of the add chain
+#pragma unroll
+        for (int q = 0; q < DT; ++q) {
+          const double wx = (q % 2 == 1) ? 4.0 : 2.0;  // i0 is even
+          const double x = tile[lane][q];
+          acc += wx * (SQUARE ? x * x : x);
+        }
+      } else {
+        for (int q = 0; q < lim; ++q) {
+          const int i = i0 + q;
+          const double wx = (i % 2 == 1) ? 4.0 : 2.0;
+          const double x = tile[lane][q];
+          acc += wx * (SQUARE ? x * x : x);
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
   if (j0 + lane < ny) rowAcc[j0 + lane] = acc;
 }
 
-__global__ void k_simpson_total(const double* __restrict__ rowAcc, int nx, int ny, double* out) {
-  double total = 0.0;  // cahn_hilliard.cpp:165-176
-  for (int j = 0; j < ny; ++j) {
-    const double wy = (j % 2 == 1) ? 4.0 : 2.0;
-    total += wy * rowAcc[j];
+// total = sum_j wy_j * rowAcc_j in row order (cahn_hilliard.cpp:165-176):
+// the block stages rowAcc through shared memory (coalesced, in flight
+// together), thread 0 folds it in order.
+constexpr int TT = 1024, TCH = 4096;
+__global__ void __launch_bounds__(TT) k_simpson_total(const double* __restrict__ rowAcc, int nx, int ny, double* out) {
+  __shared__ double sa[TCH];
+  double total = 0.0;
+  for (int j0 = 0; j0 < ny; j0 += TCH) {
+    const int m = min(TCH, ny - j0);
+    for (int k = threadIdx.x; k < m; k += TT) sa[k] = rowAcc[j0 + k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int k = 0;
+      for (; k + 8 <= m; k += 8) {  // j0 + k even: the weights of a group are fixed
+#pragma unroll
+        for (int u = 0; u < 8; ++u) total += ((u % 2 == 1) ? 4.0 : 2.0) * sa[k + u];
+      }
+      for (; k < m; ++k) {
+        const int j = j0 + k;
+        const double wy = (j % 2 == 1) ? 4.0 : 2.0;
+        total += wy * sa[k];
+      }
+    }
+    __syncthreads();
   }
-  *out = total / (9.0 * static_cast<double>(nx) * static_cast<double>(ny));
+  if (threadIdx.x == 0) *out = total / (9.0 * static_cast<double>(nx) * static_cast<double>(ny));
 }
 
 __global__ void k_to_complex(const double* __restrict__ v, long long n, cufftDoubleComplex* __restrict__ c) {
@@ -107,11 +156,25 @@ __global__ void __launch_bounds__(RB) k_k1_partial(const cufftDoubleComplex* __r
   }
 }
 
-__global__ void k_k1_final(const double* __restrict__ part, int nb, double* out) {
+// Partials staged through shared memory, then folded in block order by one
+// thread (nb <= 2048 partials).
+__global__ void __launch_bounds__(256) k_k1_final(const double* __restrict__ part, int nb, double* out) {
+  __shared__ double sp[2 * 2048];
+  for (int k = threadIdx.x; k < 2 * nb; k += 256) sp[k] = part[k];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   double num = 0.0, den = 0.0;
-  for (int b = 0; b < nb; ++b) {
-    num += part[2 * b];
-    den += part[2 * b + 1];
+  int b = 0;
+  for (; b + 8 <= nb; b += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      num += sp[2 * (b + u)];
+      den += sp[2 * (b + u) + 1];
+    }
+  }
+  for (; b < nb; ++b) {
+    num += sp[2 * b];
+    den += sp[2 * b + 1];
   }
   out[0] = num;
   out[1] = den;
@@ -130,7 +193,7 @@ void device_simpson(const double* v, int nx, int ny, bool square, double* out, c
   else
     k_simpson_rows<false><<<(ny + DT - 1) / DT, DT, 0, s>>>(v, nx, ny, buf);
   check_launch("simpson rows kernel");
-  k_simpson_total<<<1, 1, 0, s>>>(buf, nx, ny, buf + ny);
+  k_simpson_total<<<1, TT, 0, s>>>(buf, nx, ny, buf + ny);
   check_launch("simpson total kernel");
   SG_CUDA(cudaMemcpyAsync(out, buf + ny, sizeof(double), cudaMemcpyDeviceToHost, s));
   SG_CUDA(cudaFreeAsync(buf, s));
@@ -174,7 +237,7 @@ double device_k1(const double* v, int nx, int ny, double dx, double dy, cudaStre
   const cufftResult fr = cufftExecZ2Z(plan, c, c, CUFFT_FORWARD);
   count_launch();
   if (fr != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftExecZ2Z failed");
-  const int nb = 296;
+  const int nb = 1184;  // partial sums (<= 2048, k_k1_final)
   double* part = nullptr;
   retain_async_pool();
   SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * (2 * nb + 2), s));
@@ -182,7 +245,7 @@ double device_k1(const double* v, int nx, int ny, double dx, double dy, cudaStre
   const double kyScale = 2.0 * 3.14159265358979323846 / (dy * ny);
   k_k1_partial<<<nb, RB, 0, s>>>(c, nx, ny, kxScale, kyScale, part);
   check_launch("k1 partial kernel");
-  k_k1_final<<<1, 1, 0, s>>>(part, nb, part + 2 * nb);
+  k_k1_final<<<1, 256, 0, s>>>(part, nb, part + 2 * nb);
   check_launch("k1 final kernel");
   double nd[2];
   SG_CUDA(cudaMemcpyAsync(nd, part + 2 * nb, sizeof nd, cudaMemcpyDeviceToHost, s));

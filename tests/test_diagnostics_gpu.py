@@ -75,3 +75,36 @@ def test_run_cadence(sg):
     snaps = []
     sg.run(p, 1, 1, sg.RunSink(diagEvery=0, snapEvery=5, onSnapshot=lambda g, s, t: snaps.append(s)))
     assert snaps == [0, 5, 10]
+
+
+def _simpson_np(v, square=False):
+    """composite Simpson mean in the reference's order (cahn_hilliard.cpp:
+    161-176): per row a left-to-right sum (np.cumsum accumulates
+    sequentially), then rows in order."""
+    ny, nx = v.shape
+    f = v * v if square else v
+    wx = np.where(np.arange(nx) % 2 == 1, 4.0, 2.0)
+    wy = np.where(np.arange(ny) % 2 == 1, 4.0, 2.0)
+    row = np.cumsum(wx[None, :] * f, axis=1)[:, -1]
+    return np.cumsum(wy * row)[-1] / (9.0 * float(nx) * float(ny))
+
+
+@pytest.mark.parametrize("nx,ny", [(2, 2), (16, 16), (18, 6), (32, 64), (66, 34), (96, 40), (128, 16),
+                                   (2048, 256), (256, 2048), (4096, 8)])
+def test_simpson_bitwise_over_shapes(sg, nx, ny):
+    """The device Simpson reduction (one warp per 32 rows, chunks fetched two
+    ahead) keeps the reference's summation order on every shape: ragged
+    chunks (nx not a multiple of 32), fewer rows than a warp, many chunks."""
+    v = np.random.default_rng(nx * 7 + ny).uniform(-1, 1, (ny, nx))
+    g = sg.Grid2D(nx, ny)
+    g.values = v
+    assert sg.simpson_mean(g) == _simpson_np(v)
+
+
+@pytest.mark.parametrize("nx,ny", [(16, 16), (32, 64), (128, 16), (1024, 512)])
+def test_s_metric_bitwise_vs_reference_shapes(sg, ref, nx, ny):
+    v = np.random.default_rng(nx + ny).uniform(-1, 1, (ny, nx))
+    g = sg.Grid2D(nx, ny, TWO_PI / nx, TWO_PI / ny)
+    g.values = v
+    s_ref, _ = ref.ch_diagnostics(v, TWO_PI / nx, TWO_PI / ny)
+    assert sg.s_metric(g) == s_ref
