@@ -1,3 +1,4 @@
+"""CH diagnostics() cost against the step time (1024^2, 4096^2, 8192^2)."""
 import sys, time
 sys.path.insert(0, ".")
 import paper_1902_09931_b200 as sg
