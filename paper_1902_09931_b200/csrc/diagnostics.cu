@@ -32,57 +32,62 @@ constexpr int DT = 32;
 
 // rowAcc[j] = sum_i (i odd ? 4 : 2) * f(v_ij), f = identity or square,
 // accumulated left to right (cahn_hilliard.cpp:166-172, 179-185). One warp
-// per 32 rows; each 32-column chunk is loaded coalesced (one 256 B row
-// segment per load), transposed through shared memory, and the chunks two
-// ahead are already in flight in registers, so the per-row dependent add
-// chain (the bitwise order admits no other) never waits on memory. (Loading
-// each chunk only when it was needed: 112 us for 1024^2.)
+// per 32 rows; 32-column chunks stream into a 5-stage shared-memory ring
+// with 8 B cp.async (each lane one column of 32 rows: coalesced 256 B row
+// segments, transposed on the way, no registers held), four chunks ahead of
+// the per-row dependent add chain — the bitwise order admits no other.
+// (Loading each chunk when needed: 112 us for 1024^2; two chunks ahead in
+// registers: 37 us.)
+constexpr int SR_ST = 5;
 template <bool SQUARE>
 __global__ void __launch_bounds__(DT) k_simpson_rows(const double* __restrict__ v, int nx, int ny,
                                                       double* __restrict__ rowAcc) {
-  __shared__ double tile[DT][DT + 1];
+  __shared__ double ring[SR_ST][DT][DT + 1];
   const int j0 = blockIdx.x * DT;
   const int lane = threadIdx.x;
   const int nChunks = (nx + DT - 1) / DT;
-  double pre[2][DT];  // chunks k+1 and k+2, element (row r, column lane)
-  auto fetch = [&](double* dst, int c) {
-    const int i = c * DT + lane;
-#pragma unroll
-    for (int r = 0; r < DT; ++r) {
-      const int j = j0 + r;
-      dst[r] = (c < nChunks && j < ny && i < nx) ? __ldg(v + static_cast<long long>(j) * nx + i) : 0.0;
-    }
-  };
-  fetch(pre[0], 0);
-  fetch(pre[1], 1);
-  double acc = 0.0;
-  for (int c = 0; c < nChunks; c += 2) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {  // chunk c + h, from pre[h]
-      const int cc = c + h;
-      if (cc >= nChunks) break;
-#pragma unroll
-      for (int r = 0; r < DT; ++r) tile[r][lane] = pre[h][r];
-      __syncwarp();
-      fetch(pre[h], cc + 2);
-      const int i0 = cc * DT, lim = min(DT, nx - i0);
-      if (lim == DT) {  // unrolled: the loads and products run ahead of the add chain
-#pragma unroll
-        for (int q = 0; q < DT; ++q) {
-          const double wx = (q % 2 == 1) ? 4.0 : 2.0;  // i0 is even
-          const double x = tile[lane][q];
-          acc += wx * (SQUARE ? x * x : x);
-        }
-      } else {
-        for (int q = 0; q < lim; ++q) {
-          const int i = i0 + q;
-          const double wx = (i % 2 == 1) ? 4.0 : 2.0;
-          const double x = tile[lane][q];
-          acc += wx * (SQUARE ? x * x : x);
+  auto issue = [&](int c) {
+    if (c < nChunks) {
+      double(*t)[DT + 1] = ring[c % SR_ST];
+      const int i = c * DT + lane;
+      for (int r = 0; r < DT; ++r) {
+        const int j = j0 + r;
+        if (j < ny && i < nx) {
+          const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&t[r][lane]));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst),
+                       "l"(v + static_cast<long long>(j) * nx + i)
+                       : "memory");
+        } else {
+          t[r][lane] = 0.0;
         }
       }
-      __syncwarp();
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int c = 0; c < SR_ST - 1; ++c) issue(c);
+  double acc = 0.0;
+  for (int c = 0; c < nChunks; ++c) {
+    issue(c + SR_ST - 1);  // its slot held chunk c - 1, released by the last __syncwarp
+    asm volatile("cp.async.wait_group %0;" ::"n"(SR_ST - 1) : "memory");
+    __syncwarp();  // every lane's copies of chunk c have landed
+    const double(*t)[DT + 1] = ring[c % SR_ST];
+    const int i0 = c * DT, lim = min(DT, nx - i0);
+    if (lim == DT) {  // unrolled: the loads and products run ahead of the add chain
+#pragma unroll
+      for (int q = 0; q < DT; ++q) {
+        const double wx = (q % 2 == 1) ? 4.0 : 2.0;  // i0 is even
+        const double x = t[lane][q];
+        acc += wx * (SQUARE ? x * x : x);
+      }
+    } else {
+      for (int q = 0; q < lim; ++q) {
+        const int i = i0 + q;
+        const double wx = (i % 2 == 1) ? 4.0 : 2.0;
+        const double x = t[lane][q];
+        acc += wx * (SQUARE ? x * x : x);
+      }
+    }
+    __syncwarp();
   }
   if (j0 + lane < ny) rowAcc[j0 + lane] = acc;
 }
