@@ -1604,22 +1604,18 @@ sg_status sg_ch_diagnostics(sg_ch_t ch, double* t, double* s, double* k1Inv) {
     if (!ch) sg::logic("CHStepper: destroyed");
     auto& st = *ch->st;
     SG_CUDA(cudaSetDevice(st.device));
-    SG_CUDA(cudaStreamSynchronize(st.stream));
+    // queued behind the pending steps on the stepper's own stream
     const double* f = st.cur();
     const double dx = st.p.lx / st.p.nx, dy = st.p.ly / st.p.ny;
     if (t) *t = static_cast<double>(st.step) * st.p.dt;
-    double m2 = 0.0;
-    sg::device_simpson(f, st.p.nx, st.p.ny, true, &m2, st.stream);
+    double r[3];  // <C^2>, k1 num, k1 den
+    sg::device_ch_diagnostics(f, st.p.nx, st.p.ny, dx, dy, r, st.stream);
+    const double m2 = r[0];
     if (m2 >= 1.0 - 1e-12) throw sg::Error(SG_ERR_DOMAIN, "s_metric: mixture saturated, <C^2> reached 1");
     if (s) *s = 1.0 / (1.0 - m2);
-    double k1inv = 0.0;
-    try {
-      k1inv = 1.0 / sg::device_k1(f, st.p.nx, st.p.ny, dx, dy, st.stream);
-    } catch (const sg::Error& e) {
-      if (e.status != SG_ERR_DOMAIN) throw;
-      k1inv = 0.0;  // an identically zero field has no spectral length scale
-    }
-    if (k1Inv) *k1Inv = k1inv;
+    // an identically zero field has no spectral length scale: 1/k1 := 0
+    // (k1_metric's domain_error, caught as in CHStepper::diagnostics)
+    if (k1Inv) *k1Inv = r[2] == 0.0 ? 0.0 : 1.0 / (r[1] / r[2]);
   });
 }
 

@@ -261,6 +261,45 @@ double device_k1(const double* v, int nx, int ny, double dx, double dy, cudaStre
   return nd[0] / nd[1];
 }
 
+// CHStepper::diagnostics in one stream pass: <C^2> by Simpson and the k1
+// spectrum sums, one 3-double read-back and one synchronisation
+// (out = {<C^2>, num, den}).
+void device_ch_diagnostics(const double* v, int nx, int ny, double dx, double dy, double* out, cudaStream_t s) {
+  if (nx % 2 != 0 || ny % 2 != 0) invalid("simpson_mean: nx and ny must be even");
+  if (nx < 1 || ny < 1 || (nx & (nx - 1)) || (ny & (ny - 1)))
+    invalid("fft_2d: grid dimensions must be powers of two");
+  const long long n = static_cast<long long>(nx) * ny;
+  const int nb = 1184;
+  double* buf = nullptr;  // [results 4][rowAcc ny][partials 2 nb]
+  cufftDoubleComplex* c = nullptr;
+  retain_async_pool();
+  SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(double) * (4 + ny + 2 * nb), s));
+  SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(cufftDoubleComplex) * n, s));
+  double* rows = buf + 4;
+  double* part = rows + ny;
+  k_simpson_rows<true><<<(ny + DT - 1) / DT, DT, 0, s>>>(v, nx, ny, rows);
+  check_launch("simpson rows kernel");
+  k_simpson_total<<<1, TT, 0, s>>>(rows, nx, ny, buf);
+  check_launch("simpson total kernel");
+  k_to_complex<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(v, n, c);
+  check_launch("k1 complex kernel");
+  const cufftHandle plan = cached_plan(nx, ny);
+  cufftSetStream(plan, s);
+  const cufftResult fr = cufftExecZ2Z(plan, c, c, CUFFT_FORWARD);
+  count_launch();
+  if (fr != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftExecZ2Z failed");
+  const double kxScale = 2.0 * 3.14159265358979323846 / (dx * nx);
+  const double kyScale = 2.0 * 3.14159265358979323846 / (dy * ny);
+  k_k1_partial<<<nb, RB, 0, s>>>(c, nx, ny, kxScale, kyScale, part);
+  check_launch("k1 partial kernel");
+  k_k1_final<<<1, 256, 0, s>>>(part, nb, buf + 1);
+  check_launch("k1 final kernel");
+  SG_CUDA(cudaMemcpyAsync(out, buf, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaFreeAsync(c, s));
+  SG_CUDA(cudaFreeAsync(buf, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+}
+
 }  // namespace sg
 
 // ------------------------------------------------------------------ C ABI

@@ -111,5 +111,7 @@ void launch_weno(const double* phi, const double* u, const double* v, double* ou
 // Diagnostics (diagnostics.cu).
 void device_simpson(const double* v, int nx, int ny, bool square, double* out, cudaStream_t s);
 double device_k1(const double* v, int nx, int ny, double dx, double dy, cudaStream_t s);
+// {<v^2> (Simpson), k1 num, k1 den} in one pass and one synchronisation.
+void device_ch_diagnostics(const double* v, int nx, int ny, double dx, double dy, double* out, cudaStream_t s);
 
 }  // namespace sg
