@@ -8,8 +8,9 @@
 //    per row accumulates rowAcc = sum_i wx_i * v_ij in the reference's order
 //    (rows staged through shared-memory tiles so loads stay coalesced), then
 //    one thread folds total += wy_j * rowAcc_j in row order.
-//  * k1_metric: 2D FFT by cuFFT (Z2Z, forward, unnormalized like fft_2d,
-//    fft.cpp:54-61) and a deterministic two-level reduction of
+//  * k1_metric: 2D FFT by cuFFT (real-to-complex D2Z, forward, unnormalized
+//    like fft_2d, fft.cpp:54-61; the half spectrum with Hermitian weights)
+//    and a deterministic two-level reduction of
 //    num = sum |C_k|^2, den = sum |C_k|^2 / |k| over k != 0. The reference's
 //    radix-2 FFT and serial sums round differently: agreement is to ~1e-13
 //    relative (tests use 1e-10), which is well inside the reference's own
@@ -120,30 +121,30 @@ __global__ void __launch_bounds__(TT) k_simpson_total(const double* __restrict__
   if (threadIdx.x == 0) *out = total / (9.0 * static_cast<double>(nx) * static_cast<double>(ny));
 }
 
-__global__ void k_to_complex(const double* __restrict__ v, long long n, cufftDoubleComplex* __restrict__ c) {
-  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k < n) c[k] = make_cuDoubleComplex(v[k], 0.0);
-}
 
 constexpr int RB = 256;
 
-// Per-block partial sums of |C|^2 and |C|^2/|k| (k1_metric, cahn_hilliard.cpp:196-208).
+// Per-block partial sums of |C|^2 and |C|^2/|k| (k1_metric, cahn_hilliard.cpp:
+// 196-208) over the half spectrum of the real-to-complex transform
+// (ny x (nx/2 + 1)): a real field's spectrum is Hermitian, |C(-k)| = |C(k)|,
+// so interior columns stand for themselves and their mirror (weight 2).
 __global__ void __launch_bounds__(RB) k_k1_partial(const cufftDoubleComplex* __restrict__ s, int nx, int ny,
                                                    double kxScale, double kyScale, double* __restrict__ part) {
   __shared__ double sn[RB], sd[RB];
-  const long long n = static_cast<long long>(nx) * ny;
+  const int nh = nx / 2 + 1;
+  const long long n = static_cast<long long>(nh) * ny;
   double num = 0.0, den = 0.0;
   for (long long k = static_cast<long long>(blockIdx.x) * RB + threadIdx.x; k < n;
        k += static_cast<long long>(gridDim.x) * RB) {
-    const int j = static_cast<int>(k / nx), i = static_cast<int>(k % nx);
+    const int j = static_cast<int>(k / nh), i = static_cast<int>(k % nh);
     if (i == 0 && j == 0) continue;
     const int mj = (j < ny / 2) ? j : j - ny;
-    const int mi = (i < nx / 2) ? i : i - nx;
     const cufftDoubleComplex z = s[k];
+    const double w = (i == 0 || 2 * i == nx) ? 1.0 : 2.0;
     const double power = z.x * z.x + z.y * z.y;  // std::norm
-    const double kmag = hypot(kxScale * mi, kyScale * mj);
-    num += power;
-    den += power / kmag;
+    const double kmag = hypot(kxScale * i, kyScale * mj);
+    num += w * power;
+    den += w * (power / kmag);
   }
   sn[threadIdx.x] = num;
   sd[threadIdx.x] = den;
@@ -222,7 +223,7 @@ cufftHandle cached_plan(int nx, int ny) {
   auto it = cache.plans.find(key);
   if (it != cache.plans.end()) return it->second;
   cufftHandle plan;
-  if (cufftPlan2d(&plan, ny, nx, CUFFT_Z2Z) != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftPlan2d failed");
+  if (cufftPlan2d(&plan, ny, nx, CUFFT_D2Z) != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftPlan2d failed");
   cache.plans[key] = plan;
   return plan;
 }
@@ -234,14 +235,13 @@ double device_k1(const double* v, int nx, int ny, double dx, double dy, cudaStre
   const long long n = static_cast<long long>(nx) * ny;
   cufftDoubleComplex* c = nullptr;
   retain_async_pool();
-  SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(cufftDoubleComplex) * n, s));
-  k_to_complex<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(v, n, c);
-  check_launch("k1 complex kernel");
+  SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(cufftDoubleComplex) * (nx / 2 + 1) * ny, s));
   const cufftHandle plan = cached_plan(nx, ny);
   cufftSetStream(plan, s);
-  const cufftResult fr = cufftExecZ2Z(plan, c, c, CUFFT_FORWARD);
+  // out of place: the real input (the field) is not modified
+  const cufftResult fr = cufftExecD2Z(plan, const_cast<double*>(v), c);
   count_launch();
-  if (fr != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftExecZ2Z failed");
+  if (fr != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftExecD2Z failed");
   const int nb = 1184;  // partial sums (<= 2048, k_k1_final)
   double* part = nullptr;
   retain_async_pool();
@@ -274,20 +274,19 @@ void device_ch_diagnostics(const double* v, int nx, int ny, double dx, double dy
   cufftDoubleComplex* c = nullptr;
   retain_async_pool();
   SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(double) * (4 + ny + 2 * nb), s));
-  SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(cufftDoubleComplex) * n, s));
+  SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(cufftDoubleComplex) * (nx / 2 + 1) * ny, s));
   double* rows = buf + 4;
   double* part = rows + ny;
   k_simpson_rows<true><<<(ny + DT - 1) / DT, DT, 0, s>>>(v, nx, ny, rows);
   check_launch("simpson rows kernel");
   k_simpson_total<<<1, TT, 0, s>>>(rows, nx, ny, buf);
   check_launch("simpson total kernel");
-  k_to_complex<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(v, n, c);
-  check_launch("k1 complex kernel");
   const cufftHandle plan = cached_plan(nx, ny);
   cufftSetStream(plan, s);
-  const cufftResult fr = cufftExecZ2Z(plan, c, c, CUFFT_FORWARD);
+  // out of place: the real input (the field) is not modified
+  const cufftResult fr = cufftExecD2Z(plan, const_cast<double*>(v), c);
   count_launch();
-  if (fr != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftExecZ2Z failed");
+  if (fr != CUFFT_SUCCESS) throw Error(SG_ERR_CUDA, "cufftExecD2Z failed");
   const double kxScale = 2.0 * 3.14159265358979323846 / (dx * nx);
   const double kyScale = 2.0 * 3.14159265358979323846 / (dy * ny);
   k_k1_partial<<<nb, RB, 0, s>>>(c, nx, ny, kxScale, kyScale, part);
