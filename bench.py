@@ -347,6 +347,7 @@ def extras(sg, torch, stream, peak):
     out["cfg1_512sq_10apps_ms"] = best * 1e3
     out["stencil_variants_16384sq_fp64"] = bench_variants(sg, torch, stream, peak)
     out["penta_general_periodic"] = bench_penta_general(sg, torch, peak)
+    out["weno5_advect_8192sq_fp64"] = bench_weno(sg, torch, peak)
     if hasattr(sg, "CHStepper"):
         out.update(bench_ch(sg, torch))
     return out
@@ -380,6 +381,59 @@ def bench_penta_general(sg, torch, peak, B=65536, n=1024, reps=10):
     torch.cuda.empty_cache()
     return {"batch": B, "n": n, "solve_ms": ms, "unknowns_per_s": B * n / (ms * 1e-3),
             "hbm_frac": alg / (ms * 1e-3) / 1e9 / peak}
+
+
+def bench_weno(sg, torch, peak, n=8192, reps=10, ref_n=1024):
+    """weno_advect (weno.cpp:50-94) through the C ABI on device-resident
+    fields: reads phi, u, v and writes the tendency (32 B/pt), ~150 FP64 ops
+    per point incl. four divisions. The reference's CPU weno_advect is timed
+    beside it on a ref_n^2 sample with all host cores (oracle/_ref)."""
+    import ctypes as C
+    import os
+    import numpy as np
+    from paper_1902_09931_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(5)
+    phi, u, v = (torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g) - 0.5 for _ in range(3))
+    out = torch.empty_like(phi)
+    dx = 2 * np.pi / n
+    st = torch.cuda.current_stream()
+
+    def call():
+        _lib.check(_lib.lib().sg_weno_advect(C.c_void_p(phi.data_ptr()), C.c_void_p(u.data_ptr()),
+                                             C.c_void_p(v.data_ptr()), n, n, dx, dx, C.c_void_p(out.data_ptr()),
+                                             1, C.c_void_p(st.cuda_stream)))
+    for _ in range(3):
+        call()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        call()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    pts = n * n
+    res = {"gpts_s": pts / (ms * 1e-3) / 1e9, "kernel_ms": ms,
+           "hbm_frac": 32 * pts / (ms * 1e-3) / 1e9 / peak, "inputs": "device-resident, 3 reads + 1 write of 8 B/pt",
+           "l2": "inputs 1.6 GB >> L2"}
+    del phi, u, v, out
+    torch.cuda.empty_cache()
+    try:
+        from oracle.oracle import Reference
+        ref = Reference()
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        rng = np.random.default_rng(6)
+        a, b, c = (rng.uniform(-0.5, 0.5, (ref_n, ref_n)) for _ in range(3))
+        d = 2 * np.pi / ref_n
+        ref.weno_advect(a, b, c, d, d, cores, cores)
+        t0 = time.perf_counter()
+        ref.weno_advect(a, b, c, d, d, cores, cores)
+        secs = time.perf_counter() - t0
+        res["reference_cpu"] = {"gpts_s": ref_n * ref_n / secs / 1e9, "cores": cores,
+                                "sample": f"{ref_n}x{ref_n} weno_advect (oracle/_ref), numTiles=numWorkers={cores}"}
+    except Exception as exc:  # the reference build is optional on a bare box
+        res["reference_cpu"] = {"error": str(exc)[:200]}
+    return res
 
 
 def bench_variants(sg, torch, stream, peak, n=16384, launches=20):

@@ -36,13 +36,17 @@ __device__ __forceinline__ double weno_combine(double v1, double v2, double v3, 
 }
 
 // weno_derivative_7: w(k) = phi(x + (k-3) h), left-biased iff velocity >= 0.
+// Both biases combine the same six scaled differences d_k = (w(k+1) - w(k))
+// * invH (left: d0..d4, right: d5..d1), so the side is a per-lane select of
+// the five inputs and ONE weno_combine runs — no divergent second copy of
+// its eight divisions where neighbouring lanes' velocities differ in sign.
 template <typename W>
 __device__ __forceinline__ double weno_d7(W w, double invH, bool left) {
-  if (left)
-    return weno_combine((w(1) - w(0)) * invH, (w(2) - w(1)) * invH, (w(3) - w(2)) * invH, (w(4) - w(3)) * invH,
-                        (w(5) - w(4)) * invH);
-  return weno_combine((w(6) - w(5)) * invH, (w(5) - w(4)) * invH, (w(4) - w(3)) * invH, (w(3) - w(2)) * invH,
-                      (w(2) - w(1)) * invH);
+  double d[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) d[k] = (w(k + 1) - w(k)) * invH;
+  return weno_combine(left ? d[0] : d[5], left ? d[1] : d[4], left ? d[2] : d[3], left ? d[3] : d[2],
+                      left ? d[4] : d[1]);
 }
 
 __device__ __forceinline__ int wrapi(int i, int n) {
