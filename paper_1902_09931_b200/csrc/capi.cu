@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -291,7 +292,15 @@ static sg_slab_desc full_grid_desc(const sg_plan_s* p) {
 static void pipelined_host_compute(sg_plan_s* p, sg_plan_s::Buf& in, sg_plan_s::Buf& out, cudaStream_t s) {
   const int ny = p->ny, top = p->ext.top, bottom = p->ext.bottom;
   const size_t rowBytes = static_cast<size_t>(p->nx) * p->elem();
-  int rows = std::max((ny + 31) / 32, std::max(std::max(top, bottom), 1));
+  // chunk count: the pipeline's fill (first H2D) and drain (last D2H) cost
+  // one chunk each. Config 4 e2e: 32 chunks 5.77, 64 5.87, 128 5.99, 256
+  // 5.90 Gpts/s. SG_PIPE_CHUNKS overrides (A/B).
+  static const int chunks = [] {
+    const char* e = std::getenv("SG_PIPE_CHUNKS");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : 128;
+  }();
+  int rows = std::max((ny + chunks - 1) / chunks, std::max(std::max(top, bottom), 1));
   const int nch = (ny + rows - 1) / rows;
   if (!p->sH2D) SG_CUDA(cudaStreamCreateWithFlags(&p->sH2D, cudaStreamNonBlocking));
   if (!p->sD2H) SG_CUDA(cudaStreamCreateWithFlags(&p->sD2H, cudaStreamNonBlocking));
