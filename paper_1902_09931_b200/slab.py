@@ -256,7 +256,7 @@ class SlabStencil:
         self.a, self.b = self.b, self.a
         self._out ^= 1
 
-    def apply_host(self, hin, hout, chunks: int = 16):
+    def apply_host(self, hin, hout, chunks: int = 0):
         """End-to-end application from/to pinned HOST memory: the own rows
         are uploaded in `chunks` row blocks on a copy stream (first and last
         block first, so the halo exchange can start early), each block's
@@ -273,6 +273,8 @@ class SlabStencil:
         if not hasattr(self, "_h2d"):
             self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
         h2d, d2h = self._h2d, self._d2h
+        if chunks <= 0:  # fill and drain cost one block each: many blocks (SG_SLAB_CHUNKS overrides)
+            chunks = int(os.environ.get("SG_SLAB_CHUNKS", "64"))
         chunks = max(1, min(chunks, own))
         bounds = [(own * c // chunks, own * (c + 1) // chunks) for c in range(chunks)]
         order = [0, chunks - 1] + list(range(1, chunks - 1)) if chunks > 1 else [0]
