@@ -758,7 +758,12 @@ static_assert(RG >= 2, "the first operand group must cover rows 0 and 1");
 // RHS kernel then writes its output row-major (coalesced) instead of
 // transposed. Four ring slots instead of five pay for the raw buffers; the
 // TMA traffic moves to a fifth warp (the transform warps only transform).
-constexpr int XIN_TW = 3;  // transform warps (1-3) of the XIN sweep
+// (CH step with 2 / 3 / 4 transform warps: 87.1 / 87.2 / 89.7 us at 1024^2,
+// 1.154 / 1.152 / 1.157 ms at 8192^2.)
+#ifndef SG_XIN_TW
+#define SG_XIN_TW 3
+#endif
+constexpr int XIN_TW = SG_XIN_TW;  // transform warps (1..XIN_TW) of the XIN sweep
 // Raw zT buffers of the XIN sweep (ring slots: 4 with two raw buffers, 3
 // with three). With the TMA producer in its own warp, two suffice:
 // sweep_trace at 8192^2 y / x-sweep 375 / 352 us (two) against 379 / 362
@@ -1313,7 +1318,7 @@ bool encode_map3(CUtensorMap* m, const double* p, uint64_t d0, uint64_t d1, uint
 bool sweep_maps(const PentaTables& f, int B, int n, const double* z, SweepMaps* maps, int rows = SW_RS) {
   if (B % 2 != 0 || (reinterpret_cast<uintptr_t>(z) & 15)) return false;
   if (std::getenv("SG_SWEEP_KERNEL") && std::strcmp(std::getenv("SG_SWEEP_KERNEL"), "reg") == 0) return false;
-  std::memset(maps, 0, sizeof(*maps));
+  *maps = SweepMaps{};
   if (!encode_map(&maps->z, z, 2, B, n, 32, rows)) return false;
   const double* t[5] = {f.m1, f.m2, f.dInv, f.ap, f.bp};
   for (int k = 0; k < 5; ++k) {
