@@ -106,7 +106,6 @@ __global__ void k_init(unsigned long long seed, double amp, long long count, dou
 
 constexpr int TS = 32;  // output tile edge
 constexpr int HALO = 2;
-constexpr int TE = TS + 2 * HALO;
 
 __device__ __forceinline__ int wrapi(int i, int n) {
   int r = i % n;

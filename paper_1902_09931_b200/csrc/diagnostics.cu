@@ -232,7 +232,6 @@ cufftHandle cached_plan(int nx, int ny) {
 double device_k1(const double* v, int nx, int ny, double dx, double dy, cudaStream_t s) {
   if (nx < 1 || ny < 1 || (nx & (nx - 1)) || (ny & (ny - 1)))
     invalid("fft_2d: grid dimensions must be powers of two");
-  const long long n = static_cast<long long>(nx) * ny;
   cufftDoubleComplex* c = nullptr;
   retain_async_pool();
   SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&c), sizeof(cufftDoubleComplex) * (nx / 2 + 1) * ny, s));
@@ -268,7 +267,6 @@ void device_ch_diagnostics(const double* v, int nx, int ny, double dx, double dy
   if (nx % 2 != 0 || ny % 2 != 0) invalid("simpson_mean: nx and ny must be even");
   if (nx < 1 || ny < 1 || (nx & (nx - 1)) || (ny & (ny - 1)))
     invalid("fft_2d: grid dimensions must be powers of two");
-  const long long n = static_cast<long long>(nx) * ny;
   const int nb = 1184;
   double* buf = nullptr;  // [results 4][rowAcc ny][partials 2 nb]
   cufftDoubleComplex* c = nullptr;
