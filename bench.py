@@ -8,15 +8,27 @@ synthetic random field. One step = one stencil application (compute + swap,
 stencil.cpp:197-235). value = Gpoints/s over all ranks; the input (8 GiB) is
 far larger than L2 (126 MB), so no L2 flush is needed between steps.
 
-Multi-GPU (torchrun, N>1): weak scaling — every rank owns a 32768 x 32768
-y-slab of a periodic N*32768-row grid and exchanges one halo row with each
-ring neighbour over NCCL per step (paper_1902_09931_b200/slab.py), overlapped
-with interior compute.
+Multi-GPU: `--gpus N` with N > 1 runs N ranks, one process per GPU. Without
+torchrun's environment bench.py re-launches itself under
+`torch.distributed.run --nproc-per-node N` (127.0.0.1); under torchrun it
+checks WORLD_SIZE == N. Each rank's slab lives on GPU local_rank % (visible
+GPUs) — on a box with fewer GPUs than ranks (tests) the ranks share devices
+and the process group falls back to gloo. Reported at N > 1:
+  * value (headline, weak scaling): every rank owns a 32768 x 32768 y-slab of
+    a periodic (N*32768) x 32768 grid; halo rows go to the ring neighbours
+    over NVLink, stored straight into their buffers by the stencil kernel
+    (P2P, CUDA IPC) — or NCCL send/recv overlapped with the interior rows;
+  * strong: the 32768^2 grid itself split into N slabs;
+  * e2e: the strong geometry end to end from pinned host memory;
+  * extra.cfg5_ch_8192sq_dist: BASELINE config 5 (Cahn-Hilliard ADI,
+    8192^2) on the N ranks (DistCHStepper, P2P form), steps/s, with the
+    reference CHStepper's s/step on this host's cores beside it.
+Device time is CUDA events on the launching stream, max over ranks.
 
 Also reported: `e2e` (same metric through the C-ABI with HOST pinned grids,
 H2D + kernel + D2H per step), `roofline` (dominant kernel vs the measured HBM
 copy bandwidth), `cpu_baseline` (the reference library, oracle/_ref, on this
-host's cores over a bounded sample), `clocks`, `gpu_launches`, and `extra`
+host's cores, the full 32768^2 grid), `clocks`, `gpu_launches`, and `extra`
 (secondary configs: FP32 variant, batched 1D config 2, config 1, CH ADI).
 
 `--impl reference` times the reference's own CPU implementation on the same
@@ -119,44 +131,67 @@ def dist_env():
 
 def reference_arm(args, rank, world):
     """Time the reference CPU implementation (oracle/_ref: the unmodified
-    reference library, all host threads) on a bounded sample of the config."""
+    reference library, all host threads) on the same config: the full
+    NX x NY grid, steady_clock around compute() only (bench.cpp:33-40),
+    after a steady-state warm-up. Each step is one full-grid application;
+    the step count is capped so the run stays within about a minute."""
     if rank != 0:
         return
-    # warm-up of at least 10 calls: the first compute() calls of a fresh
-    # worker pool run well below the pool's steady state
-    line = cpu_reference_sample(reps=args.steps, warmup=max(args.warmup, 10))
-    out = {"metric": METRIC, "value": line["value"], "unit": UNIT, "n_gpus": world, "steps": line["reps"],
-           "warmup": args.warmup, "ms_per_step": line["ms_per_app_sample"], "higher_is_better": True,
+    nx = args.nx
+    line = cpu_reference_sample(nx, target_s=args.ref_seconds * 5, max_reps=args.steps,
+                                warmup=max(args.warmup, 3), single_worker=True)
+    out = {"metric": METRIC, "value": line["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": line["reps"],
+           "warmup": max(args.warmup, 3), "ms_per_step": line["ms_per_app"], "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": WORKLOAD, "nx": NX, "ny": NY, "sample_rows": line["rows"]},
+           "config": {"workload": WORKLOAD if nx == NX else f"{WORKLOAD} (test size {nx}x{nx})",
+                      "nx": nx, "ny": nx, "sample_rows": nx},
            "impl": "reference",
            "cpu_baseline": {"value": line["value"], "unit": UNIT, "cores": line["cores"],
-                            "kind": line["kind"], "sample": line["sample"]},
+                            "kind": line["kind"], "sample": line["sample"], "cpu_model": line["cpu_model"],
+                            "one_worker": line.get("one_worker")},
            "e2e": {"value": line["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
-def cpu_reference_sample(target_s=12.0, rows=2048, reps=None, warmup=1):
-    """Reference compute() on a 32768 x `rows` periodic band, numWorkers =
-    numTiles = host threads, steady_clock around compute() only
-    (bench.cpp:33-40). Falls back to the C restatement (kind "port") only
-    if the reference library was never built."""
+def host_cores():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_reference_sample(nx=NX, target_s=12.0, max_reps=200, warmup=3, single_worker=False):
+    """Reference compute() on the FULL nx x nx periodic grid of the config,
+    numWorkers = numTiles = host threads, steady_clock around compute() only
+    (bench.cpp:33-40), mean over as many applications as fit in ~target_s
+    (at least 2). single_worker adds one numWorkers=1 application (§8(d)).
+    Falls back to the C restatement (kind "port") only if the reference
+    library was never built."""
     import numpy as np
     from oracle.oracle import Reference, Restatement
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    cores = host_cores()
     rng = np.random.default_rng(4)
-    inp = rng.uniform(-1.0, 1.0, (rows, NX))
+    inp = rng.uniform(-1.0, 1.0, (nx, nx))
     w = rng.uniform(-1.0, 1.0, 9)
+    pts = nx * nx
+    one = None
     try:
         ref = Reference()
         kind = "reference"
-        if reps is None:  # size the sample to ~target_s of CPU work
-            t1 = ref.stencil_timed(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3", tiles=min(cores, rows),
-                                   workers=cores, warmup=1, reps=1)
-            reps = max(1, min(200, int(target_s / max(t1, 1e-6))))
-            warmup = 0
-        secs = ref.stencil_timed(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3", tiles=min(cores, rows),
-                                 workers=cores, warmup=warmup, reps=reps)
+        run = dict(fn="fn_weighted_3x3", tiles=min(cores, nx), workers=cores)
+        t1 = ref.stencil_timed(inp, (1, 1, 1, 1), w, warmup=warmup, reps=1, **run)
+        reps = int(max(2, min(max_reps, target_s / max(t1, 1e-6))))
+        secs = ref.stencil_timed(inp, (1, 1, 1, 1), w, warmup=0, reps=reps, **run)
+        if single_worker:
+            s1 = ref.stencil_timed(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3", tiles=1, workers=1, warmup=0, reps=1)
+            one = {"value": pts / s1 / 1e9, "unit": UNIT, "workers": 1, "s_per_app": s1}
     except FileNotFoundError:
         orc = Restatement()
         kind = "port"
@@ -165,11 +200,30 @@ def cpu_reference_sample(target_s=12.0, rows=2048, reps=None, warmup=1):
         reps = 1
         orc.stencil(inp, (1, 1, 1, 1), w, fn="fn_weighted_3x3")
         secs = time.perf_counter() - t0
-    pts = rows * NX
-    return {"value": pts / secs / 1e9, "cores": cores, "kind": kind, "reps": reps, "rows": rows,
-            "ms_per_app_sample": secs * 1e3,
-            "sample": f"{NX}x{rows} periodic band of the {NX}x{NY} config (fn_weighted_3x3, FP64), "
+    return {"value": pts / secs / 1e9, "cores": cores, "kind": kind, "reps": reps, "rows": nx,
+            "ms_per_app": secs * 1e3, "cpu_model": cpu_model(), "one_worker": one,
+            "sample": f"the full {nx}x{nx} periodic grid (fn_weighted_3x3, FP64), {warmup} warm-up + "
                       f"{reps} timed compute() calls, numWorkers=numTiles={cores}"}
+
+
+def cpu_baseline_line(args):
+    cb = cpu_reference_sample(args.nx, target_s=args.ref_seconds)
+    return {"value": cb["value"], "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"], "sample": cb["sample"],
+            "cpu_model": cb["cpu_model"]}
+
+
+def cpu_reference_ch(n, steps=3):
+    """Seconds per CHStepper::step of the reference (oracle/_ref) at n x n on
+    this host's cores (numTiles = numWorkers = cores), construction excluded
+    (ch_timed: steady_clock around `steps` steps) — config 5's CPU baseline."""
+    try:
+        from oracle.oracle import Reference, ch_params
+        cores = host_cores()
+        s = Reference().ch_timed(ch_params(n), steps, warmup=0, tiles=cores, workers=cores)
+        return {"s_per_step": s, "steps_s": 1.0 / s, "cores": cores, "timed_steps": steps,
+                "kind": "reference (oracle/_ref CHStepper::step)", "cpu_model": cpu_model()}
+    except Exception as e:  # reported context only
+        return {"error": repr(e)[:200]}
 
 
 # --------------------------------------------------------------------- ours
@@ -283,7 +337,7 @@ def pcie_ceiling(torch, hin, hout, chunks=16):
         return {"error": repr(e)}
 
 
-def extras(sg, torch, stream, peak):
+def extras(sg, torch, stream, peak, args):
     """Secondary BASELINE.json configs, short runs; reported, not headline."""
     import numpy as np
     out = {}
@@ -350,8 +404,8 @@ def extras(sg, torch, stream, peak):
     out["stencil_variants_16384sq_fp64"] = bench_variants(sg, torch, stream, peak)
     out["penta_general_periodic"] = bench_penta_general(sg, torch, peak)
     out["weno5_advect_8192sq_fp64"] = bench_weno(sg, torch, peak)
-    if hasattr(sg, "CHStepper"):
-        out.update(bench_ch(sg, torch))
+    if not args.skip_ch:
+        out.update(bench_ch(sg, torch, args))
     return out
 
 
@@ -482,7 +536,7 @@ def bench_variants(sg, torch, stream, peak, n=16384, launches=20):
     return res
 
 
-def bench_ch(sg, torch, n=1024, steps=1000):
+def bench_ch(sg, torch, args, n=1024, steps=1000):
     p = sg.CHParams(nx=n, ny=n)
     p.dt = 0.1 * p.dx()
     p.T = steps * p.dt
@@ -520,19 +574,40 @@ def bench_ch(sg, torch, n=1024, steps=1000):
     except Exception as e:  # reported context only
         out["cfg3_ch_1024sq_reference_steps_s"] = {"error": repr(e)}
     # Config 5's grid (8192^2) on ONE GPU: the single-device stepper, 40 steps.
-    p = sg.CHParams(nx=8192, ny=8192)
+    n5 = args.ch_n
+    p = sg.CHParams(nx=n5, ny=n5)
     p.dt = 0.1 * p.dx()
     p.T = 1.0
     st = sg.CHStepper(p)
     st.step_many(5)
     st.synchronize()
     t0 = time.perf_counter()
-    st.step_many(40)
+    st.step_many(args.ch_steps)
     st.synchronize()
     dt = time.perf_counter() - t0
-    out["cfg5_grid_ch_8192sq_1gpu_steps_s"] = 40 / dt
+    out["cfg5_grid_ch_8192sq_1gpu_steps_s"] = args.ch_steps / dt
     del st
     torch.cuda.empty_cache()
+    # the distributed stepper (config 5's multi-GPU path) at world = 1, and
+    # the reference CHStepper at 8192^2 on this host's cores beside it
+    from paper_1902_09931_b200.ch_dist import DistCHStepper
+    dst = DistCHStepper(p, 1, 0, None, mode="p2p")
+    for _ in range(3):
+        dst.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.ch_steps):
+        dst.step()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.ch_steps
+    out["cfg5_ch_8192sq_dist"] = {"steps_s": 1e3 / ms, "ms_per_step": ms, "n": n5, "n_gpus": 1,
+                                  "mode": dst.mode, "timed_steps": args.ch_steps}
+    del dst
+    torch.cuda.empty_cache()
+    if not args.skip_cpu:
+        out["cfg5_ch_8192sq_dist"]["reference_cpu"] = cpu_reference_ch(n5)
     return out
 
 
@@ -540,40 +615,43 @@ def ours_arm(args, rank, world, local_rank):
     import torch
 
     import paper_1902_09931_b200 as sg
-    torch.cuda.set_device(local_rank)
-    sg._lib.check(sg._lib.lib().sg_init(local_rank))
+    ndev = torch.cuda.device_count()
+    if ndev < 1:
+        raise SystemExit("bench.py: no CUDA device visible (there is no CPU fallback)")
+    dev = local_rank % ndev
+    torch.cuda.set_device(dev)
+    sg._lib.check(sg._lib.lib().sg_init(dev))
     peak, peak_kind = measured_peak()
     if world > 1 or args.slab:
-        from paper_1902_09931_b200 import slab
-        line = slab.bench_multi_gpu(args, rank, world, local_rank, METRIC, UNIT, WORKLOAD, peak, peak_kind, Clocks)
+        line = multi_gpu_arm(args, rank, world, local_rank, dev, ndev, peak, peak_kind)
         if line is not None:
-            if world == 1 and not args.skip_cpu:
-                cb = cpu_reference_sample(target_s=args.ref_seconds)
-                line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"],
-                                        "kind": cb["kind"], "sample": cb["sample"]}
             print(json.dumps(line), flush=True)
         return
 
+    nx = ny = args.nx
     stream = torch.cuda.Stream()
-    with Clocks(local_rank) as clk:
-        total_ms, per, launches = bench_device_stencil(sg, torch, "f64", NX, NY, args.steps, args.warmup, stream)
+    with Clocks(dev) as clk:
+        total_ms, per, launches = bench_device_stencil(sg, torch, "f64", nx, ny, args.steps, args.warmup, stream)
     clocks = clk.summary()
     ms = total_ms / args.steps
-    value = NX * NY / (ms * 1e-3) / 1e9
+    value = nx * ny / (ms * 1e-3) / 1e9
     kms = statistics.mean(per)
-    alg_bytes = NX * NY * BYTES_PER_PT["f64"]
+    alg_bytes = nx * ny * BYTES_PER_PT["f64"]
     achieved = alg_bytes / (kms * 1e-3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "traffic_r01.json"
-    if tp.exists():
+    if tp.exists() and nx == NX:
         traffic = json.loads(tp.read_text()).get("bytes_per_launch")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "nx": NX, "ny": NY, "fn": "fn_weighted_3x3",
+        "config": {"workload": WORKLOAD if nx == NX else f"{WORKLOAD} (test size {nx}x{nx})",
+                   "nx": nx, "ny": ny, "fn": "fn_weighted_3x3",
                    "boundary": "periodic", "direction": "xy", "l2": "input 8 GiB >> 126 MB L2, no flush needed",
-                   "parallelism": "single GPU"},
+                   "parallelism": "single GPU", "timed_region_s": total_ms / 1e3},
+        "strong": {"value": value, "unit": UNIT, "ms_per_step": ms,
+                   "note": "N = 1: the strong- and weak-scaling workloads are the same 32768^2 grid"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "k_tma<double,1,1,1,1,OpWeighted3x3>", "kernel_ms": kms,
@@ -584,32 +662,243 @@ def ours_arm(args, rank, world, local_rank):
         "gpu_launches": int(launches),
     }
     if not args.skip_e2e:
-        line["e2e"] = bench_e2e(sg, torch, NX, NY, args.e2e_steps)
+        line["e2e"] = bench_e2e(sg, torch, nx, ny, args.e2e_steps)
     if not args.skip_extra:
         try:
-            line["extra"] = extras(sg, torch, stream, peak)
+            line["extra"] = extras(sg, torch, stream, peak, args)
         except Exception as e:  # secondary numbers must not kill the headline
             line["extra"] = {"error": repr(e)}
     if not args.skip_cpu:
-        cb = cpu_reference_sample(target_s=args.ref_seconds)
-        line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"],
-                                "kind": cb["kind"], "sample": cb["sample"]}
+        line["cpu_baseline"] = cpu_baseline_line(args)
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ multi-GPU
+
+
+def multi_gpu_arm(args, rank, world, local_rank, dev, ndev, peak, peak_kind):
+    """N ranks, one per GPU (torchrun). Weak scaling (headline), strong
+    scaling, e2e on the strong geometry, and config 5 (CH 8192^2) on the N
+    ranks. Returns rank 0's JSON line (None elsewhere)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1902_09931_b200 import _lib
+    from paper_1902_09931_b200.slab import Slab, SlabStencil, enable_p2p_ipc
+    from paper_1902_09931_b200.stencil import Extents, FunctionStencil
+
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    shared = local_world > ndev  # ranks share GPUs (tests on a 1-GPU box): NCCL refuses that
+    backend = "gloo" if shared else "nccl"
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+    assert dist.get_world_size() == world == args.gpus, (dist.get_world_size(), world, args.gpus)
+    red_dev = f"cuda:{dev}" if backend == "nccl" else "cpu"
+
+    def reduce(x, op):
+        t = torch.tensor([float(x)], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    def sync_all():
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    nx = args.nx
+    w = list(np.random.default_rng(4).uniform(-1, 1, 9))
+    kind = FunctionStencil(Extents(1, 1, 1, 1), "fn_weighted_3x3", w)
+
+    def make(ny_total):
+        slab = Slab(nx, ny_total, world, rank, 1, 1, True)
+        st = SlabStencil(slab, (1, 1, 1, 1), kind, torch.float64, f"cuda:{dev}", dist)
+        g = torch.Generator(device=f"cuda:{dev}").manual_seed(4 + rank)
+        st.own_view(st.a).copy_(torch.rand((slab.own, nx), dtype=torch.float64, device=f"cuda:{dev}",
+                                           generator=g))
+        halo = "nccl"
+        torch.cuda.synchronize()
+        if args.halo == "p2p" and enable_p2p_ipc(st, dist):
+            halo = "p2p"
+        elif backend != "nccl":
+            raise SystemExit("bench.py: ranks sharing a GPU need the P2P halo path (gloo has no CUDA send/recv)")
+        return slab, st, halo
+
+    def timed(st, steps, clk=None):
+        for _ in range(args.warmup):
+            st.apply()
+            st.swap()
+        sync_all()
+        l0 = _lib.launch_count()
+        if clk:
+            clk.__enter__()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            st.apply()
+            st.swap()
+        e1.record()
+        torch.cuda.synchronize()
+        if clk:
+            clk.__exit__(None, None, None)
+        launches = _lib.launch_count() - l0
+        ms = reduce(e0.elapsed_time(e1) / steps, dist.ReduceOp.MAX)
+        return ms, int(reduce(launches, dist.ReduceOp.SUM))
+
+    # weak scaling (headline): one nx x nx slab per rank
+    slab, st, halo = make(nx * world)
+    clk = Clocks(dev) if rank == 0 else None
+    ms_w, launches = timed(st, args.steps, clk)
+    del st
+    torch.cuda.empty_cache()
+    sync_all()
+    # strong scaling: the nx x nx grid split into `world` slabs
+    slab_s, st, halo_s = make(nx)
+    ms_s, _ = timed(st, args.steps)
+    e2e = None
+    if not args.skip_e2e and args.e2e_steps > 0:
+        e2e = multi_gpu_e2e(args, torch, dist, st, slab_s, reduce, sync_all)
+    del st
+    torch.cuda.empty_cache()
+    sync_all()
+    ch = None
+    if not args.skip_ch:
+        ch = bench_ch_dist(args, torch, dist, rank, world, dev, backend, reduce, sync_all)
+    line = None
+    if rank == 0:
+        value = nx * nx * world / (ms_w * 1e-3) / 1e9
+        alg = nx * nx * 16  # per GPU per step
+        strong_value = nx * nx / (ms_s * 1e-3) / 1e9
+        halo_txt = ("halo rows stored into the neighbours' buffers by the stencil kernel (P2P over NVLink, "
+                    "CUDA IPC)" if halo == "p2p" else "NCCL halo send/recv overlapped with the interior rows")
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_w, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": (WORKLOAD if nx == NX else f"{WORKLOAD} (test size {nx})")
+                           + f", weak scaling: {nx}x{nx} y-slab per GPU ({nx}x{nx * world} total)",
+                           "nx": nx, "ny": nx * world, "parallelism": f"y-slab x{world}, {halo_txt}",
+                           "backend": backend, "ranks_share_gpus": shared,
+                           "l2": "input 8 GiB per GPU >> L2", "timed_region_s": ms_w * args.steps / 1e3},
+                "strong": {"value": strong_value, "unit": UNIT, "ms_per_step": ms_s,
+                           "workload": f"the {nx}x{nx} grid split into {world} y-slabs of {slab_s.own} rows",
+                           "per_gpu_hbm_frac": nx * slab_s.own * 16 / (ms_s * 1e-3) / 1e9 / peak,
+                           "halo": halo_s},
+                "roofline": {"bound": "hbm", "achieved": alg / (ms_w * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                             "frac": alg / (ms_w * 1e-3) / 1e9 / peak, "traffic": None, "peak_kind": peak_kind,
+                             "kernel": "k_tma<double,1,1,1,1,OpWeighted3x3> (P2P variant)",
+                             "note": "per-GPU algorithmic bytes / per-GPU step time incl. the halo exchange"},
+                "gpu_launches": launches}
+        if clk:
+            line["clocks"] = clk.summary()
+        if e2e:
+            line["e2e"] = e2e
+        if ch:
+            line["extra"] = {"cfg5_ch_8192sq_dist": ch}
+    dist.destroy_process_group()
+    if rank == 0 and ch and "skipped" not in ch and not args.skip_cpu:
+        line["extra"]["cfg5_ch_8192sq_dist"]["reference_cpu"] = cpu_reference_ch(args.ch_n)
+    return line
+
+
+def multi_gpu_e2e(args, torch, dist, st, slab, reduce, sync_all):
+    """The strong geometry end to end: every rank uploads its ext rows (own
+    + halo rows, read from pinned host memory — a host-resident grid), runs
+    the kernel and downloads its own output rows (SlabStencil.apply_host).
+    Wall clock between barriers, max over ranks."""
+    nx = slab.nx
+    try:
+        hin = torch.empty((slab.ext_rows, nx), dtype=torch.float64, pin_memory=True)
+        hout = torch.empty((slab.own, nx), dtype=torch.float64, pin_memory=True)
+        ok = 1.0
+    except RuntimeError:
+        ok = 0.0
+    if reduce(ok, dist.ReduceOp.MIN) < 1.0:
+        return {"error": "pinned host buffers could not be allocated"}
+    hin.uniform_(-1, 1)
+    st.apply_host(hin, hout)  # warm-up
+    sync_all()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        st.apply_host(hin, hout)
+    dt = reduce(time.perf_counter() - t0, dist.ReduceOp.MAX)
+    h2d = int(reduce(slab.ext_rows * nx * 8, dist.ReduceOp.SUM))
+    d2h = int(reduce(slab.own * nx * 8, dist.ReduceOp.SUM))
+    return {"value": nx * nx * args.e2e_steps / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+            "path": "SlabStencil.apply_host on every rank: ext rows (own + halo) uploaded from pinned host "
+                    "memory, own output rows downloaded, row-chunk pipelined; the strong-scaling geometry"}
+
+
+def bench_ch_dist(args, torch, dist, rank, world, dev, backend, reduce, sync_all):
+    """BASELINE config 5: Cahn-Hilliard ADI periodic FP64 at ch_n^2 on the
+    `world` ranks (DistCHStepper, P2P form: the all-to-alls fused into the
+    sweeps' stores; CUDA-graph replay of each step over NCCL). steps/s from
+    CUDA events on the compute stream, max over ranks."""
+    import paper_1902_09931_b200 as sg
+    from paper_1902_09931_b200.ch_dist import DistCHStepper
+    n = args.ch_n
+    if n % world:
+        return {"skipped": f"{n}x{n} does not split into {world} equal y-slabs (CHParams needs a power of two)",
+                "n_gpus": world}
+    p = sg.CHParams(nx=n, ny=n)
+    p.dt = 0.1 * p.dx()
+    p.T = 1.0
+    st = DistCHStepper(p, world, rank, dist, device=f"cuda:{dev}", mode="p2p")
+    for _ in range(3):
+        st.step()
+    sync_all()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.ch_steps):
+        st.step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = reduce(e0.elapsed_time(e1) / args.ch_steps, dist.ReduceOp.MAX)
+    mode = st.mode
+    del st
+    torch.cuda.empty_cache()
+    return {"steps_s": 1e3 / ms, "ms_per_step": ms, "n": n, "n_gpus": world, "timed_steps": args.ch_steps,
+            "mode": mode, "graphs": world == 1,
+            "path": "DistCHStepper: y-slabs; RHS + x-sweep, y-sweep, combine per step; the all-to-alls and "
+                    "halo rows are stored into the peers' buffers by the sweeps / combine (P2P)"
+                    if mode == "p2p" else "DistCHStepper NCCL form (halo + 2 all_to_all_single per step)"}
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` outside torchrun: re-launch this script under
+    torch.distributed.run with N ranks on 127.0.0.1 (rank 0 prints)."""
+    import socket
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--nx", type=int, default=NX, help="grid edge (default: the config's 32768; tests use less)")
+    ap.add_argument("--ch-n", type=int, default=8192, help="config 5 grid edge for the multi-GPU CH line")
+    ap.add_argument("--ch-steps", type=int, default=40)
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-extra", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-ch", action="store_true")
     ap.add_argument("--slab", action="store_true",
-                    help="use the multi-GPU y-slab path even at N=1 (NCCL world of one)")
+                    help="use the multi-GPU y-slab path even at N=1 (world of one)")
     ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
                     help="multi-GPU halo exchange: p2p = fused into the stencil kernel (the boundary rows are "
                          "stored into the neighbours' buffers over NVLink, CUDA IPC), falling back to nccl "
@@ -621,6 +910,10 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     ours_arm(args, rank, world, local_rank)
 
 

@@ -113,9 +113,15 @@ class DistCHStepper:
 
     def _barrier(self):
         """Orders the peers' P2P writes before this rank reads them: each
-        rank's all-reduce contribution is queued after its sweep kernel."""
+        rank's all-reduce contribution is queued after its sweep kernel
+        (NCCL). Over gloo (ranks sharing a GPU in tests): a device sync and a
+        host barrier."""
         if self.transport is None and self.world > 1:
-            self.dist.all_reduce(self._flag)
+            if self.dist.get_backend() == "nccl":
+                self.dist.all_reduce(self._flag)
+            else:
+                self.torch.cuda.current_stream().synchronize()
+                self.dist.barrier()
 
     @staticmethod
     def _p(t):

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -56,6 +57,22 @@ std::vector<std::pair<int, int>> tiles_for(int ny, int numTiles) {
   return t;
 }
 
+// numWorkers -> GPU count. 0 ("clip", the default): G = min(numWorkers,
+// visible GPUs) — a reference caller passing its host thread count gets every
+// GPU and no oversubscription. 1 ("modulo"): G = numWorkers, worker w on
+// device w % GPUs — several workers share a device (tests of the multi-GPU
+// path on a one-GPU box). SG_DEVICE_MAP=modulo selects 1 at load.
+std::atomic<int> g_device_map{-1};
+int device_map() {
+  int m = g_device_map.load();
+  if (m < 0) {
+    const char* e = std::getenv("SG_DEVICE_MAP");
+    m = e && std::strcmp(e, "modulo") == 0 ? 1 : 0;
+    g_device_map.store(m);
+  }
+  return m;
+}
+
 }  // namespace
 
 struct sg_plan_s {
@@ -78,18 +95,43 @@ struct sg_plan_s {
     bool owned = false;     // device mirror allocated by the plan
     bool devValid = false;  // device copy holds the current values
     bool hostValid = true;  // host copy holds the current values
+    bool halosValid = false;  // multi-worker: the slabs' halo rows match their owners' rows
   } buf[2];
   int inIdx = 0;
   // Host-pipelining resources (Residency::Host on large periodic grids).
   cudaStream_t sH2D = nullptr, sD2H = nullptr;
   std::vector<cudaEvent_t> events;
   bool registered[2] = {false, false};
+  // numWorkers -> GPUs (host grids only): worker w owns make_tiles(ny, G)'s
+  // w-th row block on device `device`, both bindings stored as ext slabs
+  // [top halo | own rows | bottom halo]. Empty: single-device plan.
+  struct Worker {
+    int device = 0;
+    int r0 = 0, r1 = 0;
+    cudaStream_t stream = nullptr, sH2D = nullptr, sD2H = nullptr;
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t done = nullptr;
+    std::vector<cudaEvent_t> ev;  // pipeline events
+    int own() const { return r1 - r0; }
+  };
+  std::vector<Worker> workers;
 
   size_t elem() const { return dtype == SG_F64 ? 8 : 4; }
   size_t bytes() const { return static_cast<size_t>(nx) * ny * (dtype == SG_F64 ? 8 : 4); }
 
   void release() {
     if (!valid) return;
+    for (auto& w : workers) {
+      cudaSetDevice(w.device);
+      if (w.stream) cudaStreamSynchronize(w.stream);
+      for (void* b : w.buf)
+        if (b) cudaFree(b);
+      for (auto e : w.ev) cudaEventDestroy(e);
+      if (w.done) cudaEventDestroy(w.done);
+      for (cudaStream_t t : {w.stream, w.sH2D, w.sD2H})
+        if (t) cudaStreamDestroy(t);
+    }
+    workers.clear();
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
     for (auto& b : buf)

@@ -1387,6 +1387,13 @@ struct ChDist {
     for (int k = 0; k < 4; ++k) wx[k] = fx.t.W[k] + static_cast<size_t>(rank) * nxq;
     p2p = penta_sweep_xin(fx.t, own, p.nx, xloc, rhsT, nullptr, nullptr, y4x, stream, false, false, 0, &px) &&
           penta_sweep_xin(fy.t, nxq, p.ny, ycol, recvX, wx, y4xAll, ybuf, stream, false, false, own, &py);
+    // Runtime self-check: a TMA tensor store into every peer's receive
+    // buffers (the exact mechanism the sweeps use), read back through the
+    // mapping. A transport that maps but does not carry TMA stores (or a
+    // stale/broken mapping) leaves the caller on the collective form.
+    for (int d = 0; p2p && d < world; ++d)
+      p2p = peer_tma_probe(rx[d] + static_cast<size_t>(rank) * nxq * own, 0x5a00u + 16u * rank + d, stream) &&
+            peer_tma_probe(ry[d] + static_cast<size_t>(rank) * own * nxq, 0x6b00u + 16u * rank + d, stream);
     return p2p;
   }
 

@@ -1513,6 +1513,55 @@ bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double
 }
 
 
+// ------------------------------------------------ peer TMA store self-check
+
+// One 32 x 2 box written by a TMA tensor store from shared memory into
+// `dst` (another device's buffer over NVLink, or IPC-mapped memory), then
+// read back through generic loads. *ok = 1 iff every value arrived. The
+// pattern depends on `salt`, so a stale earlier probe cannot pass.
+__global__ void k_peer_tma_probe(const __grid_constant__ CUtensorMap map, const double* dst, unsigned salt,
+                                 int* ok) {
+  __shared__ alignas(128) double box[64];
+  const int t = threadIdx.x;
+  box[t] = static_cast<double>(salt) * 64.0 + t;
+  box[t + 32] = -(static_cast<double>(salt) * 64.0 + t + 32);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (t == 0) {
+    s_tma_store_2d(&map, 0, 0, box);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence_system();
+  }
+  __syncthreads();
+  const volatile double* v = dst;
+  const bool good = v[t] == box[t] && v[t + 32] == box[t + 32];
+  const int all = __syncthreads_and(good ? 1 : 0);
+  if (t == 0) *ok = all;
+}
+
+bool peer_tma_probe(double* dst, unsigned salt, cudaStream_t s) {
+  if (reinterpret_cast<uintptr_t>(dst) & 15) return false;
+  CUtensorMap m;
+  if (!encode_map(&m, dst, 2, 32, 2, 32, 2)) return false;
+  int* d_ok = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&d_ok), sizeof(int), s) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  int ok = 0;
+  k_peer_tma_probe<<<1, 32, 0, s>>>(m, dst, salt, d_ok);
+  bool good = cudaGetLastError() == cudaSuccess &&
+              cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+              cudaStreamSynchronize(s) == cudaSuccess;
+  cudaFreeAsync(d_ok, s);
+  cudaStreamSynchronize(s);
+  cudaGetLastError();
+  return good && ok == 1;
+}
+
+
 // ------------------------------------------------------------ PentaFactor
 
 DevicePenta::~DevicePenta() {

@@ -76,6 +76,10 @@ struct SweepPeers {
   int y4Stride = 0, y4Off = 0;
 };
 
+// Runtime self-check of the P2P path: one TMA tensor store into `dst`
+// (peer / IPC-mapped memory) plus a read-back; false if either fails.
+bool peer_tma_probe(double* dst, unsigned salt, cudaStream_t s);
+
 // ztInner: the input's unknowns are stored in blocks of ztInner per system
 // (zT[(r / ztInner)*(B*ztInner) + b*ztInner + r % ztInner]; 0 = n: plain
 // system-major) — the distributed y-sweep reads one block per source rank.

@@ -20,7 +20,6 @@ are bitwise invariant in the GPU count.
 from __future__ import annotations
 
 import os
-import time
 from dataclasses import dataclass
 
 
@@ -143,14 +142,25 @@ def local_wrap_fill(slab: Slab, ext):
 
 
 def exchange_halos(slab: Slab, ext, dist=None):
-    """Blocking halo exchange (used by tests and the simple path)."""
+    """Blocking halo exchange (setup, tests and the simple path). Over gloo,
+    which has no CUDA send/recv, device slabs are staged through host
+    copies."""
     if slab.world == 1:
         local_wrap_fill(slab, ext)
         return
+    staged = None
+    if getattr(ext, "is_cuda", False) and dist.get_backend() != "nccl":
+        staged, ext = ext, ext.cpu()
     ops = exchange_ops(slab, ext, dist)
     if ops:
         for r in dist.batch_isend_irecv(ops):
             r.wait()
+    if staged is not None:
+        top, own, bottom = slab.top, slab.own, slab.bottom
+        if top:
+            staged[0:top].copy_(ext[0:top])
+        if bottom:
+            staged[top + own:top + own + bottom].copy_(ext[top + own:top + own + bottom])
 
 
 class SlabStencil:
@@ -216,16 +226,45 @@ class SlabStencil:
         if self._barrier is not None:
             self._barrier()
         elif s.world > 1:
+            # the barrier must be ordered after THIS launch's peer stores: issue
+            # it on the stream the kernel ran on, not torch's current stream
+            with self.torch.cuda.stream(self._torch_stream(stream)):
+                self.default_barrier()
+
+    def default_barrier(self):
+        """Orders every rank's peer stores before any rank's next read: a
+        one-element NCCL all-reduce queued on the current stream (each
+        rank's contribution follows its kernel), or, over gloo (ranks sharing
+        a device in tests), a device sync + host barrier."""
+        if self.dist.get_backend() == "nccl":
             if not hasattr(self, "_flag"):
                 self._flag = self.torch.zeros(1, device=self.a.device)
             self.dist.all_reduce(self._flag)
+        else:
+            self.torch.cuda.current_stream().synchronize()
+            self.dist.barrier()
+
+    def _torch_stream(self, stream):
+        torch = self.torch
+        if stream is None:
+            return torch.cuda.current_stream()
+        if isinstance(stream, torch.cuda.Stream):
+            return stream
+        return torch.cuda.ExternalStream(int(stream))
 
     def own_view(self, buf):
         t = self.slab.top
         return buf[t:t + self.slab.own]
 
     def apply(self, stream=None):
-        """out(own rows of b) = stencil(a); returns after enqueueing."""
+        """out(own rows of b) = stencil(a); returns after enqueueing.
+
+        NCCL form: the halo sends/receives are posted FIRST — the rows sent
+        are own rows of `a`, complete once the previous application is — so
+        the NCCL stream runs the exchange while the interior-row kernel
+        (windows inside the slab) computes; the boundary-row kernels wait for
+        the exchange. Everything is ordered on `stream` (default: torch's
+        current stream)."""
         from .stencil import launch_slab
         if self.mode == "p2p":
             return self._apply_p2p(stream)
@@ -234,207 +273,114 @@ class SlabStencil:
         out_own = self.own_view(self.b)
         ia, ib = s.interior_rows()
         oa, ob = s.output_rows()
-        if ia < ib:
-            launch_slab(s.desc(lr, ia, ib), self.ext, self.kind, self.a, out_own, stream)
-        if s.world == 1:
-            local_wrap_fill(s, self.a)
-        else:
+        ts = self._torch_stream(stream)
+        works = []
+        if s.world > 1:
             ops = exchange_ops(s, self.a, self.dist)
             if ops:
-                for r in self.dist.batch_isend_irecv(ops):
-                    r.wait()  # makes the current stream wait on the NCCL stream
+                # ProcessGroupNCCL orders its stream after the CURRENT stream at
+                # this point, i.e. after the previous application only
+                with self.torch.cuda.stream(ts):
+                    works = self.dist.batch_isend_irecv(ops)
+        if ia < ib:
+            launch_slab(s.desc(lr, ia, ib), self.ext, self.kind, self.a, out_own, ts.cuda_stream)
+        if s.world == 1:
+            with self.torch.cuda.stream(ts):
+                local_wrap_fill(s, self.a)
+        else:
+            with self.torch.cuda.stream(ts):
+                for r in works:
+                    r.wait()  # makes `ts` wait on the NCCL stream
         if ia >= ib:
             if oa < ob:
-                launch_slab(s.desc(lr, oa, ob), self.ext, self.kind, self.a, out_own, stream)
+                launch_slab(s.desc(lr, oa, ob), self.ext, self.kind, self.a, out_own, ts.cuda_stream)
             return
         if oa < ia:
-            launch_slab(s.desc(lr, oa, ia), self.ext, self.kind, self.a, out_own, stream)
+            launch_slab(s.desc(lr, oa, ia), self.ext, self.kind, self.a, out_own, ts.cuda_stream)
         if ib < ob:
-            launch_slab(s.desc(lr, ib, ob), self.ext, self.kind, self.a, out_own, stream)
+            launch_slab(s.desc(lr, ib, ob), self.ext, self.kind, self.a, out_own, ts.cuda_stream)
 
     def swap(self):
         self.a, self.b = self.b, self.a
         self._out ^= 1
 
     def apply_host(self, hin, hout, chunks: int = 0):
-        """End-to-end application from/to pinned HOST memory: the own rows
-        are uploaded in `chunks` row blocks on a copy stream (first and last
-        block first, so the halo exchange can start early), each block's
-        interior output rows are computed as soon as the block below has
-        landed, and finished output blocks stream back on a second copy
-        stream while later blocks compute. Same kernels and arithmetic as
+        """End-to-end application from/to pinned HOST memory.
+
+        hin: (ext_rows, nx) host rows of the input in ext order — top halo,
+        own rows, bottom halo (global rows `slab.global_rows_of_ext()`; rows
+        outside a non-periodic grid are never read) — so a rank reading its
+        share of a host-resident grid takes its halo rows from host memory
+        and no device exchange is needed. hout: (own, nx) host output rows;
+        outside the computed window (the non-periodic frame) it is left
+        untouched, as the reference leaves its output frame (stencil.cpp:35-38).
+
+        Pipelined in row chunks on three streams: the H2D of the ext rows
+        chunk c+1 needs, the kernel on chunk c and the D2H of chunk c-1
+        overlap (PCIe is full duplex). Same kernels and arithmetic as
         `apply` (bitwise equal); returns after the D2H copies complete."""
         from .stencil import launch_slab
         torch = self.torch
         s = self.slab
-        own, top = s.own, s.top
+        H = s.top + s.bottom
         lr = (self.ext.left, self.ext.right)
         comp = torch.cuda.current_stream()
         if not hasattr(self, "_h2d"):
             self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
         h2d, d2h = self._h2d, self._d2h
-        if chunks <= 0:  # fill and drain cost one block each: many blocks (SG_SLAB_CHUNKS overrides)
-            chunks = int(os.environ.get("SG_SLAB_CHUNKS", "64"))
-        chunks = max(1, min(chunks, own))
-        bounds = [(own * c // chunks, own * (c + 1) // chunks) for c in range(chunks)]
-        order = [0, chunks - 1] + list(range(1, chunks - 1)) if chunks > 1 else [0]
-        landed = {}
-        h2d.wait_stream(comp)  # the previous step's readers of `a` are done
-        a_own, b_own = self.own_view(self.a), self.own_view(self.b)
-        for c in order:
-            r0, r1 = bounds[c]
-            with torch.cuda.stream(h2d):
-                a_own[r0:r1].copy_(hin[r0:r1], non_blocking=True)
-                landed[c] = torch.cuda.Event()
-                landed[c].record(h2d)
-        comp.wait_event(landed[0])
-        comp.wait_event(landed[chunks - 1])
-        if s.world == 1:
-            local_wrap_fill(s, self.a)
-            works = []
-        else:
-            ops = exchange_ops(s, self.a, self.dist)
-            works = self.dist.batch_isend_irecv(ops) if ops else []
-        ia, ib = s.interior_rows()
+        if tuple(hin.shape) != (s.ext_rows, s.nx) or tuple(hout.shape) != (s.own, s.nx):
+            raise ValueError("apply_host: hin must be (ext_rows, nx), hout (own, nx)")
         oa, ob = s.output_rows()
-        done = []
-        for c in range(chunks):
-            r0, r1 = bounds[c]
-            if c + 1 < chunks:
-                comp.wait_event(landed[c + 1])  # the window's bottom rows
-            lo, hi = max(r0, ia), min(r1, ib)
-            if lo < hi:
-                launch_slab(s.desc(lr, lo, hi), self.ext, self.kind, self.a, b_own, comp.cuda_stream)
+        if chunks <= 0:  # fill and drain cost one chunk each: many chunks (SG_SLAB_CHUNKS overrides)
+            chunks = int(os.environ.get("SG_SLAB_CHUNKS", "64"))
+        chunks = max(1, min(chunks, ob - oa))
+        bounds = [(oa + (ob - oa) * c // chunks, oa + (ob - oa) * (c + 1) // chunks) for c in range(chunks)]
+        desc0 = s.desc(lr, 0, 0)
+        c0, c1 = desc0["col0"], desc0["col1"]
+        full_rows = (c0, c1) == (0, s.nx)
+        h2d.wait_stream(comp)  # the previous step's readers of `a` are done
+        b_own = self.own_view(self.b)
+        landed, done = [], []
+        e0 = 0
+        for c, (r0, r1) in enumerate(bounds):
+            # output row j reads ext rows j .. j + H
+            e1 = s.ext_rows if c == chunks - 1 else r1 + H
+            with torch.cuda.stream(h2d):
+                if e1 > e0:
+                    self.a[e0:e1].copy_(hin[e0:e1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+            landed.append(ev)
+            e0 = max(e0, e1)
+        for c, (r0, r1) in enumerate(bounds):
+            comp.wait_event(landed[c])
+            if r0 < r1:
+                launch_slab(s.desc(lr, r0, r1), self.ext, self.kind, self.a, b_own, comp.cuda_stream)
             ev = torch.cuda.Event()
             ev.record(comp)
             done.append(ev)
-        for w in works:
-            w.wait()
-        edges = ((oa, ob),) if ia >= ib else ((oa, min(ia, ob)), (max(ib, oa), ob))
-        for lo, hi in edges:
-            if lo < hi:
-                launch_slab(s.desc(lr, lo, hi), self.ext, self.kind, self.a, b_own, comp.cuda_stream)
-        fin = torch.cuda.Event()
-        fin.record(comp)
-        # d2h is in-order: interior blocks first (each as soon as it is
-        # computed), the blocks holding halo-dependent rows last
-        edge = [bounds[c][0] < ia or bounds[c][1] > ib for c in range(chunks)]
         with torch.cuda.stream(d2h):
-            for c in sorted(range(chunks), key=lambda c: edge[c]):
-                r0, r1 = bounds[c]
-                d2h.wait_event(fin if edge[c] else done[c])
-                hout[r0:r1].copy_(b_own[r0:r1], non_blocking=True)
+            for c, (r0, r1) in enumerate(bounds):
+                d2h.wait_event(done[c])
+                if r0 >= r1:
+                    continue
+                if full_rows:
+                    hout[r0:r1].copy_(b_own[r0:r1], non_blocking=True)
+                else:
+                    hout[r0:r1, c0:c1].copy_(b_own[r0:r1, c0:c1], non_blocking=True)
         d2h.synchronize()
+        comp.wait_stream(d2h)
 
-
-def bench_multi_gpu(args, rank, world, local_rank, metric, unit, workload, peak, peak_kind, clocks_cls=None):
-    """Weak scaling: every rank owns a 32768 x 32768 slab of a periodic
-    (world*32768) x 32768 grid; one step = halo exchange + application.
-
-    Returns rank 0's JSON line (None elsewhere). Device time is CUDA events
-    on the compute stream, max over ranks; `e2e` adds, every step, the H2D
-    copy of the rank's slab from pinned host memory and the D2H copy of its
-    output rows (wall clock between barriers, max over ranks)."""
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-
-    from . import _lib
-    from .stencil import Extents, FunctionStencil
-    if not dist.is_initialized():
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29511")
-        os.environ.setdefault("RANK", str(rank))
-        os.environ.setdefault("WORLD_SIZE", str(world))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    nx = per = 32768
-    ny = per * world
-    slab = Slab(nx, ny, world, rank, 1, 1, True)
-    kind = FunctionStencil(Extents(1, 1, 1, 1), "fn_weighted_3x3", list(np.random.default_rng(4).uniform(-1, 1, 9)))
-    st = SlabStencil(slab, (1, 1, 1, 1), kind, torch.float64, f"cuda:{local_rank}", dist)
-    g = torch.Generator(device="cuda").manual_seed(4 + rank)
-    st.own_view(st.a).copy_(torch.rand((slab.own, nx), dtype=torch.float64, device="cuda", generator=g))
-    stream = torch.cuda.current_stream()
-    halo = "NCCL halo exchange"
-    if getattr(args, "halo", "nccl") == "p2p":
-        torch.cuda.synchronize()
-        if enable_p2p_ipc(st, dist):
-            halo = "halo rows stored into the neighbours' buffers by the stencil kernel (P2P over NVLink)"
-
-    def max_over_ranks(x):
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    for _ in range(args.warmup):
-        st.apply(stream.cuda_stream)
-        st.swap()
-    torch.cuda.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
-    l0 = _lib.launch_count()
-    clk = clocks_cls(local_rank) if (clocks_cls is not None and rank == 0) else None
-    if clk:
-        clk.__enter__()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        st.apply(stream.cuda_stream)
-        st.swap()
-    e1.record()
-    torch.cuda.synchronize()
-    if clk:
-        clk.__exit__(None, None, None)
-    launches = _lib.launch_count() - l0
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    dist.barrier()
-
-    e2e = None
-    e2e_steps = getattr(args, "e2e_steps", 3)
-    if not getattr(args, "skip_e2e", False) and e2e_steps > 0:
-        try:  # 2 x 8.6 GB of pinned host memory per rank
-            hin = torch.empty((slab.own, nx), dtype=torch.float64, pin_memory=True)
-            hout = torch.empty_like(hin, pin_memory=True)
-            ok = 1.0
-        except RuntimeError:
-            ok = 0.0
-        t_ok = torch.tensor([ok], device="cuda")
-        dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
-        if t_ok.item() < 1.0:
-            e2e_steps = 0
-            e2e = {"error": "pinned host buffers (2 x 8.6 GB per rank) could not be allocated"}
-    if not getattr(args, "skip_e2e", False) and e2e_steps > 0:
-        hin.uniform_(-1, 1)
-        torch.cuda.synchronize()
-        dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            st.apply_host(hin, hout)
-        dt = max_over_ranks(time.perf_counter() - t0)
-        e2e = {"value": nx * ny * e2e_steps / dt / 1e9, "unit": unit,
-               "h2d_bytes_per_step": slab.own * nx * 8 * world, "d2h_bytes_per_step": slab.own * nx * 8 * world,
-               "steps": e2e_steps,
-               "path": "SlabStencil.apply_host on every rank: slab uploaded from / output downloaded to pinned host memory, row-chunk pipelined"}
-    line = None
-    if rank == 0:
-        value = nx * ny / (ms * 1e-3) / 1e9
-        alg = nx * per * 16
-        line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": workload + f", weak scaling: 32768x32768 y-slab per GPU ({nx}x{ny} total)",
-                           "nx": nx, "ny": ny, "parallelism": f"y-slab x{world}, {halo}",
-                           "l2": "input 8 GiB per GPU >> L2"},
-                "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                             "frac": alg / (ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_kind": peak_kind,
-                             "note": "per-GPU step time incl. halo exchange"},
-                "gpu_launches": int(launches)}
-        if clk:
-            line["clocks"] = clk.summary()
-        if e2e:
-            line["e2e"] = e2e
-    dist.destroy_process_group()
-    return line
+    def host_ext_rows(self, grid):
+        """The (ext_rows, nx) rows apply_host reads, gathered from a full
+        (ny, nx) host grid (rows outside a non-periodic grid are zero)."""
+        import numpy as np
+        rows = self.slab.global_rows_of_ext()
+        out = np.zeros((len(rows), self.slab.nx), dtype=grid.dtype)
+        for k, g in enumerate(rows):
+            if g is not None:
+                out[k] = grid[g]
+        return out
 
 
 def enable_p2p_ipc(st: SlabStencil, dist, fill_halos: bool = True) -> bool:

@@ -14,7 +14,7 @@ ROOT = Path(__file__).resolve().parents[1]
 def test_reference_arm_prints_contract_line():
     if not (ROOT / "oracle" / "_ref" / "libstengrid_ref.so").exists():
         pytest.skip("oracle/_ref not built")
-    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1"],
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1", "--nx", "2048"],
                        cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]

@@ -123,3 +123,82 @@ def test_distributed_ch_p2p_graph_replay_world1(sg):
         assert bits_equal(st.own_rows(0).cpu().numpy(), single.field().values)
         assert bits_equal(st.own_rows(1).cpu().numpy(), single.previous_field().values)
     assert len(st._graphs) == 2
+
+
+# ------------------------------------------- config 5 at its full geometry
+
+GOLDEN_8192 = __import__("pathlib").Path(__file__).parent / "golden" / "ch8192_100steps.json"
+
+
+def _sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<f8").tobytes()).hexdigest()
+
+
+def _run_sim(ranks, steps):
+    for _ in range(steps):
+        for st in ranks:
+            st.phase_x()
+        for st in ranks:
+            st.phase_y()
+        for st in ranks:
+            st.phase_combine()
+
+
+@pytest.fixture(scope="module")
+def single_8192_100(sg):
+    """The single-GPU CHStepper after 100 steps of config 5's grid (both
+    time levels, host copies) — compared with the reference's golden digest
+    and with the distributed forms below."""
+    p = params(sg, 8192, 8192)
+    st = sg.CHStepper(p)
+    st.step_many(100)
+    out = (st.field().values.copy(), st.previous_field().values.copy())
+    del st
+    return out
+
+
+def test_config5_100_steps_single_gpu_bitwise_vs_reference_golden(single_8192_100):
+    """BASELINE config 5's grid (8192^2, CHParams defaults) after 100 steps:
+    sha256 of both time levels equals the UNMODIFIED reference CHStepper's
+    (tests/golden/make_ch8192_golden.py, oracle/_ref on 8 cores, ≈30 min).
+    North-star bar: 1e-9 rel-L2; checked here bitwise, with rel-L2 bounds
+    from the golden's norms and sample rows if the digests ever differ."""
+    import json
+    if not GOLDEN_8192.exists():
+        pytest.skip("golden digest not generated")
+    g = json.loads(GOLDEN_8192.read_text())["steps_100"]
+    c, pr = single_8192_100
+    for r, hexrow in g["rows_curr"].items():
+        want = np.frombuffer(bytes.fromhex(hexrow), dtype="<f8")
+        rel = np.linalg.norm(c[int(r)] - want) / np.linalg.norm(want)
+        assert rel <= 1e-9, (r, rel)
+    assert abs(np.linalg.norm(c) - g["l2_curr"]) <= 1e-9 * g["l2_curr"]
+    assert _sha(c) == g["sha256_curr"]
+    assert _sha(pr) == g["sha256_prev"]
+
+
+@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+def test_config5_100_steps_g8_bitwise(sg, single_8192_100, mode):
+    """Config 5 at its real geometry: 8192^2 split over G = 8 simulated ranks
+    (1024-row slabs), 100 steps, in the P2P form (all-to-alls and halos
+    stored by the sweeps / combine into the peers' buffers) and the NCCL
+    form (the blocks all_to_all_single moves, copied by LocalTransport) —
+    both time levels bitwise equal to the single-GPU stepper (which the test
+    above pins to the reference)."""
+    import torch
+    from paper_1902_09931_b200.ch_dist import DistCHStepper, LocalTransport
+    G = 8
+    p = params(sg, 8192, 8192)
+    ranks = []
+    tr = LocalTransport(ranks)
+    for r in range(G):
+        ranks.append(DistCHStepper(p, G, r, transport=tr, mode=mode))
+    assert all(st.mode == mode for st in ranks)
+    _run_sim(ranks, 100)
+    torch.cuda.synchronize()
+    c, pr = single_8192_100
+    for r, st in enumerate(ranks):
+        a, b = st.r0, st.r0 + st.own
+        assert bits_equal(st.own_rows(0).cpu().numpy(), c[a:b]), r
+        assert bits_equal(st.own_rows(1).cpu().numpy(), pr[a:b]), r

@@ -93,11 +93,11 @@ def test_apply_host_pipeline_equals_oracle(sg, orc, ext, periodic, chunks):
     st = SlabStencil(slab, ext, kind, torch.float64, "cuda")
     sentinel = -12345.678
     st.own_view(st.b).fill_(sentinel)
-    hin = torch.empty((ny, nx), dtype=torch.float64, pin_memory=True)
+    hin = torch.empty((slab.ext_rows, nx), dtype=torch.float64, pin_memory=True)
     hout = torch.full((ny, nx), sentinel, dtype=torch.float64, pin_memory=True)
     for rep in range(2):
         g = rng.uniform(-1, 1, (ny, nx))
-        hin.copy_(torch.from_numpy(g))
+        hin.copy_(torch.from_numpy(st.host_ext_rows(g)))
         st.apply_host(hin, hout, chunks=chunks)
         want = orc.stencil(g, ext, w, periodic=periodic, out=np.full_like(g, sentinel))
         assert np.array_equal(hout.numpy().view(np.uint64), want.view(np.uint64))
