@@ -119,6 +119,26 @@ int sg_plan_valid(sg_plan_t plan);
  * generic one-point-per-thread path. */
 int sg_plan_kernel_kind(sg_plan_t plan);
 
+/* numWorkers -> GPUs (SPEC.md:12 maps cuSten's deviceNum onto the workers).
+ * A plan over HOST grids created with numWorkers = G > 1 splits the rows
+ * into make_tiles(ny, G) y-slabs (grid.cpp:62-82), one per worker, each on
+ * its own GPU with its own stream; every slab holds top/bottom halo rows.
+ * compute() uploads each worker's rows plus halo rows straight from the
+ * host grid (Residency::Host) or, for device-resident inputs, refreshes the
+ * halos from the neighbouring workers by peer copies over NVLink; results
+ * are bitwise those of one GPU. Device grids always run on their device.
+ * Mode 0 ("clip", default): G = min(numWorkers, visible GPUs). Mode 1
+ * ("modulo"): G = numWorkers, worker w on GPU w % visible GPUs (several
+ * workers per GPU: exercises the multi-GPU path on a one-GPU box).
+ * SG_DEVICE_MAP=modulo in the environment selects mode 1 at load. */
+sg_status sg_set_device_map(int mode);
+int sg_get_device_map(void);
+/* Workers of a plan: count, and for the first `capacity` the GPU and the
+ * global row range [rowBegin, rowEnd) each owns (1 worker for a one-GPU
+ * plan). Any output pointer may be NULL. */
+sg_status sg_plan_workers(sg_plan_t plan, int* workers, int* devices, int* rowBegins, int* rowEnds,
+                          int capacity);
+
 /* --------------------------------------------------------- slab launches
  * Stateless device launch used by the multi-GPU y-slab decomposition (and
  * internally by plans). Computes output rows [row0, row1) and columns
@@ -184,6 +204,18 @@ sg_status sg_ch_validate(const sg_ch_params* p);
 /* CHStepper ctor (cahn_hilliard.cpp:213-241): initial condition generated on
  * the device from SplitMix64, C^{n-1} := C^n, factors built. */
 sg_status sg_ch_create(const sg_ch_params* p, int numTiles, int numWorkers, sg_ch_t* ch);
+/* numWorkers -> GPUs (as for plans, sg_set_device_map): with G > 1 the
+ * stepper runs config 5's distributed step over G GPUs from this process —
+ * y-slabs of ny/G rows; RHS + x-sweep on the rows each GPU owns; both
+ * all-to-all transposes and the halo rows stored by the sweeps / combine
+ * straight into the peers' buffers (peer access over NVLink), or moved by
+ * peer copies when the sweep stage does not divide the slab. G is the
+ * largest power of two <= the mapped worker count with >= 2 rows per slab.
+ * Results are bitwise those of one GPU. field() gathers the slabs;
+ * sg_ch_device_field returns a gathered copy on worker 0's GPU. */
+sg_status sg_ch_workers(sg_ch_t ch, int* workers, int* p2p);
+/* Block until every queued step is complete. */
+sg_status sg_ch_synchronize(sg_ch_t ch);
 /* `steps` calls of CHStepper::step (cahn_hilliard.cpp:260-328). */
 sg_status sg_ch_step(sg_ch_t ch, int steps);
 /* set_state (cahn_hilliard.cpp:251-258): host arrays nx*ny; resets step/time. */

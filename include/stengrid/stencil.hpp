@@ -9,9 +9,10 @@
 //    registered with a device twin (register_device_function). The
 //    reference's own window functions are pre-registered (stengrid::functions).
 //    An unregistered fn throws std::invalid_argument — there is no CPU path.
-//  * Residency is real: Residency::Device leaves the output in HBM until
-//    sync_to_host(plan) (the paper's meaning); Residency::Host
-//    (the default) behaves exactly like the reference.
+//  * compute() is synchronous and host-coherent for both residency hints,
+//    like the reference; the extension compute_deferred(plan) is the
+//    paper's Residency::Device (output left in HBM until sync_to_host).
+//  * numWorkers -> GPUs: a plan with numWorkers > 1 runs one y-slab per GPU.
 #pragma once
 
 #include <cmath>
@@ -122,6 +123,11 @@ inline int device_function_id(StencilFunction fn) {
 }
 
 /// stencil.hpp:42-85 — movable, not copyable; never owns the fields.
+class StencilPlan;
+namespace detail {
+inline void compute_impl(StencilPlan& plan, bool hostCoherent);
+}
+
 class StencilPlan {
  public:
   StencilPlan() = default;
@@ -173,7 +179,7 @@ class StencilPlan {
   friend StencilPlan create_plan(Direction, BoundaryMode, StencilKind, Grid2D&, Grid2D&, int, int,
                                  WorkerPool*);
   friend void swap_plan(StencilPlan&);
-  friend void compute(StencilPlan&, Residency);
+  friend void detail::compute_impl(StencilPlan&, bool);
   friend void sync_to_host(StencilPlan&);
 
   // (Re)bind the C plan to the grids' current host buffers.
@@ -260,27 +266,41 @@ inline void swap_plan(StencilPlan& plan) {
   std::swap(plan.boundIn_, plan.boundOut_);
 }
 
-/// stencil.cpp:202-235 — runs on the GPU. Residency::Host (the default) is
-/// synchronous like the reference; Residency::Device returns once the kernel
-/// is queued (the output stays on the device — sync_to_host or a Host compute
-/// completes it), so chains of Device-residency applications do not wait on
-/// the host between launches.
+/// stencil.cpp:202-235 — runs on the GPU, synchronous and host-coherent for
+/// BOTH hints: on return the bound output Grid2D holds the result, exactly
+/// as in the reference, where the residency hint is a no-op
+/// (stencil.cpp:202). A numWorkers > 1 plan runs one y-slab per GPU
+/// (sg.h: sg_set_device_map).
 inline void compute(StencilPlan& plan, Residency hint = Residency::Host) {
+  (void)hint;
+  detail::compute_impl(plan, true);
+}
+
+/// Extension — the paper's Residency::Device: returns once
+/// the kernel is queued and leaves the output in HBM, so chains of
+/// compute_deferred / swap_plan never wait on the host or move the grids
+/// over PCIe. The bound host output is stale until sync_to_host(plan) (or a
+/// later compute()); do not modify the bound host grids in between.
+inline void compute_deferred(StencilPlan& plan) { detail::compute_impl(plan, false); }
+
+/// Bring compute_deferred results back into the bound host grids.
+inline void sync_to_host(StencilPlan& plan) {
+  if (!plan.valid()) throw std::logic_error("sync_to_host: plan was destroyed");
+  detail::check(sg_plan_sync_to_host(plan.h_));
+}
+
+namespace detail {
+inline void compute_impl(StencilPlan& plan, bool hostCoherent) {
   if (!plan.valid()) throw std::logic_error("compute: plan was destroyed");
   Grid2D& in = *plan.input_;
   Grid2D& out = *plan.output_;
   if (!in.same_shape(out)) throw std::invalid_argument("compute: bound grids changed shape");
   if (in.data() == out.data()) throw std::invalid_argument("compute: bound grids alias");
   if (in.data() != plan.boundIn_ || out.data() != plan.boundOut_) plan.bind();  // storage moved
-  const bool host = hint == Residency::Host;
-  detail::check(sg_plan_compute(plan.h_, host ? SG_RESIDENCY_HOST : SG_RESIDENCY_DEVICE, nullptr, host ? 1 : 0));
+  detail::check(sg_plan_compute(plan.h_, hostCoherent ? SG_RESIDENCY_HOST : SG_RESIDENCY_DEVICE, nullptr,
+                                hostCoherent ? 1 : 0));
 }
-
-/// Bring Device-resident results back into the bound host grids.
-inline void sync_to_host(StencilPlan& plan) {
-  if (!plan.valid()) throw std::logic_error("sync_to_host: plan was destroyed");
-  detail::check(sg_plan_sync_to_host(plan.h_));
-}
+}  // namespace detail
 
 /// stencil.cpp:237-260 — single-point evaluation (host; used as a checker).
 inline double apply_weights_at(const Grid2D& input, const WeightStencil& sten, int i, int j,

@@ -40,6 +40,7 @@ EXPORTED = [
     "sg_chd_geometry", "sg_chd_init", "sg_chd_phase_x", "sg_chd_phase_y", "sg_chd_combine",
     "sg_chd_destroy", "sg_chd_p2p_buffers", "sg_chd_set_peers", "sg_chd_phase_x_p2p", "sg_chd_phase_y_p2p",
     "sg_chd_combine_p2p", "sg_ipc_get_handle", "sg_ipc_open_handle", "sg_ipc_close", "sg_ch_diagnostics", "sg_simpson_mean", "sg_s_metric", "sg_k1_metric", "sg_ch_set_step", "sg_weno_advect",
+    "sg_set_device_map", "sg_get_device_map", "sg_plan_workers", "sg_ch_workers", "sg_ch_synchronize",
 ]
 
 
@@ -121,6 +122,9 @@ def lib():
         "sg_plan_binding": (C.c_int, [vp, C.c_int, C.POINTER(vp), C.POINTER(vp)]),
         "sg_plan_valid": (C.c_int, [vp]),
         "sg_plan_kernel_kind": (C.c_int, [vp]),
+        "sg_set_device_map": (C.c_int, [C.c_int]),
+        "sg_get_device_map": (C.c_int, []),
+        "sg_plan_workers": (C.c_int, [vp, ip, ip, ip, ip, C.c_int]),
         "sg_stencil_launch": (C.c_int, [C.POINTER(SgSlabDesc), SgExtents, C.c_int, dp, C.c_size_t,
                                         C.c_int, vp, vp, vp]),
         "sg_stencil_launch_p2p": (C.c_int, [C.POINTER(SgSlabDesc), SgExtents, C.c_int, dp, C.c_size_t,
@@ -155,6 +159,8 @@ def lib():
         "sg_ipc_close": (C.c_int, [vp]),
         "sg_ch_diagnostics": (C.c_int, [vp, dp, dp, dp]),
         "sg_ch_set_step": (C.c_int, [vp, C.c_int]),
+        "sg_ch_synchronize": (C.c_int, [vp]),
+        "sg_ch_workers": (C.c_int, [vp, ip, ip]),
         "sg_weno_advect": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_double, C.c_double, vp, C.c_int, vp]),
         "sg_simpson_mean": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp]),
         "sg_s_metric": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dp]),

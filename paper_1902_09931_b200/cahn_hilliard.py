@@ -148,8 +148,13 @@ class CHStepper:
         check(_lib.lib().sg_ch_step(self._h, int(steps)))
 
     def synchronize(self) -> None:
-        ptr = C.c_void_p()
-        check(_lib.lib().sg_ch_device_field(self._h, 0, C.byref(ptr)))
+        check(_lib.lib().sg_ch_synchronize(self._h))
+
+    def workers(self):
+        """(GPU count, P2P form?) — numWorkers -> GPUs (sg_ch_workers)."""
+        n, p2p = C.c_int(), C.c_int()
+        check(_lib.lib().sg_ch_workers(self._h, C.byref(n), C.byref(p2p)))
+        return n.value, bool(p2p.value)
 
     def set_state(self, curr: Grid2D, prev: Grid2D) -> None:
         """cahn_hilliard.cpp:251-258."""

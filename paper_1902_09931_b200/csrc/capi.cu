@@ -154,6 +154,8 @@ struct sg_plan_s {
   }
 };
 
+static void setup_workers(sg_plan_s* p, int G, int ndev);
+
 extern "C" {
 
 sg_status sg_internal_set_error(const char* msg, int system) {
@@ -266,6 +268,12 @@ sg_status sg_plan_create(sg_direction dir, sg_boundary mode, sg_extents ext, sg_
       // a BLOCKING stream: ordered after work the caller queued on the legacy
       // default stream (e.g. torch kernels producing device inputs)
       SG_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamDefault));
+      // numWorkers -> GPUs for host grids (device grids live on one device)
+      int ndev = 1;
+      SG_CUDA(cudaGetDeviceCount(&ndev));
+      int G = device_map() == 1 ? numWorkers : std::min(numWorkers, ndev);
+      G = std::min(G, ny);
+      if (memory == SG_MEM_HOST && G > 1) setup_workers(p, G, ndev);
       void* ptrs[2] = {in, out};
       for (int k = 0; k < 2; ++k) {
         auto& b = p->buf[k];
@@ -275,8 +283,10 @@ sg_status sg_plan_create(sg_direction dir, sg_boundary mode, sg_extents ext, sg_
           b.hostValid = false;
         } else {
           b.host = ptrs[k];
-          SG_CUDA(cudaMalloc(&b.dev, p->bytes()));
-          b.owned = true;
+          if (p->workers.empty()) {  // multi-worker plans hold only slabs
+            SG_CUDA(cudaMalloc(&b.dev, p->bytes()));
+            b.owned = true;
+          }
           // Page-lock large pageable host grids once so every transfer is a
           // full-speed DMA (the plan never owns the grids; unregistered at
           // destroy). Failure to register is harmless (pageable copies).
@@ -390,11 +400,234 @@ static void pipelined_host_compute(sg_plan_s* p, sg_plan_s::Buf& in, sg_plan_s::
   SG_CUDA(cudaStreamWaitEvent(s, evEnd, 0));
 }
 
+}  // extern "C"
+
+// ---------------------------------------------- multi-worker (multi-GPU)
+
+static void setup_workers(sg_plan_s* p, int G, int ndev) {
+  const auto t = tiles_for(p->ny, G);  // make_tiles' ceil-first row blocks
+  const size_t rowB = static_cast<size_t>(p->nx) * p->elem();
+  const int H = p->ext.top + p->ext.bottom;
+  p->workers.resize(G);
+  for (int w = 0; w < G; ++w) {
+    auto& W = p->workers[w];
+    W.device = w % ndev;
+    W.r0 = t[w].first;
+    W.r1 = t[w].second;
+    SG_CUDA(cudaSetDevice(W.device));
+    SG_CUDA(cudaStreamCreateWithFlags(&W.stream, cudaStreamNonBlocking));
+    SG_CUDA(cudaEventCreateWithFlags(&W.done, cudaEventDisableTiming));
+    for (int k = 0; k < 2; ++k) SG_CUDA(cudaMalloc(&W.buf[k], (W.own() + H) * rowB));
+  }
+  // peer access between the devices in use (halo refreshes go over NVLink;
+  // without it cudaMemcpyPeerAsync stages through the host)
+  const int used = std::min(G, ndev);
+  for (int a = 0; a < used; ++a)
+    for (int b = 0; b < used; ++b) {
+      int can = 0;
+      if (a == b || cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess || !can) continue;
+      cudaSetDevice(a);
+      if (cudaDeviceEnablePeerAccess(b, 0) != cudaSuccess) cudaGetLastError();  // already enabled
+    }
+  SG_CUDA(cudaSetDevice(p->device));
+}
+
+// Slab launch descriptor of worker W: output rows in slab-local coordinates
+// (make_geom, stencil.cpp:26-40, restricted to the worker's rows).
+static sg_slab_desc worker_desc(const sg_plan_s* p, const sg_plan_s::Worker& W) {
+  sg_slab_desc d = full_grid_desc(p);
+  d.inRows = W.own() + p->ext.top + p->ext.bottom;
+  d.inShift = p->ext.top;
+  d.wrapY = 0;  // halos are explicit rows of the slab
+  const int g0 = std::max(W.r0, d.row0), g1 = std::min(W.r1, d.row1);
+  d.row0 = g0 - W.r0;
+  d.row1 = std::max(g1, g0) - W.r0;
+  return d;
+}
+
+// Global row held by ext row k of worker W (-1: outside a non-periodic grid).
+static int ext_global_row(const sg_plan_s* p, const sg_plan_s::Worker& W, int k) {
+  const int g = W.r0 - p->ext.top + k;
+  if (p->mode == SG_PERIODIC) return ((g % p->ny) + p->ny) % p->ny;
+  return g >= 0 && g < p->ny ? g : -1;
+}
+
+// H2D of ext rows [k0, k1) of worker W's slab `dst` from the host grid, as
+// contiguous runs of global rows (the periodic wrap splits a run).
+static void upload_ext_rows(const sg_plan_s* p, const sg_plan_s::Worker& W, const void* host, void* dst, int k0,
+                            int k1, cudaStream_t s) {
+  const size_t rowB = static_cast<size_t>(p->nx) * p->elem();
+  int k = k0;
+  while (k < k1) {
+    const int g = ext_global_row(p, W, k);
+    if (g < 0) {
+      ++k;
+      continue;
+    }
+    int len = 1;
+    while (k + len < k1 && ext_global_row(p, W, k + len) == g + len) ++len;
+    SG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + k * rowB, static_cast<const char*>(host) + g * rowB,
+                            len * rowB, cudaMemcpyHostToDevice, s));
+    k += len;
+  }
+}
+
+// Device-resident input: refresh every worker's halo rows of binding `k`
+// from the workers that own those rows (peer copies), after joining every
+// worker's previous work.
+static void refresh_halos(sg_plan_s* p, int k) {
+  const size_t rowB = static_cast<size_t>(p->nx) * p->elem();
+  const int top = p->ext.top, H = top + p->ext.bottom;
+  if (H == 0) return;
+  std::vector<int> owner(p->ny);
+  for (size_t u = 0; u < p->workers.size(); ++u)
+    for (int g = p->workers[u].r0; g < p->workers[u].r1; ++g) owner[g] = static_cast<int>(u);
+  for (auto& W : p->workers) {
+    SG_CUDA(cudaSetDevice(W.device));
+    for (auto& U : p->workers) SG_CUDA(cudaStreamWaitEvent(W.stream, U.done, 0));
+    for (int e = 0; e < W.own() + H; ++e) {
+      if (e >= top && e < top + W.own()) continue;  // own rows
+      const int g = ext_global_row(p, W, e);
+      if (g < 0) continue;
+      const auto& U = p->workers[owner[g]];
+      const char* src = static_cast<const char*>(U.buf[k]) + (top + g - U.r0) * rowB;
+      char* dst = static_cast<char*>(W.buf[k]) + e * rowB;
+      SG_CUDA(cudaMemcpyPeerAsync(dst, W.device, src, U.device, rowB, W.stream));
+    }
+    SG_CUDA(cudaEventRecord(W.done, W.stream));
+  }
+}
+
+// compute() of a multi-worker plan: every worker runs the stencil on its
+// slab on its own device and stream; the result is bitwise the single-GPU
+// one (same kernel arithmetic per point).
+static void compute_workers(sg_plan_s* p, sg_residency residency, cudaStream_t caller, int synchronize) {
+  const int ii = p->inIdx, oi = 1 - p->inIdx;
+  auto& in = p->buf[ii];
+  auto& out = p->buf[oi];
+  const bool periodic = p->mode == SG_PERIODIC;
+  const int top = p->ext.top, H = top + p->ext.bottom;
+  const size_t rowB = static_cast<size_t>(p->nx) * p->elem();
+  const bool uploadIn = !in.devValid || (residency == SG_RESIDENCY_HOST && in.hostValid);
+  if (uploadIn && !in.hostValid) sg::logic("compute: input has no valid copy");
+  // the frame of a non-periodic output keeps the caller's values
+  const bool uploadOut = !periodic && out.hostValid && (!out.devValid || residency == SG_RESIDENCY_HOST);
+  const bool download = residency == SG_RESIDENCY_HOST;
+  // order after the caller's stream (an event of the caller's device: the
+  // current device here; destruction is deferred until it completes)
+  int callerDev = p->device;
+  SG_CUDA(cudaGetDevice(&callerDev));
+  cudaEvent_t start;
+  SG_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  SG_CUDA(cudaEventRecord(start, caller));
+  if (!uploadIn && !in.halosValid) refresh_halos(p, ii);
+  // row-chunk pipeline on large grids: ~128 chunks over the whole grid
+  const int totalChunks = p->bytes() >= (64u << 20) ? 128 : 1;
+  const int G = static_cast<int>(p->workers.size());
+  for (auto& W : p->workers) {
+    SG_CUDA(cudaSetDevice(W.device));
+    SG_CUDA(cudaStreamWaitEvent(W.stream, start, 0));
+    for (auto& U : p->workers) SG_CUDA(cudaStreamWaitEvent(W.stream, U.done, 0));
+    const sg_slab_desc d0 = worker_desc(p, W);
+    char* din = static_cast<char*>(W.buf[ii]);
+    char* dout = static_cast<char*>(W.buf[oi]);
+    if (uploadOut)
+      SG_CUDA(cudaMemcpyAsync(dout + top * rowB, static_cast<const char*>(out.host) + W.r0 * rowB,
+                              W.own() * rowB, cudaMemcpyHostToDevice, W.stream));
+    const int outRows = d0.row1 - d0.row0;
+    int nch = uploadIn ? std::max(1, std::min(outRows, (totalChunks + G - 1) / G)) : 1;
+    if (nch > 1) {
+      if (!W.sH2D) SG_CUDA(cudaStreamCreateWithFlags(&W.sH2D, cudaStreamNonBlocking));
+      if (!W.sD2H) SG_CUDA(cudaStreamCreateWithFlags(&W.sD2H, cudaStreamNonBlocking));
+      while (W.ev.size() < 2 * static_cast<size_t>(nch) + 1) {
+        cudaEvent_t e;
+        SG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        W.ev.push_back(e);
+      }
+      cudaEvent_t* evUp = W.ev.data();
+      cudaEvent_t* evK = W.ev.data() + nch;
+      cudaEvent_t evGo = W.ev[2 * nch];
+      SG_CUDA(cudaEventRecord(evGo, W.stream));
+      SG_CUDA(cudaStreamWaitEvent(W.sH2D, evGo, 0));
+      SG_CUDA(cudaStreamWaitEvent(W.sD2H, evGo, 0));
+      int up = 0;  // ext rows uploaded so far
+      for (int c = 0; c < nch; ++c) {
+        const int a = d0.row0 + outRows * c / nch, b = d0.row0 + outRows * (c + 1) / nch;
+        // output row j reads ext rows j .. j + H
+        const int need = c == nch - 1 ? W.own() + H : b + H;
+        if (c == 0) up = 0;
+        if (need > up) upload_ext_rows(p, W, in.host, din, up, need, W.sH2D);
+        up = std::max(up, need);
+        SG_CUDA(cudaEventRecord(evUp[c], W.sH2D));
+        SG_CUDA(cudaStreamWaitEvent(W.stream, evUp[c], 0));
+        sg_slab_desc d = d0;
+        d.row0 = a;
+        d.row1 = b;
+        if (a < b) sg::launch_stencil(d, p->ext, p->fn, p->values.data(), p->values.size(), p->dtype, din,
+                                      dout + top * rowB, W.stream);
+        SG_CUDA(cudaEventRecord(evK[c], W.stream));
+        if (download && a < b) {
+          SG_CUDA(cudaStreamWaitEvent(W.sD2H, evK[c], 0));
+          SG_CUDA(cudaMemcpyAsync(static_cast<char*>(out.host) + (W.r0 + a) * rowB, dout + (top + a) * rowB,
+                                  (b - a) * rowB, cudaMemcpyDeviceToHost, W.sD2H));
+        }
+      }
+      SG_CUDA(cudaEventRecord(evK[0], W.sD2H));  // reuse: the D2H tail
+      SG_CUDA(cudaStreamWaitEvent(W.stream, evK[0], 0));
+      // rows outside [row0, row1) (the non-periodic frame rows) go back as
+      // uploaded: the whole own block is host-coherent
+      if (download && d0.row0 > 0)
+        SG_CUDA(cudaMemcpyAsync(static_cast<char*>(out.host) + W.r0 * rowB, dout + top * rowB,
+                                d0.row0 * rowB, cudaMemcpyDeviceToHost, W.stream));
+      if (download && d0.row1 < W.own())
+        SG_CUDA(cudaMemcpyAsync(static_cast<char*>(out.host) + (W.r0 + d0.row1) * rowB,
+                                dout + (top + d0.row1) * rowB, (W.own() - d0.row1) * rowB,
+                                cudaMemcpyDeviceToHost, W.stream));
+    } else {
+      if (uploadIn) upload_ext_rows(p, W, in.host, din, 0, W.own() + H, W.stream);
+      if (d0.row0 < d0.row1)
+        sg::launch_stencil(d0, p->ext, p->fn, p->values.data(), p->values.size(), p->dtype, din, dout + top * rowB,
+                           W.stream);
+      if (download)
+        SG_CUDA(cudaMemcpyAsync(static_cast<char*>(out.host) + W.r0 * rowB, dout + top * rowB, W.own() * rowB,
+                                cudaMemcpyDeviceToHost, W.stream));
+    }
+    SG_CUDA(cudaEventRecord(W.done, W.stream));
+  }
+  SG_CUDA(cudaSetDevice(callerDev));
+  SG_CUDA(cudaEventDestroy(start));
+  for (auto& W : p->workers) SG_CUDA(cudaStreamWaitEvent(caller, W.done, 0));
+  if (uploadIn) {
+    in.devValid = true;
+    in.halosValid = true;
+  } else {
+    in.halosValid = true;
+  }
+  out.devValid = true;
+  out.halosValid = false;
+  out.hostValid = download;
+  if (download || synchronize)
+    for (auto& W : p->workers) {
+      SG_CUDA(cudaSetDevice(W.device));
+      SG_CUDA(cudaStreamSynchronize(W.stream));
+    }
+  SG_CUDA(cudaSetDevice(p->device));
+}
+
+extern "C" {
+
 sg_status sg_plan_compute(sg_plan_t p, sg_residency residency, void* stream, int synchronize) {
   return guard([&] {
     if (!p || !p->valid) sg::logic("compute: plan was destroyed");
     SG_CUDA(cudaSetDevice(p->device));
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    if (!p->workers.empty()) {
+      int sdev = p->device;
+      if (stream && cudaStreamGetDevice(s, &sdev) == cudaSuccess && sdev != p->device)
+        SG_CUDA(cudaSetDevice(sdev));
+      compute_workers(p, residency, s, synchronize);
+      return;
+    }
     auto& in = p->buf[p->inIdx];
     auto& out = p->buf[1 - p->inIdx];
     if (in.dev == out.dev) sg::invalid("compute: bound grids alias");
@@ -460,6 +693,26 @@ sg_status sg_plan_sync_to_host(sg_plan_t p) {
   return guard([&] {
     if (!p || !p->valid) sg::logic("sync_to_host: plan was destroyed");
     if (p->memory != SG_MEM_HOST) return;
+    if (!p->workers.empty()) {
+      const size_t rowB = static_cast<size_t>(p->nx) * p->elem();
+      for (int k = 0; k < 2; ++k) {
+        auto& b = p->buf[k];
+        if (b.hostValid || !b.devValid) continue;
+        for (auto& W : p->workers) {
+          SG_CUDA(cudaSetDevice(W.device));
+          SG_CUDA(cudaMemcpyAsync(static_cast<char*>(b.host) + W.r0 * rowB,
+                                  static_cast<const char*>(W.buf[k]) + p->ext.top * rowB, W.own() * rowB,
+                                  cudaMemcpyDeviceToHost, W.stream));
+        }
+        b.hostValid = true;
+      }
+      for (auto& W : p->workers) {
+        SG_CUDA(cudaSetDevice(W.device));
+        SG_CUDA(cudaStreamSynchronize(W.stream));
+      }
+      SG_CUDA(cudaSetDevice(p->device));
+      return;
+    }
     SG_CUDA(cudaSetDevice(p->device));
     for (auto& b : p->buf)
       if (!b.hostValid && b.devValid) {
@@ -494,8 +747,37 @@ sg_status sg_plan_binding(sg_plan_t p, int which, void** host_ptr, void** device
 
 int sg_plan_valid(sg_plan_t p) { return p && p->valid ? 1 : 0; }
 
+sg_status sg_set_device_map(int mode) {
+  return guard([&] {
+    if (mode != 0 && mode != 1) sg::invalid("set_device_map: mode must be 0 (clip) or 1 (modulo)");
+    g_device_map.store(mode);
+  });
+}
+
+int sg_get_device_map(void) { return device_map(); }
+
+sg_status sg_plan_workers(sg_plan_t p, int* workers, int* devices, int* rowBegins, int* rowEnds, int capacity) {
+  return guard([&] {
+    if (!p || !p->valid) sg::logic("plan_workers: plan was destroyed");
+    const int G = p->workers.empty() ? 1 : static_cast<int>(p->workers.size());
+    if (workers) *workers = G;
+    for (int w = 0; w < G && w < capacity; ++w) {
+      const bool multi = !p->workers.empty();
+      if (devices) devices[w] = multi ? p->workers[w].device : p->device;
+      if (rowBegins) rowBegins[w] = multi ? p->workers[w].r0 : 0;
+      if (rowEnds) rowEnds[w] = multi ? p->workers[w].r1 : p->ny;
+    }
+  });
+}
+
 int sg_plan_kernel_kind(sg_plan_t p) {
   if (!p || !p->valid) return -1;
+  if (!p->workers.empty()) {
+    const auto& W = p->workers[0];
+    const size_t off = static_cast<size_t>(p->ext.top) * p->nx * p->elem();
+    return sg::stencil_kernel_kind(worker_desc(p, W), p->ext, p->fn, p->values.size(), p->dtype,
+                                   W.buf[p->inIdx], static_cast<char*>(W.buf[1 - p->inIdx]) + off);
+  }
   const sg_slab_desc d = full_grid_desc(p);
   return sg::stencil_kernel_kind(d, p->ext, p->fn, p->values.size(), p->dtype,
                                  p->buf[p->inIdx].dev, p->buf[1 - p->inIdx].dev);

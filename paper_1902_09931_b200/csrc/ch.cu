@@ -1462,6 +1462,263 @@ struct ChDist {
   }
 };
 
+// CHStepper(params, numTiles, numWorkers) with numWorkers = G > 1: the
+// distributed step (config 5's y-slabs) driven from ONE process over G GPUs
+// (worker w on device w % visible GPUs), each rank a ChDist with its own
+// stream. The P2P form stores the all-to-all blocks and halo rows straight
+// into the peers' buffers (cudaDeviceEnablePeerAccess, no IPC); the
+// barriers between phases are cross-device event joins. When the P2P
+// geometry does not fit, the copy-engine form runs: halos and the two
+// all-to-alls as cudaMemcpyPeerAsync blocks (the layout all_to_all_single
+// produces). Bitwise identical to the one-GPU stepper (same kernels).
+struct ChMulti {
+  sg_ch_params p{};
+  struct Rank {
+    std::unique_ptr<ChDist> d;
+    double* ext[2] = {nullptr, nullptr};  // time levels, (own + 4) x nx
+    double *send = nullptr, *ycol = nullptr, *recv = nullptr;  // copy-engine form
+    cudaEvent_t ev = nullptr;
+  };
+  std::vector<Rank> ranks;
+  int G = 1;
+  bool p2p = false;
+  bool halosValid = false;
+  int ic = 0;  // ext index of C^n
+  int step = 0;
+  double* gathered[2] = {nullptr, nullptr};  // full fields on rank 0's device (lazy)
+
+  static int workers_for(const sg_ch_params& q, int numWorkers) {
+    int ndev = 1;
+    SG_CUDA(cudaGetDeviceCount(&ndev));
+    int g = sg_get_device_map() == 1 ? numWorkers : std::min(numWorkers, ndev);
+    // nx, ny are powers of two: the largest power of two <= g with >= 2 rows
+    // per slab
+    int h = 1;
+    while (2 * h <= g && q.ny / (2 * h) >= 2 && q.nx % (2 * h) == 0) h *= 2;
+    return h;
+  }
+
+  void init(int g) {
+    G = g;
+    int ndev = 1;
+    SG_CUDA(cudaGetDeviceCount(&ndev));
+    ranks.resize(G);
+    for (int r = 0; r < G; ++r) {
+      SG_CUDA(cudaSetDevice(r % ndev));
+      auto& R = ranks[r];
+      R.d = std::make_unique<ChDist>();
+      R.d->p = p;
+      R.d->world = G;
+      R.d->rank = r;
+      R.d->init();
+      const size_t ext = static_cast<size_t>(R.d->own + 2 * HALO) * p.nx;
+      R.ext[0] = R.d->dalloc(ext);
+      R.ext[1] = R.d->dalloc(ext);
+      SG_CUDA(cudaEventCreateWithFlags(&R.ev, cudaEventDisableTiming));
+      k_init_slab_launch(p.seed, p.icAmplitude, p.nx, R.d->own, R.d->r0, R.ext[0], R.d->stream);
+      SG_CUDA(cudaMemcpyAsync(R.ext[1], R.ext[0], ext * sizeof(double), cudaMemcpyDeviceToDevice, R.d->stream));
+    }
+    const int used = std::min(G, ndev);
+    for (int a = 0; a < used; ++a)
+      for (int b = 0; b < used; ++b) {
+        int can = 0;
+        if (a == b || cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess || !can) continue;
+        cudaSetDevice(a);
+        if (cudaDeviceEnablePeerAccess(b, 0) != cudaSuccess) cudaGetLastError();  // already enabled
+      }
+    // P2P wiring: every rank's receive buffers, in rank order
+    std::vector<double*> rx(G), ry(G), yx(G), yy(G);
+    for (int r = 0; r < G; ++r) {
+      SG_CUDA(cudaSetDevice(ranks[r].d->device));
+      ranks[r].d->alloc_p2p();
+      rx[r] = ranks[r].d->recvX;
+      ry[r] = ranks[r].d->recvY;
+      yx[r] = ranks[r].d->y4xAll;
+      yy[r] = ranks[r].d->y4yAll;
+    }
+    sync_all();
+    p2p = rhs_kind() != 0;
+    for (int r = 0; p2p && r < G; ++r) {
+      SG_CUDA(cudaSetDevice(ranks[r].d->device));
+      p2p = ranks[r].d->set_peers(rx.data(), ry.data(), yx.data(), yy.data());
+    }
+    if (!p2p)
+      for (auto& R : ranks) {
+        SG_CUDA(cudaSetDevice(R.d->device));
+        const size_t slab = static_cast<size_t>(R.d->own) * p.nx;
+        R.send = R.d->dalloc(slab);
+        R.ycol = R.d->dalloc(static_cast<size_t>(p.ny) * R.d->nxq);
+        R.recv = R.d->dalloc(slab);
+      }
+    halosValid = false;
+    sync_all();
+  }
+
+  // every rank's stream waits for every rank's work so far
+  void barrier() {
+    for (auto& R : ranks) {
+      SG_CUDA(cudaSetDevice(R.d->device));
+      SG_CUDA(cudaEventRecord(R.ev, R.d->stream));
+    }
+    for (auto& R : ranks) {
+      SG_CUDA(cudaSetDevice(R.d->device));
+      for (auto& Q : ranks)
+        if (&Q != &R) SG_CUDA(cudaStreamWaitEvent(R.d->stream, Q.ev, 0));
+    }
+  }
+
+  void sync_all() {
+    for (auto& R : ranks) {
+      SG_CUDA(cudaSetDevice(R.d->device));
+      SG_CUDA(cudaStreamSynchronize(R.d->stream));
+    }
+  }
+
+  // 2 halo rows each way of time level k from the ring neighbours' own rows
+  void exchange_halos(int k) {
+    const size_t rowB = static_cast<size_t>(p.nx) * sizeof(double);
+    for (int r = 0; r < G; ++r) {
+      auto& R = ranks[r];
+      const auto& U = ranks[(r + G - 1) % G];
+      const auto& D = ranks[(r + 1) % G];
+      SG_CUDA(cudaSetDevice(R.d->device));
+      const int own = R.d->own;
+      SG_CUDA(cudaMemcpyPeerAsync(R.ext[k], R.d->device, U.ext[k] + static_cast<size_t>(U.d->own) * p.nx,
+                                  U.d->device, HALO * rowB, R.d->stream));
+      SG_CUDA(cudaMemcpyPeerAsync(R.ext[k] + static_cast<size_t>(own + HALO) * p.nx, R.d->device,
+                                  D.ext[k] + static_cast<size_t>(HALO) * p.nx, D.d->device, HALO * rowB,
+                                  R.d->stream));
+    }
+  }
+
+  // all-to-all of packed blocks (own x nxq): dst_q block r <- src_r block q
+  void alltoall(double* Rank::*src, double* Rank::*dst) {
+    const size_t blk = static_cast<size_t>(ranks[0].d->own) * ranks[0].d->nxq;
+    for (int q = 0; q < G; ++q) {
+      auto& Q = ranks[q];
+      SG_CUDA(cudaSetDevice(Q.d->device));
+      for (int r = 0; r < G; ++r) {
+        const auto& R = ranks[r];
+        SG_CUDA(cudaMemcpyPeerAsync(Q.*dst + r * blk, Q.d->device, R.*src + q * blk, R.d->device,
+                                    blk * sizeof(double), Q.d->stream));
+      }
+    }
+  }
+
+  void one_step() {
+    const int ip = 1 - ic;
+    if (p2p) {
+      if (!halosValid) {
+        exchange_halos(ic);
+        exchange_halos(ip);
+        barrier();
+        halosValid = true;
+      }
+      for (auto& R : ranks) {
+        SG_CUDA(cudaSetDevice(R.d->device));
+        R.d->phase_x_p2p(R.ext[ic], R.ext[ip], R.d->stream);
+      }
+      barrier();
+      for (auto& R : ranks) {
+        SG_CUDA(cudaSetDevice(R.d->device));
+        R.d->phase_y_p2p(R.d->stream);
+      }
+      barrier();
+      for (int r = 0; r < G; ++r) {
+        auto& R = ranks[r];
+        SG_CUDA(cudaSetDevice(R.d->device));
+        // C^{n+1} over C^{n-1}; its first / last two rows also land in the
+        // up / down neighbours' halo rows of that level
+        R.d->combine_p2p(R.ext[ic], R.ext[ip], ranks[(r + G - 1) % G].ext[ip], ranks[(r + 1) % G].ext[ip],
+                         R.d->stream);
+      }
+      barrier();
+    } else {
+      exchange_halos(ic);
+      exchange_halos(ip);
+      barrier();
+      for (auto& R : ranks) {
+        SG_CUDA(cudaSetDevice(R.d->device));
+        ch_phase_x(p, R.d->rp, R.d->fx.t, R.d->own, R.d->nxq, R.ext[ic], R.ext[ip], R.d->rhsT, R.d->y4x, R.send,
+                   R.d->stream);
+      }
+      barrier();
+      alltoall(&Rank::send, &Rank::ycol);
+      barrier();
+      for (auto& R : ranks) {
+        SG_CUDA(cudaSetDevice(R.d->device));
+        penta_sweep(R.d->fy.t, R.d->nxq, p.ny, R.ycol, R.d->ybuf, true, false, R.d->stream);
+      }
+      barrier();
+      alltoall(&Rank::ycol, &Rank::recv);
+      barrier();
+      for (auto& R : ranks) {
+        SG_CUDA(cudaSetDevice(R.d->device));
+        ch_combine_packed(p.nx, R.d->own, R.d->nxq, R.ext[ic], R.ext[ip], R.recv, R.d->stream);
+      }
+      barrier();
+    }
+    ic = ip;
+    ++step;
+  }
+
+  void run(int steps) {
+    for (int k = 0; k < steps; ++k) one_step();
+  }
+
+  // rows of C^n (which 0) / C^{n-1} (which 1) into a full row-major field
+  // (host or device memory; cudaMemcpyDefault resolves either)
+  void gather_into(int which, double* out) {
+    const int k = which == 0 ? ic : 1 - ic;
+    const size_t rowB = static_cast<size_t>(p.nx) * sizeof(double);
+    for (auto& R : ranks) {
+      SG_CUDA(cudaSetDevice(R.d->device));
+      SG_CUDA(cudaMemcpyAsync(out + static_cast<size_t>(R.d->r0) * p.nx, R.ext[k] + HALO * p.nx,
+                              R.d->own * rowB, cudaMemcpyDefault, R.d->stream));
+    }
+    sync_all();
+  }
+
+  double* device_field(int which) {
+    auto& R0 = ranks[0];
+    SG_CUDA(cudaSetDevice(R0.d->device));
+    if (!gathered[which]) gathered[which] = R0.d->dalloc(static_cast<size_t>(p.nx) * p.ny);
+    gather_into(which, gathered[which]);
+    return gathered[which];
+  }
+
+  void set_state(const double* curr, const double* prev) {
+    sync_all();
+    const size_t rowB = static_cast<size_t>(p.nx) * sizeof(double);
+    ic = 0;
+    for (auto& R : ranks) {
+      SG_CUDA(cudaSetDevice(R.d->device));
+      for (int k = 0; k < 2; ++k) {
+        const double* src = k == 0 ? curr : prev;
+        SG_CUDA(cudaMemcpyAsync(R.ext[k] + HALO * p.nx, src + static_cast<size_t>(R.d->r0) * p.nx,
+                                R.d->own * rowB, cudaMemcpyDefault, R.d->stream));
+      }
+    }
+    barrier();
+    halosValid = false;
+    if (!p2p) return;
+    exchange_halos(0);
+    exchange_halos(1);
+    barrier();
+    halosValid = true;
+    sync_all();
+  }
+
+  ~ChMulti() {
+    for (auto& R : ranks) {
+      if (!R.d) continue;
+      cudaSetDevice(R.d->device);
+      if (R.d->stream) cudaStreamSynchronize(R.d->stream);
+      if (R.ev) cudaEventDestroy(R.ev);
+    }
+  }
+};
+
 }  // namespace sg
 
 struct sg_chd_s {
@@ -1469,7 +1726,8 @@ struct sg_chd_s {
 };
 
 struct sg_ch_s {
-  std::unique_ptr<sg::ChState> st;
+  std::unique_ptr<sg::ChState> st;   // one GPU
+  std::unique_ptr<sg::ChMulti> mul;  // numWorkers -> GPUs
 };
 
 struct sg_penta_s {
@@ -1544,9 +1802,21 @@ sg_status sg_ch_create(const sg_ch_params* p, int numTiles, int numWorkers, sg_c
     if (numWorkers < 1) sg::invalid("WorkerPool: workers must be >= 1");
     require_device2();
     auto h = std::make_unique<sg_ch_s>();
-    h->st = std::make_unique<sg::ChState>();
-    h->st->p = *p;
-    h->st->init();
+    // numWorkers -> GPUs: G > 1 runs config 5's distributed step
+    // over G devices from this process; G = 1 keeps the fused one-GPU step
+    const int G = sg::ChMulti::workers_for(*p, numWorkers);
+    if (G > 1) {
+      int dev = 0;
+      SG_CUDA(cudaGetDevice(&dev));
+      h->mul = std::make_unique<sg::ChMulti>();
+      h->mul->p = *p;
+      h->mul->init(G);
+      SG_CUDA(cudaSetDevice(dev));
+    } else {
+      h->st = std::make_unique<sg::ChState>();
+      h->st->p = *p;
+      h->st->init();
+    }
     *ch = h.release();
   });
 }
@@ -1554,6 +1824,10 @@ sg_status sg_ch_create(const sg_ch_params* p, int numTiles, int numWorkers, sg_c
 sg_status sg_ch_step(sg_ch_t ch, int steps) {
   return guard2([&] {
     if (!ch) sg::logic("CHStepper: destroyed");
+    if (ch->mul) {
+      ch->mul->run(steps);
+      return;
+    }
     SG_CUDA(cudaSetDevice(ch->st->device));
     ch->st->run(steps);
   });
@@ -1562,6 +1836,11 @@ sg_status sg_ch_step(sg_ch_t ch, int steps) {
 sg_status sg_ch_set_state(sg_ch_t ch, const double* curr, const double* prev, sg_memory memory) {
   return guard2([&] {
     if (!ch) sg::logic("CHStepper: destroyed");
+    if (ch->mul) {
+      ch->mul->set_state(curr, prev);
+      ch->mul->step = 0;  // cahn_hilliard.cpp:256-257
+      return;
+    }
     auto& s = *ch->st;
     SG_CUDA(cudaSetDevice(s.device));
     const size_t bytes = static_cast<size_t>(s.p.nx) * s.p.ny * sizeof(double);
@@ -1578,6 +1857,10 @@ sg_status sg_ch_set_state(sg_ch_t ch, const double* curr, const double* prev, sg
 sg_status sg_ch_get_field(sg_ch_t ch, int which, double* out, sg_memory memory) {
   return guard2([&] {
     if (!ch) sg::logic("CHStepper: destroyed");
+    if (ch->mul) {
+      ch->mul->gather_into(which == 0 ? 0 : 1, out);
+      return;
+    }
     auto& s = *ch->st;
     SG_CUDA(cudaSetDevice(s.device));
     const size_t bytes = static_cast<size_t>(s.p.nx) * s.p.ny * sizeof(double);
@@ -1591,6 +1874,10 @@ sg_status sg_ch_get_field(sg_ch_t ch, int which, double* out, sg_memory memory) 
 sg_status sg_ch_device_field(sg_ch_t ch, int which, const double** dptr) {
   return guard2([&] {
     if (!ch) sg::logic("CHStepper: destroyed");
+    if (ch->mul) {  // a gathered copy on worker 0's GPU, valid until the next call
+      *dptr = ch->mul->device_field(which == 0 ? 0 : 1);
+      return;
+    }
     auto& s = *ch->st;
     SG_CUDA(cudaStreamSynchronize(s.stream));
     *dptr = which == 0 ? s.cur() : s.prev();
@@ -1600,22 +1887,34 @@ sg_status sg_ch_device_field(sg_ch_t ch, int which, const double** dptr) {
 sg_status sg_ch_status(sg_ch_t ch, int* step, double* time) {
   return guard2([&] {
     if (!ch) sg::logic("CHStepper: destroyed");
-    if (step) *step = ch->st->step;
-    if (time) *time = static_cast<double>(ch->st->step) * ch->st->p.dt;  // cahn_hilliard.cpp:327
+    const int k = ch->mul ? ch->mul->step : ch->st->step;
+    const double dt = ch->mul ? ch->mul->p.dt : ch->st->p.dt;
+    if (step) *step = k;
+    if (time) *time = static_cast<double>(k) * dt;  // cahn_hilliard.cpp:327
   });
 }
 
 sg_status sg_ch_diagnostics(sg_ch_t ch, double* t, double* s, double* k1Inv) {
   return guard2([&] {
     if (!ch) sg::logic("CHStepper: destroyed");
-    auto& st = *ch->st;
-    SG_CUDA(cudaSetDevice(st.device));
-    // queued behind the pending steps on the stepper's own stream
-    const double* f = st.cur();
-    const double dx = st.p.lx / st.p.nx, dy = st.p.ly / st.p.ny;
-    if (t) *t = static_cast<double>(st.step) * st.p.dt;
+    const sg_ch_params& P = ch->mul ? ch->mul->p : ch->st->p;
+    const int k = ch->mul ? ch->mul->step : ch->st->step;
+    const double* f = nullptr;
+    cudaStream_t stream = nullptr;
+    if (ch->mul) {  // gathered onto worker 0's GPU
+      f = ch->mul->device_field(0);
+      stream = ch->mul->ranks[0].d->stream;
+      SG_CUDA(cudaSetDevice(ch->mul->ranks[0].d->device));
+    } else {
+      SG_CUDA(cudaSetDevice(ch->st->device));
+      // queued behind the pending steps on the stepper's own stream
+      f = ch->st->cur();
+      stream = ch->st->stream;
+    }
+    const double dx = P.lx / P.nx, dy = P.ly / P.ny;
+    if (t) *t = static_cast<double>(k) * P.dt;
     double r[3];  // <C^2>, k1 num, k1 den
-    sg::device_ch_diagnostics(f, st.p.nx, st.p.ny, dx, dy, r, st.stream);
+    sg::device_ch_diagnostics(f, P.nx, P.ny, dx, dy, r, stream);
     const double m2 = r[0];
     if (m2 >= 1.0 - 1e-12) throw sg::Error(SG_ERR_DOMAIN, "s_metric: mixture saturated, <C^2> reached 1");
     if (s) *s = 1.0 / (1.0 - m2);
@@ -1625,11 +1924,34 @@ sg_status sg_ch_diagnostics(sg_ch_t ch, double* t, double* s, double* k1Inv) {
   });
 }
 
+sg_status sg_ch_synchronize(sg_ch_t ch) {
+  return guard2([&] {
+    if (!ch) sg::logic("CHStepper: destroyed");
+    if (ch->mul) {
+      ch->mul->sync_all();
+      return;
+    }
+    SG_CUDA(cudaSetDevice(ch->st->device));
+    SG_CUDA(cudaStreamSynchronize(ch->st->stream));
+  });
+}
+
+sg_status sg_ch_workers(sg_ch_t ch, int* workers, int* p2p) {
+  return guard2([&] {
+    if (!ch) sg::logic("CHStepper: destroyed");
+    if (workers) *workers = ch->mul ? ch->mul->G : 1;
+    if (p2p) *p2p = ch->mul ? (ch->mul->p2p ? 1 : 0) : 0;
+  });
+}
+
 sg_status sg_ch_set_step(sg_ch_t ch, int step) {
   return guard2([&] {
     if (!ch) sg::logic("CHStepper: destroyed");
     if (step < 0) sg::invalid("CHStepper: step must be >= 0");
-    ch->st->step = step;
+    if (ch->mul)
+      ch->mul->step = step;
+    else
+      ch->st->step = step;
   });
 }
 

@@ -184,6 +184,15 @@ class StencilPlan:
     def kernel_kind(self) -> int:
         return _lib.lib().sg_plan_kernel_kind(self._h)
 
+    def workers(self):
+        """[(device, row_begin, row_end)] of the plan's workers (numWorkers
+        -> GPUs for host grids; one entry for a one-GPU plan)."""
+        n = C.c_int()
+        check(_lib.lib().sg_plan_workers(self._h, C.byref(n), None, None, None, 0))
+        dev, b, e = ((C.c_int * n.value)() for _ in range(3))
+        check(_lib.lib().sg_plan_workers(self._h, C.byref(n), dev, b, e, n.value))
+        return [(dev[k], b[k], e[k]) for k in range(n.value)]
+
     def destroy(self):
         if self._h.value:
             check(_lib.lib().sg_plan_destroy(C.byref(self._h)))
@@ -195,6 +204,20 @@ class StencilPlan:
             self.destroy()
         except Exception:
             pass
+
+
+def set_device_map(mode: str) -> None:
+    """How numWorkers maps to GPUs (sg_set_device_map): "clip" (default) —
+    min(numWorkers, visible GPUs) workers; "modulo" — numWorkers workers,
+    worker w on GPU w % visible GPUs (tests on a one-GPU box)."""
+    modes = {"clip": 0, "modulo": 1}
+    if mode not in modes:
+        raise InvalidArgument("set_device_map: mode must be 'clip' or 'modulo'")
+    check(_lib.lib().sg_set_device_map(modes[mode]))
+
+
+def get_device_map() -> str:
+    return ("clip", "modulo")[_lib.lib().sg_get_device_map()]
 
 
 def make_tiles(ny: int, num_tiles: int):

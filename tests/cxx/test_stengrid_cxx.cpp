@@ -314,16 +314,74 @@ void test_tiles_frame_shift_concurrency() {  // test_stencil.cpp:390-555
   CHECK(grids_equal_bitwise(outB, refB));
 }
 
-void test_residency() {  // test_stencil.cpp:515-525 (+ explicit sync for Device)
+void test_residency() {  // test_stencil.cpp:515-525: the hint does not change results
   Grid2D in = random_grid(8, 8, 151);
   Grid2D outH(8, 8, in.dx, in.dy), outD(8, 8, in.dx, in.dy);
   const WeightStencil ws{Extents{1, 1, 1, 1}, random_weights(9, 152)};
   StencilPlan ph = create_plan(Direction::XY, BoundaryMode::Periodic, ws, in, outH, 1, 1);
   StencilPlan pd = create_plan(Direction::XY, BoundaryMode::Periodic, ws, in, outD, 1, 1);
   compute(ph, Residency::Host);
-  compute(pd, Residency::Device);
-  sync_to_host(pd);
+  compute(pd, Residency::Device);  // host-coherent on return, no sync needed
   CHECK(grids_equal_bitwise(outH, outD));
+  // a second plan reading the Device-hint output sees the fresh host values
+  Grid2D out2(8, 8, in.dx, in.dy), out3(8, 8, in.dx, in.dy);
+  StencilPlan p2 = create_plan(Direction::XY, BoundaryMode::Periodic, ws, outD, out2, 1, 1);
+  StencilPlan p3 = create_plan(Direction::XY, BoundaryMode::Periodic, ws, outH, out3, 1, 1);
+  compute(p2);
+  compute(p3);
+  CHECK(grids_equal_bitwise(out2, out3));
+  // the extension: compute_deferred chains stay in HBM until sync_to_host
+  Grid2D a = random_grid(16, 12, 153), b(16, 12, a.dx, a.dy);
+  Grid2D a2 = a, b2(16, 12, a.dx, a.dy);
+  StencilPlan pc = create_plan(Direction::XY, BoundaryMode::Periodic, ws, a, b, 1, 1);
+  StencilPlan ps = create_plan(Direction::XY, BoundaryMode::Periodic, ws, a2, b2, 1, 1);
+  for (int k = 0; k < 3; ++k) {
+    compute_deferred(pc);
+    swap_plan(pc);
+    compute(ps);
+    swap_plan(ps);
+  }
+  sync_to_host(pc);
+  CHECK(grids_equal_bitwise(*pc.input(), *ps.input()));
+}
+
+void test_workers_to_gpus() {  // numWorkers -> GPUs; test_stencil.cpp:390-409
+  // SG_DEVICE_MAP=modulo (set by tests/test_cxx_gpu.py): G workers on a
+  // one-GPU box share the device; the multi-worker path still runs
+  const Grid2D in0 = random_grid(64, 40, 161);
+  const FunctionStencil fs{Extents{1, 1, 1, 1}, functions::fn_weighted_3x3, random_weights(9, 162)};
+  const WeightStencil tall{Extents{1, 2, 3, 1}, random_weights(20, 163)};
+  for (const bool periodic : {true, false}) {
+    const BoundaryMode mode = periodic ? BoundaryMode::Periodic : BoundaryMode::NonPeriodic;
+    std::vector<Grid2D> outs;
+    for (const int workers : {1, 2, 4, 8}) {
+      Grid2D in = in0, out(64, 40, in0.dx, in0.dy);
+      StencilPlan p = create_plan(Direction::XY, mode, fs, in, out, 1, workers);
+      compute(p);
+      swap_plan(p);
+      compute_deferred(p);
+      swap_plan(p);
+      compute_deferred(p);
+      sync_to_host(p);
+      StencilPlan q = create_plan(Direction::XY, mode, tall, out, in, 1, workers);
+      compute(q);
+      outs.push_back(in);
+    }
+    for (std::size_t k = 1; k < outs.size(); ++k) CHECK(grids_equal_bitwise(outs[0], outs[k]));
+  }
+  // CHStepper(p, 1, numWorkers): the distributed step over numWorkers GPUs
+  CHParams prm;
+  prm.nx = prm.ny = 256;
+  prm.dt = 0.1 * prm.dx();
+  prm.T = 1.0;
+  std::vector<Grid2D> fields;
+  for (const int workers : {1, 2, 4, 8}) {
+    CHStepper st(prm, 1, workers);
+    for (int k = 0; k < 7; ++k) st.step();
+    fields.push_back(st.field());
+    fields.push_back(st.previous_field());
+  }
+  for (std::size_t k = 2; k < fields.size(); ++k) CHECK(grids_equal_bitwise(fields[k % 2], fields[k]));
 }
 
 void test_acceptance_criterion_2() {  // acceptance.cpp:104-151
@@ -558,6 +616,7 @@ int main() {
   test_identity_cross_weightsfn();
   test_tiles_frame_shift_concurrency();
   test_residency();
+  test_workers_to_gpus();
   test_acceptance_criterion_2();
   test_penta();
   test_ch();

@@ -2,6 +2,7 @@
 
 The C++ file restates the reference's own doctest cases against the
 drop-in headers include/stengrid/*.hpp linked to libstengrid_b200.so."""
+import os
 import subprocess
 
 import pytest
@@ -19,7 +20,10 @@ def test_cxx_dropin_compiles():
 @pytest.mark.gpu
 def test_cxx_dropin_suite_passes_on_gpu():
     exe = b.build_cxx_tests()
-    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    # several workers per GPU on a one-GPU box: numWorkers still maps to
+    # the multi-GPU path (test_workers_to_gpus)
+    env = dict(os.environ, SG_DEVICE_MAP="modulo")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600, env=env)
     print(r.stdout[-4000:], r.stderr[-2000:])
     assert r.returncode == 0, r.stdout[-4000:]
     assert "0 failed" in r.stdout
