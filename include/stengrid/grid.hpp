@@ -100,25 +100,30 @@ class DenseVector {
 using Array2d = DenseArray2<double>;
 using ArrayXd = DenseVector<double>;
 
-/// grid.hpp:25-49 — a uniform 2D field of doubles; (i, j) at values(j, i).
-struct Grid2D {
+/// grid.hpp:25-49 — a uniform 2D field; (i, j) at values(j, i). The
+/// reference stores doubles only (grid.hpp:13); BasicGrid2D<float> (Grid2Df)
+/// is this library's FP32 extension (north_star: FP32+FP64 stencils), accepted
+/// by create_plan / compute / swap_plan like Grid2D.
+template <typename T>
+struct BasicGrid2D {
+  using value_type = T;
   int nx = 0;
   int ny = 0;
   double dx = 1.0;
   double dy = 1.0;
-  Array2d values;
+  DenseArray2<T> values;
 
-  Grid2D() = default;
-  Grid2D(int nx_, int ny_, double dx_, double dy_) : nx(nx_), ny(ny_), dx(dx_), dy(dy_) {
+  BasicGrid2D() = default;
+  BasicGrid2D(int nx_, int ny_, double dx_, double dy_) : nx(nx_), ny(ny_), dx(dx_), dy(dy_) {
     if (nx < 1 || ny < 1) throw std::invalid_argument("Grid2D: nx and ny must be >= 1");
     if (!(dx > 0.0) || !(dy > 0.0)) throw std::invalid_argument("Grid2D: dx and dy must be > 0");
     values.setZero(ny, nx);
     detail::note_large_alloc();
   }
-  Grid2D(const Grid2D& o) : nx(o.nx), ny(o.ny), dx(o.dx), dy(o.dy), values(o.values) {
+  BasicGrid2D(const BasicGrid2D& o) : nx(o.nx), ny(o.ny), dx(o.dx), dy(o.dy), values(o.values) {
     if (values.size() > 0) detail::note_large_alloc();
   }
-  Grid2D& operator=(const Grid2D& o) {
+  BasicGrid2D& operator=(const BasicGrid2D& o) {
     if (this == &o) return *this;
     if (values.size() != o.values.size() && o.values.size() > 0) detail::note_large_alloc();
     nx = o.nx;
@@ -128,16 +133,19 @@ struct Grid2D {
     values = o.values;
     return *this;
   }
-  Grid2D(Grid2D&&) noexcept = default;
-  Grid2D& operator=(Grid2D&&) noexcept = default;
+  BasicGrid2D(BasicGrid2D&&) noexcept = default;
+  BasicGrid2D& operator=(BasicGrid2D&&) noexcept = default;
 
-  double operator()(int i, int j) const { return values(j, i); }
-  double& operator()(int i, int j) { return values(j, i); }
-  const double* data() const { return values.data(); }
-  double* data() { return values.data(); }
+  T operator()(int i, int j) const { return values(j, i); }
+  T& operator()(int i, int j) { return values(j, i); }
+  const T* data() const { return values.data(); }
+  T* data() { return values.data(); }
   std::ptrdiff_t size() const { return static_cast<std::ptrdiff_t>(nx) * ny; }
-  bool same_shape(const Grid2D& o) const { return nx == o.nx && ny == o.ny; }
+  bool same_shape(const BasicGrid2D& o) const { return nx == o.nx && ny == o.ny; }
 };
+
+using Grid2D = BasicGrid2D<double>;
+using Grid2Df = BasicGrid2D<float>;
 
 /// grid.hpp:53-62
 struct Extents {

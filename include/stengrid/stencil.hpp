@@ -123,16 +123,32 @@ inline int device_function_id(StencilFunction fn) {
 }
 
 /// stencil.hpp:42-85 — movable, not copyable; never owns the fields.
-class StencilPlan;
+/// BasicStencilPlan<double> is the reference's StencilPlan; the float
+/// instantiation (StencilPlanF) binds Grid2Df fields and runs the FP32 kernels.
+template <typename T>
+class BasicStencilPlan;
 namespace detail {
-inline void compute_impl(StencilPlan& plan, bool hostCoherent);
-}
+template <typename T>
+void compute_impl(BasicStencilPlan<T>& plan, bool hostCoherent);
+template <typename T>
+struct dtype_of;
+template <>
+struct dtype_of<double> {
+  static constexpr sg_dtype value = SG_F64;
+};
+template <>
+struct dtype_of<float> {
+  static constexpr sg_dtype value = SG_F32;
+};
+}  // namespace detail
 
-class StencilPlan {
+template <typename T>
+class BasicStencilPlan {
  public:
-  StencilPlan() = default;
-  StencilPlan(StencilPlan&& o) noexcept { *this = std::move(o); }
-  StencilPlan& operator=(StencilPlan&& o) noexcept {
+  using grid_type = BasicGrid2D<T>;
+  BasicStencilPlan() = default;
+  BasicStencilPlan(BasicStencilPlan&& o) noexcept { *this = std::move(o); }
+  BasicStencilPlan& operator=(BasicStencilPlan&& o) noexcept {
     if (this != &o) {
       destroy();
       h_ = o.h_;
@@ -153,9 +169,9 @@ class StencilPlan {
     }
     return *this;
   }
-  StencilPlan(const StencilPlan&) = delete;
-  StencilPlan& operator=(const StencilPlan&) = delete;
-  ~StencilPlan() { destroy(); }
+  BasicStencilPlan(const BasicStencilPlan&) = delete;
+  BasicStencilPlan& operator=(const BasicStencilPlan&) = delete;
+  ~BasicStencilPlan() { destroy(); }
 
   bool valid() const { return input_ != nullptr; }
   Direction direction() const { return direction_; }
@@ -163,8 +179,8 @@ class StencilPlan {
   const Extents& extents() const { return ext_; }
   const TilePlan& tiles() const { return tiles_; }
   int num_workers() const { return numWorkers_; }
-  const Grid2D* input() const { return input_; }
-  const Grid2D* output() const { return output_; }
+  const grid_type* input() const { return input_; }
+  const grid_type* output() const { return output_; }
 
   /// stencil.cpp:186-193 — idempotent; never touches the grids.
   void destroy() {
@@ -175,12 +191,12 @@ class StencilPlan {
     tiles_ = TilePlan{};
   }
 
+  // Internals used by the free functions below (create_plan, swap_plan,
+  // compute, sync_to_host); not part of the reference API.
+  struct Access;
+
  private:
-  friend StencilPlan create_plan(Direction, BoundaryMode, StencilKind, Grid2D&, Grid2D&, int, int,
-                                 WorkerPool*);
-  friend void swap_plan(StencilPlan&);
-  friend void detail::compute_impl(StencilPlan&, bool);
-  friend void sync_to_host(StencilPlan&);
+  friend struct Access;
 
   // (Re)bind the C plan to the grids' current host buffers.
   void bind() {
@@ -198,8 +214,8 @@ class StencilPlan {
     const sg_extents e{ext_.left, ext_.right, ext_.top, ext_.bottom};
     detail::check(sg_plan_create(static_cast<sg_direction>(direction_),
                                  mode_ == BoundaryMode::Periodic ? SG_PERIODIC : SG_NONPERIODIC, e,
-                                 static_cast<sg_function>(fnId_), vals, count, SG_F64, input_->data(),
-                                 output_->data(), input_->nx, input_->ny, SG_MEM_HOST, numTiles_,
+                                 static_cast<sg_function>(fnId_), vals, count, detail::dtype_of<T>::value,
+                                 input_->data(), output_->data(), input_->nx, input_->ny, SG_MEM_HOST, numTiles_,
                                  numWorkers_, &h_));
     boundIn_ = input_->data();
     boundOut_ = output_->data();
@@ -211,19 +227,46 @@ class StencilPlan {
   Extents ext_;
   StencilKind kind_;
   TilePlan tiles_;
-  Grid2D* input_ = nullptr;
-  Grid2D* output_ = nullptr;
+  grid_type* input_ = nullptr;
+  grid_type* output_ = nullptr;
   int numWorkers_ = 1;
   int numTiles_ = 1;
   int fnId_ = SG_FN_NONE;
-  const double* boundIn_ = nullptr;
-  const double* boundOut_ = nullptr;
+  const T* boundIn_ = nullptr;
+  const T* boundOut_ = nullptr;
 };
 
-/// stencil.hpp:90-92 / stencil.cpp:152-184.
-inline StencilPlan create_plan(Direction direction, BoundaryMode mode, StencilKind kind, Grid2D& input,
-                               Grid2D& output, int numTiles, int numWorkers,
-                               WorkerPool* sharedPool = nullptr) {
+template <typename T>
+struct BasicStencilPlan<T>::Access {
+  static sg_plan_t& handle(BasicStencilPlan& p) { return p.h_; }
+  static void bind(BasicStencilPlan& p) { p.bind(); }
+  static grid_type*& input(BasicStencilPlan& p) { return p.input_; }
+  static grid_type*& output(BasicStencilPlan& p) { return p.output_; }
+  static const T*& bound_in(BasicStencilPlan& p) { return p.boundIn_; }
+  static const T*& bound_out(BasicStencilPlan& p) { return p.boundOut_; }
+  static void init(BasicStencilPlan& p, Direction d, BoundaryMode m, StencilKind&& kind, grid_type& in,
+                   grid_type& out, int numTiles, int numWorkers, int fnId) {
+    p.direction_ = d;
+    p.mode_ = m;
+    p.ext_ = std::visit([](const auto& s) { return s.ext; }, kind);
+    p.kind_ = std::move(kind);
+    p.input_ = &in;
+    p.output_ = &out;
+    p.numWorkers_ = numWorkers;
+    p.numTiles_ = numTiles;
+    p.fnId_ = fnId;
+  }
+  static void set_tiles(BasicStencilPlan& p, TilePlan&& t) { p.tiles_ = std::move(t); }
+};
+
+using StencilPlan = BasicStencilPlan<double>;
+using StencilPlanF = BasicStencilPlan<float>;
+
+namespace detail {
+template <typename T>
+BasicStencilPlan<T> create_plan_impl(Direction direction, BoundaryMode mode, StencilKind kind, BasicGrid2D<T>& input,
+                                     BasicGrid2D<T>& output, int numTiles, int numWorkers, WorkerPool* sharedPool) {
+  using A = typename BasicStencilPlan<T>::Access;
   if (!input.same_shape(output)) throw std::invalid_argument("create_plan: input and output shapes differ");
   if (&input == &output || input.data() == output.data())
     throw std::invalid_argument("create_plan: input and output must be distinct buffers");
@@ -236,34 +279,52 @@ inline StencilPlan create_plan(Direction direction, BoundaryMode mode, StencilKi
   }
   if (numWorkers >= 1 && sharedPool != nullptr && sharedPool->workers() != numWorkers)
     throw std::invalid_argument("create_plan: shared pool size does not match numWorkers");
-  StencilPlan plan;
-  plan.direction_ = direction;
-  plan.mode_ = mode;
-  plan.ext_ = std::visit([](const auto& s) { return s.ext; }, kind);
-  plan.kind_ = std::move(kind);
-  plan.input_ = &input;
-  plan.output_ = &output;
-  plan.numWorkers_ = numWorkers;
-  plan.numTiles_ = numTiles;
-  plan.fnId_ = fnId < 0 ? -1 : fnId;  // -1: null function -> invalid_argument from the ABI
+  BasicStencilPlan<T> plan;
+  // fnId -1: null function -> invalid_argument from the ABI
+  A::init(plan, direction, mode, std::move(kind), input, output, numTiles, numWorkers, fnId < 0 ? -1 : fnId);
   try {
-    plan.bind();  // full validation (stencil.cpp:128-161) happens in the C ABI
+    A::bind(plan);  // full validation (stencil.cpp:128-161) happens in the C ABI
   } catch (...) {
-    plan.input_ = plan.output_ = nullptr;
+    A::input(plan) = A::output(plan) = nullptr;
     throw;
   }
-  plan.tiles_ = make_tiles(input.ny, numTiles, plan.ext_);
+  A::set_tiles(plan, make_tiles(input.ny, numTiles, plan.extents()));
   return plan;
 }
+}  // namespace detail
 
-inline void destroy_plan(StencilPlan& plan) { plan.destroy(); }
+/// stencil.hpp:90-92 / stencil.cpp:152-184.
+inline StencilPlan create_plan(Direction direction, BoundaryMode mode, StencilKind kind, Grid2D& input,
+                               Grid2D& output, int numTiles, int numWorkers,
+                               WorkerPool* sharedPool = nullptr) {
+  return detail::create_plan_impl<double>(direction, mode, std::move(kind), input, output, numTiles, numWorkers,
+                                          sharedPool);
+}
+
+/// FP32 extension: the same plan over float fields (weights / coefficients
+/// are given in double, as in the reference's kinds, and rounded to float on
+/// the device path; FunctionStencil's fn selects the device twin, which
+/// evaluates the same expression in float).
+inline StencilPlanF create_plan(Direction direction, BoundaryMode mode, StencilKind kind, Grid2Df& input,
+                                Grid2Df& output, int numTiles, int numWorkers,
+                                WorkerPool* sharedPool = nullptr) {
+  return detail::create_plan_impl<float>(direction, mode, std::move(kind), input, output, numTiles, numWorkers,
+                                         sharedPool);
+}
+
+template <typename T>
+inline void destroy_plan(BasicStencilPlan<T>& plan) {
+  plan.destroy();
+}
 
 /// stencil.cpp:197-200
-inline void swap_plan(StencilPlan& plan) {
+template <typename T>
+inline void swap_plan(BasicStencilPlan<T>& plan) {
+  using A = typename BasicStencilPlan<T>::Access;
   if (!plan.valid()) throw std::logic_error("swap_plan: plan was destroyed");
-  detail::check(sg_plan_swap(plan.h_));
-  std::swap(plan.input_, plan.output_);
-  std::swap(plan.boundIn_, plan.boundOut_);
+  detail::check(sg_plan_swap(A::handle(plan)));
+  std::swap(A::input(plan), A::output(plan));
+  std::swap(A::bound_in(plan), A::bound_out(plan));
 }
 
 /// stencil.cpp:202-235 — runs on the GPU, synchronous and host-coherent for
@@ -271,7 +332,8 @@ inline void swap_plan(StencilPlan& plan) {
 /// as in the reference, where the residency hint is a no-op
 /// (stencil.cpp:202). A numWorkers > 1 plan runs one y-slab per GPU
 /// (sg.h: sg_set_device_map).
-inline void compute(StencilPlan& plan, Residency hint = Residency::Host) {
+template <typename T>
+inline void compute(BasicStencilPlan<T>& plan, Residency hint = Residency::Host) {
   (void)hint;
   detail::compute_impl(plan, true);
 }
@@ -281,23 +343,30 @@ inline void compute(StencilPlan& plan, Residency hint = Residency::Host) {
 /// compute_deferred / swap_plan never wait on the host or move the grids
 /// over PCIe. The bound host output is stale until sync_to_host(plan) (or a
 /// later compute()); do not modify the bound host grids in between.
-inline void compute_deferred(StencilPlan& plan) { detail::compute_impl(plan, false); }
+template <typename T>
+inline void compute_deferred(BasicStencilPlan<T>& plan) {
+  detail::compute_impl(plan, false);
+}
 
 /// Bring compute_deferred results back into the bound host grids.
-inline void sync_to_host(StencilPlan& plan) {
+template <typename T>
+inline void sync_to_host(BasicStencilPlan<T>& plan) {
+  using A = typename BasicStencilPlan<T>::Access;
   if (!plan.valid()) throw std::logic_error("sync_to_host: plan was destroyed");
-  detail::check(sg_plan_sync_to_host(plan.h_));
+  detail::check(sg_plan_sync_to_host(A::handle(plan)));
 }
 
 namespace detail {
-inline void compute_impl(StencilPlan& plan, bool hostCoherent) {
+template <typename T>
+void compute_impl(BasicStencilPlan<T>& plan, bool hostCoherent) {
+  using A = typename BasicStencilPlan<T>::Access;
   if (!plan.valid()) throw std::logic_error("compute: plan was destroyed");
-  Grid2D& in = *plan.input_;
-  Grid2D& out = *plan.output_;
+  BasicGrid2D<T>& in = *A::input(plan);
+  BasicGrid2D<T>& out = *A::output(plan);
   if (!in.same_shape(out)) throw std::invalid_argument("compute: bound grids changed shape");
   if (in.data() == out.data()) throw std::invalid_argument("compute: bound grids alias");
-  if (in.data() != plan.boundIn_ || out.data() != plan.boundOut_) plan.bind();  // storage moved
-  detail::check(sg_plan_compute(plan.h_, hostCoherent ? SG_RESIDENCY_HOST : SG_RESIDENCY_DEVICE, nullptr,
+  if (in.data() != A::bound_in(plan) || out.data() != A::bound_out(plan)) A::bind(plan);  // storage moved
+  detail::check(sg_plan_compute(A::handle(plan), hostCoherent ? SG_RESIDENCY_HOST : SG_RESIDENCY_DEVICE, nullptr,
                                 hostCoherent ? 1 : 0));
 }
 }  // namespace detail

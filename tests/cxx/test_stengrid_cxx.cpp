@@ -384,6 +384,61 @@ void test_workers_to_gpus() {  // numWorkers -> GPUs; test_stencil.
   for (std::size_t k = 2; k < fields.size(); ++k) CHECK(grids_equal_bitwise(fields[k % 2], fields[k]));
 }
 
+void test_fp32_dropin() {  // FP32 extension (north_star: FP32+FP64); bar 1e-5 relative
+  // Grid2Df through the same create_plan / compute / swap_plan calls: the
+  // result is within 1e-5 (normwise, relative) of the FP64 evaluation on the
+  // float-rounded input, for weights and device functions, XY/X/Y, periodic
+  // and not, one worker and several (numWorkers -> GPUs)
+  const int nx = 97, ny = 61;  // odd sizes: the unaligned-row path too
+  const Grid2D src = random_grid(nx, ny, 171);
+  Grid2D in64(nx, ny, src.dx, src.dy);
+  Grid2Df in32(nx, ny, src.dx, src.dy);
+  for (std::ptrdiff_t k = 0; k < src.size(); ++k) {
+    in32.data()[k] = static_cast<float>(src.data()[k]);
+    in64.data()[k] = static_cast<double>(in32.data()[k]);
+  }
+  struct Case {
+    Direction d;
+    StencilKind kind;
+  };
+  const std::vector<Case> cases = {
+      {Direction::XY, FunctionStencil{Extents{1, 1, 1, 1}, functions::fn_weighted_3x3, random_weights(9, 172)}},
+      {Direction::XY, WeightStencil{Extents{1, 1, 1, 1}, random_weights(9, 173)}},
+      {Direction::XY, WeightStencil{Extents{2, 2, 2, 2}, random_weights(25, 174)}},
+      {Direction::X, WeightStencil{Extents{2, 2, 0, 0}, {1.0, -4.0, 6.0, -4.0, 1.0}}},
+      {Direction::Y, WeightStencil{Extents{0, 0, 3, 1}, random_weights(5, 175)}},
+      {Direction::XY, FunctionStencil{Extents{1, 1, 1, 1}, functions::ch_nonlinear_window, random_weights(9, 176)}},
+  };
+  for (const Case& c : cases)
+    for (const bool periodic : {true, false})
+      for (const int workers : {1, 3}) {
+        const BoundaryMode mode = periodic ? BoundaryMode::Periodic : BoundaryMode::NonPeriodic;
+        Grid2Df a = in32, b(nx, ny, src.dx, src.dy);
+        Grid2D a64 = in64, b64(nx, ny, src.dx, src.dy);
+        StencilPlanF p = create_plan(c.d, mode, c.kind, a, b, 1, workers);
+        compute(p);
+        StencilPlan q = create_plan(c.d, mode, c.kind, a64, b64, 1, 1);
+        compute(q);
+        double num = 0.0, den = 0.0;
+        for (std::ptrdiff_t k = 0; k < b64.size(); ++k) {
+          const double e = static_cast<double>(b.data()[k]) - b64.data()[k];
+          num += e * e;
+          den += b64.data()[k] * b64.data()[k];
+        }
+        const double rel = std::sqrt(num / (den > 0.0 ? den : 1.0));
+        CHECK(rel <= 1e-5);
+        if (rel > 1e-5) std::printf("  fp32 rel %.3e periodic=%d workers=%d\n", rel, periodic, workers);
+        swap_plan(p);  // the float plan swaps like the double one
+        CHECK(p.input() == &b && p.output() == &a);
+        destroy_plan(p);
+        CHECK(!p.valid());
+      }
+  Grid2Df x(8, 8, 1.0, 1.0), y(8, 9, 1.0, 1.0);
+  CHECK_THROWS_AS(create_plan(Direction::XY, BoundaryMode::Periodic,
+                              WeightStencil{Extents{1, 1, 1, 1}, std::vector<double>(9, 1.0)}, x, y, 1, 1),
+                  std::invalid_argument);
+}
+
 void test_acceptance_criterion_2() {  // acceptance.cpp:104-151
   std::mt19937_64 rng(99);
   std::uniform_real_distribution<double> val(-2.0, 2.0);
@@ -617,6 +672,7 @@ int main() {
   test_tiles_frame_shift_concurrency();
   test_residency();
   test_workers_to_gpus();
+  test_fp32_dropin();
   test_acceptance_criterion_2();
   test_penta();
   test_ch();
