@@ -507,6 +507,17 @@ def bench_variants(sg, torch, stream, peak, n=16384, launches=20):
         ("xy_nonperiodic_3x3_weights", sg.Direction.XY, sg.BoundaryMode.NonPeriodic, sg.Extents(1, 1, 1, 1), None, 9),
         ("xy_periodic_ch_nonlinear_window", sg.Direction.XY, sg.BoundaryMode.Periodic, sg.Extents(1, 1, 1, 1),
          "ch_nonlinear_window", 9),
+        # k_tma_g: asymmetric windows (test_stencil.cpp:557-568) and odd rows
+        ("x_periodic_asym_3_1_0_0_weights", sg.Direction.X, sg.BoundaryMode.Periodic, sg.Extents(3, 1, 0, 0), None, 5),
+        ("xy_periodic_asym_2_1_1_2_weights", sg.Direction.XY, sg.BoundaryMode.Periodic, sg.Extents(2, 1, 1, 2), None,
+         16),
+        ("xy_periodic_3x3_fn_weighted_odd_nx_16383", sg.Direction.XY, sg.BoundaryMode.Periodic,
+         sg.Extents(1, 1, 1, 1), "fn_weighted_3x3", 9),
+        ("xy_nonperiodic_3x3_weights_odd_nx_16383", sg.Direction.XY, sg.BoundaryMode.NonPeriodic,
+         sg.Extents(1, 1, 1, 1), None, 9),
+        # k_generic: a window past k_tma_g's 9 x 9 (11 x 11 weights)
+        ("xy_periodic_11x11_weights_generic", sg.Direction.XY, sg.BoundaryMode.Periodic, sg.Extents(5, 5, 5, 5),
+         None, 121),
     ]
     a = torch.rand((n, n), dtype=torch.float64, device="cuda")
     b = torch.zeros_like(a)
@@ -515,22 +526,34 @@ def bench_variants(sg, torch, stream, peak, n=16384, launches=20):
     for name, d, mode, ext, fn, nv in cases:
         vals = list(rng.uniform(-1, 1, nv))
         kind = sg.WeightStencil(ext, vals) if fn is None else sg.FunctionStencil(ext, fn, vals)
-        plan = sg.create_plan(d, mode, kind, a, b, 1, 1)
+        nxv = n - 1 if "odd_nx" in name else n
+        ai = a.view(-1)[: n * nxv].view(n, nxv)
+        bo = b.view(-1)[: n * nxv].view(n, nxv)
+        plan = sg.create_plan(d, mode, kind, ai, bo, 1, 1)
+        kk = plan.kernel_kind()
         with torch.cuda.stream(stream):
-            time_plan_steps(sg, torch, plan, 3, stream)
-            tot, _ = time_plan_steps(sg, torch, plan, launches, stream)
+            t2, _ = time_plan_steps(sg, torch, plan, 2, stream)
+            # >= 0.4 s per variant so the clock sampler sees it (FP64-bound
+            # windows run power-capped below the nominal clock)
+            reps = max(3 if "generic" in name else launches, int(400.0 / max(t2 / 2, 1e-3)))
+            with Clocks(torch.cuda.current_device()) as clk:
+                tot, _ = time_plan_steps(sg, torch, plan, reps, stream)
         sg.destroy_plan(plan)
-        ms = tot / launches
+        ms = tot / reps
+        csum = clk.summary()
         rows = n - (ext.top + ext.bottom if mode == sg.BoundaryMode.NonPeriodic else 0)
-        cols = n - (ext.left + ext.right if mode == sg.BoundaryMode.NonPeriodic else 0)
-        alg = 8 * (n * n + rows * cols)
+        cols = nxv - (ext.left + ext.right if mode == sg.BoundaryMode.NonPeriodic else 0)
+        alg = 8 * (n * nxv + rows * cols)
         # FP64 instructions per output point (no FMA contraction: a multiply
         # and an add per tap; the CH window adds c^3 - c per tap)
         ops = 5 * nv if fn == "ch_nonlinear_window" else 2 * nv
         rate = ops * rows * cols / (ms * 1e-3)
         res[name] = {"gpts_s": rows * cols / (ms * 1e-3) / 1e9, "kernel_ms": ms,
                      "hbm_frac": alg / (ms * 1e-3) / 1e9 / peak,
-                     "fp64_ops_per_pt": ops, "fp64_frac": rate / FP64_PEAK_OPS}
+                     "fp64_ops_per_pt": ops, "fp64_frac": rate / FP64_PEAK_OPS,
+                     "sm_mhz": csum.get("sm_mhz"), "clock_reasons": csum.get("reasons"),
+                     "fp64_frac_at_clock": (rate / (148 * 64 * csum["sm_mhz"] * 1e6)) if csum.get("sm_mhz") else None,
+                     "kernel": {2: "k_tma_g", 1: "k_tma", 0: "k_generic"}[kk], "nx": nxv}
     del a, b
     torch.cuda.empty_cache()
     return res

@@ -93,11 +93,20 @@ struct PeerRows {
 };
 
 // Stencil launch (stencil.cu). `values` are the weights (fn == SG_FN_NONE) or
-// the function coefficients; returns the kernel kind used (1 fast, 0 generic).
+// the function coefficients; returns the kernel kind used (2 k_tma_g, 1 k_tma,
+// 0 k_generic).
 int launch_stencil(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,
                    size_t count, sg_dtype dtype, const void* in, void* out, cudaStream_t stream,
                    const PeerRows& peers = PeerRows{});
-// Which kernel launch_stencil would pick, without launching.
+// k_tma_g launches (stencil_g64.cu / stencil_g32.cu): general window shapes
+// up to TMA_G_MAXW a side and any row alignment.
+constexpr int TMA_G_MAXW = 9;
+void launch_stencil_g_f64(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values, size_t count,
+                          const void* in, void* out, cudaStream_t stream, const PeerRows& peers);
+void launch_stencil_g_f32(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values, size_t count,
+                          const void* in, void* out, cudaStream_t stream, const PeerRows& peers);
+// Which kernel launch_stencil would pick, without launching (2 k_tma_g,
+// 1 k_tma, 0 k_generic).
 int stencil_kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size_t count,
                         sg_dtype dtype, const void* in, const void* out);
 // Minimum window (W, H) and coefficient count a device function reads.

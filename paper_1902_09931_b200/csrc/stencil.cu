@@ -9,19 +9,16 @@
 // receive the window packed with rowStride = W, which the reference's
 // contract allows (stencil.hpp:20-25).
 //
-// Two kernels:
-//  * k_strip — the bandwidth path. One warp owns a strip of 32*V columns
-//    (V = 16 bytes / sizeof(T): 2 doubles or 4 floats per lane, so every
-//    row load is one coalesced 512 B LDG.128 per warp) and marches down a
-//    segment of rows. Each input row is loaded from HBM exactly once per
-//    strip; horizontal neighbours come from warp shuffles, only the two
-//    strip-edge lanes load halo columns (wrapped in index math, computed
-//    once per strip). The H-row window lives in registers; loads run a
-//    D-row software prefetch ahead so ~D*512 B per warp are in flight.
-//    Weights/coefficients sit in the kernel parameter (constant) bank.
+// Three kernels:
+//  * k_tma — the bandwidth path for symmetric windows (extents <= 4 a side)
+//    on 16 B-aligned rows: TMA-staged shared-memory row ring, one producer
+//    warp, 16 consumer warps holding the window in registers.
+//  * k_tma_g — the same pipeline for every other window up to 9 x 9
+//    (asymmetric left/right and top/bottom splits) and every row pitch /
+//    pointer alignment (nx % V != 0): rows keep their global 16 B phase in
+//    shared memory.
 //  * k_generic — one thread per output point with per-tap modular wrap:
-//    any extents (including windows wider than the grid), any alignment,
-//    any row pitch. Used for tiny/odd grids and unusual extents.
+//    windows beyond 9 x 9 and device functions on non-natural windows.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -33,624 +30,13 @@
 #include <type_traits>
 
 #include "sg_internal.hpp"
+#include "stencil_kern.cuh"
 
 namespace sg {
 
 std::atomic<uint64_t> g_launches{0};
 
 namespace {
-
-constexpr int VMAX = 256;       // values carried in the parameter bank
-constexpr int GENERIC_FN_MAX = 256;  // window taps a generic device function may see
-
-template <typename T>
-struct KArgs {
-  const T* __restrict__ in;
-  T* __restrict__ out;
-  const T* __restrict__ wdev;  // weights when count > VMAX (generic path only)
-  int nx, inRows, inShift;
-  int row0, row1, col0, col1;
-  int wrapX, wrapY;
-  int left, right, top, bottom;
-  int segRows;
-  int count;
-  // P2P halo forwarding (multi-GPU y-slabs): output rows j < upRows are
-  // also stored to peerUp + j*nx (the up neighbour's bottom halo), rows
-  // j >= dnRow0 to peerDn + (j - dnRow0)*nx (the down neighbour's top
-  // halo) — peer memory over NVLink; null = none
-  T* peerUp;
-  T* peerDn;
-  int upRows, dnRow0;
-  T v[VMAX];
-};
-
-// Store one output value (and its P2P halo copies).
-template <typename T>
-__device__ __forceinline__ void put_out(const KArgs<T>& a, long long j, long long i, T v) {
-  a.out[j * a.nx + i] = v;
-  if (a.peerUp && j < a.upRows) a.peerUp[j * a.nx + i] = v;
-  if (a.peerDn && j >= a.dnRow0) a.peerDn[(j - a.dnRow0) * a.nx + i] = v;
-}
-
-// ----------------------------------------------------------- window ops
-// Device twins of the reference's window functions. Same expression trees,
-// evaluated without contraction, so FP64 results are bitwise identical.
-struct OpWeights {};  // marker: weight stencil
-
-struct OpChNonlinear {  // cahn_hilliard.cpp:36-47
-  template <typename T>
-  __device__ static T apply(const T* w, const T* coe, int rs) {
-    T acc = T(0);
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-      for (int p = 0; p < 3; ++p) {
-        const T v = w[q * rs + p];
-        acc += coe[q * 3 + p] * (v * v * v - v);
-      }
-    return acc;
-  }
-};
-struct OpCentralDifference {  // tools/main.cpp:47-49
-  template <typename T>
-  __device__ static T apply(const T* w, const T* coe, int) {
-    return (w[0] - T(2) * w[1] + w[2]) * coe[0];
-  }
-};
-struct OpCenter {  // tests/test_stencil.cpp:68
-  template <typename T>
-  __device__ static T apply(const T* w, const T*, int rs) {
-    return w[rs + 1];
-  }
-};
-struct OpCentralSecond {  // tests/test_stencil.cpp:70-77
-  template <typename T>
-  __device__ static T apply(const T* w, const T* coe, int) {
-    T acc = T(0);
-    acc += coe[0] * w[0];
-    acc += (T(-2) * coe[0]) * w[1];
-    acc += coe[0] * w[2];
-    return acc;
-  }
-};
-struct OpLapCubeDiffFirst {  // tests/test_stencil.cpp:79-85
-  template <typename T>
-  __device__ static T g(T v) { return v * v * v - v; }
-  template <typename T>
-  __device__ static T apply(const T* w, const T* coe, int rs) {
-    const T gm = g(w[rs + 1]);
-    const T x = (g(w[rs]) - T(2) * gm) + g(w[rs + 2]);
-    const T y = (g(w[1]) - T(2) * gm) + g(w[2 * rs + 1]);
-    return coe[0] * x + coe[1] * y;
-  }
-};
-struct OpWeighted3x3 {  // tests/test_stencil.cpp:88-93
-  template <typename T>
-  __device__ static T apply(const T* w, const T* coe, int rs) {
-    T acc = T(0);
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-      for (int p = 0; p < 3; ++p) acc += coe[q * 3 + p] * w[q * rs + p];
-    return acc;
-  }
-};
-
-template <typename T>
-struct VecT;
-template <>
-struct VecT<double> {
-  static constexpr int V = 2;
-  using type = double2;
-};
-template <>
-struct VecT<float> {
-  static constexpr int V = 4;
-  using type = float4;
-};
-
-template <typename T>
-__device__ __forceinline__ T shfl_up(T v, int d) {
-  return __shfl_up_sync(0xffffffffu, v, d);
-}
-template <typename T>
-__device__ __forceinline__ T shfl_down(T v, int d) {
-  return __shfl_down_sync(0xffffffffu, v, d);
-}
-
-__device__ __forceinline__ int wrap_idx(long long i, int n) {
-  long long r = i % n;
-  return static_cast<int>(r < 0 ? r + n : r);
-}
-
-constexpr int STRIP_WARPS = 4;
-
-// --------------------------------------------------------------- k_strip
-template <typename T, int L, int R, int TP, int BT, int D, typename Op>
-__global__ void __launch_bounds__(STRIP_WARPS * 32) k_strip(const __grid_constant__ KArgs<T> a) {
-  using VT = typename VecT<T>::type;
-  constexpr int V = VecT<T>::V;
-  constexpr int SW = 32 * V;
-  constexpr int H = TP + BT + 1;
-  constexpr int W = L + R + 1;
-  constexpr int E = L + V + R;
-  constexpr int LL = L > 0 ? L : 1;
-  constexpr int RR = R > 0 ? R : 1;
-
-  const int lane = threadIdx.x & 31;
-  const int strip = blockIdx.x * STRIP_WARPS + (threadIdx.x >> 5);
-  const int x0 = strip * SW;
-  if (x0 >= a.nx) return;  // warp-uniform
-  const int ra = a.row0 + blockIdx.y * a.segRows;
-  const int rb = min(ra + a.segRows, a.row1);
-  if (ra >= rb) return;
-
-  const int nx = a.nx;
-  const int xb = x0 + lane * V;
-  const bool laneValid = xb < nx;
-  const int xc = laneValid ? xb : nx - V;  // clamped (value unused)
-
-  // Halo columns: shuffled from neighbour lanes where they hold the column,
-  // otherwise loaded directly with the wrap resolved once here.
-  int hlCol[LL], hrCol[RR];
-  bool hlDir[LL], hrDir[RR];
-#pragma unroll
-  for (int k = 1; k <= L; ++k) {
-    const int dl = (k + V - 1) / V;
-    const int c = xb - k;
-    hlDir[k - 1] = lane < dl;
-    hlCol[k - 1] = a.wrapX ? wrap_idx(c, nx) : max(min(c, nx - 1), 0);
-  }
-#pragma unroll
-  for (int k = 1; k <= R; ++k) {
-    const int dr = (V - 1 + k) / V;
-    const int c = xb + V - 1 + k;
-    hrDir[k - 1] = (lane + dr > 31) || (c >= nx);
-    hrCol[k - 1] = a.wrapX ? wrap_idx(c, nx) : max(min(c, nx - 1), 0);
-  }
-
-  struct Raw {
-    VT c;
-    T hl[LL];
-    T hr[RR];
-  };
-  const T* __restrict__ in = a.in;
-  auto fetch = [&](int row, Raw& r) {
-    const T* base = in + static_cast<long long>(row) * nx;
-    r.c = __ldg(reinterpret_cast<const VT*>(base + xc));
-#pragma unroll
-    for (int k = 0; k < L; ++k) r.hl[k] = hlDir[k] ? __ldg(base + hlCol[k]) : T(0);
-#pragma unroll
-    for (int k = 0; k < R; ++k) r.hr[k] = hrDir[k] ? __ldg(base + hrCol[k]) : T(0);
-  };
-  auto expand = [&](const Raw& r, T* e) {
-    T c[V];
-    if constexpr (V == 2) {
-      c[0] = r.c.x;
-      c[1] = r.c.y;
-    } else {
-      c[0] = r.c.x;
-      c[1] = r.c.y;
-      c[2] = r.c.z;
-      c[3] = r.c.w;
-    }
-#pragma unroll
-    for (int k = 1; k <= L; ++k) {
-      const int dl = (k + V - 1) / V;
-      const T s = shfl_up(c[V * dl - k], dl);
-      e[L - k] = hlDir[k - 1] ? r.hl[k - 1] : s;
-    }
-#pragma unroll
-    for (int v = 0; v < V; ++v) e[L + v] = c[v];
-#pragma unroll
-    for (int k = 1; k <= R; ++k) {
-      const int dr = (V - 1 + k) / V;
-      const T s = shfl_down(c[(k - 1) % V], dr);
-      e[L + V - 1 + k] = hrDir[k - 1] ? r.hr[k - 1] : s;
-    }
-  };
-
-  // Input rows ra+inShift-TP .. rb-1+inShift+BT, wrapped iff wrapY.
-  const int nIn = (rb - ra) + H - 1;
-  int rf = ra + a.inShift - TP;
-  if (a.wrapY) rf = wrap_idx(rf, a.inRows);
-  auto advance = [&](int& r) {
-    ++r;
-    if (a.wrapY) {
-      if (r == a.inRows) r = 0;
-    } else if (r >= a.inRows) {
-      r = a.inRows - 1;
-    }
-  };
-
-  Raw ring[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    if (k < nIn) fetch(rf, ring[k]);
-    advance(rf);
-  }
-  T win[H][E];
-  T* __restrict__ out = a.out;
-  for (int t0 = 0; t0 < nIn; t0 += D) {
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const int t = t0 + k;
-      if (t < nIn) {
-        T e[E];
-        expand(ring[k], e);
-        if (t + D < nIn) fetch(rf, ring[k]);
-        advance(rf);
-#pragma unroll
-        for (int q = 0; q < H - 1; ++q)
-#pragma unroll
-          for (int p = 0; p < E; ++p) win[q][p] = win[q + 1][p];
-#pragma unroll
-        for (int p = 0; p < E; ++p) win[H - 1][p] = e[p];
-        if (t >= H - 1) {
-          const int j = ra + t - (H - 1);
-          T res[V];
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            if constexpr (std::is_same_v<Op, OpWeights>) {
-              T acc = T(0);
-#pragma unroll
-              for (int q = 0; q < H; ++q)
-#pragma unroll
-                for (int p = 0; p < W; ++p) acc += a.v[q * W + p] * win[q][v + p];
-              res[v] = acc;
-            } else {
-              T w[H * W];
-#pragma unroll
-              for (int q = 0; q < H; ++q)
-#pragma unroll
-                for (int p = 0; p < W; ++p) w[q * W + p] = win[q][v + p];
-              res[v] = Op::template apply<T>(w, a.v, W);
-            }
-          }
-          if (laneValid) {
-            T* orow = out + static_cast<long long>(j) * nx;
-            if (xb >= a.col0 && xb + V <= a.col1) {
-              VT o;
-              if constexpr (V == 2) {
-                o.x = res[0];
-                o.y = res[1];
-              } else {
-                o.x = res[0];
-                o.y = res[1];
-                o.z = res[2];
-                o.w = res[3];
-              }
-              *reinterpret_cast<VT*>(orow + xb) = o;
-            } else {
-#pragma unroll
-              for (int v = 0; v < V; ++v)
-                if (xb + v >= a.col0 && xb + v < a.col1) orow[xb + v] = res[v];
-            }
-          }
-        }
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------- k_tma
-// The TMA-staged variant of k_strip (the default fast path). Each warp owns
-// a strip as in k_strip, but rows are staged into a per-warp shared-memory
-// ring by the bulk-copy engine (cp.async.bulk, TMA 1D, completion on an
-// mbarrier per stage): ONE copy per row brings the strip's 32*V columns
-// plus the L/R halo columns (rounded out to 16 B) — halos are loaded once
-// and never shuffled; only edge strips add a 16-32 B wrap copy. Registers
-// hold just the H-row window, so occupancy is ~2.5x k_strip's and the ring
-// keeps S*RPS rows per warp in flight without register cost.
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!ok);
-}
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-// The mbarrier receives one arrival when all prior cp.async of this thread land.
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// CTA geometry: TMA_WARPS consumer warps side by side cover CW columns; one
-// producer warp streams rows (CW + halos) into a STAGES x RPS ring.
-#ifndef SG_TMA_WARPS
-#define SG_TMA_WARPS 16
-#endif
-constexpr int TMA_WARPS = SG_TMA_WARPS;
-// Release of a ring stage by the consumers: every thread arrives on the
-// "empty" mbarrier (1), or each warp's lane 0 after __syncwarp (0).
-#ifndef SG_EMPTY_ALL_LANES
-#define SG_EMPTY_ALL_LANES 1
-#endif
-
-template <typename T, int L, int R, int TP, int BT>
-struct TmaGeom {
-  static constexpr int V = VecT<T>::V;
-  static constexpr int SW = 32 * V;
-  static constexpr int CW = TMA_WARPS * SW;
-  static constexpr int LP = ((L + V - 1) / V) * V;  // left pad, 16 B granules
-  static constexpr int RP = ((R + V - 1) / V) * V;
-  static constexpr int ROW = LP + CW + RP;  // elements per staged row (~2 KB)
-  static constexpr int H = TP + BT + 1;
-  // Rows per stage: a multiple of H so the register window is a ring whose
-  // slot for every unrolled row is a compile-time constant (no moves).
-  static constexpr int RPS = H >= 2 ? H : 2;
-  static constexpr int STAGES = (9 + RPS - 1) / RPS >= 2 ? (9 + RPS - 1) / RPS : 2;
-  static constexpr size_t stage_bytes = static_cast<size_t>(RPS) * ROW * sizeof(T);
-  static constexpr size_t smem_bytes = STAGES * stage_bytes + 2 * STAGES * sizeof(uint64_t);
-};
-
-template <typename T, int L, int R, int TP, int BT, typename Op>
-__global__ void __launch_bounds__((TMA_WARPS + 1) * 32) k_tma(const __grid_constant__ KArgs<T> a) {
-  using G = TmaGeom<T, L, R, TP, BT>;
-  using VT = typename VecT<T>::type;
-  constexpr int V = G::V, SW = G::SW, CW = G::CW, LP = G::LP, RP = G::RP, ROW = G::ROW;
-  constexpr int H = G::H, RPS = G::RPS, STAGES = G::STAGES;
-  constexpr int W = L + R + 1;
-  constexpr int E = L + V + R;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* ring = reinterpret_cast<T*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * G::stage_bytes);
-  uint64_t* empty = full + STAGES;
-
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int nx = a.nx;
-  const int cx0 = blockIdx.x * CW;
-  const int ra = a.row0 + blockIdx.y * a.segRows;
-  const int rb = min(ra + a.segRows, a.row1);
-  if (ra >= rb) return;  // CTA-uniform
-  const int nIn = (rb - ra) + H - 1;
-  const int nStages = (nIn + RPS - 1) / RPS;
-
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < STAGES; ++k) {
-      mbar_init(&full[k], 2);  // expect_tx arrival + cp.async (halo) arrival
-      mbar_init(&empty[k], SG_EMPTY_ALL_LANES ? TMA_WARPS * 32 : TMA_WARPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == TMA_WARPS) {
-    // ---------------- producer: per row, one bulk copy of the CTA's own
-    // columns (128 B aligned, whole lines: no over-fetch) and 16 B cp.async
-    // granules for the halo columns (wrapped in index math at grid edges).
-    if (lane != 0) return;
-    const int validC = min(CW, nx - cx0);
-    const uint32_t mainBytes = static_cast<uint32_t>(validC * sizeof(T));
-    int hsrc[(LP + RP) / V > 0 ? (LP + RP) / V : 1];
-    int hdst[(LP + RP) / V > 0 ? (LP + RP) / V : 1];
-    int nh = 0;
-#pragma unroll
-    for (int k = 0; k < LP / V; ++k) {
-      const int c = cx0 - LP + k * V;
-      if (c >= 0 || a.wrapX) {
-        hsrc[nh] = c >= 0 ? c : c + nx;
-        hdst[nh++] = k * V;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < RP / V; ++k) {
-      const int c = cx0 + validC + k * V;
-      if (c < nx || a.wrapX) {
-        hsrc[nh] = c < nx ? c : c - nx;
-        hdst[nh++] = LP + validC + k * V;
-      }
-    }
-    int rf = ra + a.inShift - TP;
-    if (a.wrapY) rf = wrap_idx(rf, a.inRows);
-    const T* __restrict__ in = a.in;
-    for (int g = 0; g < nStages; ++g) {
-      const int slot = g % STAGES;
-      if (g >= STAGES) mbar_wait(&empty[slot], ((g / STAGES) + 1) & 1);
-      mbar_expect_tx(&full[slot], mainBytes * RPS);
-      T* sstage = ring + slot * (RPS * ROW);
-#pragma unroll
-      for (int k = 0; k < RPS; ++k) {
-        const T* grow = in + static_cast<long long>(rf) * nx;
-        T* srow = sstage + k * ROW;
-        bulk_g2s(srow + LP, grow + cx0, mainBytes, &full[slot]);
-        for (int h = 0; h < nh; ++h) cp_async16(srow + hdst[h], grow + hsrc[h]);
-        ++rf;
-        if (a.wrapY) {
-          if (rf == a.inRows) rf = 0;
-        } else if (rf >= a.inRows) {
-          rf = a.inRows - 1;
-        }
-      }
-      cp_async_mbar_arrive(&full[slot]);
-    }
-    return;
-  }
-
-  // ---------------- consumers
-  const int xb = cx0 + warp * SW + lane * V;
-  const bool laneValid = xb < nx;
-  // Weight stencils with tall windows (H >= 5) keep H PENDING OUTPUT
-  // accumulators instead of H input rows: each arriving input row adds its
-  // tap row to every output that needs it. Output o still accumulates its
-  // taps row by row (q ascending, then p) — the reference's order — since
-  // rows arrive top to bottom. Registers: H*V + E instead of H*E (a 9x9
-  // window would otherwise spill).
-  constexpr bool ACC = std::is_same_v<Op, OpWeights> && H >= 5;
-  T win[ACC ? 1 : H][E];  // ring: input row t lives in win[t % H]
-  T pend[ACC ? H : 1][V];  // ACC: output started at local input row u lives in pend[u % H]
-  T* __restrict__ orow = a.out + static_cast<long long>(ra - (H - 1)) * nx + xb;
-  const bool vecStore = laneValid && xb >= a.col0 && xb + V <= a.col1;
-  const long long rowStep = nx;
-  int j = ra - (H - 1);  // output row completed by the current input row
-  for (int g = 0; g < nStages; ++g) {
-    const int slot = g % STAGES;
-    mbar_wait(&full[slot], (g / STAGES) & 1);
-    const T* sbase = ring + slot * (RPS * ROW) + LP + warp * SW + lane * V;
-#pragma unroll
-    for (int k = 0; k < RPS; ++k) {
-      const T* srow = sbase + k * ROW;
-      T* e = win[ACC ? 0 : k % H];
-      const VT c = *reinterpret_cast<const VT*>(srow);
-      if constexpr (V == 2) {
-        e[L] = c.x;
-        e[L + 1] = c.y;
-      } else {
-        e[L] = c.x;
-        e[L + 1] = c.y;
-        e[L + 2] = c.z;
-        e[L + 3] = c.w;
-      }
-      // Horizontal halos: scalar shared loads at a 16 B lane stride (2-way
-      // bank conflicts, ~0.1 per output in ncu). Shuffling them from the
-      // neighbouring lanes' vectors instead removed 83 % of the conflicts
-      // but measured slower (3x3 98.4 -> 97.2 % of HBM, 5x5 FP64-bound
-      // 0.63 -> 0.47): the loads are not on the critical resource.
-#pragma unroll
-      for (int p = 0; p < L; ++p) e[p] = srow[p - L];
-#pragma unroll
-      for (int p = 0; p < R; ++p) e[L + V + p] = srow[V + p];
-      // Output row j uses input rows j-TP .. j+BT = the H most recent rows,
-      // oldest in slot (k + 1) % H.
-      T res[V];
-      if constexpr (ACC) {
-        // this row is tap row q of the output started q rows ago (slot
-        // (k - q) mod H; RPS is a multiple of H, so slots are compile-time)
-#pragma unroll
-        for (int q = 0; q < H; ++q) {
-          T* acc = pend[((k - q) % H + H) % H];
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            if (q == 0) acc[v] = T(0);
-#pragma unroll
-            for (int p = 0; p < W; ++p) acc[v] += a.v[q * W + p] * e[v + p];
-          }
-        }
-#pragma unroll
-        for (int v = 0; v < V; ++v) res[v] = pend[(k + 1) % H][v];  // completed (q = H-1 just added)
-      } else {
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        if constexpr (std::is_same_v<Op, OpWeights>) {
-          T acc = T(0);
-#pragma unroll
-          for (int q = 0; q < H; ++q)
-#pragma unroll
-            for (int p = 0; p < W; ++p) acc += a.v[q * W + p] * win[(k + 1 + q) % H][v + p];
-          res[v] = acc;
-        } else {
-          T w[H * W];
-#pragma unroll
-          for (int q = 0; q < H; ++q)
-#pragma unroll
-            for (int p = 0; p < W; ++p) w[q * W + p] = win[(k + 1 + q) % H][v + p];
-          res[v] = Op::template apply<T>(w, a.v, W);
-        }
-      }
-      }
-      if (j >= ra && j < rb) {  // warp-uniform
-        if (vecStore) {
-          VT o;
-          if constexpr (V == 2) {
-            o.x = res[0];
-            o.y = res[1];
-          } else {
-            o.x = res[0];
-            o.y = res[1];
-            o.z = res[2];
-            o.w = res[3];
-          }
-          *reinterpret_cast<VT*>(orow) = o;
-          if (a.peerUp && j < a.upRows)  // warp-uniform
-            *reinterpret_cast<VT*>(a.peerUp + static_cast<long long>(j) * nx + xb) = o;
-          if (a.peerDn && j >= a.dnRow0)
-            *reinterpret_cast<VT*>(a.peerDn + static_cast<long long>(j - a.dnRow0) * nx + xb) = o;
-        } else if (laneValid) {
-#pragma unroll
-          for (int v = 0; v < V; ++v)
-            if (xb + v >= a.col0 && xb + v < a.col1) put_out(a, j, xb + v, res[v]);
-        }
-      }
-      ++j;
-      orow += rowStep;
-    }
-    // every lane of this warp has read the stage
-    if constexpr (SG_EMPTY_ALL_LANES) {
-      mbar_arrive(&empty[slot]);  // each thread releases its own reads of the slot
-    } else {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-    }
-  }
-}
-
-// ------------------------------------------------------------- k_generic
-template <typename T, typename Op>
-__global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T> a) {
-  const int i = a.col0 + blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = a.row0 + blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= a.col1 || j >= a.row1) return;
-  const int W = a.left + a.right + 1;
-  const int H = a.top + a.bottom + 1;
-  const T* __restrict__ in = a.in;
-  if constexpr (std::is_same_v<Op, OpWeights>) {
-    const T* wt = a.count <= VMAX ? a.v : a.wdev;
-    T acc = T(0);
-    for (int q = 0; q < H; ++q) {
-      long long r = static_cast<long long>(j) + a.inShift - a.top + q;
-      if (a.wrapY) r = wrap_idx(r, a.inRows);
-      const T* rowp = in + r * a.nx;
-      for (int p = 0; p < W; ++p) {
-        long long c = static_cast<long long>(i) - a.left + p;
-        if (a.wrapX) c = wrap_idx(c, a.nx);
-        acc += wt[q * W + p] * rowp[c];
-      }
-    }
-    put_out(a, j, i, acc);
-  } else {
-    T w[GENERIC_FN_MAX];
-    for (int q = 0; q < H; ++q) {
-      long long r = static_cast<long long>(j) + a.inShift - a.top + q;
-      if (a.wrapY) r = wrap_idx(r, a.inRows);
-      const T* rowp = in + r * a.nx;
-      for (int p = 0; p < W; ++p) {
-        long long c = static_cast<long long>(i) - a.left + p;
-        if (a.wrapX) c = wrap_idx(c, a.nx);
-        w[q * W + p] = rowp[c];
-      }
-    }
-    put_out(a, j, i, Op::template apply<T>(w, a.v, W));
-  }
-}
 
 // -------------------------------------------------------------- dispatch
 struct FnInfo {
@@ -667,104 +53,63 @@ constexpr FnInfo kFn[SG_FN_COUNT] = {
     {"fn_weighted_3x3", 3, 3, 9},
 };
 
-template <typename Op, typename F>
-bool with_op(int fn, F&& f) {
-  switch (fn) {
-    case SG_FN_NONE: f(OpWeights{}); return true;
-    case SG_FN_CH_NONLINEAR: f(OpChNonlinear{}); return true;
-    case SG_FN_CENTRAL_DIFFERENCE: f(OpCentralDifference{}); return true;
-    case SG_FN_CENTER: f(OpCenter{}); return true;
-    case SG_FN_CENTRAL_SECOND: f(OpCentralSecond{}); return true;
-    case SG_FN_LAP_CUBE_DIFF_FIRST: f(OpLapCubeDiffFirst{}); return true;
-    case SG_FN_WEIGHTED_3X3: f(OpWeighted3x3{}); return true;
-    default: return false;
-  }
-}
-
-// Fast-path coverage: symmetric extents up to 4 for weight stencils; the
-// natural window of each device function.
-bool strip_supported(const sg_extents& e, int fn) {
-  if (e.left != e.right || e.top != e.bottom) return false;
-  if (fn == SG_FN_NONE) return e.left <= 4 && e.top <= 4;
+// Natural window of a device function (the shape its reference test uses);
+// the pipelined kernels serve functions on their natural window only.
+bool fn_natural(const sg_extents& e, int fn) {
   if (fn == SG_FN_CENTRAL_DIFFERENCE || fn == SG_FN_CENTRAL_SECOND)
-    return e.left == 1 && e.top == 0;
-  return e.left == 1 && e.top == 1;
+    return e.left == 1 && e.right == 1 && e.top == 0 && e.bottom == 0;
+  return e.left == 1 && e.right == 1 && e.top == 1 && e.bottom == 1;
 }
 
+// k_tma: symmetric weight windows up to 4 a side, natural function windows.
+bool strip_supported(const sg_extents& e, int fn) {
+  if (fn != SG_FN_NONE) return fn_natural(e, fn);
+  return e.left == e.right && e.top == e.bottom && e.left <= 4 && e.top <= 4;
+}
+
+// k_tma_g: any weight window up to 9 x 9, natural function windows.
+bool general_supported(const sg_extents& e, int fn) {
+  if (fn != SG_FN_NONE) return fn_natural(e, fn);
+  return e.left + e.right + 1 <= TMA_G_MAXW && e.top + e.bottom + 1 <= TMA_G_MAXW;
+}
+
+// 2 = k_tma_g, 1 = k_tma, 0 = k_generic
 template <typename T>
-bool strip_eligible(const sg_slab_desc& d, const sg_extents& e, int fn, size_t count,
-                    const void* in, const void* out) {
+int kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size_t count, const void* in,
+                const void* out) {
   constexpr int V = VecT<T>::V;
-  if (!strip_supported(e, fn)) return false;
-  if (count > static_cast<size_t>(VMAX)) return false;
-  if (d.nx % V != 0) return false;
-  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) % 16 != 0) return false;
-  return true;
-}
-
-// Prefetch depth: keep the raw-row ring near 64 32-bit registers per lane.
-template <typename T, int L>
-constexpr int prefetch_depth() {
-  constexpr int words = (VecT<T>::V + 2 * L) * static_cast<int>(sizeof(T) / 4);
-  constexpr int d = 64 / words;
-  return d >= 8 ? 8 : d >= 4 ? 4 : 2;
-}
-
-int sm_count() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
-
-// SG_STENCIL_KERNEL=reg selects the register-prefetch k_strip (kept for A/B
-// measurements); the default is the TMA-staged k_tma.
-bool use_tma() {
-  static const bool v = [] {
-    const char* e = std::getenv("SG_STENCIL_KERNEL");
-    return !(e && std::strcmp(e, "reg") == 0);
-  }();
-  return v;
+  if (count > static_cast<size_t>(VMAX)) return 0;
+  const uintptr_t pin = reinterpret_cast<uintptr_t>(in), pout = reinterpret_cast<uintptr_t>(out);
+  const bool aligned = d.nx % V == 0 && (pin | pout) % 16 == 0;
+  if (aligned && strip_supported(e, fn)) return 1;
+  if ((pin | pout) % sizeof(T) == 0 && general_supported(e, fn)) return 2;
+  return 0;
 }
 
 template <typename T, int L, int TP, typename Op>
-void launch_strip_lt(const KArgs<T>& a, dim3 grid, cudaStream_t s) {
-  if (use_tma()) {
-    using G = TmaGeom<T, L, L, TP, TP>;
-    auto kern = k_tma<T, L, L, TP, TP, Op>;
-    static int ctasPerSm = 0;  // per instantiation
-    if (ctasPerSm == 0) {
-      SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(G::smem_bytes)));
-      SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctasPerSm, kern, (TMA_WARPS + 1) * 32, G::smem_bytes));
-      if (ctasPerSm < 1) ctasPerSm = 1;
-    }
-    // Row segments: one wave of CTAs when the grid is small (each CTA's
-    // pipeline start-up is then paid once), 512-row segments (several waves)
-    // when it is large.
-    const int gx = (a.nx + G::CW - 1) / G::CW;
-    const int rows = a.row1 - a.row0;
-    const long long cap = 1LL * sm_count() * ctasPerSm;
-    long long seg = (1LL * rows * gx + cap - 1) / cap;
-    seg = std::max<long long>(seg, std::min(rows, 2 * G::RPS));
-    seg = std::min<long long>(seg, 512);
-    KArgs<T> b = a;
-    b.segRows = static_cast<int>(seg);
-    dim3 g2(gx, static_cast<unsigned>((rows + seg - 1) / seg));
-    kern<<<g2, (TMA_WARPS + 1) * 32, G::smem_bytes, s>>>(b);
-    return;
+void launch_tma_lt(const KArgs<T>& a, cudaStream_t s) {
+  using G = TmaGeom<T, L, L, TP, TP>;
+  auto kern = k_tma<T, L, L, TP, TP, Op>;
+  static int ctasPerSm = 0;  // per instantiation
+  if (ctasPerSm == 0) {
+    SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(G::smem_bytes)));
+    SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctasPerSm, kern, (TMA_WARPS + 1) * 32, G::smem_bytes));
+    if (ctasPerSm < 1) ctasPerSm = 1;
   }
-  constexpr int D = prefetch_depth<T, L>();
-  k_strip<T, L, L, TP, TP, D, Op><<<grid, STRIP_WARPS * 32, 0, s>>>(a);
+  const int gx = (a.nx + G::CW - 1) / G::CW;
+  const int rows = a.row1 - a.row0;
+  KArgs<T> b = a;
+  b.segRows = tma_segment_rows(rows, gx, ctasPerSm, G::RPS);
+  dim3 g2(gx, static_cast<unsigned>((rows + b.segRows - 1) / b.segRows));
+  kern<<<g2, (TMA_WARPS + 1) * 32, G::smem_bytes, s>>>(b);
 }
 
 template <typename T, typename Op>
-void launch_strip(const KArgs<T>& a, const sg_extents& e, dim3 grid, cudaStream_t s) {
+void launch_tma(const KArgs<T>& a, const sg_extents& e, cudaStream_t s) {
 #define SG_CASE(LV, TV) \
-  if (e.left == LV && e.top == TV) return launch_strip_lt<T, LV, TV, Op>(a, grid, s);
+  if (e.left == LV && e.top == TV) return launch_tma_lt<T, LV, TV, Op>(a, s);
   if constexpr (std::is_same_v<Op, OpWeights>) {
     SG_CASE(0, 0) SG_CASE(1, 0) SG_CASE(2, 0) SG_CASE(3, 0) SG_CASE(4, 0)
     SG_CASE(0, 1) SG_CASE(1, 1) SG_CASE(2, 1) SG_CASE(3, 1) SG_CASE(4, 1)
@@ -778,60 +123,28 @@ void launch_strip(const KArgs<T>& a, const sg_extents& e, dim3 grid, cudaStream_
     SG_CASE(1, 1)
   }
 #undef SG_CASE
-  invalid("internal: no strip kernel for these extents");
+  invalid("internal: no k_tma instantiation for these extents");
 }
-
 
 template <typename T>
 int launch_typed(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,
                  size_t count, const void* in, void* out, cudaStream_t s, const PeerRows& peers) {
   const int rows = d.row1 - d.row0;
   const int cols = d.col1 - d.col0;
-  if (rows <= 0 || cols <= 0) return strip_eligible<T>(d, e, fn, count, in, out) ? 1 : 0;
-  KArgs<T> a;
-  std::memset(static_cast<void*>(&a), 0, sizeof(a));
-  a.in = static_cast<const T*>(in);
-  a.out = static_cast<T*>(out);
-  a.wdev = nullptr;
-  a.nx = d.nx;
-  a.inRows = d.inRows;
-  a.inShift = d.inShift;
-  a.row0 = d.row0;
-  a.row1 = d.row1;
-  a.col0 = d.col0;
-  a.col1 = d.col1;
-  a.wrapX = d.wrapX;
-  a.wrapY = d.wrapY;
-  a.left = e.left;
-  a.right = e.right;
-  a.top = e.top;
-  a.bottom = e.bottom;
-  a.count = static_cast<int>(count);
-  a.peerUp = static_cast<T*>(peers.up);
-  a.peerDn = static_cast<T*>(peers.dn);
-  a.upRows = peers.upRows;
-  a.dnRow0 = peers.dnRow0;
-  if ((a.peerUp || a.peerDn) && !use_tma() && strip_eligible<T>(d, e, fn, count, in, out))
-    invalid("stencil: P2P halo forwarding needs the TMA kernel (SG_STENCIL_KERNEL=reg)");
-  const size_t nv = std::min(count, static_cast<size_t>(VMAX));
-  for (size_t k = 0; k < nv; ++k) a.v[k] = static_cast<T>(values[k]);
-
-  if (strip_eligible<T>(d, e, fn, count, in, out)) {
-    constexpr int V = VecT<T>::V;
-    const int strips = (d.nx + 32 * V - 1) / (32 * V);
-    const int gx = (strips + STRIP_WARPS - 1) / STRIP_WARPS;
-    // Aim for >= 8 resident warps' worth of work per SM-slot; long
-    // segments amortise the (H-1)-row vertical halo.
-    const long long targetWarps = 1LL * sm_count() * 16 * 6;
-    long long seg = (1LL * rows * strips + targetWarps - 1) / targetWarps;
-    const int H = e.top + e.bottom + 1;
-    seg = std::max<long long>(seg, std::min(rows, std::max(4, 2 * H)));
-    seg = std::min<long long>(seg, 512);
-    a.segRows = static_cast<int>(seg);
-    const int gy = static_cast<int>((rows + seg - 1) / seg);
-    dim3 grid(gx, gy);
-    with_op<void>(fn, [&](auto op) { launch_strip<T, decltype(op)>(a, e, grid, s); });
-    check_launch("stencil strip kernel");
+  const int kind = kernel_kind<T>(d, e, fn, count, in, out);
+  if (rows <= 0 || cols <= 0) return kind;
+  if (kind == 2) {
+    if constexpr (std::is_same_v<T, double>)
+      launch_stencil_g_f64(d, e, fn, values, count, in, out, s, peers);
+    else
+      launch_stencil_g_f32(d, e, fn, values, count, in, out, s, peers);
+    check_launch("stencil k_tma_g kernel");
+    return 2;
+  }
+  KArgs<T> a = make_args<T>(d, e, values, count, in, out, peers);
+  if (kind == 1) {
+    with_op<void>(fn, [&](auto op) { launch_tma<T, decltype(op)>(a, e, s); });
+    check_launch("stencil k_tma kernel");
     return 1;
   }
 
@@ -871,15 +184,15 @@ const char* function_name(int fn) {
 
 int stencil_kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size_t count,
                         sg_dtype dtype, const void* in, const void* out) {
-  return dtype == SG_F64 ? strip_eligible<double>(d, e, fn, count, in, out)
-                         : strip_eligible<float>(d, e, fn, count, in, out);
+  return dtype == SG_F64 ? kernel_kind<double>(d, e, fn, count, in, out)
+                         : kernel_kind<float>(d, e, fn, count, in, out);
 }
 
 int launch_stencil(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,
                    size_t count, sg_dtype dtype, const void* in, void* out, cudaStream_t stream,
                    const PeerRows& peers) {
   if (fn != SG_FN_NONE && (e.left + e.right + 1) * (e.top + e.bottom + 1) > GENERIC_FN_MAX &&
-      !strip_supported(e, fn))
+      !general_supported(e, fn))
     invalid("create_plan: device function windows are limited to 256 taps");
   if (dtype == SG_F64) return launch_typed<double>(d, e, fn, values, count, in, out, stream, peers);
   if (dtype == SG_F32) return launch_typed<float>(d, e, fn, values, count, in, out, stream, peers);

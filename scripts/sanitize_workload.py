@@ -1,6 +1,7 @@
 """Small end-to-end workload over every kernel family, for compute-sanitizer
 (memcheck / racecheck / synccheck): stencils (TMA fast path FP64/FP32,
-tall windows, non-periodic, generic), uniform and general penta solves, CH
+tall windows, non-periodic, generic; k_tma_g on asymmetric windows, odd
+rows and misaligned bases), uniform and general penta solves, CH
 steps (transposed-input sweeps, steady-state step, tail combine), the
 distributed CH P2P step and the slab P2P halo forwarding on simulated ranks."""
 import sys
@@ -30,6 +31,18 @@ for dt in (torch.float64, torch.float32):
         plan = sg.create_plan(sg.Direction.XY, mode, kind, a, b, 1, 1)
         sg.compute(plan)
         sg.destroy_plan(plan)
+    # k_tma_g: asymmetric windows, odd rows (every 16 B phase), misaligned base
+    for nx, off in ((97, 0), (2053, 1), (256, 1)):
+        buf_a = torch.rand(41 * nx + 1, dtype=dt, device="cuda")
+        buf_b = torch.zeros(41 * nx + 1, dtype=dt, device="cuda")
+        a2, b2 = buf_a[off:off + 41 * nx].view(41, nx), buf_b[off:off + 41 * nx].view(41, nx)
+        for ext, mode in [((3, 1, 0, 0), sg.BoundaryMode.Periodic), ((2, 1, 1, 2), sg.BoundaryMode.NonPeriodic),
+                          ((1, 1, 1, 1), sg.BoundaryMode.Periodic), ((0, 8, 4, 4), sg.BoundaryMode.Periodic)]:
+            nv = (ext[0] + ext[1] + 1) * (ext[2] + ext[3] + 1)
+            plan = sg.create_plan(sg.Direction.XY, mode, sg.WeightStencil(sg.Extents(*ext), list(rng.uniform(-1, 1, nv))),
+                                  a2, b2, 1, 1)
+            sg.compute(plan)
+            sg.destroy_plan(plan)
 # penta
 for periodic in (True, False):
     m = sg.PentaBatch(70, 40, periodic)

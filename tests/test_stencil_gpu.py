@@ -135,7 +135,7 @@ def test_function_stencils_bitwise(sg, orc, fn, ext, ncoe, periodic, shape):
     inp = rng.uniform(-1.5, 1.5, (ny, nx))
     coe = rng.uniform(-2, 2, max(ncoe, 1))[:ncoe]
     got = run_gpu(sg, inp, ext, coe, direction=direction_of(ext), periodic=periodic, fn=fn,
-                  expect_kind=1 if nx % 2 == 0 else 0)
+                  expect_kind=1 if nx % 2 == 0 else 2)
     want = orc.stencil(inp, ext, coe, periodic=periodic, fn=fn)
     assert bits_equal(got, want)
 
@@ -407,6 +407,116 @@ def test_concurrent_plans_on_disjoint_buffers(sg, orc):
     [t.join() for t in ts]
     for x, go in zip(ins, outs):
         assert bits_equal(go.values, orc.stencil(x, (2, 1, 1, 2), w))
+
+
+# ------------------------------------------- general shapes / alignments
+
+
+def _general_cases():
+    """Asymmetric windows up to 9 x 9 (every left/right and top/bottom split
+    of a few widths/heights) — k_tma_g's territory."""
+    cases = [(3, 1, 0, 0), (0, 2, 0, 0), (2, 1, 1, 2), (0, 1, 0, 1), (1, 0, 2, 0), (4, 0, 0, 4),
+             (0, 0, 3, 1), (0, 0, 0, 2), (3, 2, 1, 0), (1, 3, 4, 2), (8, 0, 0, 0), (0, 0, 0, 8),
+             (5, 3, 2, 6), (0, 8, 8, 0), (6, 2, 1, 1), (2, 2, 4, 3)]
+    return cases
+
+
+@pytest.mark.parametrize("ext", _general_cases())
+@pytest.mark.parametrize("periodic", [True, False])
+@pytest.mark.parametrize("nx", [320, 97, 2053])
+def test_general_kernel_asymmetric_and_odd_bitwise(sg, orc, ext, periodic, nx):
+    """k_tma_g: asymmetric windows (test_stencil.cpp:557-568 generalised) and
+    odd row pitches (rows at every 16 B phase), periodic and not, one column
+    block and several — bitwise vs the oracle, frame untouched."""
+    rng = np.random.default_rng(hash((ext, nx, periodic)) & 0xFFFF)
+    l, r, t, b = ext
+    ny = 41
+    if l + r >= nx or t + b >= ny:
+        pytest.skip("window wider than the grid")
+    inp = rng.uniform(-1, 1, (ny, nx))
+    w = rng.uniform(-2, 2, (l + r + 1) * (t + b + 1))
+    sentinel = np.full_like(inp, -12345.678)
+    got = run_gpu(sg, inp, ext, w, direction=direction_of(ext), periodic=periodic, out=sentinel,
+                  expect_kind=2)
+    want = orc.stencil(inp, ext, w, periodic=periodic, out=sentinel)
+    assert bits_equal(got, want)
+
+
+def test_reference_asymmetric_case_3_1_0_0(sg, orc):
+    """test_stencil.cpp:557-568: X stencil {3,1,0,0} on a periodic grid equals
+    the single-point evaluation everywhere."""
+    rng = np.random.default_rng(557)
+    inp = rng.uniform(-1, 1, (16, 64))
+    w = [0.5, -1.0, 2.0, 0.25, -0.75]
+    got = run_gpu(sg, inp, (3, 1, 0, 0), w, direction=0, expect_kind=2)
+    assert bits_equal(got, orc.stencil(inp, (3, 1, 0, 0), w))
+
+
+@pytest.mark.parametrize("fn,ext,ncoe", FUNCS)
+def test_general_kernel_functions_misaligned_pointers(sg, orc, fn, ext, ncoe):
+    """Device grids whose base pointers are 8 B off 16 B alignment (a view one
+    element into an allocation) run k_tma_g, bitwise."""
+    import torch
+    rng = np.random.default_rng(77)
+    ny, nx = 33, 256
+    inp = rng.uniform(-1.5, 1.5, (ny, nx))
+    coe = rng.uniform(-2, 2, max(ncoe, 1))[:ncoe]
+    bi = torch.zeros(ny * nx + 1, dtype=torch.float64, device="cuda")
+    bo = torch.zeros(ny * nx + 3, dtype=torch.float64, device="cuda")
+    ti = bi[1:].view(ny, nx)
+    to = bo[3:].view(ny, nx)
+    ti.copy_(torch.from_numpy(inp))
+    kind = sg.FunctionStencil(sg.Extents(*ext), fn, list(coe))
+    for periodic in (True, False):
+        to.zero_()
+        plan = sg.create_plan(direction_of(ext), sg.BoundaryMode.Periodic if periodic else sg.BoundaryMode.NonPeriodic,
+                              kind, ti, to, 1, 1)
+        assert plan.kernel_kind() == 2
+        sg.compute(plan)
+        want = orc.stencil(inp, ext, coe, periodic=periodic, fn=fn)
+        assert bits_equal(to.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("ext", [(1, 1, 1, 1), (3, 1, 0, 0), (2, 1, 1, 2), (4, 4, 4, 4)])
+@pytest.mark.parametrize("nx", [255, 1026, 4099])
+def test_general_kernel_fp32_odd_rows(sg, orc, ext, nx):
+    """FP32 at every 16 B row phase (nx % 4 != 0): 1e-5 vs the FP64 oracle on
+    the float-rounded input."""
+    import torch
+    rng = np.random.default_rng(nx)
+    ny = 37
+    inp32 = rng.uniform(-1, 1, (ny, nx)).astype(np.float32)
+    l, r, t, b = ext
+    w = rng.uniform(-2, 2, (l + r + 1) * (t + b + 1))
+    ti = torch.from_numpy(inp32).cuda()
+    to = torch.zeros_like(ti)
+    plan = sg.create_plan(direction_of(ext), sg.BoundaryMode.Periodic, sg.WeightStencil(sg.Extents(*ext), list(w)),
+                          ti, to, 1, 1)
+    assert plan.kernel_kind() == (1 if (nx % 4 == 0 and l == r and t == b) else 2)
+    sg.compute(plan)
+    got = to.cpu().numpy().astype(np.float64)
+    want = orc.stencil(inp32.astype(np.float64), ext, w)
+    assert np.max(np.abs(got - want)) <= 1e-5 * np.max(np.abs(want))
+
+
+def test_general_kernel_large_odd_grid_shift_property(sg, orc):
+    """4097 x 3001 periodic {2,1,1,2}: bitwise vs the oracle, and the
+    cyclic-shift equivariance (test_stencil.cpp:442-460) on the device."""
+    import torch
+    rng = np.random.default_rng(4097)
+    w = rng.uniform(-1, 1, 16)
+    inp = rng.uniform(-1, 1, (3001, 4097))
+    ti = torch.from_numpy(inp).cuda()
+    to, t2 = torch.empty_like(ti), torch.empty_like(ti)
+    kind = sg.WeightStencil(sg.Extents(2, 1, 1, 2), list(w))
+    p = sg.create_plan(sg.Direction.XY, sg.BoundaryMode.Periodic, kind, ti, to, 1, 1)
+    assert p.kernel_kind() == 2
+    sg.compute(p)
+    assert bits_equal(to.cpu().numpy(), orc.stencil(inp, (2, 1, 1, 2), w))
+    sh = torch.roll(ti, shifts=(17, -301), dims=(0, 1)).contiguous()
+    p2 = sg.create_plan(sg.Direction.XY, sg.BoundaryMode.Periodic, kind, sh, t2, 1, 1)
+    sg.compute(p2)
+    assert torch.equal(torch.roll(to, shifts=(17, -301), dims=(0, 1)), t2)
 
 
 # ----------------------------------------------------------------- FP32
