@@ -521,14 +521,13 @@ __device__ __forceinline__ void tp_tile_origin(int t, int tilesX, int band, int&
   j0 = (b * band + r % band) * RY;
 }
 
+// The pipeline of one CTA (index cta of nCta walking the tiles).
 template <bool NONLINEAR>
-__global__ void __launch_bounds__(TP_THREADS, 1) k_rhs_tp(const double* __restrict__ cc, const double* __restrict__ cp,
-                                                         const double* __restrict__ wv, const CorrTables cy,
-                                                         double* __restrict__ cnew, double* __restrict__ rhs,
-                                                         int nx, int ny, int band,
-                                                         const __grid_constant__ RhsParams P,
-                                                         const __grid_constant__ TpMaps M) {
-  extern __shared__ __align__(128) unsigned char tp_raw[];
+__device__ __forceinline__ void rhs_tp_body(const double* __restrict__ cc, const double* __restrict__ cp,
+                                            const double* __restrict__ wv, const CorrTables& cy,
+                                            double* __restrict__ cnew, double* __restrict__ rhs, int nx, int ny,
+                                            int band, const RhsParams& P, const TpMaps& M, int cta, int nCta,
+                                            unsigned char* tp_raw) {
   TpStage* st = reinterpret_cast<TpStage*>(tp_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(tp_raw + TP_NST * sizeof(TpStage));
   uint64_t* empty = full + TP_NST;
@@ -543,14 +542,14 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_rhs_tp(const double* __restri
   }
   __syncthreads();
   pdl_wait();
-  const int myTiles = blockIdx.x < nTiles ? (nTiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int myTiles = cta < nTiles ? (nTiles - 1 - cta) / nCta + 1 : 0;
 
   if (warp == 8 * TP_NG) {  // ---- producer (one thread)
     if (lane != 0) return;
     for (int k = 0; k < myTiles; ++k) {
       const int s = k % TP_NST;
       if (k >= TP_NST) ch_mbar_wait(empty + s, ((k / TP_NST) - 1) & 1);
-      const int tile = blockIdx.x + k * gridDim.x;
+      const int tile = cta + k * nCta;
       int i0, j0;
       tp_tile_origin(tile, tilesX, band, i0, j0);
       TpStage& S = st[s];
@@ -591,7 +590,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_rhs_tp(const double* __restri
     // first pins the phase (tile k - 2 NST was this group's own release).
     if (k >= TP_NST) ch_mbar_wait(empty + s, ((k / TP_NST) - 1) & 1);
     ch_mbar_wait(full + s, (k / TP_NST) & 1);
-    const int tile = blockIdx.x + k * gridDim.x;
+    const int tile = cta + k * nCta;
     int i0, j0;
     tp_tile_origin(tile, tilesX, band, i0, j0);
     TpStage& S = st[s];
@@ -729,6 +728,17 @@ __global__ void __launch_bounds__(TP_THREADS, 1) k_rhs_tp(const double* __restri
       *reinterpret_cast<double2*>(rhs + static_cast<long long>(j0 + y0 + r) * nx + i0 + x0) = o;
     }
   }
+}
+
+template <bool NONLINEAR>
+__global__ void __launch_bounds__(TP_THREADS, 1) k_rhs_tp(const double* __restrict__ cc, const double* __restrict__ cp,
+                                                         const double* __restrict__ wv, const CorrTables cy,
+                                                         double* __restrict__ cnew, double* __restrict__ rhs,
+                                                         int nx, int ny, int band,
+                                                         const __grid_constant__ RhsParams P,
+                                                         const __grid_constant__ TpMaps M) {
+  extern __shared__ __align__(128) unsigned char tp_raw[];
+  rhs_tp_body<NONLINEAR>(cc, cp, wv, cy, cnew, rhs, nx, ny, band, P, M, blockIdx.x, gridDim.x, tp_raw);
 }
 
 int ch_sm_count() {
@@ -1090,6 +1100,7 @@ struct ChState {
   // transposed with the x Woodbury correction (no transpose kernel)
   double* xT = nullptr;
   bool xpipe = false;
+
   DevicePenta fx, fy;
   RhsParams rp{};
   // CUDA graphs keyed by (kind, ic, ip): kind 0 = full step, 1 = head (step
@@ -1167,6 +1178,7 @@ struct ChState {
     // the transposed-input sweep pipeline (see xpipe)
     if (xin_ok() && rhs_kind() == 1 && p.nx % RX == 0) {
       xT = dalloc(cnt);
+
       xpipe = penta_sweep_xin(fx.t, p.ny, p.nx, xT, rhsT, nullptr, nullptr, y4x, stream, false, false) &&
               penta_sweep_xin(fy.t, p.nx, p.ny, w, xT, fx.t.W, y4x, y4y, stream, false, false);
     }
