@@ -53,7 +53,8 @@ typedef enum sg_function {
   SG_FN_CENTRAL_SECOND = 4,       /* fn_central_second, tests/test_stencil.cpp:70-77 (3x1, 1 coe) */
   SG_FN_LAP_CUBE_DIFF_FIRST = 5,  /* fn_lap_cube_diff_first, tests/test_stencil.cpp:79-85 (3x3, 2 coe) */
   SG_FN_WEIGHTED_3X3 = 6,         /* fn_weighted_3x3, tests/test_stencil.cpp:88-93 (3x3, 9 coe) */
-  SG_FN_COUNT = 7
+  SG_FN_COUNT = 7,
+  SG_FN_JIT_BASE = 1000           /* functions registered from source: 1000, 1001, ... */
 } sg_function;
 
 typedef struct sg_extents { int left, right, top, bottom; } sg_extents; /* grid.hpp:53-62 */
@@ -74,6 +75,22 @@ sg_status sg_init(int device);
 int sg_function_min_coe(int fn);
 /* Name of a device window function ("ch_nonlinear_window", ...). */
 const char* sg_function_name(int fn);
+/* Register a window function from CUDA C++ SOURCE — the reference's
+ * StencilFunction is arbitrary user code (stencil.hpp:20-25), which a GPU
+ * cannot call through a host pointer. `body` is the body of
+ *     template <typename T> T fn(const T* window, const T* coe, int rowStride)
+ * (T = double, or float for FP32 plans; entry (p, q) of the window is
+ * window[q*rowStride + p], exactly the reference's contract), e.g.
+ *     "return (window[0] - 2.0 * window[1] + window[2]) * coe[0];"
+ * It is compiled at run time by NVRTC for sm_100a with --fmad=false (the
+ * reference's -ffp-contract=off) into the library's own stencil kernels,
+ * once per (dtype, window shape, kernel) on first use; FP64 results equal a
+ * host evaluation of the same expression bitwise. *fnId receives the id
+ * (>= SG_FN_JIT_BASE) to pass as sg_plan_create's fn; any window is accepted
+ * (the function must not read outside it, as in the reference), with up to
+ * 256 coefficients. A body that does not compile returns
+ * SG_ERR_INVALID_ARGUMENT with the compiler log in sg_last_error(). */
+sg_status sg_register_function_source(const char* name, const char* body, int* fnId);
 
 /* ----------------------------------------------------------- grid helpers */
 /* wrap(i, n): grid.cpp:42-47. SG_ERR_INVALID_ARGUMENT if n <= 0. */

@@ -6,7 +6,8 @@
 //
 // Differences a caller can observe:
 //  * StencilFunction pointers are host code; a FunctionStencil's fn must be
-//    registered with a device twin (register_device_function). The
+//    registered with a device twin (register_device_function) or with its
+//    source (register_device_function_source: compiled at run time). The
 //    reference's own window functions are pre-registered (stengrid::functions).
 //    An unregistered fn throws std::invalid_argument — there is no CPU path.
 //  * compute() is synchronous and host-coherent for both residency hints,
@@ -19,6 +20,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <variant>
 #include <vector>
 
@@ -113,6 +115,25 @@ inline void register_device_function(StencilFunction hostFn, sg_function deviceF
     throw std::invalid_argument("register_device_function: bad arguments");
   std::lock_guard<std::mutex> lk(detail::registry_mutex());
   detail::registry()[hostFn] = deviceFn;
+}
+
+/// Extension — register a host window function together with its SOURCE:
+/// `body` is the body of  T fn(const T* window, const T* coe, int rowStride)
+/// (the same statements as the host function, T = double or float), which the
+/// library compiles at run time (NVRTC, sm_100a, no FMA contraction) into its
+/// stencil kernels (sg.h: sg_register_function_source). After this call
+/// FunctionStencil{ext, hostFn, coe} runs on the GPU like the reference's own
+/// functions; FP64 results equal the host function's bitwise when the body is
+/// the same expression. Throws std::invalid_argument (with the compiler log)
+/// if the body does not compile.
+inline int register_device_function_source(StencilFunction hostFn, const std::string& body,
+                                           const std::string& name = "user_function") {
+  if (hostFn == nullptr) throw std::invalid_argument("register_device_function_source: null function");
+  int id = -1;
+  detail::check(sg_register_function_source(name.c_str(), body.c_str(), &id));
+  std::lock_guard<std::mutex> lk(detail::registry_mutex());
+  detail::registry()[hostFn] = id;
+  return id;
 }
 
 inline int device_function_id(StencilFunction fn) {

@@ -10,8 +10,8 @@ from ._lib import (CudaError, DomainError, InvalidArgument, LogicError, NoDevice
                    PentaSolveError, launch_count)
 from .stencil import (BoundaryMode, Direction, Extents, FunctionStencil, Grid2D, Residency,
                       StencilPlan, WeightStencil, compute, create_plan, destroy_plan,
-                      get_device_map, launch_slab, make_tiles, mark_host_dirty, set_device_map, swap_plan,
-                      sync_to_host, wrap)
+                      get_device_map, launch_slab, make_tiles, mark_host_dirty, register_function_source,
+                      set_device_map, swap_plan, sync_to_host, wrap)
 
 from .penta import (Axis, PentaBatch, PentaFactor, PeriodicPentaFactor, RhsBatch,
                     build_hyperdiffusion_operator, deinterleave, interleave, solve_batch,
@@ -34,6 +34,6 @@ __all__ = [
     "nonlinear_laplacian_coefficients", "RunSink", "run", "simpson_mean", "s_metric", "k1_metric",
     "BoundaryMode", "Direction", "Extents", "FunctionStencil", "Grid2D", "Residency",
     "StencilPlan", "WeightStencil", "compute", "create_plan", "destroy_plan", "launch_slab",
-    "make_tiles", "mark_host_dirty", "set_device_map", "get_device_map", "swap_plan", "sync_to_host", "wrap", "InvalidArgument",
+    "make_tiles", "mark_host_dirty", "register_function_source", "set_device_map", "get_device_map", "swap_plan", "sync_to_host", "wrap", "InvalidArgument",
     "LogicError", "DomainError", "PentaSolveError", "CudaError", "NoDeviceError", "launch_count",
 ]

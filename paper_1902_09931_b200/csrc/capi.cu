@@ -245,6 +245,8 @@ sg_status sg_plan_create(sg_direction dir, sg_boundary mode, sg_extents ext, sg_
         sg::invalid(std::string("create_plan: too few coefficients for ") + sg::function_name(fn));
       if (W * H > 256 && !(W == 3 && H <= 3))
         sg::invalid("create_plan: device function windows are limited to 256 taps");
+      if (fn >= SG_FN_JIT_BASE && count > 256)
+        sg::invalid("create_plan: at most 256 coefficients for a source function");
     }
     if (numWorkers < 1) sg::invalid("create_plan: numWorkers must be >= 1");
     auto tiles = tiles_for(ny, numTiles);

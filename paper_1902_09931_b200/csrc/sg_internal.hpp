@@ -109,6 +109,14 @@ void launch_stencil_g_f32(const sg_slab_desc& d, const sg_extents& e, int fn, co
 // 1 k_tma, 0 k_generic).
 int stencil_kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size_t count,
                         sg_dtype dtype, const void* in, const void* out);
+// Window functions registered from source (sg_jit.cu): ids from
+// SG_FN_JIT_BASE, compiled by NVRTC per (dtype, window, kernel) on first use.
+bool jit_function(int fn, std::string* name);
+const char* jit_function_name(int fn);
+int jit_register(const std::string& name, const std::string& body);
+int launch_stencil_jit(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values, size_t count,
+                       sg_dtype dtype, const void* in, void* out, cudaStream_t stream, const PeerRows& peers,
+                       bool launch);
 // Minimum window (W, H) and coefficient count a device function reads.
 bool function_shape(int fn, int* minW, int* minH, int* minCoe);
 const char* function_name(int fn);

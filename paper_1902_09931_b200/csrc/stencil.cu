@@ -171,6 +171,11 @@ int launch_typed(const sg_slab_desc& d, const sg_extents& e, int fn, const doubl
 }  // namespace
 
 bool function_shape(int fn, int* minW, int* minH, int* minCoe) {
+  if (jit_function(fn, nullptr)) {  // source functions: any window (the user's contract)
+    *minW = *minH = 1;
+    *minCoe = 0;
+    return true;
+  }
   if (fn < 0 || fn >= SG_FN_COUNT) return false;
   *minW = kFn[fn].minW;
   *minH = kFn[fn].minH;
@@ -179,11 +184,14 @@ bool function_shape(int fn, int* minW, int* minH, int* minCoe) {
 }
 
 const char* function_name(int fn) {
+  if (fn >= SG_FN_JIT_BASE) return jit_function_name(fn);
   return (fn >= 0 && fn < SG_FN_COUNT) ? kFn[fn].name : nullptr;
 }
 
 int stencil_kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size_t count,
                         sg_dtype dtype, const void* in, const void* out) {
+  if (fn >= SG_FN_JIT_BASE)
+    return launch_stencil_jit(d, e, fn, nullptr, count, dtype, in, const_cast<void*>(out), nullptr, PeerRows{}, false);
   return dtype == SG_F64 ? kernel_kind<double>(d, e, fn, count, in, out)
                          : kernel_kind<float>(d, e, fn, count, in, out);
 }
@@ -191,6 +199,8 @@ int stencil_kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size
 int launch_stencil(const sg_slab_desc& d, const sg_extents& e, int fn, const double* values,
                    size_t count, sg_dtype dtype, const void* in, void* out, cudaStream_t stream,
                    const PeerRows& peers) {
+  if (fn >= SG_FN_JIT_BASE)
+    return launch_stencil_jit(d, e, fn, values, count, dtype, in, out, stream, peers, true);
   if (fn != SG_FN_NONE && (e.left + e.right + 1) * (e.top + e.bottom + 1) > GENERIC_FN_MAX &&
       !general_supported(e, fn))
     invalid("create_plan: device function windows are limited to 256 taps");

@@ -15,458 +15,10 @@
 #include <type_traits>
 
 #include "sg_internal.hpp"
+#include "stencil_dev.cuh"
 
 namespace sg {
 namespace {
-
-constexpr int VMAX = 256;       // values carried in the parameter bank
-constexpr int GENERIC_FN_MAX = 256;  // window taps a generic device function may see
-
-template <typename T>
-struct KArgs {
-  const T* __restrict__ in;
-  T* __restrict__ out;
-  const T* __restrict__ wdev;  // weights when count > VMAX (generic path only)
-  int nx, inRows, inShift;
-  int row0, row1, col0, col1;
-  int wrapX, wrapY;
-  int left, right, top, bottom;
-  int segRows;
-  int count;
-  // P2P halo forwarding (multi-GPU y-slabs): output rows j < upRows are
-  // also stored to peerUp + j*nx (the up neighbour's bottom halo), rows
-  // j >= dnRow0 to peerDn + (j - dnRow0)*nx (the down neighbour's top
-  // halo) — peer memory over NVLink; null = none
-  T* peerUp;
-  T* peerDn;
-  int upRows, dnRow0;
-  T v[VMAX];
-};
-
-// Store one output value (and its P2P halo copies).
-template <typename T>
-__device__ __forceinline__ void put_out(const KArgs<T>& a, long long j, long long i, T v) {
-  a.out[j * a.nx + i] = v;
-  if (a.peerUp && j < a.upRows) a.peerUp[j * a.nx + i] = v;
-  if (a.peerDn && j >= a.dnRow0) a.peerDn[(j - a.dnRow0) * a.nx + i] = v;
-}
-
-// ----------------------------------------------------------- window ops
-// Device twins of the reference's window functions. Same expression trees,
-// evaluated without contraction, so FP64 results are bitwise identical.
-struct OpWeights {};  // marker: weight stencil
-
-struct OpChNonlinear {  // cahn_hilliard.cpp:36-47
-  template <typename T>
-  __device__ static T apply(const T* w, const T* coe, int rs) {
-    T acc = T(0);
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-      for (int p = 0; p < 3; ++p) {
-        const T v = w[q * rs + p];
-        acc += coe[q * 3 + p] * (v * v * v - v);
-      }
-    return acc;
-  }
-};
-struct OpCentralDifference {  // tools/main.cpp:47-49
-  template <typename T>
-  __device__ static T apply(const T* w, const T* coe, int) {
-    return (w[0] - T(2) * w[1] + w[2]) * coe[0];
-  }
-};
-struct OpCenter {  // tests/test_stencil.cpp:68
-  template <typename T>
-  __device__ static T apply(const T* w, const T*, int rs) {
-    return w[rs + 1];
-  }
-};
-struct OpCentralSecond {  // tests/test_stencil.cpp:70-77
-  template <typename T>
-  __device__ static T apply(const T* w, const T* coe, int) {
-    T acc = T(0);
-    acc += coe[0] * w[0];
-    acc += (T(-2) * coe[0]) * w[1];
-    acc += coe[0] * w[2];
-    return acc;
-  }
-};
-struct OpLapCubeDiffFirst {  // tests/test_stencil.cpp:79-85
-  template <typename T>
-  __device__ static T g(T v) { return v * v * v - v; }
-  template <typename T>
-  __device__ static T apply(const T* w, const T* coe, int rs) {
-    const T gm = g(w[rs + 1]);
-    const T x = (g(w[rs]) - T(2) * gm) + g(w[rs + 2]);
-    const T y = (g(w[1]) - T(2) * gm) + g(w[2 * rs + 1]);
-    return coe[0] * x + coe[1] * y;
-  }
-};
-struct OpWeighted3x3 {  // tests/test_stencil.cpp:88-93
-  template <typename T>
-  __device__ static T apply(const T* w, const T* coe, int rs) {
-    T acc = T(0);
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-      for (int p = 0; p < 3; ++p) acc += coe[q * 3 + p] * w[q * rs + p];
-    return acc;
-  }
-};
-
-template <typename T>
-struct VecT;
-template <>
-struct VecT<double> {
-  static constexpr int V = 2;
-  using type = double2;
-};
-template <>
-struct VecT<float> {
-  static constexpr int V = 4;
-  using type = float4;
-};
-
-__device__ __forceinline__ int wrap_idx(long long i, int n) {
-  long long r = i % n;
-  return static_cast<int>(r < 0 ? r + n : r);
-}
-
-// ---------------------------------------------------------------- k_tma
-// The fast path. Each consumer warp owns a strip of 32*V columns (V = 16
-// bytes / sizeof(T)) and marches down a segment of rows; rows are staged into a per-warp shared-memory
-// ring by the bulk-copy engine (cp.async.bulk, TMA 1D, completion on an
-// mbarrier per stage): ONE copy per row brings the strip's 32*V columns
-// plus the L/R halo columns (rounded out to 16 B) — halos are loaded once
-// and never shuffled; only edge strips add a 16-32 B wrap copy. Registers
-// hold just the H-row window, and the ring keeps S*RPS rows per warp in
-// flight without register cost. (A register-prefetch variant with shuffled
-// halos, k_strip, took 3.39 ms against k_tma's 2.62 ms for the 32768^2
-// FP64 3x3 in ncu, profiles/r01_k_strip_f64_3x3_ncu_summary.txt; removed.)
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!ok);
-}
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-// The mbarrier receives one arrival when all prior cp.async of this thread land.
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// CTA geometry: TMA_WARPS consumer warps side by side cover CW columns; one
-// producer warp streams rows (CW + halos) into a STAGES x RPS ring.
-#ifndef SG_TMA_WARPS
-#define SG_TMA_WARPS 16
-#endif
-constexpr int TMA_WARPS = SG_TMA_WARPS;
-// Release of a ring stage by the consumers: every thread arrives on the
-// "empty" mbarrier (1), or each warp's lane 0 after __syncwarp (0).
-#ifndef SG_EMPTY_ALL_LANES
-#define SG_EMPTY_ALL_LANES 1
-#endif
-
-template <typename T, int L, int R, int TP, int BT>
-struct TmaGeom {
-  static constexpr int V = VecT<T>::V;
-  static constexpr int SW = 32 * V;
-  static constexpr int CW = TMA_WARPS * SW;
-  static constexpr int LP = ((L + V - 1) / V) * V;  // left pad, 16 B granules
-  static constexpr int RP = ((R + V - 1) / V) * V;
-  static constexpr int ROW = LP + CW + RP;  // elements per staged row (~2 KB)
-  static constexpr int H = TP + BT + 1;
-  // Rows per stage: a multiple of H so the register window is a ring whose
-  // slot for every unrolled row is a compile-time constant (no moves).
-  static constexpr int RPS = H >= 2 ? H : 2;
-  static constexpr int STAGES = (9 + RPS - 1) / RPS >= 2 ? (9 + RPS - 1) / RPS : 2;
-  static constexpr size_t stage_bytes = static_cast<size_t>(RPS) * ROW * sizeof(T);
-  static constexpr size_t smem_bytes = STAGES * stage_bytes + 2 * STAGES * sizeof(uint64_t);
-};
-
-// Launch bounds of k_tma: the compiler's register choice (one CTA per SM
-// guaranteed); SG_TMA_MINB2=1 sizes for two where the rings fit — measured
-// slower (3x3 0.97 -> 0.93 of HBM, 5x5 0.61 -> 0.50 at 16384^2 FP64).
-#ifndef SG_TMA_MINB2
-#define SG_TMA_MINB2 -1
-#endif
-template <typename T, int L, int R, int TP, int BT>
-constexpr int tma_min_blocks() {
-  constexpr bool fits2 = 2 * TmaGeom<T, L, R, TP, BT>::smem_bytes <= 227 * 1024;
-  if (SG_TMA_MINB2 == 0 || !fits2) return 1;
-  if (SG_TMA_MINB2 == 1) return 2;
-  return 1;
-}
-
-template <typename T, int L, int R, int TP, int BT, typename Op>
-__global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tma_min_blocks<T, L, R, TP, BT>())) k_tma(const __grid_constant__ KArgs<T> a) {
-  using G = TmaGeom<T, L, R, TP, BT>;
-  using VT = typename VecT<T>::type;
-  constexpr int V = G::V, SW = G::SW, CW = G::CW, LP = G::LP, RP = G::RP, ROW = G::ROW;
-  constexpr int H = G::H, RPS = G::RPS, STAGES = G::STAGES;
-  constexpr int W = L + R + 1;
-  constexpr int E = L + V + R;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* ring = reinterpret_cast<T*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * G::stage_bytes);
-  uint64_t* empty = full + STAGES;
-
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int nx = a.nx;
-  const int cx0 = blockIdx.x * CW;
-  const int ra = a.row0 + blockIdx.y * a.segRows;
-  const int rb = min(ra + a.segRows, a.row1);
-  if (ra >= rb) return;  // CTA-uniform
-  const int nIn = (rb - ra) + H - 1;
-  const int nStages = (nIn + RPS - 1) / RPS;
-
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < STAGES; ++k) {
-      mbar_init(&full[k], 2);  // expect_tx arrival + cp.async (halo) arrival
-      mbar_init(&empty[k], SG_EMPTY_ALL_LANES ? TMA_WARPS * 32 : TMA_WARPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == TMA_WARPS) {
-    // ---------------- producer: per row, one bulk copy of the CTA's own
-    // columns (128 B aligned, whole lines: no over-fetch) and 16 B cp.async
-    // granules for the halo columns (wrapped in index math at grid edges).
-    if (lane != 0) return;
-    const int validC = min(CW, nx - cx0);
-    const uint32_t mainBytes = static_cast<uint32_t>(validC * sizeof(T));
-    int hsrc[(LP + RP) / V > 0 ? (LP + RP) / V : 1];
-    int hdst[(LP + RP) / V > 0 ? (LP + RP) / V : 1];
-    int nh = 0;
-#pragma unroll
-    for (int k = 0; k < LP / V; ++k) {
-      const int c = cx0 - LP + k * V;
-      if (c >= 0 || a.wrapX) {
-        hsrc[nh] = c >= 0 ? c : c + nx;
-        hdst[nh++] = k * V;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < RP / V; ++k) {
-      const int c = cx0 + validC + k * V;
-      if (c < nx || a.wrapX) {
-        hsrc[nh] = c < nx ? c : c - nx;
-        hdst[nh++] = LP + validC + k * V;
-      }
-    }
-    int rf = ra + a.inShift - TP;
-    if (a.wrapY) rf = wrap_idx(rf, a.inRows);
-    const T* __restrict__ in = a.in;
-    for (int g = 0; g < nStages; ++g) {
-      const int slot = g % STAGES;
-      if (g >= STAGES) mbar_wait(&empty[slot], ((g / STAGES) + 1) & 1);
-      mbar_expect_tx(&full[slot], mainBytes * RPS);
-      T* sstage = ring + slot * (RPS * ROW);
-#pragma unroll
-      for (int k = 0; k < RPS; ++k) {
-        const T* grow = in + static_cast<long long>(rf) * nx;
-        T* srow = sstage + k * ROW;
-        bulk_g2s(srow + LP, grow + cx0, mainBytes, &full[slot]);
-        for (int h = 0; h < nh; ++h) cp_async16(srow + hdst[h], grow + hsrc[h]);
-        ++rf;
-        if (a.wrapY) {
-          if (rf == a.inRows) rf = 0;
-        } else if (rf >= a.inRows) {
-          rf = a.inRows - 1;
-        }
-      }
-      cp_async_mbar_arrive(&full[slot]);
-    }
-    return;
-  }
-
-  // ---------------- consumers
-  const int xb = cx0 + warp * SW + lane * V;
-  const bool laneValid = xb < nx;
-  // Weight stencils with tall windows (H >= 5) keep H PENDING OUTPUT
-  // accumulators instead of H input rows: each arriving input row adds its
-  // tap row to every output that needs it. Output o still accumulates its
-  // taps row by row (q ascending, then p) — the reference's order — since
-  // rows arrive top to bottom. Registers: H*V + E instead of H*E (a 9x9
-  // window would otherwise spill).
-  constexpr bool ACC = std::is_same_v<Op, OpWeights> && H >= 5;
-  T win[ACC ? 1 : H][E];  // ring: input row t lives in win[t % H]
-  T pend[ACC ? H : 1][V];  // ACC: output started at local input row u lives in pend[u % H]
-  T* __restrict__ orow = a.out + static_cast<long long>(ra - (H - 1)) * nx + xb;
-  const bool vecStore = laneValid && xb >= a.col0 && xb + V <= a.col1;
-  const long long rowStep = nx;
-  int j = ra - (H - 1);  // output row completed by the current input row
-  for (int g = 0; g < nStages; ++g) {
-    const int slot = g % STAGES;
-    mbar_wait(&full[slot], (g / STAGES) & 1);
-    const T* sbase = ring + slot * (RPS * ROW) + LP + warp * SW + lane * V;
-#pragma unroll
-    for (int k = 0; k < RPS; ++k) {
-      const T* srow = sbase + k * ROW;
-      T* e = win[ACC ? 0 : k % H];
-      const VT c = *reinterpret_cast<const VT*>(srow);
-      if constexpr (V == 2) {
-        e[L] = c.x;
-        e[L + 1] = c.y;
-      } else {
-        e[L] = c.x;
-        e[L + 1] = c.y;
-        e[L + 2] = c.z;
-        e[L + 3] = c.w;
-      }
-      // Horizontal halos: scalar shared loads at a 16 B lane stride (2-way
-      // bank conflicts, ~0.1 per output in ncu). Shuffling them from the
-      // neighbouring lanes' vectors instead removed 83 % of the conflicts
-      // but measured slower (3x3 98.4 -> 97.2 % of HBM, 5x5 FP64-bound
-      // 0.63 -> 0.47): the loads are not on the critical resource.
-#pragma unroll
-      for (int p = 0; p < L; ++p) e[p] = srow[p - L];
-#pragma unroll
-      for (int p = 0; p < R; ++p) e[L + V + p] = srow[V + p];
-      // Output row j uses input rows j-TP .. j+BT = the H most recent rows,
-      // oldest in slot (k + 1) % H.
-      T res[V];
-      if constexpr (ACC) {
-        // this row is tap row q of the output started q rows ago (slot
-        // (k - q) mod H; RPS is a multiple of H, so slots are compile-time)
-#pragma unroll
-        for (int q = 0; q < H; ++q) {
-          T* acc = pend[((k - q) % H + H) % H];
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            if (q == 0) acc[v] = T(0);
-#pragma unroll
-            for (int p = 0; p < W; ++p) acc[v] += a.v[q * W + p] * e[v + p];
-          }
-        }
-#pragma unroll
-        for (int v = 0; v < V; ++v) res[v] = pend[(k + 1) % H][v];  // completed (q = H-1 just added)
-      } else {
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        if constexpr (std::is_same_v<Op, OpWeights>) {
-          T acc = T(0);
-#pragma unroll
-          for (int q = 0; q < H; ++q)
-#pragma unroll
-            for (int p = 0; p < W; ++p) acc += a.v[q * W + p] * win[(k + 1 + q) % H][v + p];
-          res[v] = acc;
-        } else {
-          T w[H * W];
-#pragma unroll
-          for (int q = 0; q < H; ++q)
-#pragma unroll
-            for (int p = 0; p < W; ++p) w[q * W + p] = win[(k + 1 + q) % H][v + p];
-          res[v] = Op::template apply<T>(w, a.v, W);
-        }
-      }
-      }
-      if (j >= ra && j < rb) {  // warp-uniform
-        if (vecStore) {
-          VT o;
-          if constexpr (V == 2) {
-            o.x = res[0];
-            o.y = res[1];
-          } else {
-            o.x = res[0];
-            o.y = res[1];
-            o.z = res[2];
-            o.w = res[3];
-          }
-          *reinterpret_cast<VT*>(orow) = o;
-          if (a.peerUp && j < a.upRows)  // warp-uniform
-            *reinterpret_cast<VT*>(a.peerUp + static_cast<long long>(j) * nx + xb) = o;
-          if (a.peerDn && j >= a.dnRow0)
-            *reinterpret_cast<VT*>(a.peerDn + static_cast<long long>(j - a.dnRow0) * nx + xb) = o;
-        } else if (laneValid) {
-#pragma unroll
-          for (int v = 0; v < V; ++v)
-            if (xb + v >= a.col0 && xb + v < a.col1) put_out(a, j, xb + v, res[v]);
-        }
-      }
-      ++j;
-      orow += rowStep;
-    }
-    // every lane of this warp has read the stage
-    if constexpr (SG_EMPTY_ALL_LANES) {
-      mbar_arrive(&empty[slot]);  // each thread releases its own reads of the slot
-    } else {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-    }
-  }
-}
-
-// ------------------------------------------------------------- k_generic
-template <typename T, typename Op>
-__global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T> a) {
-  const int i = a.col0 + blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = a.row0 + blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= a.col1 || j >= a.row1) return;
-  const int W = a.left + a.right + 1;
-  const int H = a.top + a.bottom + 1;
-  const T* __restrict__ in = a.in;
-  if constexpr (std::is_same_v<Op, OpWeights>) {
-    const T* wt = a.count <= VMAX ? a.v : a.wdev;
-    T acc = T(0);
-    for (int q = 0; q < H; ++q) {
-      long long r = static_cast<long long>(j) + a.inShift - a.top + q;
-      if (a.wrapY && (r < 0 || r >= a.inRows)) r = wrap_idx(r, a.inRows);
-      const T* rowp = in + r * a.nx;
-      for (int p = 0; p < W; ++p) {
-        long long c = static_cast<long long>(i) - a.left + p;
-        if (a.wrapX && (c < 0 || c >= a.nx)) c = wrap_idx(c, a.nx);  // modulo only at the edges
-        acc += wt[q * W + p] * rowp[c];
-      }
-    }
-    put_out(a, j, i, acc);
-  } else {
-    T w[GENERIC_FN_MAX];
-    for (int q = 0; q < H; ++q) {
-      long long r = static_cast<long long>(j) + a.inShift - a.top + q;
-      if (a.wrapY && (r < 0 || r >= a.inRows)) r = wrap_idx(r, a.inRows);
-      const T* rowp = in + r * a.nx;
-      for (int p = 0; p < W; ++p) {
-        long long c = static_cast<long long>(i) - a.left + p;
-        if (a.wrapX && (c < 0 || c >= a.nx)) c = wrap_idx(c, a.nx);  // modulo only at the edges
-        w[q * W + p] = rowp[c];
-      }
-    }
-    put_out(a, j, i, Op::template apply<T>(w, a.v, W));
-  }
-}
 
 // Kernel arguments of one slab launch (plain descriptor -> KArgs).
 template <typename T>

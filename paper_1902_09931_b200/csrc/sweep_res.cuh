@@ -374,6 +374,7 @@ __device__ __forceinline__ void sweep_res_body(const PentaTables& f, const Sweep
       if (lane != 0) return;
       auto load_raw = [&](int g) {
         double* rb = raw + (g % NR) * GEO::RAW;
+        s_mbar_expect_tx(&rawfull[g % NR], (RS * 32 + (XIN == 1 ? 4 * RS : 0)) * 8);
         if (maps.ztBox) {  // one 4D box: RS/16 chunks of 16 unknowns x 32 systems
           const int r = g * RS;
           s_tma_4d(rb, &maps.zt, 0, b0, (r % maps.ztInner) / 16, r / maps.ztInner, &rawfull[g % NR]);

@@ -73,7 +73,8 @@ class WeightStencil:
 class FunctionStencil:
     """stencil.hpp:29-33 — a window function plus coefficients. ``fn`` names
     one of the device window functions (``FUNCTIONS``) — the device twin of
-    the reference's host function pointer. ``None`` is the null pointer."""
+    the reference's host function pointer — or a function registered from
+    source (``register_function_source``). ``None`` is the null pointer."""
     ext: Extents
     fn: Union[str, int, None]
     coe: Sequence[float] = field(default_factory=list)
@@ -135,6 +136,26 @@ def _shape(x):
     raise InvalidArgument("stengrid: grids are Grid2D (host) or 2D CUDA tensors (device)")
 
 
+# name -> id of the functions registered from source (register_function_source)
+SOURCE_FUNCTIONS: dict = {}
+
+
+def register_function_source(name: str, body: str) -> int:
+    """Register a window function from CUDA C++ source (sg.h:
+    sg_register_function_source). ``body`` is the body of
+    ``T fn(const T* window, const T* coe, int rowStride)`` — the reference's
+    StencilFunction contract (stencil.hpp:20-25), entry (p, q) at
+    ``window[q*rowStride + p]``. Compiled by NVRTC (sm_100a, no FMA
+    contraction) into the library's stencil kernels on first use. Returns the
+    function id; ``FunctionStencil(ext, name, coe)`` then selects it.
+    Raises InvalidArgument (with the compiler log) if the body does not
+    compile."""
+    fid = C.c_int(-1)
+    check(_lib.lib().sg_register_function_source(name.encode(), body.encode(), C.byref(fid)))
+    SOURCE_FUNCTIONS[name] = fid.value
+    return fid.value
+
+
 def _kind_values(kind):
     if isinstance(kind, WeightStencil):
         return 0, np.ascontiguousarray(np.asarray(kind.weights, dtype=np.float64))
@@ -143,9 +164,12 @@ def _kind_values(kind):
         if fn is None:
             fid = -1
         elif isinstance(fn, str):
-            if fn not in FUNCTIONS:
+            if fn in SOURCE_FUNCTIONS:
+                fid = SOURCE_FUNCTIONS[fn]
+            elif fn in FUNCTIONS:
+                fid = FUNCTIONS[fn]
+            else:
                 raise InvalidArgument(f"create_plan: no device twin registered for function {fn!r}")
-            fid = FUNCTIONS[fn]
         else:
             fid = int(fn)
         return fid, np.ascontiguousarray(np.asarray(kind.coe, dtype=np.float64))

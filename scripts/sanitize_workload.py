@@ -43,6 +43,16 @@ for dt in (torch.float64, torch.float32):
                                   a2, b2, 1, 1)
             sg.compute(plan)
             sg.destroy_plan(plan)
+# a window function registered from source (NVRTC-compiled kernels)
+sg.register_function_source("san_fn", "return window[rowStride + 1] * coe[0] - window[0];")
+for nx in (256, 97):
+    a3 = torch.rand((40, nx), dtype=torch.float64, device="cuda")
+    b3 = torch.zeros_like(a3)
+    for ext in ((1, 1, 1, 1), (2, 1, 1, 2), (5, 5, 5, 5)):
+        plan = sg.create_plan(sg.Direction.XY, sg.BoundaryMode.Periodic,
+                              sg.FunctionStencil(sg.Extents(*ext), "san_fn", [0.5]), a3, b3, 1, 1)
+        sg.compute(plan)
+        sg.destroy_plan(plan)
 # penta
 for periodic in (True, False):
     m = sg.PentaBatch(70, 40, periodic)

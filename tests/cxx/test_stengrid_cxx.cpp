@@ -439,6 +439,48 @@ void test_fp32_dropin() {  // FP32 extension (north_star: FP32+FP64); bar 1e-5 r
                   std::invalid_argument);
 }
 
+// A user's own window function (the reference's central feature,
+// stencil.hpp:20-25): the host function and its body as source.
+double user_fn(const double* window, const double* coe, int rowStride) {
+  const double c = window[rowStride + 1];
+  double acc = c * c * coe[0];
+  acc += (window[0] - window[2 * rowStride + 2]) * coe[1];
+  acc += window[rowStride] * window[rowStride + 2] - coe[2];
+  return acc;
+}
+
+void test_source_function() {
+  const char* body = R"(
+    const T c = window[rowStride + 1];
+    T acc = c * c * coe[0];
+    acc += (window[0] - window[2 * rowStride + 2]) * coe[1];
+    acc += window[rowStride] * window[rowStride + 2] - coe[2];
+    return acc;)";
+  const Grid2D in0 = random_grid(97, 45, 181);
+  const FunctionStencil fs{Extents{1, 1, 1, 1}, user_fn, {0.5, -1.25, 0.75}};
+  // unregistered: there is no CPU path
+  {
+    Grid2D a = in0, b(97, 45, in0.dx, in0.dy);
+    CHECK_THROWS_AS(create_plan(Direction::XY, BoundaryMode::Periodic, fs, a, b, 1, 1), std::invalid_argument);
+  }
+  CHECK_THROWS_AS(register_device_function_source(user_fn, "return undefined_name;"), std::invalid_argument);
+  CHECK(register_device_function_source(user_fn, body, "user_fn") >= SG_FN_JIT_BASE);
+  for (const bool periodic : {true, false}) {
+    const BoundaryMode mode = periodic ? BoundaryMode::Periodic : BoundaryMode::NonPeriodic;
+    Grid2D a = in0, b(97, 45, in0.dx, in0.dy);
+    StencilPlan p = create_plan(Direction::XY, mode, fs, a, b, 1, 1);
+    compute(p);
+    int bad = 0;
+    const int lo = periodic ? 0 : 1;
+    for (int j = lo; j < 45 - lo; ++j)
+      for (int i = lo; i < 97 - lo; ++i) {
+        const double want = apply_function_at(a, fs, i, j, mode);  // the host function itself
+        if (std::memcmp(&want, &b.values(j, i), sizeof(double)) != 0) ++bad;
+      }
+    CHECK(bad == 0);
+  }
+}
+
 void test_acceptance_criterion_2() {  // acceptance.cpp:104-151
   std::mt19937_64 rng(99);
   std::uniform_real_distribution<double> val(-2.0, 2.0);
@@ -663,22 +705,29 @@ void test_weno() {  // test_weno.cpp: constant field, shape errors
 
 }  // namespace
 
+void run_test(const char* name, void (*fn)()) {
+  std::printf("[ %s ]\n", name);
+  std::fflush(stdout);
+  fn();
+}
+
 int main() {
-  test_create_plan_rejects_invalid_setups();
-  test_lifecycle();
-  test_swap_and_two_pass();
-  test_sine_and_convergence();
-  test_identity_cross_weightsfn();
-  test_tiles_frame_shift_concurrency();
-  test_residency();
-  test_workers_to_gpus();
-  test_fp32_dropin();
-  test_acceptance_criterion_2();
-  test_penta();
-  test_ch();
-  test_diagnostics_and_run();
-  test_snapshot_and_checkpoint();
-  test_weno();
+  run_test("test_create_plan_rejects_invalid_setups", test_create_plan_rejects_invalid_setups);
+  run_test("test_lifecycle", test_lifecycle);
+  run_test("test_swap_and_two_pass", test_swap_and_two_pass);
+  run_test("test_sine_and_convergence", test_sine_and_convergence);
+  run_test("test_identity_cross_weightsfn", test_identity_cross_weightsfn);
+  run_test("test_tiles_frame_shift_concurrency", test_tiles_frame_shift_concurrency);
+  run_test("test_residency", test_residency);
+  run_test("test_workers_to_gpus", test_workers_to_gpus);
+  run_test("test_fp32_dropin", test_fp32_dropin);
+  run_test("test_source_function", test_source_function);
+  run_test("test_acceptance_criterion_2", test_acceptance_criterion_2);
+  run_test("test_penta", test_penta);
+  run_test("test_ch", test_ch);
+  run_test("test_diagnostics_and_run", test_diagnostics_and_run);
+  run_test("test_snapshot_and_checkpoint", test_snapshot_and_checkpoint);
+  run_test("test_weno", test_weno);
   std::printf("%d checks passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
