@@ -571,6 +571,27 @@ def bench_ch(sg, torch, args, n=1024, steps=1000):
     st.synchronize()
     dt = time.perf_counter() - t0
     out = {"cfg3_ch_1024sq_steps_s": steps / dt, "cfg3_ch_1024sq_1000steps_s": dt}
+    # opt-in partitioned sweeps (sg_ch_set_partition): not bitwise; deviation
+    # from the bitwise path (= the reference) after 100 steps reported beside
+    import numpy as np
+    ref100 = sg.CHStepper(p)
+    ref100.step_many(100)
+    c_ref = ref100.field().values.copy()
+    del ref100
+    part = {}
+    for P in (4, 8):
+        sp = sg.CHStepper(p)
+        sp.set_partition(P)
+        sp.step_many(100)
+        err = float(np.linalg.norm(sp.field().values - c_ref) / np.linalg.norm(c_ref))
+        sp.step_many(20)
+        sp.synchronize()
+        t0 = time.perf_counter()
+        sp.step_many(steps)
+        sp.synchronize()
+        part[f"P{P}"] = {"steps_s": steps / (time.perf_counter() - t0), "rel_l2_after_100_steps_vs_bitwise": err}
+        del sp
+    out["cfg3_ch_1024sq_partitioned_opt_in"] = part
     # end to end through the public API: host initial state uploaded
     # (set_state), 1000 steps, field read back to the host
     import numpy as np

@@ -181,6 +181,10 @@ class CHStepper {
     detail::check(sg_ch_step(h_, n));
     dirty_ = true;
   }
+  /// Extension (sg.h: sg_ch_set_partition): partitioned x/y sweeps with
+  /// `segments` segments per system — shorter recurrences, results NOT
+  /// bitwise the reference's; 0 or 1 restores the bitwise default.
+  void set_partition(int segments) { detail::check(sg_ch_set_partition(h_, segments)); }
 
   /// cahn_hilliard.cpp:251-258
   void set_state(const Grid2D& curr, const Grid2D& prev) {

@@ -231,6 +231,18 @@ sg_status sg_ch_create(const sg_ch_params* p, int numTiles, int numWorkers, sg_c
  * Results are bitwise those of one GPU. field() gathers the slabs;
  * sg_ch_device_field returns a gathered copy on worker 0's GPU. */
 sg_status sg_ch_workers(sg_ch_t ch, int* workers, int* p2p);
+/* Extension (opt-in, single GPU): partitioned sweeps. With segments = P >= 2
+ * every x / y system's unknowns are split into P segments solved as
+ * independent chains (SPIKE-type: local solves with the segment factor,
+ * a 4P x 4P interface system per system, a rank-4 correction per segment),
+ * so the sequential recurrence per CTA is n / P rows instead of n — the
+ * latency bound of the bitwise sweeps on grids with few systems per SM.
+ * NOT bitwise equal to the reference (different operation order); the
+ * deviation is measured in tests/test_ch_partition_gpu.py and DESIGN.md
+ * against the north-star bar (1e-9 relative L2 after 100 steps).
+ * segments = 0 or 1 restores the bitwise default. Needs nx % 64 == 0 and
+ * segment lengths n / P that are multiples of 64. */
+sg_status sg_ch_set_partition(sg_ch_t ch, int segments);
 /* Block until every queued step is complete. */
 sg_status sg_ch_synchronize(sg_ch_t ch);
 /* `steps` calls of CHStepper::step (cahn_hilliard.cpp:260-328). */

@@ -41,7 +41,7 @@ EXPORTED = [
     "sg_chd_destroy", "sg_chd_p2p_buffers", "sg_chd_set_peers", "sg_chd_phase_x_p2p", "sg_chd_phase_y_p2p",
     "sg_chd_combine_p2p", "sg_ipc_get_handle", "sg_ipc_open_handle", "sg_ipc_close", "sg_ch_diagnostics", "sg_simpson_mean", "sg_s_metric", "sg_k1_metric", "sg_ch_set_step", "sg_weno_advect",
     "sg_set_device_map", "sg_get_device_map", "sg_plan_workers", "sg_ch_workers", "sg_ch_synchronize",
-    "sg_register_function_source",
+    "sg_register_function_source", "sg_ch_set_partition",
 ]
 
 
@@ -111,6 +111,7 @@ def lib():
         "sg_function_min_coe": (C.c_int, [C.c_int]),
         "sg_function_name": (C.c_char_p, [C.c_int]),
         "sg_register_function_source": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_int)]),
+        "sg_ch_set_partition": (C.c_int, [C.c_void_p, C.c_int]),
         "sg_wrap": (C.c_int, [C.c_int64, C.c_int, ip]),
         "sg_make_tiles": (C.c_int, [C.c_int, C.c_int, ip, ip]),
         "sg_plan_create": (C.c_int, [C.c_int, C.c_int, SgExtents, C.c_int, dp, C.c_size_t, C.c_int,

@@ -150,6 +150,13 @@ class CHStepper:
     def synchronize(self) -> None:
         check(_lib.lib().sg_ch_synchronize(self._h))
 
+    def set_partition(self, segments: int) -> None:
+        """Extension (sg_ch_set_partition): partitioned x/y sweeps with
+        ``segments`` segments per system (>= 2; 0/1 = the bitwise default).
+        Not bitwise equal to the reference; see DESIGN.md for the measured
+        deviation."""
+        check(_lib.lib().sg_ch_set_partition(self._h, int(segments)))
+
     def workers(self):
         """(GPU count, P2P form?) — numWorkers -> GPUs (sg_ch_workers)."""
         n, p2p = C.c_int(), C.c_int()

@@ -942,6 +942,23 @@ void launch_transpose_correct(const double* zT, double* w, int nx, int own, int 
 }
 
 // Single GPU: C^{n+1} = (2 C^n - C^{n-1}) + (w - (Wy0[j] y0[i] + ... + Wy3[j] y3[i])), over C^{n-1}.
+// Partitioned y-sweep correction in place on row-major w (row j = the
+// y-unknown, column i = the y-system): w -= V0 c0 + V1 c1 + W0 c2 + W1 c3
+// with the spikes at row j (vec[q*ny + j], tiled) and the coefficients of
+// (segment j / m, column i) — the expression order of penta.cpp:283-284.
+__global__ void __launch_bounds__(256) k_seg_correct_rows(double* __restrict__ w, int nx, int ny,
+                                                          const double* __restrict__ vec,
+                                                          const double* __restrict__ coef, int m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  pdl_wait();
+  if (i >= nx) return;
+  const long long sB = nx, o = static_cast<long long>(j / m) * 4 * sB + i;
+  const double v0 = __ldg(vec + j), v1 = __ldg(vec + ny + j), v2 = __ldg(vec + 2LL * ny + j),
+               v3 = __ldg(vec + 3LL * ny + j);
+  w[static_cast<long long>(j) * nx + i] -=
+      v0 * __ldg(coef + o) + v1 * __ldg(coef + o + sB) + v2 * __ldg(coef + o + 2 * sB) + v3 * __ldg(coef + o + 3 * sB);
+}
+
 __global__ void __launch_bounds__(256) k_combine(const double* __restrict__ cc, double* __restrict__ cpNext,
                                                  const double* __restrict__ w, int nx, int ny,
                                                  const CorrTables t) {
@@ -1100,6 +1117,12 @@ struct ChState {
   // transposed with the x Woodbury correction (no transpose kernel)
   double* xT = nullptr;
   bool xpipe = false;
+  // Opt-in partitioned sweeps (sg_ch_set_partition, SegPenta): P segments
+  // per system; gx/gy interface values, cx/cy correction coefficients
+  // ([P][4][systems]). 0 = the bitwise default.
+  int partP = 0;
+  std::unique_ptr<SegPenta> sx, sy;
+  double *gx = nullptr, *cx = nullptr, *gy = nullptr, *cy = nullptr;
 
   DevicePenta fx, fy;
   RhsParams rp{};
@@ -1216,6 +1239,22 @@ struct ChState {
     } else {
       launch_rhs(p.nonlinearEnabled, field[c], field[q], rhsT, geom, rp, s, pdl);
     }
+    if (partP) {
+      // partitioned: local solves, interface solves, corrections (the x
+      // correction on the y-sweep's load, the y correction in place on w;
+      // y4y stays zero, so the combine's W . y4y term adds exactly 0)
+      const double* wc[4] = {sx->vec, sx->vec + nx, sx->vec + 2LL * nx, sx->vec + 3LL * nx};
+      if (!penta_sweep_seg(*sx, ny, xT, rhsT, nullptr, nullptr, 0, gx, s, pdl))
+        throw Error(SG_ERR_CUDA, "internal: partitioned x-sweep unavailable");
+      penta_seg_reduce(*sx, ny, gx, cx, s, pdl);
+      if (!penta_sweep_seg(*sy, nx, w, xT, wc, cx, sx->m, gy, s, pdl))
+        throw Error(SG_ERR_CUDA, "internal: partitioned y-sweep unavailable");
+      penta_seg_reduce(*sy, nx, gy, cy, s, pdl);
+      launch_ex(k_seg_correct_rows, dim3((nx + 255) / 256, ny), dim3(256), 0, s, pdl, w, nx, ny,
+                static_cast<const double*>(sy->vec), static_cast<const double*>(cy), sy->m);
+      check_launch("ch partitioned y correction kernel");
+      return;
+    }
     if (xpipe) {
       // x-sweep: rhs (row-major) read transposed -> xT (interleaved);
       // y-sweep: xT read transposed + x-corrected -> w (row-major)
@@ -1246,6 +1285,45 @@ struct ChState {
     launch_ex(k_combine, dim3((nx + 255) / 256, ny), dim3(256), 0, s, pdl_enabled(),
               static_cast<const double*>(field[c]), field[q], static_cast<const double*>(w), nx, ny, ty);
     check_launch("ch combine kernel");
+  }
+
+  // Opt-in partitioned sweeps (P >= 2 segments per system; P <= 1: the
+  // bitwise default). Results differ from the reference's operation order;
+  // DESIGN.md gives the measured deviation.
+  void set_partition(int P) {
+    SG_CUDA(cudaStreamSynchronize(stream));
+    for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+    graphs.clear();
+    solveK = -1;
+    if (P <= 1) {
+      partP = 0;
+      return;
+    }
+    if (!xpipe) invalid("CHStepper: partitioned sweeps need the transposed-input pipeline (nx % 64 == 0)");
+    const double dx = p.lx / p.nx, dy = p.ly / p.ny;
+    const double sxg = kTwoThirds * p.D * p.gamma * p.dt / pow4(dx);
+    const double syg = kTwoThirds * p.D * p.gamma * p.dt / pow4(dy);
+    auto mk = [&](double sig, int n) {
+      auto sp = std::make_unique<SegPenta>();  // k_fill_bands' values
+      sp->build(sig, -4.0 * sig, 1.0 + 6.0 * sig, -4.0 * sig, sig, n, P, stream);
+      return sp;
+    };
+    auto nx_ = mk(sxg, p.nx), ny_ = mk(syg, p.ny);
+    if (!gx) {
+      gx = dalloc(16 * static_cast<size_t>(p.ny) * 4);
+      cx = dalloc(16 * static_cast<size_t>(p.ny) * 4);
+      gy = dalloc(16 * static_cast<size_t>(p.nx) * 4);
+      cy = dalloc(16 * static_cast<size_t>(p.nx) * 4);
+    }
+    const double* wc[4] = {nx_->vec, nx_->vec + p.nx, nx_->vec + 2LL * p.nx, nx_->vec + 3LL * p.nx};
+    if (!penta_sweep_seg(*nx_, p.ny, xT, rhsT, nullptr, nullptr, 0, gx, stream, false, false) ||
+        !penta_sweep_seg(*ny_, p.nx, w, xT, wc, cx, nx_->m, gy, stream, false, false))
+      invalid("CHStepper: partitioned sweeps unavailable for this grid (segments must be multiples of 64 rows)");
+    sx = std::move(nx_);
+    sy = std::move(ny_);
+    SG_CUDA(cudaMemsetAsync(y4y, 0, 4 * static_cast<size_t>(p.nx) * sizeof(double), stream));
+    SG_CUDA(cudaStreamSynchronize(stream));
+    partP = P;
   }
 
   cudaGraphExec_t graph(int kind, int c, int q) {
@@ -1842,6 +1920,16 @@ sg_status sg_ch_step(sg_ch_t ch, int steps) {
     }
     SG_CUDA(cudaSetDevice(ch->st->device));
     ch->st->run(steps);
+  });
+}
+
+sg_status sg_ch_set_partition(sg_ch_t ch, int segments) {
+  return guard2([&] {
+    if (!ch) sg::logic("CHStepper: destroyed");
+    if (segments < 0 || segments > 16) sg::invalid("CHStepper: partition segments must be in [0, 16]");
+    if (ch->mul) sg::invalid("CHStepper: partitioned sweeps are single-GPU only");
+    SG_CUDA(cudaSetDevice(ch->st->device));
+    ch->st->set_partition(segments);
   });
 }
 

@@ -635,7 +635,7 @@ void launch_sweep_tma(const PentaTables& f, const SweepMaps& maps, int B, int n,
 
 template <int RS, int XIN>
 void launch_sweep_res_t(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
-                        cudaStream_t s, bool pdl, const SweepFuse& fuse) {
+                        cudaStream_t s, bool pdl, const SweepFuse& fuse, int segs = 1) {
   constexpr size_t smem = RRGeom<RS, XIN>::SMEM;
   static bool configured = false;
   if (!configured) {
@@ -646,22 +646,23 @@ void launch_sweep_res_t(bool periodic, const PentaTables& f, const SweepMaps& ma
     configured = true;
   }
   const int blocks = (B + 31) / 32;
-  launch_ex(periodic ? k_sweep_res<true, RS, XIN> : k_sweep_res<false, RS, XIN>, dim3(blocks),
+  launch_ex(periodic ? k_sweep_res<true, RS, XIN> : k_sweep_res<false, RS, XIN>, dim3(blocks, segs),
             dim3(XIN ? 32 * (2 + XIN_TW) : 64), smem, s, pdl, f, maps, B, n, y4, fuse);
 }
 
 void launch_sweep_res(bool periodic, const PentaTables& f, const SweepMaps& maps, int B, int n, double* y4,
-                      cudaStream_t s, bool pdl, int rs, int xin = 0, const SweepFuse& fuse = SweepFuse{}) {
+                      cudaStream_t s, bool pdl, int rs, int xin = 0, const SweepFuse& fuse = SweepFuse{},
+                      int segs = 1) {
   const bool wide = rs == RR_RS_WIDE;
   if (xin == 1) {
-    if (wide) launch_sweep_res_t<RR_RS_WIDE, 1>(periodic, f, maps, B, n, y4, s, pdl, fuse);
-    else launch_sweep_res_t<RR_RS, 1>(periodic, f, maps, B, n, y4, s, pdl, fuse);
+    if (wide) launch_sweep_res_t<RR_RS_WIDE, 1>(periodic, f, maps, B, n, y4, s, pdl, fuse, segs);
+    else launch_sweep_res_t<RR_RS, 1>(periodic, f, maps, B, n, y4, s, pdl, fuse, segs);
   } else if (xin == 2) {
-    if (wide) launch_sweep_res_t<RR_RS_WIDE, 2>(periodic, f, maps, B, n, y4, s, pdl, fuse);
-    else launch_sweep_res_t<RR_RS, 2>(periodic, f, maps, B, n, y4, s, pdl, fuse);
+    if (wide) launch_sweep_res_t<RR_RS_WIDE, 2>(periodic, f, maps, B, n, y4, s, pdl, fuse, segs);
+    else launch_sweep_res_t<RR_RS, 2>(periodic, f, maps, B, n, y4, s, pdl, fuse, segs);
   } else {
-    if (wide) launch_sweep_res_t<RR_RS_WIDE, 0>(periodic, f, maps, B, n, y4, s, pdl, fuse);
-    else launch_sweep_res_t<RR_RS, 0>(periodic, f, maps, B, n, y4, s, pdl, fuse);
+    if (wide) launch_sweep_res_t<RR_RS_WIDE, 0>(periodic, f, maps, B, n, y4, s, pdl, fuse, segs);
+    else launch_sweep_res_t<RR_RS, 0>(periodic, f, maps, B, n, y4, s, pdl, fuse, segs);
   }
 }
 
@@ -749,6 +750,162 @@ bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double
   return true;
 }
 
+
+// ------------------------------------------------ partitioned sweep (SegPenta)
+
+bool penta_sweep_seg(const SegPenta& sp, int B, double* z, const double* zT, const double* const* Wc,
+                     const double* yc, int ycSeg, double* gIf, cudaStream_t s, bool pdl, bool launch) {
+  const int n = sp.n, m = sp.m, P = sp.P;
+  if (P < 1 || !sp.local.t.uniform || !use_resident_sweep()) return false;
+  if ((reinterpret_cast<uintptr_t>(zT) & 15) || (reinterpret_cast<uintptr_t>(z) & 15) || (B & 1) || n % 16) return false;
+  int rs = sweep_res_rows(B * P);
+  if (m % rs) rs = RR_RS;
+  if (m % rs || m < rs) return false;
+  SweepMaps maps = SweepMaps{};
+  if (!encode_map(&maps.z, z, 2, B, n, 32, rs)) return false;
+  const double* t[5] = {sp.local.t.m1, sp.local.t.m2, sp.local.t.dInv, sp.local.t.ap, sp.local.t.bp};
+  for (int k = 0; k < 5; ++k)
+    if ((reinterpret_cast<uintptr_t>(t[k]) & 15) || !encode_map(&maps.t[k], t[k], 1, m, 1, rs, 1)) return false;
+  maps.ztBox = n % rs == 0 && encode_map4_zt(&maps.zt, zT, n, B, n, rs) ? 1 : 0;
+  if (!maps.ztBox && !encode_map3(&maps.zt, zT, n, B, 1, 16, 32, 1, true)) return false;
+  maps.ztInner = n;
+  maps.segRows = m;
+  SweepFuse fuse;
+  if (Wc) {
+    if (reinterpret_cast<uintptr_t>(yc) & 15) return false;
+    if (ycSeg) {
+      if (ycSeg % 32 || B % ycSeg) return false;
+      if (!encode_map3(&maps.yc[0], yc, n, 4, B / ycSeg, rs, 4, 1, false)) return false;
+      maps.ycSeg = ycSeg;
+    } else if (!encode_map(&maps.yc[0], yc, 2, n, 4, rs, 4)) {
+      return false;
+    }
+    for (int k = 0; k < 4; ++k) fuse.Wc[k] = Wc[k];
+    fuse.yc = yc;
+  }
+  if (!launch) return true;
+  launch_sweep_res(false, sp.local.t, maps, B, m, gIf, s, pdl, rs, Wc ? 1 : 2, fuse, P);
+  check_launch("penta partitioned sweep kernel");
+  return true;
+}
+
+namespace {
+// z = Rinv * G for every system (G: the 4P interface values of system b,
+// segment-major as gIf), one thread per (system b, interface unknown i =
+// 4j + q): a dot product of length 4P (Rinv row i is warp-uniform: a
+// broadcast). z_i is the t_{j,q} (q < 2) or b_{j,q-2} (q >= 2) of segment
+// j: coefficient slot q of segment j - 1 (as its t_{k+1}) or j + 1 (as its
+// b_{k-1}).
+__global__ void __launch_bounds__(128) k_seg_reduce(const double* __restrict__ gIf, const double* __restrict__ Rinv,
+                                                    int P, int B, double* __restrict__ coef) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+  pdl_wait();
+  if (b >= B) return;
+  const int N = 4 * P;
+  const double* row = Rinv + static_cast<long long>(i) * N;
+  double acc = 0.0;
+  for (int jj = 0; jj < N; ++jj) acc += __ldg(row + jj) * __ldg(gIf + static_cast<long long>(jj) * B + b);
+  const int j = i / 4, q = i % 4;
+  const int k = q < 2 ? (j + P - 1) % P : (j + 1) % P;
+  coef[static_cast<long long>(k * 4 + q) * B + b] = acc;
+}
+}  // namespace
+
+void penta_seg_reduce(const SegPenta& sp, int B, const double* gIf, double* coef, cudaStream_t s, bool pdl) {
+  launch_ex(k_seg_reduce, dim3((B + 127) / 128, 4 * sp.P), dim3(128), 0, s, pdl, gIf, static_cast<const double*>(sp.Rinv),
+            sp.P, B, coef);
+  check_launch("penta partitioned interface solve kernel");
+}
+
+SegPenta::~SegPenta() {
+  for (void* q : allocs) cudaFree(q);
+}
+
+void SegPenta::build(double e, double c, double d, double a, double b, int n_, int P_, cudaStream_t s) {
+  if (P_ < 1 || P_ > 16 || n_ % P_ || n_ / P_ < 8) invalid("partitioned sweep: need 1 <= P <= 16, P | n, n / P >= 8");
+  n = n_;
+  P = P_;
+  m = n / P;
+  auto dalloc = [&](size_t cnt) {
+    void* q = nullptr;
+    SG_CUDA(cudaMalloc(&q, cnt * sizeof(double)));
+    allocs.push_back(q);
+    return static_cast<double*>(q);
+  };
+  // local factor: the m x m leading block (no corners)
+  std::vector<double> hb(5 * static_cast<size_t>(m));
+  const double bv[5] = {e, c, d, a, b};
+  for (int k = 0; k < 5; ++k)
+    for (int r = 0; r < m; ++r) hb[static_cast<size_t>(k) * m + r] = bv[k];
+  double* bands = dalloc(5 * static_cast<size_t>(m));
+  SG_CUDA(cudaMemcpyAsync(bands, hb.data(), hb.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  local.build(1, m, false, true, bands, bands + m, bands + 2 * m, bands + 3 * m, bands + 4 * m, s);
+  // spikes: A_loc [V0 V1 W0 W1] = [B0 B1 C0 C1], four systems interleaved (r*4 + col)
+  std::vector<double> hz(4 * static_cast<size_t>(m), 0.0);
+  hz[(m - 2) * 4 + 0] = b;  // row m-2 couples to the next segment's row 0 (coefficient b)
+  hz[(m - 1) * 4 + 0] = a;  // row m-1: a * next row 0 + b * next row 1
+  hz[(m - 1) * 4 + 1] = b;
+  hz[0 * 4 + 2] = e;        // row 0: e * prev row m-2 + c * prev row m-1
+  hz[0 * 4 + 3] = c;
+  hz[1 * 4 + 3] = e;        // row 1: e * prev row m-1
+  double* zs = dalloc(hz.size());
+  SG_CUDA(cudaMemcpyAsync(zs, hz.data(), hz.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  penta_sweep(local.t, 4, m, zs, nullptr, false, true, s);
+  SG_CUDA(cudaMemcpyAsync(hz.data(), zs, hz.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  std::vector<double> hv(4 * static_cast<size_t>(n));
+  for (int q = 0; q < 4; ++q)
+    for (int r = 0; r < n; ++r) hv[static_cast<size_t>(q) * n + r] = hz[static_cast<size_t>(r % m) * 4 + q];
+  vec = dalloc(hv.size());
+  SG_CUDA(cudaMemcpyAsync(vec, hv.data(), hv.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  // reduced system R z = G over z = (t_k0, t_k1, b_k0, b_k1)_k:
+  //   rows {0, 1, m-2, m-1} of  x_k + V t_{k+1} + W b_{k-1} = g_k
+  const int N = 4 * P;
+  std::vector<double> R(static_cast<size_t>(N) * N, 0.0), I(static_cast<size_t>(N) * N, 0.0);
+  const int rowsOf[4] = {0, 1, m - 2, m - 1};
+  for (int k = 0; k < P; ++k) {
+    const int kp = (k + 1) % P, km = (k + P - 1) % P;
+    for (int q = 0; q < 4; ++q) {
+      const int i = 4 * k + q, r = rowsOf[q];
+      R[static_cast<size_t>(i) * N + i] += 1.0;
+      R[static_cast<size_t>(i) * N + 4 * kp + 0] += hz[static_cast<size_t>(r) * 4 + 0];
+      R[static_cast<size_t>(i) * N + 4 * kp + 1] += hz[static_cast<size_t>(r) * 4 + 1];
+      R[static_cast<size_t>(i) * N + 4 * km + 2] += hz[static_cast<size_t>(r) * 4 + 2];
+      R[static_cast<size_t>(i) * N + 4 * km + 3] += hz[static_cast<size_t>(r) * 4 + 3];
+    }
+    (void)km;
+  }
+  for (int i = 0; i < N; ++i) I[static_cast<size_t>(i) * N + i] = 1.0;
+  // Gauss-Jordan with partial pivoting
+  for (int col = 0; col < N; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < N; ++r)
+      if (std::fabs(R[static_cast<size_t>(r) * N + col]) > std::fabs(R[static_cast<size_t>(piv) * N + col])) piv = r;
+    if (R[static_cast<size_t>(piv) * N + col] == 0.0) throw Error(SG_ERR_PENTA_SOLVE, "partitioned sweep: singular interface system", 0);
+    if (piv != col)
+      for (int j = 0; j < N; ++j) {
+        std::swap(R[static_cast<size_t>(piv) * N + j], R[static_cast<size_t>(col) * N + j]);
+        std::swap(I[static_cast<size_t>(piv) * N + j], I[static_cast<size_t>(col) * N + j]);
+      }
+    const double inv = 1.0 / R[static_cast<size_t>(col) * N + col];
+    for (int j = 0; j < N; ++j) {
+      R[static_cast<size_t>(col) * N + j] *= inv;
+      I[static_cast<size_t>(col) * N + j] *= inv;
+    }
+    for (int r = 0; r < N; ++r) {
+      if (r == col) continue;
+      const double f = R[static_cast<size_t>(r) * N + col];
+      if (f == 0.0) continue;
+      for (int j = 0; j < N; ++j) {
+        R[static_cast<size_t>(r) * N + j] -= f * R[static_cast<size_t>(col) * N + j];
+        I[static_cast<size_t>(r) * N + j] -= f * I[static_cast<size_t>(col) * N + j];
+      }
+    }
+  }
+  Rinv = dalloc(I.size());
+  SG_CUDA(cudaMemcpyAsync(Rinv, I.data(), I.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+}
 
 // ------------------------------------------------ peer TMA store self-check
 

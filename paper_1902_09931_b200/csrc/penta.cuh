@@ -87,6 +87,47 @@ bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double
                      const double* yc, double* y4, cudaStream_t s, bool pdl, bool launch = true, int ztInner = 0,
                      const SweepPeers* peers = nullptr);
 
+// Partitioned (SPIKE-type) solve of a uniform CYCLIC pentadiagonal operator
+// — an opt-in alternative to the bitwise sweep for latency-bound batches
+// (few systems, long chains: CH 1024^2 on one GPU, config 5's 1024 systems
+// of 8192 per GPU): every system's n unknowns form P segments of m = n / P
+// rows, solved independently (B * P chains of m rows instead of B of n) with
+// the factor of the segment-local operator A_loc (non-periodic, m x m); the
+// segments couple through the operator's 2 x 2 corner blocks, so
+//   x_k = g_k - (V0 t_{k+1,0} + V1 t_{k+1,1} + W0 b_{k-1,0} + W1 b_{k-1,1})
+// with g_k = A_loc^{-1} f_k, the spikes [V0 V1] = A_loc^{-1} B and
+// [W0 W1] = A_loc^{-1} C (B, C the couplings to the next / previous
+// segment), and (t_k, b_k) the first / last two unknowns of segment k: the
+// 4P interface unknowns solve a reduced system R z = G (G the interface
+// values of the g_k), identical for all systems, inverted once on the host.
+// P = 1 is the Woodbury form of the periodic sweep. Not bitwise equal to the
+// reference's order of operations (penta.cpp:160-295); see DESIGN.md.
+struct SegPenta {
+  int n = 0, P = 0, m = 0;
+  DevicePenta local;          // factor of A_loc (non-periodic, length m)
+  double* vec = nullptr;      // [4][n]: V0, V1, W0, W1, tiled over the n unknowns (row r: local row r % m)
+  double* Rinv = nullptr;     // [4P][4P], row-major; interface unknowns per segment: t0, t1, b0, b1
+  std::vector<void*> allocs;
+  SegPenta() = default;
+  SegPenta(const SegPenta&) = delete;
+  SegPenta& operator=(const SegPenta&) = delete;
+  ~SegPenta();
+  // Uniform bands (row r: e x_{r-2} + c x_{r-1} + d x_r + a x_{r+1} + b x_{r+2},
+  // cyclic) given on the host; builds the local factor, the spikes and R^{-1}.
+  void build(double e, double c, double d, double a, double b, int n, int P, cudaStream_t s);
+};
+// Sweep of B systems (one CTA per 32 systems and segment) reading its input
+// transposed (zT[b*n + r], as penta_sweep_xin; Wc/yc: the previous sweep's
+// correction applied on load, yc holding one [4][n] plane per ycSeg systems
+// when that sweep was partitioned, ycSeg = 0 otherwise). Writes the local
+// solutions g (uncorrected) to z (interleaved) and the interface values to
+// gIf[(k*4 + q)*B + b] (q: g[0], g[1], g[m-2], g[m-1]). False if unavailable.
+bool penta_sweep_seg(const SegPenta& sp, int B, double* z, const double* zT, const double* const* Wc,
+                     const double* yc, int ycSeg, double* gIf, cudaStream_t s, bool pdl, bool launch = true);
+// Interface solve: coef[(k*4 + q)*B + b] = (t_{k+1,0}, t_{k+1,1}, b_{k-1,0},
+// b_{k-1,1}) of segment k from gIf — the coefficients of the correction.
+void penta_seg_reduce(const SegPenta& sp, int B, const double* gIf, double* coef, cudaStream_t s, bool pdl);
+
 // lu4_solve, penta.cpp:61-70.
 __device__ __forceinline__ void lu4_solve_dev(const double* K, const int* piv, double* y) {
 #pragma unroll

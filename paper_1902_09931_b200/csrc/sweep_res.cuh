@@ -32,6 +32,17 @@ struct alignas(64) SweepMaps {
   int ztBox = 0;     // 1: zt is the 4D view {16, B, ztInner / 16, n / ztInner}, box {16, 32, RS/16, 1}
   int npeer = 0;     // 0: final results stay in z
   int prow = 0;
+  // Partitioned (SPIKE-type) sweep: each system's unknowns are segments of
+  // segRows rows, segment blockIdx.y of a CTA's 32 systems solved as an
+  // independent non-periodic system with the segment-local factor (the
+  // `n` of the kernel is then segRows; z / zt / yc rows are offset by
+  // blockIdx.y * segRows). The interface values g[0], g[1], g[m-2], g[m-1]
+  // of every (segment, system) go to y4[(seg * 4 + k) * B + b].
+  int segRows = 0;
+  // XIN 1 after a partitioned sweep: yc holds one [4][n] plane of
+  // coefficients per segment of THAT sweep (ycSeg rows each, along this
+  // sweep's systems); 3D map {n, 4, planes}, box {RS, 4, 1}
+  int ycSeg = 0;
 };
 
 // Fusions of the transposed-input sweep (k_sweep_res XIN, the CH step):
@@ -252,6 +263,8 @@ __device__ __forceinline__ void sweep_res_body(const PentaTables& f, const Sweep
   uint64_t* slotfree = rawfree + GEO::NRAW;    // XIN: forward slot stored, writable
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b0 = cta * 32;
+  const int seg = maps.segRows ? static_cast<int>(blockIdx.y) : 0;
+  const int rb0 = seg * maps.segRows;  // first row of this CTA's segment in z / zt / yc
   const int nS = (n + RS - 1) / RS;
   const int keep = nS < NST ? nS : NST;  // forward stages resident at the turn
   if (threadIdx.x == 0) {
@@ -287,13 +300,13 @@ __device__ __forceinline__ void sweep_res_body(const PentaTables& f, const Sweep
     auto load = [&](int s, int G) {
       double* st = rr_smem + s * STG;
       s_mbar_expect_tx(&full[s], TX);
-      s_tma_2d(st, &maps.z, b0, G * RS, &full[s]);
+      s_tma_2d(st, &maps.z, b0, rb0 + G * RS, &full[s]);
       for (int k = 0; k < 5; ++k) s_tma_1d(st + RS * 32 + k * FAC, &maps.t[k], G * RS, &full[s]);
       if constexpr (XIN)  // no transform on refetched rows: the transform arrivals now
         s_mbar_arrive_cnt(&full[s], 32 * XIN_TW);
     };
     auto store = [&](int s, int G) {
-      s_tma_store_2d(&maps.z, b0, G * RS, rr_smem + s * STG);
+      s_tma_store_2d(&maps.z, b0, rb0 + G * RS, rr_smem + s * STG);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     };
     if constexpr (XIN) {
@@ -376,15 +389,20 @@ __device__ __forceinline__ void sweep_res_body(const PentaTables& f, const Sweep
         double* rb = raw + (g % NR) * GEO::RAW;
         s_mbar_expect_tx(&rawfull[g % NR], (RS * 32 + (XIN == 1 ? 4 * RS : 0)) * 8);
         if (maps.ztBox) {  // one 4D box: RS/16 chunks of 16 unknowns x 32 systems
-          const int r = g * RS;
+          const int r = rb0 + g * RS;
           s_tma_4d(rb, &maps.zt, 0, b0, (r % maps.ztInner) / 16, r / maps.ztInner, &rawfull[g % NR]);
         } else {
           for (int x = 0; x < RS / 16; ++x) {
-            const int r = g * RS + x * 16;
+            const int r = rb0 + g * RS + x * 16;
             s_tma_3d(rb + x * 512, &maps.zt, r % maps.ztInner, b0, r / maps.ztInner, &rawfull[g % NR]);
           }
         }
-        if constexpr (XIN == 1) s_tma_2d(rb + RS * 32, &maps.yc[0], g * RS, 0, &rawfull[g % NR]);
+        if constexpr (XIN == 1) {
+          if (maps.ycSeg)  // the coefficient plane of the segment holding these systems
+            s_tma_3d(rb + RS * 32, &maps.yc[0], rb0 + g * RS, 0, b0 / maps.ycSeg, &rawfull[g % NR]);
+          else
+            s_tma_2d(rb + RS * 32, &maps.yc[0], rb0 + g * RS, 0, &rawfull[g % NR]);
+        }
       };
       for (int g = 0; g < NR - 1 && g < nS; ++g) load_raw(g);
       for (int g = 0; g < nS; ++g) {
@@ -666,6 +684,16 @@ __device__ __forceinline__ void sweep_res_body(const PentaTables& f, const Sweep
       if (fuse.py4[d])
 #pragma unroll
         for (int k = 0; k < 4; ++k) fuse.py4[d][static_cast<long long>(k) * fuse.y4Stride + fuse.y4Off + b] = y[k];
+  } else {
+    if (maps.segRows) {  // interface values of this (segment, system)
+      const int b = b0 + lane;
+      if (b >= B) return;
+      const long long sB = B, o = static_cast<long long>(seg) * 4 * sB + b;
+      y4[o] = zz0;
+      y4[o + sB] = zz1;
+      y4[o + 2 * sB] = zn2;
+      y4[o + 3 * sB] = zn1;
+    }
   }
 }
 
