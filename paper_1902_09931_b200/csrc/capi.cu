@@ -377,9 +377,11 @@ static void pipelined_host_compute(sg_plan_s* p, sg_plan_s::Buf& in, sg_plan_s::
     SG_CUDA(cudaMemcpyAsync(din + off, hin + off, top * rowBytes, cudaMemcpyHostToDevice, p->sH2D));
   }
   for (int k = 0; k < nch; ++k) {
-    const int a = k * rows, b = std::min(ny, a + rows);
+    // rows [ny - top, ny) went up first (chunk 0's wrapped halo) and chunk
+    // 0's kernel may be reading them: never write them again
+    const int a = k * rows, b = std::min(std::min(ny, a + rows), ny - top);
     const size_t off = static_cast<size_t>(a) * rowBytes;
-    SG_CUDA(cudaMemcpyAsync(din + off, hin + off, (b - a) * rowBytes, cudaMemcpyHostToDevice, p->sH2D));
+    if (b > a) SG_CUDA(cudaMemcpyAsync(din + off, hin + off, (b - a) * rowBytes, cudaMemcpyHostToDevice, p->sH2D));
     SG_CUDA(cudaEventRecord(evH2D[k], p->sH2D));
   }
   sg_slab_desc d = full_grid_desc(p);

@@ -1828,7 +1828,14 @@ struct sg_penta_s {
   // milliseconds once the pool has released them)
   double* y4 = nullptr;   // periodic: y = K^{-1} V^T z, 4 x B
   double* tmp = nullptr;  // host-memory solves: device copy of the rhs
+  // Solves on one factor share the scratch: the mutex guards its lazy
+  // allocation and the enqueue, `last` orders a solve after the previous
+  // one even on another stream (concurrent solves on one factor serialise;
+  // the reference's solve_in_place is const but its scratch is per call).
+  std::mutex mu;
+  cudaEvent_t last = nullptr;
   ~sg_penta_s() {
+    if (last) cudaEventDestroy(last);
     if (y4) cudaFree(y4);
     if (tmp) cudaFree(tmp);
   }
@@ -2122,6 +2129,9 @@ sg_status sg_penta_solve(sg_penta_t f, double* rhs, sg_memory memory, void* stre
     if (!f) sg::logic("penta: destroyed factor");
     SG_CUDA(cudaSetDevice(f->device));
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : f->stream;
+    std::lock_guard<std::mutex> lk(f->mu);
+    if (!f->last) SG_CUDA(cudaEventCreateWithFlags(&f->last, cudaEventDisableTiming));
+    else SG_CUDA(cudaStreamWaitEvent(s, f->last, 0));
     const int B = f->f->B, n = f->f->n;
     const size_t bytes = static_cast<size_t>(B) * n * sizeof(double);
     double* z = rhs;
@@ -2136,6 +2146,7 @@ sg_status sg_penta_solve(sg_penta_t f, double* rhs, sg_memory memory, void* stre
       SG_CUDA(cudaMemcpyAsync(rhs, f->tmp, bytes, cudaMemcpyDeviceToHost, s));
       synchronize = 1;
     }
+    SG_CUDA(cudaEventRecord(f->last, s));
     if (synchronize) SG_CUDA(cudaStreamSynchronize(s));
   });
 }
