@@ -942,23 +942,6 @@ void launch_transpose_correct(const double* zT, double* w, int nx, int own, int 
 }
 
 // Single GPU: C^{n+1} = (2 C^n - C^{n-1}) + (w - (Wy0[j] y0[i] + ... + Wy3[j] y3[i])), over C^{n-1}.
-// Partitioned y-sweep correction in place on row-major w (row j = the
-// y-unknown, column i = the y-system): w -= V0 c0 + V1 c1 + W0 c2 + W1 c3
-// with the spikes at row j (vec[q*ny + j], tiled) and the coefficients of
-// (segment j / m, column i) — the expression order of penta.cpp:283-284.
-__global__ void __launch_bounds__(256) k_seg_correct_rows(double* __restrict__ w, int nx, int ny,
-                                                          const double* __restrict__ vec,
-                                                          const double* __restrict__ coef, int m) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
-  pdl_wait();
-  if (i >= nx) return;
-  const long long sB = nx, o = static_cast<long long>(j / m) * 4 * sB + i;
-  const double v0 = __ldg(vec + j), v1 = __ldg(vec + ny + j), v2 = __ldg(vec + 2LL * ny + j),
-               v3 = __ldg(vec + 3LL * ny + j);
-  w[static_cast<long long>(j) * nx + i] -=
-      v0 * __ldg(coef + o) + v1 * __ldg(coef + o + sB) + v2 * __ldg(coef + o + 2 * sB) + v3 * __ldg(coef + o + 3 * sB);
-}
-
 __global__ void __launch_bounds__(256) k_combine(const double* __restrict__ cc, double* __restrict__ cpNext,
                                                  const double* __restrict__ w, int nx, int ny,
                                                  const CorrTables t) {
@@ -1118,11 +1101,11 @@ struct ChState {
   double* xT = nullptr;
   bool xpipe = false;
   // Opt-in partitioned sweeps (sg_ch_set_partition, SegPenta): P segments
-  // per system; gx/gy interface values, cx/cy correction coefficients
+  // per system; gx/gy interface values, cx the x correction coefficients
   // ([P][4][systems]). 0 = the bitwise default.
   int partP = 0;
   std::unique_ptr<SegPenta> sx, sy;
-  double *gx = nullptr, *cx = nullptr, *gy = nullptr, *cy = nullptr;
+  double *gx = nullptr, *cx = nullptr, *gy = nullptr;
 
   DevicePenta fx, fy;
   RhsParams rp{};
@@ -1249,10 +1232,7 @@ struct ChState {
       penta_seg_reduce(*sx, ny, gx, cx, s, pdl);
       if (!penta_sweep_seg(*sy, nx, w, xT, wc, cx, sx->m, gy, s, pdl))
         throw Error(SG_ERR_CUDA, "internal: partitioned y-sweep unavailable");
-      penta_seg_reduce(*sy, nx, gy, cy, s, pdl);
-      launch_ex(k_seg_correct_rows, dim3((nx + 255) / 256, ny), dim3(256), 0, s, pdl, w, nx, ny,
-                static_cast<const double*>(sy->vec), static_cast<const double*>(cy), sy->m);
-      check_launch("ch partitioned y correction kernel");
+      penta_seg_finish_rows(*sy, nx, w, gy, s, pdl);
       return;
     }
     if (xpipe) {
@@ -1313,7 +1293,6 @@ struct ChState {
       gx = dalloc(16 * static_cast<size_t>(p.ny) * 4);
       cx = dalloc(16 * static_cast<size_t>(p.ny) * 4);
       gy = dalloc(16 * static_cast<size_t>(p.nx) * 4);
-      cy = dalloc(16 * static_cast<size_t>(p.nx) * 4);
     }
     const double* wc[4] = {nx_->vec, nx_->vec + p.nx, nx_->vec + 2LL * p.nx, nx_->vec + 3LL * p.nx};
     if (!penta_sweep_seg(*nx_, p.ny, xT, rhsT, nullptr, nullptr, 0, gx, stream, false, false) ||

@@ -796,24 +796,94 @@ namespace {
 // broadcast). z_i is the t_{j,q} (q < 2) or b_{j,q-2} (q >= 2) of segment
 // j: coefficient slot q of segment j - 1 (as its t_{k+1}) or j + 1 (as its
 // b_{k-1}).
+template <int P>
 __global__ void __launch_bounds__(128) k_seg_reduce(const double* __restrict__ gIf, const double* __restrict__ Rinv,
-                                                    int P, int B, double* __restrict__ coef) {
+                                                    int B, double* __restrict__ coef) {
+  constexpr int N = 4 * P;
   const int b = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
   pdl_wait();
   if (b >= B) return;
-  const int N = 4 * P;
+  // all N loads in flight before the dot product (N is compile-time)
+  double g[N];
+#pragma unroll
+  for (int jj = 0; jj < N; ++jj) g[jj] = __ldg(gIf + static_cast<long long>(jj) * B + b);
   const double* row = Rinv + static_cast<long long>(i) * N;
   double acc = 0.0;
-  for (int jj = 0; jj < N; ++jj) acc += __ldg(row + jj) * __ldg(gIf + static_cast<long long>(jj) * B + b);
+#pragma unroll
+  for (int jj = 0; jj < N; ++jj) acc += __ldg(row + jj) * g[jj];
   const int j = i / 4, q = i % 4;
   const int k = q < 2 ? (j + P - 1) % P : (j + 1) % P;
   coef[static_cast<long long>(k * 4 + q) * B + b] = acc;
 }
+
+// The interface solve fused with the correction of a ROW-MAJOR result
+// (w[j*B + i]: row j = unknown, column i = system; the CH y-sweep's output):
+// a CTA takes 128 systems and `rows` rows of one segment, computes the 4
+// coefficients of its (segment, system) once — the dot products of
+// k_seg_reduce, same order — and applies them to its rows:
+// w -= V0 c0 + V1 c1 + W0 c2 + W1 c3 (penta.cpp:283-284's expression).
+template <int P>
+__global__ void __launch_bounds__(128) k_seg_finish_rows(double* __restrict__ w, int B, const double* __restrict__ vec,
+                                                         int n, const double* __restrict__ gIf,
+                                                         const double* __restrict__ Rinv, int m, int rows) {
+  constexpr int N = 4 * P;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j0 = blockIdx.y * rows;
+  pdl_wait();
+  if (i >= B) return;
+  const int seg = j0 / m, kp = (seg + 1) % P, km = (seg + P - 1) % P;
+  const int zi[4] = {4 * kp, 4 * kp + 1, 4 * km + 2, 4 * km + 3};
+  double g[N];
+#pragma unroll
+  for (int jj = 0; jj < N; ++jj) g[jj] = __ldg(gIf + static_cast<long long>(jj) * B + i);
+  double c[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double* row = Rinv + static_cast<long long>(zi[q]) * N;
+    double acc = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < N; ++jj) acc += __ldg(row + jj) * g[jj];
+    c[q] = acc;
+  }
+#pragma unroll 4
+  for (int r = 0; r < rows; ++r) {
+    const int j = j0 + r;
+    double* p = w + static_cast<long long>(j) * B + i;
+    *p -= __ldg(vec + j) * c[0] + __ldg(vec + n + j) * c[1] + __ldg(vec + 2LL * n + j) * c[2] +
+          __ldg(vec + 3LL * n + j) * c[3];
+  }
+}
+
+template <typename F>
+void with_segs(int P, F&& f) {
+  switch (P) {
+    case 1: return f(std::integral_constant<int, 1>{});
+    case 2: return f(std::integral_constant<int, 2>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 8: return f(std::integral_constant<int, 8>{});
+    case 16: return f(std::integral_constant<int, 16>{});
+    default: invalid("partitioned sweep: segments must be 1, 2, 4, 8 or 16");
+  }
+}
 }  // namespace
 
+void penta_seg_finish_rows(const SegPenta& sp, int B, double* w, const double* gIf, cudaStream_t s, bool pdl) {
+  static const int rowsPer = [] {
+    const char* e = std::getenv("SG_SEG_ROWS");
+    return e ? std::atoi(e) : 8;
+  }();
+  const int rows = sp.m % rowsPer == 0 ? rowsPer : sp.m;
+  with_segs(sp.P, [&](auto pc) {
+    launch_ex(k_seg_finish_rows<decltype(pc)::value>, dim3((B + 127) / 128, sp.n / rows), dim3(128), 0, s, pdl, w,
+              B, static_cast<const double*>(sp.vec), sp.n, gIf, static_cast<const double*>(sp.Rinv), sp.m, rows);
+  });
+  check_launch("penta partitioned interface solve + row correction kernel");
+}
+
 void penta_seg_reduce(const SegPenta& sp, int B, const double* gIf, double* coef, cudaStream_t s, bool pdl) {
-  launch_ex(k_seg_reduce, dim3((B + 127) / 128, 4 * sp.P), dim3(128), 0, s, pdl, gIf, static_cast<const double*>(sp.Rinv),
-            sp.P, B, coef);
+  with_segs(sp.P, [&](auto pc) {
+    launch_ex(k_seg_reduce<decltype(pc)::value>, dim3((B + 127) / 128, 4 * sp.P), dim3(128), 0, s, pdl, gIf,
+              static_cast<const double*>(sp.Rinv), B, coef);
+  });
   check_launch("penta partitioned interface solve kernel");
 }
 
@@ -822,7 +892,8 @@ SegPenta::~SegPenta() {
 }
 
 void SegPenta::build(double e, double c, double d, double a, double b, int n_, int P_, cudaStream_t s) {
-  if (P_ < 1 || P_ > 16 || n_ % P_ || n_ / P_ < 8) invalid("partitioned sweep: need 1 <= P <= 16, P | n, n / P >= 8");
+  if ((P_ & (P_ - 1)) || P_ < 1 || P_ > 16 || n_ % P_ || n_ / P_ < 8)
+    invalid("partitioned sweep: need P in {1, 2, 4, 8, 16}, P | n, n / P >= 8");
   n = n_;
   P = P_;
   m = n / P;

@@ -127,6 +127,9 @@ bool penta_sweep_seg(const SegPenta& sp, int B, double* z, const double* zT, con
 // Interface solve: coef[(k*4 + q)*B + b] = (t_{k+1,0}, t_{k+1,1}, b_{k-1,0},
 // b_{k-1,1}) of segment k from gIf — the coefficients of the correction.
 void penta_seg_reduce(const SegPenta& sp, int B, const double* gIf, double* coef, cudaStream_t s, bool pdl);
+// The interface solve fused with the correction of a row-major result
+// w[r*B + b] (rows = the unknowns; the CH y-sweep's output) in place.
+void penta_seg_finish_rows(const SegPenta& sp, int B, double* w, const double* gIf, cudaStream_t s, bool pdl);
 
 // lu4_solve, penta.cpp:61-70.
 __device__ __forceinline__ void lu4_solve_dev(const double* K, const int* piv, double* y) {

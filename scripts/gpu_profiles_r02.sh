@@ -13,3 +13,13 @@ ncu --set full --clock-control none --import-source on -k regex:k_tma -s 2 -c 1 
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_ --csv --log-file gpurun_out/r2_ch1024_launches.csv python scripts/profile_ch.py --n 1024 --steps 20 > /dev/null 2>&1; echo ncu5=$?
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_ --csv --log-file gpurun_out/r2_ch1024_part8_launches.csv python scripts/profile_ch.py --n 1024 --steps 20 --partition 8 > /dev/null 2>&1; echo ncu6=$?
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_ --csv --log-file gpurun_out/r2_ch8192_launches.csv python scripts/profile_ch.py --n 8192 --steps 6 > /dev/null 2>&1; echo ncu7=$?
+# summaries (the .ncu-rep files are too large to bring back together)
+for r in r2_k_tma_f64 r2_k_tma_g_odd3x3 r2_k_tma_g_3100 r2_k_tma_9x9; do
+  python scripts/ncu_summary.py gpurun_out/$r.ncu-rep > gpurun_out/${r}_ncu_summary.txt 2>&1
+  ncu -i gpurun_out/$r.ncu-rep --page raw --csv --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum > gpurun_out/${r}_traffic.csv 2>/dev/null
+  rm -f gpurun_out/$r.ncu-rep
+done
+for f in r2_bench_launches r2_ch1024_launches r2_ch1024_part8_launches r2_ch8192_launches; do
+  python scripts/launch_summary.py gpurun_out/$f.csv > gpurun_out/$f.txt 2>&1
+done
+du -sh gpurun_out
