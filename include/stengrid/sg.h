@@ -110,6 +110,14 @@ sg_status sg_plan_create(sg_direction dir, sg_boundary mode, sg_extents ext, sg_
                          const double* values, size_t count, sg_dtype dtype, void* in, void* out,
                          int nx, int ny, sg_memory memory, int numTiles, int numWorkers,
                          sg_plan_t* plan);
+/* HOST grids whose two device mirrors would not fit in free device memory
+ * (or any host plan with SG_STREAM_PLANS=1 in the environment at creation;
+ * SG_STREAM_ROWS sets the chunk height) get a STREAMED plan: no mirrors,
+ * every compute streams the grid through a ring of three row-chunk buffers
+ * (chunk rows + halo rows; H2D, kernels and D2H overlapped on three
+ * streams), so grids larger than HBM work — the reason for the paper's
+ * tiling. Such a plan is always host-coherent and
+ * synchronous (DEVICE residency behaves as HOST). */
 /* compute (stencil.cpp:202-235). HOST residency: host grids are
  * authoritative — the input is uploaded, the output downloaded. DEVICE
  * residency: the input is uploaded only if its device copy is stale, the

@@ -115,6 +115,22 @@ struct sg_plan_s {
     int own() const { return r1 - r0; }
   };
   std::vector<Worker> workers;
+  // Streamed (out-of-core) host plan: no full-size device mirrors; every
+  // compute() streams the grid through a ring of NSLOT row-chunk buffers
+  // (chunkRows output rows + top/bottom halo rows each) — host grids larger
+  // than the device's memory work, as the paper's tiling intended
+  // (PAPER.md:120-129). Chosen when the two mirrors would not fit in free
+  // device memory (SG_STREAM_PLANS=1 forces it; SG_STREAM_ROWS sets the
+  // chunk height).
+  static constexpr int NSLOT = 3;
+  bool streamed = false;
+  int chunkRows = 0;
+  struct Slot {
+    void* in = nullptr;
+    void* out = nullptr;
+    cudaEvent_t loaded = nullptr, computed = nullptr, drained = nullptr;
+    bool used = false;
+  } slots[NSLOT];
 
   size_t elem() const { return dtype == SG_F64 ? 8 : 4; }
   size_t bytes() const { return static_cast<size_t>(nx) * ny * (dtype == SG_F64 ? 8 : 4); }
@@ -134,6 +150,15 @@ struct sg_plan_s {
     workers.clear();
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
+    if (sD2H) cudaStreamSynchronize(sD2H);
+    for (auto& sl : slots) {
+      if (sl.in) cudaFree(sl.in);
+      if (sl.out) cudaFree(sl.out);
+      for (cudaEvent_t e : {sl.loaded, sl.computed, sl.drained})
+        if (e) cudaEventDestroy(e);
+      sl = Slot{};
+    }
+    streamed = false;
     for (auto& b : buf)
       if (b.owned && b.dev) cudaFree(b.dev);
     for (int k = 0; k < 2; ++k)
@@ -155,6 +180,25 @@ struct sg_plan_s {
 };
 
 static void setup_workers(sg_plan_s* p, int G, int ndev);
+
+// The slot ring of a streamed compute (streamed plans, and large
+// non-periodic Residency::Host computes of mirrored plans): chunk height
+// SG_STREAM_ROWS, else ~128 MiB of output rows, at least one row.
+static void setup_streaming(sg_plan_s* p) {
+  const size_t rowB = static_cast<size_t>(p->nx) * p->elem();
+  const int H = p->ext.top + p->ext.bottom;
+  int rows = 0;
+  if (const char* e = std::getenv("SG_STREAM_ROWS")) rows = std::atoi(e);
+  if (rows <= 0) rows = static_cast<int>(std::max<size_t>(1, (128ull << 20) / rowB));
+  rows = std::min(rows, p->ny);
+  p->chunkRows = rows;
+  for (auto& sl : p->slots) {
+    SG_CUDA(cudaMalloc(&sl.in, (static_cast<size_t>(rows) + H) * rowB));
+    SG_CUDA(cudaMalloc(&sl.out, static_cast<size_t>(rows) * rowB));
+    for (cudaEvent_t* e : {&sl.loaded, &sl.computed, &sl.drained})
+      SG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+}
 
 extern "C" {
 
@@ -276,6 +320,16 @@ sg_status sg_plan_create(sg_direction dir, sg_boundary mode, sg_extents ext, sg_
       int G = device_map() == 1 ? numWorkers : std::min(numWorkers, ndev);
       G = std::min(G, ny);
       if (memory == SG_MEM_HOST && G > 1) setup_workers(p, G, ndev);
+      if (memory == SG_MEM_HOST && p->workers.empty()) {
+        const char* force = std::getenv("SG_STREAM_PLANS");
+        size_t freeB = 0, totalB = 0;
+        SG_CUDA(cudaMemGetInfo(&freeB, &totalB));
+        const bool fits = 2 * p->bytes() + (512ull << 20) < freeB;
+        if ((force && force[0] == '1') || !fits) {
+          setup_streaming(p);
+          p->streamed = true;
+        }
+      }
       void* ptrs[2] = {in, out};
       for (int k = 0; k < 2; ++k) {
         auto& b = p->buf[k];
@@ -285,7 +339,7 @@ sg_status sg_plan_create(sg_direction dir, sg_boundary mode, sg_extents ext, sg_
           b.hostValid = false;
         } else {
           b.host = ptrs[k];
-          if (p->workers.empty()) {  // multi-worker plans hold only slabs
+          if (p->workers.empty() && !p->streamed) {  // multi-worker / streamed plans hold no mirrors
             SG_CUDA(cudaMalloc(&b.dev, p->bytes()));
             b.owned = true;
           }
@@ -337,6 +391,76 @@ static sg_slab_desc full_grid_desc(const sg_plan_s* p) {
     d.col1 = std::max(hi, fastLo);
   }
   return d;
+}
+
+// Streamed host plan: rows [a, b) of the computed range per chunk. The
+// input slot holds global rows a - top .. b + bottom - 1 (wrapped modulo ny
+// when periodic; a non-periodic range never leaves the grid), the kernel
+// computes the chunk's rows into the output slot (the same slab launch the
+// multi-GPU path uses: inShift = top, no y wrap), and the output rows go
+// back — only the computed columns of a non-periodic grid, so the host
+// frame stays untouched (stencil.cpp:35-38). H2D, kernels and D2H run on
+// three streams over a ring of NSLOT slots.
+static void streamed_host_compute(sg_plan_s* p, sg_plan_s::Buf& in, sg_plan_s::Buf& out, cudaStream_t s) {
+  const int ny = p->ny, top = p->ext.top, bottom = p->ext.bottom, R = p->chunkRows;
+  const size_t eb = p->elem(), rowB = static_cast<size_t>(p->nx) * eb;
+  if (!p->sH2D) SG_CUDA(cudaStreamCreateWithFlags(&p->sH2D, cudaStreamNonBlocking));
+  if (!p->sD2H) SG_CUDA(cudaStreamCreateWithFlags(&p->sD2H, cudaStreamNonBlocking));
+  const sg_slab_desc g = full_grid_desc(p);
+  const bool periodic = p->mode == SG_PERIODIC;
+  cudaEvent_t start = nullptr;
+  if (p->events.empty()) {
+    p->events.resize(1);
+    SG_CUDA(cudaEventCreateWithFlags(&p->events[0], cudaEventDisableTiming));
+  }
+  start = p->events[0];
+  SG_CUDA(cudaEventRecord(start, s));
+  SG_CUDA(cudaStreamWaitEvent(p->sH2D, start, 0));
+  SG_CUDA(cudaStreamWaitEvent(p->sD2H, start, 0));
+  const auto* hin = static_cast<const char*>(in.host);
+  auto* hout = static_cast<char*>(out.host);
+  int k = 0;
+  for (int a = g.row0; a < g.row1; a += R, ++k) {
+    const int b = std::min(a + R, g.row1);
+    auto& sl = p->slots[k % sg_plan_s::NSLOT];
+    // the slot's previous chunk: its kernel has read `in`, its D2H has read `out`
+    if (sl.used) {
+      SG_CUDA(cudaStreamWaitEvent(p->sH2D, sl.computed, 0));
+    }
+    // input rows a - top .. b + bottom - 1, split where they wrap
+    char* din = static_cast<char*>(sl.in);
+    int row = a - top, dst = 0;
+    const int last = b + bottom;
+    while (row < last) {
+      const int gr = periodic ? ((row % ny) + ny) % ny : row;
+      const int n = std::min(last - row, ny - gr);
+      SG_CUDA(cudaMemcpyAsync(din + static_cast<size_t>(dst) * rowB, hin + static_cast<size_t>(gr) * rowB,
+                              static_cast<size_t>(n) * rowB, cudaMemcpyHostToDevice, p->sH2D));
+      row += n;
+      dst += n;
+    }
+    SG_CUDA(cudaEventRecord(sl.loaded, p->sH2D));
+    SG_CUDA(cudaStreamWaitEvent(s, sl.loaded, 0));
+    if (sl.used) SG_CUDA(cudaStreamWaitEvent(s, sl.drained, 0));
+    sg_slab_desc d = g;
+    d.inRows = (b - a) + top + bottom;
+    d.inShift = top;
+    d.row0 = 0;
+    d.row1 = b - a;
+    d.wrapY = 0;
+    sg::launch_stencil(d, p->ext, p->fn, p->values.data(), p->values.size(), p->dtype, sl.in, sl.out, s);
+    SG_CUDA(cudaEventRecord(sl.computed, s));
+    SG_CUDA(cudaStreamWaitEvent(p->sD2H, sl.computed, 0));
+    const size_t c0 = static_cast<size_t>(g.col0) * eb, w = static_cast<size_t>(g.col1 - g.col0) * eb;
+    if (w > 0)
+      SG_CUDA(cudaMemcpy2DAsync(hout + static_cast<size_t>(a) * rowB + c0, rowB, static_cast<char*>(sl.out) + c0,
+                                rowB, w, static_cast<size_t>(b - a), cudaMemcpyDeviceToHost, p->sD2H));
+    SG_CUDA(cudaEventRecord(sl.drained, p->sD2H));
+    sl.used = true;
+  }
+  SG_CUDA(cudaStreamSynchronize(p->sD2H));
+  SG_CUDA(cudaStreamSynchronize(s));
+  for (auto& sl : p->slots) sl.used = false;
 }
 
 // Residency::Host on a large periodic grid: stream the grid through the GPU
@@ -634,8 +758,23 @@ sg_status sg_plan_compute(sg_plan_t p, sg_residency residency, void* stream, int
     }
     auto& in = p->buf[p->inIdx];
     auto& out = p->buf[1 - p->inIdx];
+    if (p->streamed) {  // always host-coherent and synchronous (no device mirrors)
+      if (in.host == out.host) sg::invalid("compute: bound grids alias");
+      streamed_host_compute(p, in, out, s);
+      return;
+    }
     if (in.dev == out.dev) sg::invalid("compute: bound grids alias");
     const bool periodic = p->mode == SG_PERIODIC;
+    if (p->memory == SG_MEM_HOST && !periodic && residency == SG_RESIDENCY_HOST && in.hostValid &&
+        out.hostValid && p->bytes() >= (64u << 20)) {
+      // a large non-periodic host compute: the streamed pipeline (its frame
+      // handling downloads only the computed columns); the mirrors go stale
+      if (!p->slots[0].in) setup_streaming(p);
+      streamed_host_compute(p, in, out, s);
+      in.devValid = false;
+      out.devValid = false;
+      return;
+    }
     if (p->memory == SG_MEM_HOST && periodic && residency == SG_RESIDENCY_HOST && in.hostValid &&
         p->bytes() >= (64u << 20)) {
       pipelined_host_compute(p, in, out, s);
@@ -782,7 +921,15 @@ int sg_plan_kernel_kind(sg_plan_t p) {
     return sg::stencil_kernel_kind(worker_desc(p, W), p->ext, p->fn, p->values.size(), p->dtype,
                                    W.buf[p->inIdx], static_cast<char*>(W.buf[1 - p->inIdx]) + off);
   }
-  const sg_slab_desc d = full_grid_desc(p);
+  sg_slab_desc d = full_grid_desc(p);
+  if (p->streamed) {
+    d.inRows = p->chunkRows + p->ext.top + p->ext.bottom;
+    d.inShift = p->ext.top;
+    d.row0 = 0;
+    d.row1 = p->chunkRows;
+    d.wrapY = 0;
+    return sg::stencil_kernel_kind(d, p->ext, p->fn, p->values.size(), p->dtype, p->slots[0].in, p->slots[0].out);
+  }
   return sg::stencil_kernel_kind(d, p->ext, p->fn, p->values.size(), p->dtype,
                                  p->buf[p->inIdx].dev, p->buf[1 - p->inIdx].dev);
 }
