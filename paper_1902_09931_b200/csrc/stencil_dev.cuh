@@ -574,7 +574,7 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tmag_min_blocks<T, W, H
 
   if (threadIdx.x == 0) {
     for (int k = 0; k < STAGES; ++k) {
-      mbar_init(&full[k], 2);  // expect_tx arrival + cp.async arrival
+      mbar_init(&full[k], 1 + 32);  // expect_tx arrival + the producer warp's cp.async arrivals
       mbar_init(&empty[k], TMA_WARPS * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -583,10 +583,12 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tmag_min_blocks<T, W, H
   __syncthreads();
 
   if (warp == TMA_WARPS) {
-    // ---------------- producer (lane 0): per row, the 16 B-aligned middle
-    // of the CTA's columns as one bulk copy, head/tail elements and halo
-    // columns (wrapped in index math) as element cp.async
-    if (lane != 0) return;
+    // ---------------- producer warp: per row, lane 0 issues the 16 B-aligned
+    // middle of the CTA's columns as one bulk copy; the unaligned head/tail
+    // elements and the halo columns (wrapped in index math) are spread over
+    // lanes 1.. as element cp.async (one each), so the per-row element work
+    // is not serialised in one thread; every lane's copies arrive on the
+    // stage barrier through cp.async.mbarrier.arrive
     const int validC = min(CW, nx - cx0);
     const int l = a.left, r = a.right;
     const T* __restrict__ in = a.in;
@@ -606,8 +608,10 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tmag_min_blocks<T, W, H
         tx += static_cast<uint32_t>(((validC - head) / V) * V * sizeof(T));
         w2.next(a.inRows, a.wrapY);
       }
-      if (tx) mbar_expect_tx(&full[slot], tx);
-      else mbar_arrive(&full[slot]);
+      if (lane == 0) {
+        if (tx) mbar_expect_tx(&full[slot], tx);
+        else mbar_arrive(&full[slot]);
+      }
       T* sstage = ring + slot * (RPS * ROW);
 #pragma unroll
       for (int k = 0; k < RPS; ++k) {
@@ -616,18 +620,22 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tmag_min_blocks<T, W, H
         T* srow = sstage + k * ROW + HP + ph;  // column cx0 of this row
         const int head = ph ? min(V - ph, validC) : 0;
         const int mid = ((validC - head) / V) * V;
-        for (int t = 0; t < head; ++t) cp_async_elem(srow + t, grow + cx0 + t);
-        if (mid) bulk_g2s(srow + head, grow + cx0 + head, static_cast<uint32_t>(mid * sizeof(T)), &full[slot]);
-        for (int t = head + mid; t < validC; ++t) cp_async_elem(srow + t, grow + cx0 + t);
-        for (int p = 1; p <= l; ++p) {
-          const int c = cx0 - p;
-          if (c >= 0) cp_async_elem(srow - p, grow + c);
-          else if (a.wrapX) cp_async_elem(srow - p, grow + c + nx);
-        }
-        for (int p = 0; p < r; ++p) {
-          const int c = cx0 + validC + p;
-          if (c < nx) cp_async_elem(srow + validC + p, grow + c);
-          else if (a.wrapX) cp_async_elem(srow + validC + p, grow + c - nx);
+        const int tl = validC - head - mid;
+        if (lane == 0 && mid)
+          bulk_g2s(srow + head, grow + cx0 + head, static_cast<uint32_t>(mid * sizeof(T)), &full[slot]);
+        int e = lane - 1;  // this lane's element copy, if any
+        if (e >= 0 && e < head) {
+          cp_async_elem(srow + e, grow + cx0 + e);
+        } else if ((e -= head) >= 0 && e < tl) {
+          cp_async_elem(srow + head + mid + e, grow + cx0 + head + mid + e);
+        } else if ((e -= tl) >= 0 && e < l) {
+          const int c = cx0 - 1 - e;
+          if (c >= 0) cp_async_elem(srow - 1 - e, grow + c);
+          else if (a.wrapX) cp_async_elem(srow - 1 - e, grow + c + nx);
+        } else if ((e -= l) >= 0 && e < r) {
+          const int c = cx0 + validC + e;
+          if (c < nx) cp_async_elem(srow + validC + e, grow + c);
+          else if (a.wrapX) cp_async_elem(srow + validC + e, grow + c - nx);
         }
       }
       rw = w2;
