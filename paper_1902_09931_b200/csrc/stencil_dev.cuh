@@ -270,7 +270,7 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tma_min_blocks<T, L, R,
 
   if (threadIdx.x == 0) {
     for (int k = 0; k < STAGES; ++k) {
-      mbar_init(&full[k], 2);  // expect_tx arrival + cp.async (halo) arrival
+      mbar_init(&full[k], 1 + 32);  // expect_tx arrival + the producer warp's cp.async arrivals
       mbar_init(&empty[k], SG_EMPTY_ALL_LANES ? TMA_WARPS * 32 : TMA_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -279,10 +279,11 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tma_min_blocks<T, L, R,
   __syncthreads();
 
   if (warp == TMA_WARPS) {
-    // ---------------- producer: per row, one bulk copy of the CTA's own
-    // columns (128 B aligned, whole lines: no over-fetch) and 16 B cp.async
-    // granules for the halo columns (wrapped in index math at grid edges).
-    if (lane != 0) return;
+    // ---------------- producer warp: per row, lane 0 issues one bulk copy of
+    // the CTA's own columns (128 B aligned, whole lines: no over-fetch),
+    // lanes 1.. one 16 B cp.async granule each for the halo columns (wrapped
+    // in index math at grid edges); every lane arrives on the stage barrier
+    // through cp.async.mbarrier.arrive
     const int validC = min(CW, nx - cx0);
     const uint32_t mainBytes = static_cast<uint32_t>(validC * sizeof(T));
     int hsrc[(LP + RP) / V > 0 ? (LP + RP) / V : 1];
@@ -304,20 +305,29 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tma_min_blocks<T, L, R,
         hdst[nh++] = LP + validC + k * V;
       }
     }
+    // this lane's granule (lane h + 1 takes granule h)
+    int mySrc = 0, myDst = 0;
+    const bool mine = lane >= 1 && lane - 1 < nh;
+#pragma unroll
+    for (int h = 0; h < (LP + RP) / V; ++h)
+      if (lane - 1 == h) {
+        mySrc = hsrc[h];
+        myDst = hdst[h];
+      }
     int rf = ra + a.inShift - TP;
     if (a.wrapY) rf = wrap_idx(rf, a.inRows);
     const T* __restrict__ in = a.in;
     for (int g = 0; g < nStages; ++g) {
       const int slot = g % STAGES;
       if (g >= STAGES) mbar_wait(&empty[slot], ((g / STAGES) + 1) & 1);
-      mbar_expect_tx(&full[slot], mainBytes * RPS);
+      if (lane == 0) mbar_expect_tx(&full[slot], mainBytes * RPS);
       T* sstage = ring + slot * (RPS * ROW);
 #pragma unroll
       for (int k = 0; k < RPS; ++k) {
         const T* grow = in + static_cast<long long>(rf) * nx;
         T* srow = sstage + k * ROW;
-        bulk_g2s(srow + LP, grow + cx0, mainBytes, &full[slot]);
-        for (int h = 0; h < nh; ++h) cp_async16(srow + hdst[h], grow + hsrc[h]);
+        if (lane == 0) bulk_g2s(srow + LP, grow + cx0, mainBytes, &full[slot]);
+        if (mine) cp_async16(srow + myDst, grow + mySrc);
         ++rf;
         if (a.wrapY) {
           if (rf == a.inRows) rf = 0;
