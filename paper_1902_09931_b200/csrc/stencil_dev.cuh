@@ -26,6 +26,12 @@ typedef decltype(sizeof(0)) size_t;
   }
 #endif
 
+// Weight windows at least this tall accumulate pending outputs (ACC) instead
+// of holding the input window in registers.
+#ifndef SG_ACC_MIN_H
+#define SG_ACC_MIN_H 5
+#endif
+
 SG_DEV_BEGIN
 
 template <typename A, typename B>
@@ -349,7 +355,7 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tma_min_blocks<T, L, R,
   // taps row by row (q ascending, then p) — the reference's order — since
   // rows arrive top to bottom. Registers: H*V + E instead of H*E (a 9x9
   // window would otherwise spill).
-  constexpr bool ACC = sg_same<Op, OpWeights>::value && H >= 5;
+  constexpr bool ACC = sg_same<Op, OpWeights>::value && H >= SG_ACC_MIN_H;
   T win[ACC ? 1 : H][E];  // ring: input row t lives in win[t % H]
   T pend[ACC ? H : 1][V];  // ACC: output started at local input row u lives in pend[u % H]
   T* __restrict__ orow = a.out + static_cast<long long>(ra - (H - 1)) * nx + xb;
@@ -662,7 +668,7 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tmag_min_blocks<T, W, H
   const unsigned outOff = static_cast<unsigned>(reinterpret_cast<uintptr_t>(a.out) / sizeof(T));
   const bool peers = a.peerUp != nullptr || a.peerDn != nullptr;
   const bool peerVec = nx % V == 0;  // peer rows share the output rows' phase only then
-  constexpr bool ACC = sg_same<Op, OpWeights>::value && H >= 5;
+  constexpr bool ACC = sg_same<Op, OpWeights>::value && H >= SG_ACC_MIN_H;
   T win[ACC ? 1 : H][E];   // ring: input row t lives in win[t % H]
   T pend[ACC ? H : 1][V];  // ACC: output started at local input row u lives in pend[u % H]
   RowWalk rw;
