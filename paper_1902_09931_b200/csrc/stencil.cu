@@ -103,7 +103,7 @@ void launch_tma_lt(const KArgs<T>& a, cudaStream_t s) {
   KArgs<T> b = a;
   b.segRows = tma_segment_rows(rows, gx, ctasPerSm, G::RPS);
   dim3 g2(gx, static_cast<unsigned>((rows + b.segRows - 1) / b.segRows));
-  kern<<<g2, (TMA_WARPS + 1) * 32, G::smem_bytes, s>>>(b);
+  launch_ex(kern, g2, dim3((TMA_WARPS + 1) * 32), G::smem_bytes, s, stencil_pdl(), b);
 }
 
 template <typename T, typename Op>

@@ -283,6 +283,9 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tma_min_blocks<T, L, R,
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
+  // programmatic dependent launch: the prologue above overlaps the previous
+  // kernel's tail; no global memory is touched before its completion
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == TMA_WARPS) {
     // ---------------- producer warp: per row, lane 0 issues one bulk copy of
@@ -597,6 +600,9 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tmag_min_blocks<T, W, H
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
+  // programmatic dependent launch: the prologue above overlaps the previous
+  // kernel's tail; no global memory is touched before its completion
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == TMA_WARPS) {
     // ---------------- producer warp: per row, lane 0 issues the 16 B-aligned

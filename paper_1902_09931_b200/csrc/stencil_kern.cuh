@@ -52,6 +52,18 @@ KArgs<T> make_args(const sg_slab_desc& d, const sg_extents& e, const double* val
   return a;
 }
 
+// Stencil launches as programmatic dependents of the previous kernel on the
+// stream (the kernels wait before any global access): back-to-back
+// applications overlap launch and prologue with the predecessor's tail.
+// SG_STENCIL_PDL=0 disables (A/B).
+inline bool stencil_pdl() {
+  static const bool v = [] {
+    const char* e = std::getenv("SG_STENCIL_PDL");
+    return !(e && e[0] == '0') && pdl_enabled();
+  }();
+  return v;
+}
+
 inline int sm_count() {
   static int n = [] {
     int dev = 0, v = 148;
