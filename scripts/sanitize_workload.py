@@ -53,6 +53,24 @@ for nx in (256, 97):
                               sg.FunctionStencil(sg.Extents(*ext), "san_fn", [0.5]), a3, b3, 1, 1)
         sg.compute(plan)
         sg.destroy_plan(plan)
+# streamed host plan (ring of row chunks) and the opt-in partitioned CH sweeps
+import os
+os.environ["SG_STREAM_PLANS"], os.environ["SG_STREAM_ROWS"] = "1", "5"
+gi = sg.Grid2D.from_array(rng.uniform(-1, 1, (23, 70)))
+go = sg.Grid2D.from_array(np.zeros((23, 70)))
+for mode in (sg.BoundaryMode.Periodic, sg.BoundaryMode.NonPeriodic):
+    plan = sg.create_plan(sg.Direction.XY, mode, sg.WeightStencil(sg.Extents(2, 1, 1, 2), list(rng.uniform(-1, 1, 16))),
+                          gi, go, 1, 1)
+    sg.compute(plan)
+    sg.destroy_plan(plan)
+del os.environ["SG_STREAM_PLANS"], os.environ["SG_STREAM_ROWS"]
+pp = sg.CHParams(nx=256, ny=256)
+pp.dt = 0.1 * pp.dx()
+pp.T = 1.0
+sp = sg.CHStepper(pp)
+sp.set_partition(4)
+sp.step_many(3)
+sp.synchronize()
 # penta
 for periodic in (True, False):
     m = sg.PentaBatch(70, 40, periodic)
