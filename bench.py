@@ -683,7 +683,7 @@ def ours_arm(args, rank, world, local_rank):
     alg_bytes = nx * ny * BYTES_PER_PT["f64"]
     achieved = alg_bytes / (kms * 1e-3) / 1e9
     traffic = None
-    tp = ROOT / "profiles" / "traffic_r01.json"
+    tp = ROOT / "profiles" / "traffic_r02.json"
     if tp.exists() and nx == NX:
         traffic = json.loads(tp.read_text()).get("bytes_per_launch")
     line = {
