@@ -31,6 +31,10 @@ typedef decltype(sizeof(0)) size_t;
 #ifndef SG_ACC_MIN_H
 #define SG_ACC_MIN_H 5
 #endif
+// Ring stages of tall windows (H >= 5): at least this many (A/B knob).
+#ifndef SG_TALL_STAGES
+#define SG_TALL_STAGES 2
+#endif
 
 SG_DEV_BEGIN
 
@@ -232,7 +236,8 @@ struct TmaGeom {
   // Rows per stage: a multiple of H so the register window is a ring whose
   // slot for every unrolled row is a compile-time constant (no moves).
   static constexpr int RPS = H >= 2 ? H : 2;
-  static constexpr int STAGES = (9 + RPS - 1) / RPS >= 2 ? (9 + RPS - 1) / RPS : 2;
+  static constexpr int STAGES_BASE = (9 + RPS - 1) / RPS >= 2 ? (9 + RPS - 1) / RPS : 2;
+  static constexpr int STAGES = STAGES_BASE < SG_TALL_STAGES && H >= 5 ? SG_TALL_STAGES : STAGES_BASE;
   static constexpr size_t stage_bytes = static_cast<size_t>(RPS) * ROW * sizeof(T);
   static constexpr size_t smem_bytes = STAGES * stage_bytes + 2 * STAGES * sizeof(uint64_t);
 };
@@ -522,7 +527,8 @@ struct TmaGGeom {
   static constexpr int HP = ((W - 1 + V - 1) / V) * V;  // halo room either side (any split of W - 1)
   static constexpr int ROW = HP + CW + V + HP;          // + V: the row's 16 B phase
   static constexpr int RPS = H >= 2 ? H : 2;
-  static constexpr int STAGES = (9 + RPS - 1) / RPS >= 2 ? (9 + RPS - 1) / RPS : 2;
+  static constexpr int STAGES_BASE = (9 + RPS - 1) / RPS >= 2 ? (9 + RPS - 1) / RPS : 2;
+  static constexpr int STAGES = STAGES_BASE < SG_TALL_STAGES && H >= 5 ? SG_TALL_STAGES : STAGES_BASE;
   static constexpr size_t stage_bytes = static_cast<size_t>(RPS) * ROW * sizeof(T);
   static constexpr size_t smem_bytes = STAGES * stage_bytes + 2 * STAGES * sizeof(uint64_t);
 };
