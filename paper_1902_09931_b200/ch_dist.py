@@ -244,6 +244,7 @@ def ipc_handle_functions():
     offset in it; opening maps the peer's allocation (its base is appended
     to `bases`, for sg_ipc_close) and re-applies the offset."""
     bases = []
+    mapped = {}  # allocation handle -> mapped base: an allocation is opened once per process
 
     def get_handle(ptr):
         h = (C.c_char * 64)()
@@ -252,10 +253,13 @@ def ipc_handle_functions():
         return bytes(h) + off.value.to_bytes(8, "little")
 
     def open_handle(hb):
-        ptr = C.c_void_p()
-        check(_lib.lib().sg_ipc_open_handle((C.c_char * 64).from_buffer_copy(hb[:64]), C.byref(ptr)))
-        bases.append(ptr.value)
-        return ptr.value + int.from_bytes(hb[64:72], "little")
+        key = bytes(hb[:64])
+        if key not in mapped:  # two buffers in one peer allocation share the mapping
+            ptr = C.c_void_p()
+            check(_lib.lib().sg_ipc_open_handle((C.c_char * 64).from_buffer_copy(hb[:64]), C.byref(ptr)))
+            bases.append(ptr.value)
+            mapped[key] = ptr.value
+        return mapped[key] + int.from_bytes(hb[64:72], "little")
 
     return get_handle, open_handle, bases
 
