@@ -17,8 +17,9 @@
 //    (asymmetric left/right and top/bottom splits) and every row pitch /
 //    pointer alignment (nx % V != 0): rows keep their global 16 B phase in
 //    shared memory.
-//  * k_generic — one thread per output point with per-tap modular wrap:
-//    windows beyond 9 x 9 and device functions on non-natural windows.
+//  * k_generic — windows beyond 9 x 9 and device functions on non-natural
+//    windows: a shared-memory input tile per 32 x 32 outputs (one thread per
+//    point from global memory when the tile would not fit).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -161,8 +162,10 @@ int launch_typed(const sg_slab_desc& d, const sg_extents& e, int fn, const doubl
     a.wdev = wtmp;
   }
   dim3 block(32, 8);
-  dim3 grid((cols + 31) / 32, (rows + 7) / 8);
-  with_op<void>(fn, [&](auto op) { k_generic<T, decltype(op)><<<grid, block, 0, s>>>(a); });
+  const size_t tileB = generic_tile_bytes<T>(e);
+  a.gtile = tileB > 0 ? 1 : 0;
+  dim3 grid((cols + 31) / 32, tileB > 0 ? (rows + 31) / 32 : (rows + 7) / 8);
+  with_op<void>(fn, [&](auto op) { k_generic<T, decltype(op)><<<grid, block, tileB, s>>>(a); });
   check_launch("stencil generic kernel");
   if (wtmp) SG_CUDA(cudaFreeAsync(wtmp, s));
   return 0;

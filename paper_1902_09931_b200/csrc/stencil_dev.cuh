@@ -68,6 +68,10 @@ struct KArgs {
   T* peerUp;
   T* peerDn;
   int upRows, dnRow0;
+  // k_generic: 1 = stage a (32 + W - 1) x (32 + H - 1) input tile in shared
+  // memory per 32 x 32 outputs (dynamic shared memory of that size), 0 =
+  // read every tap from global memory (windows whose tile would not fit)
+  int gtile;
   T v[VMAX];
 };
 
@@ -472,14 +476,70 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tma_min_blocks<T, L, R,
 }
 
 // ------------------------------------------------------------- k_generic
+// Windows the pipelined kernels do not take (beyond 9 x 9, device functions
+// on non-natural windows). Tiled (a.gtile): a 256-thread CTA computes 32 x
+// 32 outputs from a (32 + W - 1) x (32 + H - 1) input tile staged once in
+// shared memory (coalesced loads, the periodic wrap applied while staging);
+// every tap then comes from shared memory. Function windows are handed over
+// IN the tile with rowStride = the tile pitch (the reference's contract
+// allows any stride, stencil.hpp:20-25). Untiled: one thread per point, taps
+// from global memory (windows too large for a tile). Accumulation order is
+// the reference's either way.
 template <typename T, typename Op>
 __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T> a) {
-  const int i = a.col0 + blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = a.row0 + blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= a.col1 || j >= a.row1) return;
   const int W = a.left + a.right + 1;
   const int H = a.top + a.bottom + 1;
   const T* __restrict__ in = a.in;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (a.gtile) {
+    extern __shared__ __align__(16) unsigned char gsm[];
+    T* tile = reinterpret_cast<T*>(gsm);
+    const int TW = 32 + W - 1, TH = 32 + H - 1;
+    const int i0 = a.col0 + blockIdx.x * 32, j0 = a.row0 + blockIdx.y * 32;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int e = tid; e < TW * TH; e += 256) {
+      const int ty = e / TW, tx = e - ty * TW;
+      long long r = static_cast<long long>(j0) + a.inShift - a.top + ty;
+      if (a.wrapY) {
+        if (r < 0 || r >= a.inRows) r = wrap_idx(r, a.inRows);
+      } else {
+        r = r < 0 ? 0 : (r >= a.inRows ? a.inRows - 1 : r);  // feeds only outputs that are not stored
+      }
+      long long c = static_cast<long long>(i0) - a.left + tx;
+      if (a.wrapX) {
+        if (c < 0 || c >= a.nx) c = wrap_idx(c, a.nx);
+      } else {
+        c = c < 0 ? 0 : (c >= a.nx ? a.nx - 1 : c);
+      }
+      tile[e] = in[r * a.nx + c];
+    }
+    __syncthreads();
+    const int i = i0 + threadIdx.x;
+    if (i >= a.col1) return;
+#pragma unroll 1
+    for (int k = 0; k < 4; ++k) {
+      const int yy = threadIdx.y + 8 * k, j = j0 + yy;
+      if (j >= a.row1) break;
+      const T* base = tile + yy * TW + threadIdx.x;
+      if constexpr (sg_same<Op, OpWeights>::value) {
+        const T* wt = a.count <= VMAX ? a.v : a.wdev;
+        T acc = T(0);
+        for (int q = 0; q < H; ++q) {
+          const T* rowp = base + q * TW;
+          const T* wq = wt + q * W;
+#pragma unroll 4
+          for (int p = 0; p < W; ++p) acc += wq[p] * rowp[p];
+        }
+        put_out(a, j, i, acc);
+      } else {
+        put_out(a, j, i, Op::template apply<T>(base, a.v, TW));
+      }
+    }
+    return;
+  }
+  const int i = a.col0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = a.row0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= a.col1 || j >= a.row1) return;
   if constexpr (sg_same<Op, OpWeights>::value) {
     const T* wt = a.count <= VMAX ? a.v : a.wdev;
     T acc = T(0);
@@ -509,7 +569,6 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T
     put_out(a, j, i, Op::template apply<T>(w, a.v, W));
   }
 }
-
 
 // ------------------------------------------------------------- k_tma_g
 // (design notes: stencil_g.cuh)

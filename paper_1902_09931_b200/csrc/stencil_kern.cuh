@@ -64,6 +64,14 @@ inline bool stencil_pdl() {
   return v;
 }
 
+// k_generic's staged input tile (32 + W - 1) x (32 + H - 1) in bytes, or 0
+// when it would exceed 48 KB (taps are then read from global memory).
+template <typename T>
+size_t generic_tile_bytes(const sg_extents& e) {
+  const size_t b = static_cast<size_t>(32 + e.left + e.right) * (32 + e.top + e.bottom) * sizeof(T);
+  return b <= (48u << 10) ? b : 0;
+}
+
 inline int sm_count() {
   static int n = [] {
     int dev = 0, v = 148;
