@@ -756,3 +756,22 @@ def test_fp32_paths_and_frames(sg, orc, periodic, ext, shape):
         inner = np.ones((ny, nx), bool)
     err = np.max(np.abs(got[inner].astype(np.float64) - want[inner]))
     assert err <= 1e-5 * np.max(np.abs(want[inner]))
+
+
+@pytest.mark.parametrize("ext", [(5, 5, 5, 5), (7, 2, 0, 9), (0, 12, 3, 3), (30, 29, 30, 28), (40, 40, 1, 1)])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_generic_kernel_wide_windows_bitwise(sg, orc, ext, periodic):
+    """k_generic: windows past 9 x 9 — tiled through shared memory, or (tile
+    over 48 KB: the 60 x 59 and 81 x 3 windows) per point from global
+    memory; periodic wrap on odd grid sizes, frame untouched."""
+    rng = np.random.default_rng(sum(ext) + periodic)
+    l, r, t, b = ext
+    nx, ny = 101, 67
+    if l + r >= nx or t + b >= ny:
+        pytest.skip("window wider than the grid")
+    inp = rng.uniform(-1, 1, (ny, nx))
+    w = rng.uniform(-1, 1, (l + r + 1) * (t + b + 1))
+    sentinel = np.full_like(inp, -12345.678)
+    got = run_gpu(sg, inp, ext, w, direction=direction_of(ext), periodic=periodic, out=sentinel, expect_kind=0)
+    want = orc.stencil(inp, ext, w, periodic=periodic, out=sentinel)
+    assert bits_equal(got, want)
