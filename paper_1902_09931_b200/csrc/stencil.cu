@@ -96,7 +96,7 @@ void launch_tma_lt(const KArgs<T>& a, cudaStream_t s) {
     SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(G::smem_bytes)));
     SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctasPerSm, kern, (TMA_WARPS + 1) * 32, G::smem_bytes));
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctasPerSm, kern, (G::NW + 1) * 32, G::smem_bytes));
     if (ctasPerSm < 1) ctasPerSm = 1;
   }
   const int gx = (a.nx + G::CW - 1) / G::CW;
@@ -104,7 +104,7 @@ void launch_tma_lt(const KArgs<T>& a, cudaStream_t s) {
   KArgs<T> b = a;
   b.segRows = tma_segment_rows(rows, gx, ctasPerSm, G::RPS);
   dim3 g2(gx, static_cast<unsigned>((rows + b.segRows - 1) / b.segRows));
-  launch_ex(kern, g2, dim3((TMA_WARPS + 1) * 32), G::smem_bytes, s, stencil_pdl(), b);
+  launch_ex(kern, g2, dim3((G::NW + 1) * 32), G::smem_bytes, s, stencil_pdl(), b);
 }
 
 template <typename T, typename Op>

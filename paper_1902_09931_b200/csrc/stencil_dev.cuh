@@ -216,12 +216,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// CTA geometry: TMA_WARPS consumer warps side by side cover CW columns; one
+// CTA geometry: NW consumer warps side by side cover CW columns; one
 // producer warp streams rows (CW + halos) into a STAGES x RPS ring.
+// Light windows use 16 consumers (a 17-warp CTA, CW = 1024 FP64 columns:
+// 32768-wide grids split into whole blocks). Register-heavy windows use 15,
+// a 16-warp CTA — four warps on each of the SM's four sub-partitions, so a
+// thread may hold 128 registers: with 17 warps one sub-partition hosts five
+// and its 16 K-register file caps every thread at ~96. Measured at 16384^2
+// FP64 (whole builds, 15 vs 16): 5x5 weights 0.61 -> 0.68 of HBM, 9x9 0.158
+// -> 0.178, {2,1,1,2} 0.71 -> 0.83, odd-row 3x3 0.84 -> 0.90; but the
+// headline 32768^2 3x3 function 415 -> 396 Gpts/s (FP32 800 -> 764: ragged
+// 960-column blocks), so light windows keep 16.
 #ifndef SG_TMA_WARPS
 #define SG_TMA_WARPS 16
 #endif
+#ifndef SG_TMA_WARPS_HEAVY
+#define SG_TMA_WARPS_HEAVY 15
+#endif
 constexpr int TMA_WARPS = SG_TMA_WARPS;
+// consumer warps of k_tma (window height H) and of k_tma_g (W x H window)
+__host__ __device__ constexpr int tma_nw(int H) { return H >= 5 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS; }
+__host__ __device__ constexpr int tmag_nw(int W, int H) { return W * H >= 9 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS; }
 // Release of a ring stage by the consumers: every thread arrives on the
 // "empty" mbarrier (1), or each warp's lane 0 after __syncwarp (0).
 #ifndef SG_EMPTY_ALL_LANES
@@ -232,7 +247,8 @@ template <typename T, int L, int R, int TP, int BT>
 struct TmaGeom {
   static constexpr int V = VecT<T>::V;
   static constexpr int SW = 32 * V;
-  static constexpr int CW = TMA_WARPS * SW;
+  static constexpr int NW = tma_nw(TP + BT + 1);
+  static constexpr int CW = NW * SW;
   static constexpr int LP = ((L + V - 1) / V) * V;  // left pad, 16 B granules
   static constexpr int RP = ((R + V - 1) / V) * V;
   static constexpr int ROW = LP + CW + RP;  // elements per staged row (~2 KB)
@@ -261,7 +277,7 @@ constexpr int tma_min_blocks() {
 }
 
 template <typename T, int L, int R, int TP, int BT, typename Op>
-__global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tma_min_blocks<T, L, R, TP, BT>())) k_tma(const __grid_constant__ KArgs<T> a) {
+__global__ void __launch_bounds__((TmaGeom<T, L, R, TP, BT>::NW + 1) * 32, (tma_min_blocks<T, L, R, TP, BT>())) k_tma(const __grid_constant__ KArgs<T> a) {
   using G = TmaGeom<T, L, R, TP, BT>;
   using VT = typename VecT<T>::type;
   constexpr int V = G::V, SW = G::SW, CW = G::CW, LP = G::LP, RP = G::RP, ROW = G::ROW;
@@ -286,7 +302,7 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tma_min_blocks<T, L, R,
   if (threadIdx.x == 0) {
     for (int k = 0; k < STAGES; ++k) {
       mbar_init(&full[k], 1 + 32);  // expect_tx arrival + the producer warp's cp.async arrivals
-      mbar_init(&empty[k], SG_EMPTY_ALL_LANES ? TMA_WARPS * 32 : TMA_WARPS);
+      mbar_init(&empty[k], SG_EMPTY_ALL_LANES ? G::NW * 32 : G::NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -296,7 +312,7 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tma_min_blocks<T, L, R,
   // kernel's tail; no global memory is touched before its completion
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (warp == TMA_WARPS) {
+  if (warp == G::NW) {
     // ---------------- producer warp: per row, lane 0 issues one bulk copy of
     // the CTA's own columns (128 B aligned, whole lines: no over-fetch),
     // lanes 1.. one 16 B cp.async granule each for the halo columns (wrapped
@@ -582,7 +598,8 @@ template <typename T, int W, int H>
 struct TmaGGeom {
   static constexpr int V = VecT<T>::V;
   static constexpr int SW = 32 * V;
-  static constexpr int CW = TMA_WARPS * SW;
+  static constexpr int NW = tmag_nw(W, H);
+  static constexpr int CW = NW * SW;
   static constexpr int HP = ((W - 1 + V - 1) / V) * V;  // halo room either side (any split of W - 1)
   static constexpr int ROW = HP + CW + V + HP;          // + V: the row's 16 B phase
   static constexpr int RPS = H >= 2 ? H : 2;
@@ -631,7 +648,7 @@ constexpr int tmag_min_blocks() {
 }
 
 template <typename T, int W, int H, typename Op>
-__global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tmag_min_blocks<T, W, H>())) k_tma_g(const __grid_constant__ KArgs<T> a) {
+__global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_blocks<T, W, H>())) k_tma_g(const __grid_constant__ KArgs<T> a) {
   using G = TmaGGeom<T, W, H>;
   using VT = typename VecT<T>::type;
   constexpr int V = G::V, SW = G::SW, CW = G::CW, HP = G::HP, ROW = G::ROW;
@@ -659,7 +676,7 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tmag_min_blocks<T, W, H
   if (threadIdx.x == 0) {
     for (int k = 0; k < STAGES; ++k) {
       mbar_init(&full[k], 1 + 32);  // expect_tx arrival + the producer warp's cp.async arrivals
-      mbar_init(&empty[k], TMA_WARPS * 32);
+      mbar_init(&empty[k], G::NW * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -669,7 +686,7 @@ __global__ void __launch_bounds__((TMA_WARPS + 1) * 32, (tmag_min_blocks<T, W, H
   // kernel's tail; no global memory is touched before its completion
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (warp == TMA_WARPS) {
+  if (warp == G::NW) {
     // ---------------- producer warp: per row, lane 0 issues the 16 B-aligned
     // middle of the CTA's columns as one bulk copy; the unaligned head/tail
     // elements and the halo columns (wrapped in index math) are spread over
