@@ -402,6 +402,7 @@ def extras(sg, torch, stream, peak, args):
     sg.destroy_plan(plan)
     out["cfg1_512sq_10apps_ms"] = best * 1e3
     out["stencil_variants_16384sq_fp64"] = bench_variants(sg, torch, stream, peak)
+    out["stencil_variants_16384sq_fp32"] = bench_variants(sg, torch, stream, peak, dtype="f32")
     out["penta_general_periodic"] = bench_penta_general(sg, torch, peak)
     out["weno5_advect_8192sq_fp64"] = bench_weno(sg, torch, peak)
     if not args.skip_ch:
@@ -492,12 +493,14 @@ def bench_weno(sg, torch, peak, n=8192, reps=10, ref_n=1024):
     return res
 
 
-def bench_variants(sg, torch, stream, peak, n=16384, launches=20):
+def bench_variants(sg, torch, stream, peak, n=16384, launches=20, dtype="f64"):
     """HBM roofline fraction of the fast path across the API surface
     (directions, boundary modes, window sizes, weights vs functions) on a
-    16384^2 FP64 grid (2 GiB per field >> L2)."""
+    16384^2 grid (2 GiB per FP64 field >> L2); dtype "f32" runs a subset in
+    FP32 (rows at four 16 B phases for the odd widths)."""
     import numpy as np
     rng = np.random.default_rng(9)
+    f32 = dtype == "f32"
     cases = [
         ("x_nonperiodic_5pt_weights", sg.Direction.X, sg.BoundaryMode.NonPeriodic, sg.Extents(2, 2, 0, 0), None, 5),
         ("y_periodic_5pt_weights", sg.Direction.Y, sg.BoundaryMode.Periodic, sg.Extents(0, 0, 2, 2), None, 5),
@@ -519,8 +522,13 @@ def bench_variants(sg, torch, stream, peak, n=16384, launches=20):
         ("xy_periodic_11x11_weights_generic", sg.Direction.XY, sg.BoundaryMode.Periodic, sg.Extents(5, 5, 5, 5),
          None, 121),
     ]
-    a = torch.rand((n, n), dtype=torch.float64, device="cuda")
+    if f32:
+        keep = ("xy_periodic_3x3_weights", "xy_periodic_5x5_weights", "x_periodic_asym_3_1_0_0_weights",
+                "xy_periodic_asym_2_1_1_2_weights", "xy_periodic_3x3_fn_weighted_odd_nx_16383")
+        cases = [c for c in cases if c[0] in keep]
+    a = torch.rand((n, n), dtype=torch.float32 if f32 else torch.float64, device="cuda")
     b = torch.zeros_like(a)
+    esz = 4 if f32 else 8
     stream.wait_stream(torch.cuda.current_stream())
     res = {}
     for name, d, mode, ext, fn, nv in cases:
@@ -543,16 +551,18 @@ def bench_variants(sg, torch, stream, peak, n=16384, launches=20):
         csum = clk.summary()
         rows = n - (ext.top + ext.bottom if mode == sg.BoundaryMode.NonPeriodic else 0)
         cols = nxv - (ext.left + ext.right if mode == sg.BoundaryMode.NonPeriodic else 0)
-        alg = 8 * (n * nxv + rows * cols)
+        alg = esz * (n * nxv + rows * cols)
         # FP64 instructions per output point (no FMA contraction: a multiply
         # and an add per tap; the CH window adds c^3 - c per tap)
         ops = 5 * nv if fn == "ch_nonlinear_window" else 2 * nv
         rate = ops * rows * cols / (ms * 1e-3)
+        fp = "fp32" if f32 else "fp64"
+        lanes = 128 if f32 else 64  # FP32 / FP64 lanes per SM per cycle
         res[name] = {"gpts_s": rows * cols / (ms * 1e-3) / 1e9, "kernel_ms": ms,
                      "hbm_frac": alg / (ms * 1e-3) / 1e9 / peak,
-                     "fp64_ops_per_pt": ops, "fp64_frac": rate / FP64_PEAK_OPS,
+                     f"{fp}_ops_per_pt": ops, f"{fp}_frac": rate / (148 * lanes * 1.965e9),
                      "sm_mhz": csum.get("sm_mhz"), "clock_reasons": csum.get("reasons"),
-                     "fp64_frac_at_clock": (rate / (148 * 64 * csum["sm_mhz"] * 1e6)) if csum.get("sm_mhz") else None,
+                     f"{fp}_frac_at_clock": (rate / (148 * lanes * csum["sm_mhz"] * 1e6)) if csum.get("sm_mhz") else None,
                      "kernel": {2: "k_tma_g", 1: "k_tma", 0: "k_generic"}[kk], "nx": nxv}
     del a, b
     torch.cuda.empty_cache()
