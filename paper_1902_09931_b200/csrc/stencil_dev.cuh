@@ -810,8 +810,48 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
       }
       if (j >= ra && j < rb) {  // warp-uniform
         const long long jo = static_cast<long long>(j) * nx;
-        const bool rowVec = ((outOff + static_cast<unsigned>(j) * unx) & (V - 1)) == 0;
-        if (laneFull && rowVec && (!peers || peerVec)) {
+        const int pho = static_cast<int>((outOff + static_cast<unsigned>(j) * unx) & (V - 1));
+        const bool rowVec = pho == 0;
+        // (only with the 16-warp geometry's register headroom: on 17-warp
+        // CTAs the extra registers cost more than the stores save)
+        if (G::NW == SG_TMA_WARPS_HEAVY && !rowVec && !peers) {
+          // misaligned output row: realign across lanes. The row's 16 B
+          // groups start at column xb + sh; lane t stores the group made of
+          // its res[sh..V-1] and lane t+1's res[0..sh-1] (shuffled down) as
+          // one vector; what no group of this warp covers (lane 0's first sh
+          // columns, lane 31's last V - sh, groups reaching outside
+          // [col0, col1)) goes out element by element.
+          const int sh = V - pho;
+          T nb[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v) nb[v] = __shfl_down_sync(0xffffffffu, res[v], 1);
+          const int gc = xb + sh;
+          const bool mine = lane < 31 && gc >= a.col0 && gc + V <= a.col1;
+          const bool prev = lane > 0 && gc - V >= a.col0 && gc <= a.col1;
+          if (mine) {
+            T o[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) o[v] = v + sh < V ? res[v + sh] : nb[v + sh - V];
+            VT ov;
+            if constexpr (V == 2) {
+              ov.x = o[0];
+              ov.y = o[1];
+            } else {
+              ov.x = o[0];
+              ov.y = o[1];
+              ov.z = o[2];
+              ov.w = o[3];
+            }
+            *reinterpret_cast<VT*>(a.out + jo + gc) = ov;
+          }
+          if (laneValid) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const bool covered = v < sh ? prev : mine;
+              if (!covered && xb + v >= a.col0 && xb + v < a.col1) a.out[jo + xb + v] = res[v];
+            }
+          }
+        } else if (laneFull && rowVec && (!peers || peerVec)) {
           VT o;
           if constexpr (V == 2) {
             o.x = res[0];
