@@ -837,9 +837,18 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
           const bool mine = lane < 31 && gc >= a.col0 && gc + V <= a.col1;
           const bool prev = lane > 0 && gc - V >= a.col0 && gc <= a.col1;
           if (mine) {
+            // o[v] = res[v + sh] or nb[v + sh - V], selected with
+            // compile-time indices (a runtime index would put res in local
+            // memory)
             T o[V];
 #pragma unroll
-            for (int v = 0; v < V; ++v) o[v] = v + sh < V ? res[v + sh] : nb[v + sh - V];
+            for (int v = 0; v < V; ++v) {
+              T x = res[0];
+#pragma unroll
+              for (int c = 1; c < V; ++c)
+                if (sh == c) x = v + c < V ? res[v + c] : nb[v + c - V];
+              o[v] = x;
+            }
             VT ov;
             if constexpr (V == 2) {
               ov.x = o[0];
