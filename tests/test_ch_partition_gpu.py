@@ -81,3 +81,21 @@ def test_partition_rejects_bad_segments(sg):
         st.set_partition(3)  # 256 / 3 is not a whole number of 64-row stages
     with pytest.raises(sg.InvalidArgument):
         st.set_partition(17)
+
+
+def test_partition_is_single_gpu_only(sg):
+    """numWorkers > 1 steppers (config 5's distributed step) keep the bitwise
+    sweeps: the partitioned mode is rejected there (at 8192^2
+    any reordering exceeds the 1e-9 bar)."""
+    p = sg.CHParams(nx=256, ny=256)
+    p.dt = 0.1 * p.dx()
+    p.T = 1.0
+    old = sg.get_device_map()
+    sg.set_device_map("modulo")
+    try:
+        st = sg.CHStepper(p, 1, 2)
+        assert st.workers()[0] == 2
+        with pytest.raises(sg.InvalidArgument):
+            st.set_partition(4)
+    finally:
+        sg.set_device_map(old)
