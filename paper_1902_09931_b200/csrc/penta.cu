@@ -378,22 +378,20 @@ __global__ void __launch_bounds__(SWEEP_THREADS) k_sweep(const PentaTables f, in
 constexpr int SW_RS = 32;   // rows per stage
 constexpr int SW_NSTG = 4;  // stages in flight
 
-template <bool UNIFORM>
 struct SweepSmem {
-  // doubles per factor table per stage; tensor-TMA destinations must be
-  // 128 B aligned, so the uniform (SW_RS-long) tables get a 16-double slot
-  static constexpr int FAC = UNIFORM ? (SW_RS + 15) / 16 * 16 : SW_RS * 32;
+  // doubles per factor table per stage (per-system tables: one RS x 32 box)
+  static constexpr int FAC = SW_RS * 32;
   static constexpr int STAGE = SW_RS * 32 + 3 * FAC;
   static constexpr int STAGE_PAD = (STAGE * 8 + 127) / 128 * 16;  // doubles, 128 B aligned stride
   static constexpr size_t bytes = static_cast<size_t>(SW_NSTG) * STAGE_PAD * 8 + 2 * SW_NSTG * 8;
 };
 
-template <bool UNIFORM, bool PERIODIC, int MODE>
+template <bool PERIODIC, int MODE>
 __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __grid_constant__ SweepMaps maps,
                                                   int B, int n, double* __restrict__ z, double* __restrict__ y4) {
   // Warp 0: consumer (32 systems, the dependency chain). Warp 1 lane 0:
   // producer (tensor-TMA issue), so the chain never stalls on issue code.
-  using SM = SweepSmem<UNIFORM>;
+  using SM = SweepSmem;
   extern __shared__ __align__(128) double sw_smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sw_smem + SW_NSTG * SM::STAGE_PAD);
   uint64_t* empty = full + SW_NSTG;
@@ -405,7 +403,7 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
   constexpr int FAC = SM::FAC;
   constexpr int RS = SW_RS;
   constexpr uint32_t ZB = RS * 32 * 8;
-  constexpr uint32_t FB = (UNIFORM ? RS : RS * 32) * 8;  // bytes per factor box
+  constexpr uint32_t FB = RS * 32 * 8;  // bytes per factor box
   const int nS = (n + RS - 1) / RS;  // stages per pass
   const int total = 2 * nS;
   if (threadIdx.x == 0) {
@@ -440,10 +438,7 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
         s_tma_2d(st, &maps.z, b0, r0, &full[slot]);
         for (int k = 0; k < nt; ++k) {
           const CUtensorMap* m = &maps.t[pass == 0 ? k : 2 + k];  // fwd: m1, m2; bwd: dInv, ap, bp
-          if (UNIFORM)
-            s_tma_1d(st + RS * 32 + k * FAC, m, r0, &full[slot]);
-          else
-            s_tma_2d(st + RS * 32 + k * FAC, m, b0, r0, &full[slot]);
+          s_tma_2d(st + RS * 32 + k * FAC, m, b0, r0, &full[slot]);
         }
       }
     }
@@ -452,7 +447,7 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
 
   // -------------------------------------------------------------- consumer
   auto fac = [&](const double* st, int k, int row) -> double {
-    return UNIFORM ? st[RS * 32 + k * FAC + row] : st[RS * 32 + k * FAC + row * 32 + lane];
+    return st[RS * 32 + k * FAC + row * 32 + lane];
   };
   auto zin = [&](const double* st, int k) -> double { return st[k * 32 + lane]; };
   double* zc = z + b;
@@ -595,7 +590,7 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
     if (lane == 0) s_mbar_arrive(&empty[slot]);
   }
   if constexpr (PERIODIC) {
-    const int sys = UNIFORM ? 0 : b;
+    const int sys = b;
     if (!active) return;
     const double* cw = f.cw + sys * 6;
     double y[4];
@@ -611,19 +606,19 @@ __global__ void __launch_bounds__(64) k_sweep_tma(const PentaTables f, const __g
 #pragma unroll 4
       for (int r = 0; r < n; ++r) {
         const long long idx = r * sB;
-        const double w0 = tab(f.W[0], r, b, B, UNIFORM), w1 = tab(f.W[1], r, b, B, UNIFORM),
-                     w2 = tab(f.W[2], r, b, B, UNIFORM), w3 = tab(f.W[3], r, b, B, UNIFORM);
+        const double w0 = tab(f.W[0], r, b, B, false), w1 = tab(f.W[1], r, b, B, false),
+                     w2 = tab(f.W[2], r, b, B, false), w3 = tab(f.W[3], r, b, B, false);
         zc[idx] -= w0 * y[0] + w1 * y[1] + w2 * y[2] + w3 * y[3];
       }
     }
   }
 }
 
-template <bool U, bool P, int M>
+template <bool P, int M>
 void launch_sweep_tma(const PentaTables& f, const SweepMaps& maps, int B, int n, double* z, double* y4,
                       cudaStream_t s) {
-  auto kern = k_sweep_tma<U, P, M>;
-  using SM = SweepSmem<U>;
+  auto kern = k_sweep_tma<P, M>;
+  using SM = SweepSmem;
   static bool configured = false;
   if (!configured) {
     SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SM::bytes)));
@@ -707,21 +702,18 @@ void penta_sweep(const PentaTables& f, int B, int n, double* z, double* y4, bool
   }
   SweepMaps maps;
   const int rs = sweep_res_rows(B);
-  if (f.uniform && (!periodic || fusedCorrection) && use_resident_sweep() && sweep_maps(f, B, n, z, &maps, rs)) {
+  if (f.uniform && (!periodic || fusedCorrection) && sweep_maps(f, B, n, z, &maps, rs)) {
     launch_sweep_res(periodic, f, maps, B, n, y4, s, pdl, rs);
     check_launch("penta sweep (TMA, resident turn) kernel");
     return;
   }
-  if (sweep_maps(f, B, n, z, &maps)) {
-    if (f.uniform) {
-      if (!periodic) launch_sweep_tma<true, false, 0>(f, maps, B, n, z, y4, s);
-      else if (fusedCorrection) launch_sweep_tma<true, true, 1>(f, maps, B, n, z, y4, s);
-      else launch_sweep_tma<true, true, 0>(f, maps, B, n, z, y4, s);
-    } else {
-      if (!periodic) launch_sweep_tma<false, false, 0>(f, maps, B, n, z, y4, s);
-      else if (fusedCorrection) launch_sweep_tma<false, true, 1>(f, maps, B, n, z, y4, s);
-      else launch_sweep_tma<false, true, 0>(f, maps, B, n, z, y4, s);
-    }
+  // general per-system tables: the streaming TMA sweep (uniform operators
+  // that reach here — odd batches, unaligned rhs, SG_SWEEP_KERNEL=reg — take
+  // the register-prefetch sweep below)
+  if (!f.uniform && sweep_maps(f, B, n, z, &maps)) {
+    if (!periodic) launch_sweep_tma<false, 0>(f, maps, B, n, z, y4, s);
+    else if (fusedCorrection) launch_sweep_tma<true, 1>(f, maps, B, n, z, y4, s);
+    else launch_sweep_tma<true, 0>(f, maps, B, n, z, y4, s);
     check_launch("penta sweep (TMA) kernel");
     return;
   }
@@ -756,7 +748,7 @@ bool penta_sweep_xin(const PentaTables& f, int B, int n, double* z, const double
 bool penta_sweep_seg(const SegPenta& sp, int B, double* z, const double* zT, const double* const* Wc,
                      const double* yc, int ycSeg, double* gIf, cudaStream_t s, bool pdl, bool launch) {
   const int n = sp.n, m = sp.m, P = sp.P;
-  if (P < 1 || !sp.local.t.uniform || !use_resident_sweep()) return false;
+  if (P < 1 || !sp.local.t.uniform) return false;
   if ((reinterpret_cast<uintptr_t>(zT) & 15) || (reinterpret_cast<uintptr_t>(z) & 15) || (B & 1) || n % 16) return false;
   int rs = sweep_res_rows(B * P);
   if (m % rs) rs = RR_RS;

@@ -82,7 +82,12 @@ int kernel_kind(const sg_slab_desc& d, const sg_extents& e, int fn, size_t count
   if (count > static_cast<size_t>(VMAX)) return 0;
   const uintptr_t pin = reinterpret_cast<uintptr_t>(in), pout = reinterpret_cast<uintptr_t>(out);
   const bool aligned = d.nx % V == 0 && (pin | pout) % 16 == 0;
-  if (aligned && strip_supported(e, fn)) return 1;
+  // SG_STENCIL_KIND=g (experiments): route k_tma's cases to k_tma_g
+  static const bool forceG = [] {
+    const char* v = std::getenv("SG_STENCIL_KIND");
+    return v && v[0] == 'g';
+  }();
+  if (aligned && strip_supported(e, fn) && !(forceG && general_supported(e, fn))) return 1;
   if ((pin | pout) % sizeof(T) == 0 && general_supported(e, fn)) return 2;
   return 0;
 }

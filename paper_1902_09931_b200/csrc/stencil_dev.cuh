@@ -238,6 +238,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #ifndef SG_TMA_WARPS
 #define SG_TMA_WARPS 16
 #endif
+#ifndef SG_REALIGN_F32
+#define SG_REALIGN_F32 1
+#endif
 #ifndef SG_TMA_WARPS_HEAVY
 #define SG_TMA_WARPS_HEAVY 15
 #endif
@@ -622,6 +625,34 @@ struct TmaGGeom {
   static constexpr size_t smem_bytes = STAGES * stage_bytes + 2 * STAGES * sizeof(uint64_t);
 };
 
+// Columns of one staged row that move as a single bulk copy: [a0, a1),
+// both 16 B aligned in global memory (V elements). The CTA needs
+// [cx0, cx0 + validC) plus halos; where the row's phase ph != 0 the bulk
+// copy over-fetches to the aligned boundaries as long as the extra columns
+// lie inside the same grid row (they are then exactly the halo columns the
+// window reads, with the same values, so those halo copies are skipped);
+// otherwise (the row's first CTA at cx0 = 0, or a tail that would cross the
+// row end where periodic x wraps) the ragged head [cx0, cx0 + hc) and tail
+// [ts, cx0 + validC) move as element cp.async. Over-fetching replaces up to
+// 2 * (V - 1) element copies per row with nothing (FP32: 6 of them).
+template <int V>
+struct RowSpan {
+  int a0, a1, hc, ts;
+  __device__ RowSpan(int ph, int cx0, int validC, int nx) {
+    const int e = cx0 + validC;
+    if (ph == 0) a0 = cx0;
+    else if (cx0 >= ph) a0 = cx0 - ph;  // over-fetch the head (same row)
+    else a0 = cx0 + (V - ph);  // first aligned column; [cx0, a0) as elements
+    const int endPh = (ph + validC) & (V - 1);
+    if (endPh == 0) a1 = e;
+    else if (e + (V - endPh) <= nx) a1 = e + (V - endPh);  // over-fetch the tail (same row)
+    else a1 = e - endPh;
+    hc = a0 > cx0 ? min(a0, e) - cx0 : 0;
+    if (a1 <= a0) a1 = a0;  // no bulk copy: the whole span moves as elements
+    ts = a1 > a0 ? min(a1, e) : cx0 + hc;
+  }
+};
+
 // Source row of the t-th staged row of a CTA: rows wrap (periodic y) or
 // clamp to the grid (rows past a non-periodic edge feed only outputs that
 // are never stored).
@@ -721,8 +752,8 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
       for (int k = 0; k < RPS; ++k) {
         src[k] = w2.cur;
         const int ph = static_cast<int>((inOff + static_cast<unsigned>(w2.cur) * unx) & (V - 1));
-        const int head = ph ? min(V - ph, validC) : 0;
-        tx += static_cast<uint32_t>(((validC - head) / V) * V * sizeof(T));
+        const RowSpan<V> sp(ph, cx0, validC, nx);
+        tx += static_cast<uint32_t>((sp.a1 - sp.a0) * sizeof(T));
         w2.next(a.inRows, a.wrapY);
       }
       if (lane == 0) {
@@ -735,24 +766,34 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
         const T* grow = in + static_cast<long long>(src[k]) * nx;
         const int ph = static_cast<int>((inOff + static_cast<unsigned>(src[k]) * unx) & (V - 1));
         T* srow = sstage + k * ROW + HP + ph;  // column cx0 of this row
-        const int head = ph ? min(V - ph, validC) : 0;
-        const int mid = ((validC - head) / V) * V;
-        const int tl = validC - head - mid;
-        if (lane == 0 && mid)
-          bulk_g2s(srow + head, grow + cx0 + head, static_cast<uint32_t>(mid * sizeof(T)), &full[slot]);
+        const RowSpan<V> sp(ph, cx0, validC, nx);
+        if (lane == 0 && sp.a1 > sp.a0)
+          bulk_g2s(srow + (sp.a0 - cx0), grow + sp.a0, static_cast<uint32_t>((sp.a1 - sp.a0) * sizeof(T)),
+                   &full[slot]);
+        const int e1 = cx0 + validC;
         int e = lane - 1;  // this lane's element copy, if any
-        if (e >= 0 && e < head) {
+        if (e >= 0 && e < sp.hc) {
           cp_async_elem(srow + e, grow + cx0 + e);
-        } else if ((e -= head) >= 0 && e < tl) {
-          cp_async_elem(srow + head + mid + e, grow + cx0 + head + mid + e);
-        } else if ((e -= tl) >= 0 && e < l) {
+        } else if ((e -= sp.hc) >= 0 && e < e1 - sp.ts) {
+          cp_async_elem(srow + (sp.ts - cx0) + e, grow + sp.ts + e);
+        } else if ((e -= e1 - sp.ts) >= 0 && e < l) {
           const int c = cx0 - 1 - e;
-          if (c >= 0) cp_async_elem(srow - 1 - e, grow + c);
-          else if (a.wrapX) cp_async_elem(srow - 1 - e, grow + c + nx);
+          if (sp.a1 > sp.a0 && c >= sp.a0) {
+            // already staged by the over-fetched bulk copy
+          } else if (c >= 0) {
+            cp_async_elem(srow - 1 - e, grow + c);
+          } else if (a.wrapX) {
+            cp_async_elem(srow - 1 - e, grow + c + nx);
+          }
         } else if ((e -= l) >= 0 && e < r) {
-          const int c = cx0 + validC + e;
-          if (c < nx) cp_async_elem(srow + validC + e, grow + c);
-          else if (a.wrapX) cp_async_elem(srow + validC + e, grow + c - nx);
+          const int c = e1 + e;
+          if (sp.a1 > sp.a0 && c < sp.a1) {
+            // already staged by the over-fetched bulk copy
+          } else if (c < nx) {
+            cp_async_elem(srow + validC + e, grow + c);
+          } else if (a.wrapX) {
+            cp_async_elem(srow + validC + e, grow + c - nx);
+          }
         }
       }
       rw = w2;
@@ -785,6 +826,8 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
       rw.next(a.inRows, a.wrapY);
       const T* srow = sbase + k * ROW + ph;  // window column 0 of the lane's first output
       T* e = win[ACC ? 0 : k % H];
+      // (scalar reads: 16 B vector reads + runtime-phase selects measured
+      // slower, FP32 4x4 0.64 -> 0.60 of HBM, 3x3 odd 0.76 -> 0.68)
 #pragma unroll
       for (int p = 0; p < E; ++p) e[p] = srow[p];
       T res[V];
@@ -827,7 +870,7 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
         const bool rowVec = pho == 0;
         // (only with the 16-warp geometry's register headroom: on 17-warp
         // CTAs the extra registers cost more than the stores save)
-        if (G::NW == SG_TMA_WARPS_HEAVY && !rowVec && !peers) {
+        if ((G::NW == SG_TMA_WARPS_HEAVY || (SG_REALIGN_F32 && sizeof(T) == 4)) && !rowVec && !peers) {
           // misaligned output row: realign across lanes. The row's 16 B
           // groups start at column xb + sh; lane t stores the group made of
           // its res[sh..V-1] and lane t+1's res[0..sh-1] (shuffled down) as

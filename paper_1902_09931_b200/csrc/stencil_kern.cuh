@@ -89,7 +89,18 @@ inline int tma_segment_rows(int rows, int gx, int ctasPerSm, int rps) {
   long long seg = (1LL * rows * gx + cap - 1) / cap;
   seg = std::max<long long>(seg, std::min(rows, 2 * rps));
   seg = std::min<long long>(seg, 512);
-  return static_cast<int>(seg);
+  // rounding up twice (rows per segment, then segments per column) can
+  // leave a handful of CTAs past the last full wave (16384^2 FP32 3x3:
+  // 9 x 33 = 297 CTAs on 296 slots, the 297th running its 499 rows alone);
+  // take the segment length with the fewest waves x rows per CTA
+  auto cost = [&](long long s) {
+    const long long ctas = 1LL * gx * ((rows + s - 1) / s);
+    return ((ctas + cap - 1) / cap) * s;
+  };
+  long long best = seg;
+  for (long long s = seg + 1; s <= std::min<long long>(rows, seg + seg / 4 + 1); ++s)
+    if (cost(s) < cost(best)) best = s;
+  return static_cast<int>(best);
 }
 
 template <typename Op, typename F>

@@ -779,14 +779,6 @@ inline bool sweep_maps(const PentaTables& f, int B, int n, const double* z, Swee
   return true;
 }
 
-inline bool use_resident_sweep() {
-  static const bool v = [] {
-    const char* e = std::getenv("SG_SWEEP_KERNEL");
-    return !(e && std::strcmp(e, "tma") == 0);
-  }();
-  return v;
-}
-
 // Stage height for a batch of B systems (one CTA per 32 systems).
 inline int sweep_res_rows(int B) {
   static const int sms = [] {
@@ -805,7 +797,7 @@ inline bool xin_prepare(const PentaTables& f, int B, int n, double* z, const dou
                         const double* yc, int ztInner, const SweepPeers* peers, SweepMaps* maps, SweepFuse* fuse,
                         int* rsOut) {
   // Uniform periodic operator, resident-turn sweep only (the CH sweeps).
-  if (!f.uniform || !use_resident_sweep()) return false;
+  if (!f.uniform) return false;
   if (ztInner <= 0) ztInner = n;
   if ((reinterpret_cast<uintptr_t>(zT) & 15) || (n & 1) || n % ztInner || ztInner % 16) return false;
   if (Wc && (reinterpret_cast<uintptr_t>(yc) & 15)) return false;
