@@ -35,6 +35,28 @@ typedef decltype(sizeof(0)) size_t;
 #ifndef SG_TALL_STAGES
 #define SG_TALL_STAGES 2
 #endif
+// Deep rings for tall windows (H >= 5) on one CTA per SM: as many stages
+// as the shared-memory budget holds (up to SG_DEEP_MAX), so the single CTA
+// keeps the producer far enough ahead of its long consumer rows. Bit 0:
+// k_tma, bit 1: k_tma_g. Measured at 16384^2 (scripts/exp/deep_ab.sh):
+// FP32 5x5 0.79 -> 0.94 of HBM, FP64 5x5 on odd rows 0.51 -> 0.57; short
+// windows lose with deep rings (3x3 0.97 -> 0.90, 5x1 0.93 -> 0.62), so
+// they keep the 9-row ring.
+#ifndef SG_DEEP_STAGES
+#define SG_DEEP_STAGES 3
+#endif
+#ifndef SG_DEEP_MAX
+#define SG_DEEP_MAX 8
+#endif
+#ifndef SG_SMEM_BUDGET
+#define SG_SMEM_BUDGET (220 * 1024)
+#endif
+__host__ __device__ constexpr int deep_stages(int base, unsigned long long stageBytes, bool deep) {
+  if (!deep) return base;
+  const long long fit = static_cast<long long>(SG_SMEM_BUDGET / stageBytes);
+  const long long d = fit < SG_DEEP_MAX ? fit : SG_DEEP_MAX;
+  return d > base ? static_cast<int>(d) : base;
+}
 
 SG_DEV_BEGIN
 
@@ -273,8 +295,10 @@ struct TmaGeom {
   // slot for every unrolled row is a compile-time constant (no moves).
   static constexpr int RPS = H >= 2 ? H : 2;
   static constexpr int STAGES_BASE = (9 + RPS - 1) / RPS >= 2 ? (9 + RPS - 1) / RPS : 2;
-  static constexpr int STAGES = STAGES_BASE < SG_TALL_STAGES && H >= 5 ? SG_TALL_STAGES : STAGES_BASE;
   static constexpr size_t stage_bytes = static_cast<size_t>(RPS) * ROW * sizeof(T);
+  static constexpr int STAGES =
+      deep_stages(STAGES_BASE < SG_TALL_STAGES && H >= 5 ? SG_TALL_STAGES : STAGES_BASE, stage_bytes,
+                  (SG_DEEP_STAGES & 1) != 0 && H >= 5);
   static constexpr size_t smem_bytes = STAGES * stage_bytes + 2 * STAGES * sizeof(uint64_t);
 };
 
@@ -620,8 +644,10 @@ struct TmaGGeom {
   static constexpr int ROW = HP + CW + V + HP;          // + V: the row's 16 B phase
   static constexpr int RPS = H >= 2 ? H : 2;
   static constexpr int STAGES_BASE = (9 + RPS - 1) / RPS >= 2 ? (9 + RPS - 1) / RPS : 2;
-  static constexpr int STAGES = STAGES_BASE < SG_TALL_STAGES && H >= 5 ? SG_TALL_STAGES : STAGES_BASE;
   static constexpr size_t stage_bytes = static_cast<size_t>(RPS) * ROW * sizeof(T);
+  static constexpr int STAGES =  // (one CTA per SM where tmag_min_blocks says so)
+      deep_stages(STAGES_BASE < SG_TALL_STAGES && H >= 5 ? SG_TALL_STAGES : STAGES_BASE, stage_bytes,
+                  (SG_DEEP_STAGES & 2) != 0 && H >= 5 && !(W <= 3 && H <= 6));
   static constexpr size_t smem_bytes = STAGES * stage_bytes + 2 * STAGES * sizeof(uint64_t);
 };
 
