@@ -217,6 +217,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// expect_tx without an arrival (the arrival comes once per stage)
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -758,71 +763,80 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
 
   if (warp == G::NW) {
     // ---------------- producer warp: per row, lane 0 issues the 16 B-aligned
-    // middle of the CTA's columns as one bulk copy; the unaligned head/tail
-    // elements and the halo columns (wrapped in index math) are spread over
-    // lanes 1.. as element cp.async (one each), so the per-row element work
-    // is not serialised in one thread; every lane's copies arrive on the
-    // stage barrier through cp.async.mbarrier.arrive
+    // span of the CTA's columns as one bulk copy (RowSpan); the elements the
+    // span leaves out — ragged head/tail columns of the row's first/last
+    // CTA, halo columns outside it (wrapped in index math) — go one per lane
+    // (lanes 1..) as element cp.async. Everything that depends only on the
+    // row's 16 B phase is resolved once per CTA for each of the V phases, so
+    // the per-row producer work is a phase lookup, one expect_tx + bulk copy
+    // (lane 0) and at most one element copy per lane: the single producer
+    // warp must issue a stage faster than the consumers drain one (measured:
+    // FP32 4x4 windows were producer-issue-bound at ~150 instructions/row).
+    // Every lane's copies arrive on the stage barrier through
+    // cp.async.mbarrier.arrive; lane 0 adds the bytes row by row
+    // (mbarrier.expect_tx, measured faster than one arrive.expect_tx per
+    // stage computed up front: FP32 odd 3x3 0.885 vs 0.853) and arrives once
+    // per stage.
     const int validC = min(CW, nx - cx0);
     const int l = a.left, r = a.right;
     const T* __restrict__ in = a.in;
+    // lane k >= 1 owns column offset o (relative to cx0) from the disjoint
+    // lists: left halo [-l, 0), head [0, min(V-1, validC)), tail
+    // [max(V-1, validC-(V-1)), validC), right halo [validC, validC + r)
+    int o = 0x40000000;
+    {
+      int k = lane - 1;
+      const int nh = min(V - 1, validC);
+      const int t0 = max(V - 1, validC - (V - 1));
+      if (k >= 0 && k < l) o = k - l;
+      else if ((k -= l) >= 0 && k < nh) o = k;
+      else if ((k -= nh) >= 0 && k < validC - t0) o = t0 + k;
+      else if ((k -= validC - t0) >= 0 && k < r) o = validC + k;
+    }
+    const int c = cx0 + o;  // the lane's global column (unwrapped)
+    const bool inside = c >= 0 && c < nx;
+    const bool srcOk = o != 0x40000000 && (inside || a.wrapX);
+    const int srcCol = inside ? c : (c < 0 ? c + nx : c - nx);
+    int bA0[V], bN[V];  // per phase: bulk span start and length (lane 0)
+    unsigned need = 0;  // per phase: this lane's element copy is needed
+#pragma unroll
+    for (int ph = 0; ph < V; ++ph) {
+      const RowSpan<V> sp(ph, cx0, validC, nx);
+      bA0[ph] = sp.a0;
+      bN[ph] = sp.a1 - sp.a0;
+      const bool covered = inside && sp.a1 > sp.a0 && c >= sp.a0 && c < sp.a1;
+      if (srcOk && !covered) need |= 1u << ph;
+    }
     RowWalk rw;
     rw.init(r0, a.inRows, a.wrapY);
     for (int g = 0; g < nStages; ++g) {
       const int slot = g % STAGES;
       if (g >= STAGES) mbar_wait(&empty[slot], ((g / STAGES) + 1) & 1);
-      int src[RPS];
-      uint32_t tx = 0;
-      RowWalk w2 = rw;
-#pragma unroll
-      for (int k = 0; k < RPS; ++k) {
-        src[k] = w2.cur;
-        const int ph = static_cast<int>((inOff + static_cast<unsigned>(w2.cur) * unx) & (V - 1));
-        const RowSpan<V> sp(ph, cx0, validC, nx);
-        tx += static_cast<uint32_t>((sp.a1 - sp.a0) * sizeof(T));
-        w2.next(a.inRows, a.wrapY);
-      }
-      if (lane == 0) {
-        if (tx) mbar_expect_tx(&full[slot], tx);
-        else mbar_arrive(&full[slot]);
-      }
       T* sstage = ring + slot * (RPS * ROW);
 #pragma unroll
       for (int k = 0; k < RPS; ++k) {
-        const T* grow = in + static_cast<long long>(src[k]) * nx;
-        const int ph = static_cast<int>((inOff + static_cast<unsigned>(src[k]) * unx) & (V - 1));
+        const T* grow = in + static_cast<long long>(rw.cur) * nx;
+        const int ph = static_cast<int>((inOff + static_cast<unsigned>(rw.cur) * unx) & (V - 1));
+        rw.next(a.inRows, a.wrapY);
         T* srow = sstage + k * ROW + HP + ph;  // column cx0 of this row
-        const RowSpan<V> sp(ph, cx0, validC, nx);
-        if (lane == 0 && sp.a1 > sp.a0)
-          bulk_g2s(srow + (sp.a0 - cx0), grow + sp.a0, static_cast<uint32_t>((sp.a1 - sp.a0) * sizeof(T)),
-                   &full[slot]);
-        const int e1 = cx0 + validC;
-        int e = lane - 1;  // this lane's element copy, if any
-        if (e >= 0 && e < sp.hc) {
-          cp_async_elem(srow + e, grow + cx0 + e);
-        } else if ((e -= sp.hc) >= 0 && e < e1 - sp.ts) {
-          cp_async_elem(srow + (sp.ts - cx0) + e, grow + sp.ts + e);
-        } else if ((e -= e1 - sp.ts) >= 0 && e < l) {
-          const int c = cx0 - 1 - e;
-          if (sp.a1 > sp.a0 && c >= sp.a0) {
-            // already staged by the over-fetched bulk copy
-          } else if (c >= 0) {
-            cp_async_elem(srow - 1 - e, grow + c);
-          } else if (a.wrapX) {
-            cp_async_elem(srow - 1 - e, grow + c + nx);
+        if (lane == 0) {
+          int a0 = bA0[0], nb = bN[0];
+#pragma unroll
+          for (int q = 1; q < V; ++q)
+            if (ph == q) {
+              a0 = bA0[q];
+              nb = bN[q];
+            }
+          if (nb > 0) {
+            const uint32_t bytes = static_cast<uint32_t>(nb * sizeof(T));
+            mbar_expect_tx_only(&full[slot], bytes);
+            bulk_g2s(srow + (a0 - cx0), grow + a0, bytes, &full[slot]);
           }
-        } else if ((e -= l) >= 0 && e < r) {
-          const int c = e1 + e;
-          if (sp.a1 > sp.a0 && c < sp.a1) {
-            // already staged by the over-fetched bulk copy
-          } else if (c < nx) {
-            cp_async_elem(srow + validC + e, grow + c);
-          } else if (a.wrapX) {
-            cp_async_elem(srow + validC + e, grow + c - nx);
-          }
+        } else if ((need >> ph) & 1u) {
+          cp_async_elem(srow + o, grow + srcCol);
         }
       }
-      rw = w2;
+      if (lane == 0) mbar_arrive(&full[slot]);
       cp_async_mbar_arrive(&full[slot]);
     }
     return;
