@@ -1,6 +1,7 @@
 # Round-2 final evidence: full GPU suite + smoke, bench + reference arm,
 # launch lists, ncu --set full summaries (headline k_tma, k_tma_g odd/asym,
-# 9x9, partitioned CH sweep), sanitizer (memcheck, racecheck).
+# 9x9, partitioned CH sweep). (compute-sanitizer is closed on the GPU pool;
+# profiles/r02_compute_sanitizer.txt is the earlier round-2 run.)
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f_smoke.log 2>&1; echo smoke=$?; tail -1 gpurun_out/f_smoke.log
 timeout 2400 python -m pytest tests/ -q -m gpu --durations=5 > gpurun_out/f_pytest.log 2>&1; echo pytest=$?; tail -3 gpurun_out/f_pytest.log
@@ -18,8 +19,4 @@ for r in f_k_tma_f64 f_k_tma_g_odd3x3 f_k_tma_g_3100 f_k_tma_g_2112 f_k_sweep_pa
   rm -f gpurun_out/$r.ncu-rep
 done
 for f in f_bench_launches f_ch1024_part8_launches; do python scripts/launch_summary.py gpurun_out/$f.csv > gpurun_out/$f.txt 2>&1; done
-for tool in memcheck racecheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_workload.py > gpurun_out/f_sanitizer_$tool.log 2>&1
-  echo "$tool rc=$?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|workload OK" gpurun_out/f_sanitizer_$tool.log | head -3
-done
 du -sh gpurun_out
