@@ -553,8 +553,10 @@ def bench_variants(sg, torch, stream, peak, n=16384, launches=20, dtype="f64"):
         cols = nxv - (ext.left + ext.right if mode == sg.BoundaryMode.NonPeriodic else 0)
         alg = esz * (n * nxv + rows * cols)
         # FP64 instructions per output point (no FMA contraction: a multiply
-        # and an add per tap; the CH window adds c^3 - c per tap)
-        ops = 5 * nv if fn == "ch_nonlinear_window" else 2 * nv
+        # and an add per tap; the CH window adds c^3 - c once per INPUT point —
+        # the kernel's register window shares it between the windows that
+        # read the point, so 2 * 9 + 3, not 5 per tap)
+        ops = 2 * nv + 3 if fn == "ch_nonlinear_window" else 2 * nv
         rate = ops * rows * cols / (ms * 1e-3)
         fp = "fp32" if f32 else "fp64"
         lanes = 128 if f32 else 64  # FP32 / FP64 lanes per SM per cycle

@@ -77,6 +77,16 @@ struct sg_same<A, A> {
 __device__ __forceinline__ double sg_mac(double acc, double w, double x) { return acc + w * x; }
 __device__ __forceinline__ float sg_mac(float acc, float w, float x) { return __fmaf_rn(w, x, acc); }
 
+// The vector-store condition of the pipelined kernels as a warp vote (see
+// k_tma). SG_STORE_VOTE=0 keeps the per-lane condition (A/B).
+#ifndef SG_STORE_VOTE
+#define SG_STORE_VOTE 1
+#endif
+template <bool VOTE>
+__device__ __forceinline__ bool sg_store_vote(bool lane) {
+  return SG_STORE_VOTE && VOTE ? __all_sync(0xffffffffu, lane) : lane;
+}
+
 constexpr int VMAX = 256;       // values carried in the parameter bank
 constexpr int GENERIC_FN_MAX = 256;  // window taps a generic device function may see
 
@@ -271,9 +281,24 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #ifndef SG_TMA_WARPS_HEAVY
 #define SG_TMA_WARPS_HEAVY 15
 #endif
+// k_tma windows at least SG_TALL_H rows tall (9 x 9 weights: FP64-bound, H
+// x V pending-output chains per lane) on SG_TMA_WARPS_TALL consumers: with
+// the weights in uniform registers (sg_store_vote) the 128-register cap of
+// the 16-warp CTA spills ~30 values per row; 7 consumers have 255.
+// Measured at 16384^2 (scripts/exp/tall_ab.sh): 9 x 9 0.179 -> 0.186 of HBM
+// (11 consumers: 0.174); k_tma_g's odd-row 9 x 9 loses with it (0.165 ->
+// 0.162) and keeps the heavy geometry.
+#ifndef SG_TMA_WARPS_TALL
+#define SG_TMA_WARPS_TALL 7
+#endif
+#ifndef SG_TALL_H
+#define SG_TALL_H 8
+#endif
 constexpr int TMA_WARPS = SG_TMA_WARPS;
 // consumer warps of k_tma (window height H) and of k_tma_g (W x H window)
-__host__ __device__ constexpr int tma_nw(int H) { return H >= 5 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS; }
+__host__ __device__ constexpr int tma_nw(int H) {
+  return H >= SG_TALL_H ? SG_TMA_WARPS_TALL : H >= 5 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS;
+}
 // (k_tma_g: FP64 always on the 16-warp geometry — its odd-row store
 // realignment needs the registers: {3,1,0,0} on odd rows 0.76 -> 0.82 —
 // FP32 light windows stay on 17 warps: FP32 {3,1,0,0} 0.89 -> 0.69 with 16)
@@ -432,7 +457,14 @@ __global__ void __launch_bounds__((TmaGeom<T, L, R, TP, BT>::NW + 1) * 32, (tma_
   T win[ACC ? 1 : H][E];  // ring: input row t lives in win[t % H]
   T pend[ACC ? H : 1][V];  // ACC: output started at local input row u lives in pend[u % H]
   T* __restrict__ orow = a.out + static_cast<long long>(ra - (H - 1)) * nx + xb;
-  const bool vecStore = laneValid && xb >= a.col0 && xb + V <= a.col1;
+  // Warp-uniform (a vote) for FP64 tall weight windows: a lane-dependent
+  // branch around the stores keeps ptxas from holding the weights in uniform
+  // registers (DMUL R, R, UR) — it reloads the taps from the parameter bank
+  // with LDC.64 instead (9 x 9: ~90 LDC per row). Partial warps then take
+  // the element path. Measured at 16384^2 (scripts/exp/vote_ab.sh): FP64 7 x
+  // 7 0.33 -> 0.37 of HBM, 5 x 5 +2 %; the light windows lose with it (3 x
+  // 3 1.03 -> 0.95, FP32 5 x 5 0.94 -> 0.92), so they keep the lane test.
+  const bool vecStore = sg_store_vote<sizeof(T) == 8 && H >= 5>(laneValid && xb >= a.col0 && xb + V <= a.col1);
   const long long rowStep = nx;
   int j = ra - (H - 1);  // output row completed by the current input row
   for (int g = 0; g < nStages; ++g) {
@@ -846,7 +878,13 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
   const int xo = warp * SW + lane * V;  // lane's first output column - cx0
   const int xb = cx0 + xo;
   const bool laneValid = xb < nx;
-  const bool laneFull = laneValid && xb >= a.col0 && xb + V <= a.col1;
+  // a warp vote (see k_tma) for windows of more than 9 taps, and FP32 3 x 3
+  // (16384^2, odd and even rows: FP32 {2,1,1,2} odd 0.71 -> 0.75, 3 x 3 odd
+  // 0.89 -> 0.91, FP64 {2,1,1,2} 0.70 -> 0.80 odd, 0.82 -> 0.89 even,
+  // {1,2,2,1} +7 %, 5 x 5 odd +8 %); FP64 3 x 3 on odd rows loses with it
+  // (0.93 -> 0.90), {3,1,0,0} is neutral
+  const bool laneFull = sg_store_vote<(W * H > 9 || (sizeof(T) == 4 && W * H == 9))>(
+      laneValid && xb >= a.col0 && xb + V <= a.col1);
   const unsigned outOff = static_cast<unsigned>(reinterpret_cast<uintptr_t>(a.out) / sizeof(T));
   const bool peers = a.peerUp != nullptr || a.peerDn != nullptr;
   const bool peerVec = nx % V == 0;  // peer rows share the output rows' phase only then
