@@ -87,6 +87,36 @@ __device__ __forceinline__ bool sg_store_vote(bool lane) {
   return SG_STORE_VOTE && VOTE ? __all_sync(0xffffffffu, lane) : lane;
 }
 
+// Pending-output windows this tall keep a shifting accumulator ring (ROT in
+// k_tma / k_tma_g) instead of a ring indexed by the unrolled row.
+#ifndef SG_ROT_MIN_H
+#define SG_ROT_MIN_H 8
+#endif
+
+// One input row e[0 .. V+W-1] of a weight window with H x V pending outputs:
+// pend[q] holds the output started q rows ago; this row is its tap row q.
+// Adds the row to every pending output (taps of one output still in the
+// reference's row-major order), hands back the completed output (q = H-1)
+// and shifts the ring by one row (pend[0] restarts at 0).
+template <typename T, int W, int H, int V>
+__device__ __forceinline__ void sg_acc_rows_rot(T (&pend)[H][V], const T* __restrict__ wts, const T* e, T* res) {
+#pragma unroll
+  for (int q = 0; q < H; ++q)
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      T acc = q == 0 ? T(0) : pend[q][v];
+#pragma unroll
+      for (int p = 0; p < W; ++p) acc = sg_mac(acc, wts[q * W + p], e[v + p]);
+      pend[q][v] = acc;
+    }
+#pragma unroll
+  for (int v = 0; v < V; ++v) res[v] = pend[H - 1][v];
+#pragma unroll
+  for (int q = H - 1; q > 0; --q)
+#pragma unroll
+    for (int v = 0; v < V; ++v) pend[q][v] = pend[q - 1][v];
+}
+
 constexpr int VMAX = 256;       // values carried in the parameter bank
 constexpr int GENERIC_FN_MAX = 256;  // window taps a generic device function may see
 
@@ -454,6 +484,11 @@ __global__ void __launch_bounds__((TmaGeom<T, L, R, TP, BT>::NW + 1) * 32, (tma_
   // rows arrive top to bottom. Registers: H*V + E instead of H*E (a 9x9
   // window would otherwise spill).
   constexpr bool ACC = sg_same<Op, OpWeights>::value && H >= SG_ACC_MIN_H;
+  // ROT (windows >= SG_ROT_MIN_H rows): the pending outputs shift one slot
+  // per row (pend[q] = the output started q rows ago) so the row loop stays
+  // rolled — 9 unrolled rows of a 9 x 9 window are ~3.5 k instructions and
+  // stalled on instruction fetch; the shift costs (H - 1) x V moves per row
+  constexpr bool ROT = ACC && H >= SG_ROT_MIN_H;
   T win[ACC ? 1 : H][E];  // ring: input row t lives in win[t % H]
   T pend[ACC ? H : 1][V];  // ACC: output started at local input row u lives in pend[u % H]
   T* __restrict__ orow = a.out + static_cast<long long>(ra - (H - 1)) * nx + xb;
@@ -471,7 +506,7 @@ __global__ void __launch_bounds__((TmaGeom<T, L, R, TP, BT>::NW + 1) * 32, (tma_
     const int slot = g % STAGES;
     mbar_wait(&full[slot], (g / STAGES) & 1);
     const T* sbase = ring + slot * (RPS * ROW) + LP + warp * SW + lane * V;
-#pragma unroll
+#pragma unroll(ROT ? 1 : RPS)
     for (int k = 0; k < RPS; ++k) {
       const T* srow = sbase + k * ROW;
       T* e = win[ACC ? 0 : k % H];
@@ -497,7 +532,9 @@ __global__ void __launch_bounds__((TmaGeom<T, L, R, TP, BT>::NW + 1) * 32, (tma_
       // Output row j uses input rows j-TP .. j+BT = the H most recent rows,
       // oldest in slot (k + 1) % H.
       T res[V];
-      if constexpr (ACC) {
+      if constexpr (ROT) {
+        sg_acc_rows_rot<T, W, H, V>(pend, a.v, e, res);
+      } else if constexpr (ACC) {
         // this row is tap row q of the output started q rows ago (slot
         // (k - q) mod H; RPS is a multiple of H, so slots are compile-time)
 #pragma unroll
@@ -889,6 +926,7 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
   const bool peers = a.peerUp != nullptr || a.peerDn != nullptr;
   const bool peerVec = nx % V == 0;  // peer rows share the output rows' phase only then
   constexpr bool ACC = sg_same<Op, OpWeights>::value && H >= SG_ACC_MIN_H;
+  constexpr bool ROT = ACC && H >= SG_ROT_MIN_H;  // (see k_tma)
   T win[ACC ? 1 : H][E];   // ring: input row t lives in win[t % H]
   T pend[ACC ? H : 1][V];  // ACC: output started at local input row u lives in pend[u % H]
   RowWalk rw;
@@ -898,7 +936,7 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
     const int slot = g % STAGES;
     mbar_wait(&full[slot], (g / STAGES) & 1);
     const T* sbase = ring + slot * (RPS * ROW) + HP + xo - a.left;
-#pragma unroll
+#pragma unroll(ROT ? 1 : RPS)
     for (int k = 0; k < RPS; ++k) {
       const int ph = static_cast<int>((inOff + static_cast<unsigned>(rw.cur) * unx) & (V - 1));
       rw.next(a.inRows, a.wrapY);
@@ -909,7 +947,9 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
 #pragma unroll
       for (int p = 0; p < E; ++p) e[p] = srow[p];
       T res[V];
-      if constexpr (ACC) {
+      if constexpr (ROT) {
+        sg_acc_rows_rot<T, W, H, V>(pend, a.v, e, res);
+      } else if constexpr (ACC) {
 #pragma unroll
         for (int q = 0; q < H; ++q) {
           T* acc = pend[((k - q) % H + H) % H];
