@@ -3,9 +3,15 @@
 // B200 C ABI (stengrid/sg.h). Same names, signatures and exceptions.
 //
 // Storage: the reference uses an Eigen row-major array purely as storage
-// (SURVEY.md §8(c)); here `Array2d` is a dense row-major container with the
+// (SURVEY.md §8(c)). When <Eigen/Core> is on the include path (or
+// STENGRID_USE_EIGEN is defined) `Array2d` / `ArrayXd` ARE the reference's
+// Eigen types, so caller code that applies Eigen expressions to
+// `Grid2D::values` compiles unchanged; otherwise (this image has no Eigen;
+// STENGRID_NO_EIGEN forces it) they are dense row-major containers with the
 // members the reference API and its tests use (setZero, setConstant,
-// operator()(row, col), data, size, rows, cols, transpose, swap).
+// operator()(row, col), data, size, rows, cols, transpose, swap). The library
+// itself only exchanges raw pointers (data()) with the C ABI, so both
+// storages bind the same libstengrid_b200.so.
 #pragma once
 
 #include <algorithm>
@@ -20,6 +26,11 @@
 #include "stengrid/errors.hpp"
 #include "stengrid/sg.h"
 
+#if !defined(STENGRID_NO_EIGEN) && (defined(STENGRID_USE_EIGEN) || __has_include(<Eigen/Core>))
+#include <Eigen/Core>
+#define STENGRID_EIGEN_STORAGE 1
+#endif
+
 namespace stengrid {
 
 namespace detail {
@@ -32,6 +43,13 @@ inline std::int64_t large_alloc_count() noexcept { return large_alloc_counter().
 inline void note_large_alloc() noexcept { large_alloc_counter().fetch_add(1, std::memory_order_relaxed); }
 }  // namespace detail
 
+#ifdef STENGRID_EIGEN_STORAGE
+/// The reference's storage types (grid.hpp:13, penta.hpp).
+template <typename T>
+using DenseArray2 = Eigen::Array<T, Eigen::Dynamic, Eigen::Dynamic, Eigen::RowMajor>;
+template <typename T>
+using DenseVector = Eigen::Array<T, Eigen::Dynamic, 1>;
+#else
 /// Dense row-major 2D array of T (the subset of Eigen::Array the reference uses).
 template <typename T>
 class DenseArray2 {
@@ -95,6 +113,8 @@ class DenseVector {
  private:
   std::vector<T> v_;
 };
+
+#endif  // STENGRID_EIGEN_STORAGE
 
 /// Row-major storage backing every field: entry (j, i) at j*nx + i.
 using Array2d = DenseArray2<double>;
