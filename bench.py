@@ -557,6 +557,8 @@ def bench_variants(sg, torch, stream, peak, n=16384, launches=20, dtype="f64"):
         # the kernel's register window shares it between the windows that
         # read the point, so 2 * 9 + 3, not 5 per tap)
         ops = 2 * nv + 3 if fn == "ch_nonlinear_window" else 2 * nv
+        if f32 and fn is None:
+            ops = nv  # FP32 taps contract to one FFMA each (sg_mac)
         rate = ops * rows * cols / (ms * 1e-3)
         fp = "fp32" if f32 else "fp64"
         lanes = 128 if f32 else 64  # FP32 / FP64 lanes per SM per cycle
