@@ -117,6 +117,12 @@ __device__ __forceinline__ void sg_acc_rows_rot(T (&pend)[H][V], const T* __rest
     for (int v = 0; v < V; ++v) pend[q][v] = pend[q - 1][v];
 }
 
+// k_generic weight windows: 4 output rows per thread reusing each staged
+// row (1), or one output per pass (0, A/B)
+#ifndef SG_GENERIC_ROWS4
+#define SG_GENERIC_ROWS4 1
+#endif
+
 constexpr int VMAX = 256;       // values carried in the parameter bank
 constexpr int GENERIC_FN_MAX = 256;  // window taps a generic device function may see
 
@@ -645,6 +651,41 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T
     }
     __syncthreads();
     const int i = i0 + threadIdx.x;
+    if constexpr (sg_same<Op, OpWeights>::value && SG_GENERIC_ROWS4) {
+      // each thread: 4 consecutive output rows of one column. Every staged
+      // row is read once and added to each output it is a tap row of —
+      // per output still tap rows ascending, then columns (the reference's
+      // order). No lane-dependent exit before the loops (it would cost the
+      // uniform datapath for the weights, cf. k_tma); lanes past col1
+      // compute on clamped tile values and do not store.
+      const int y0 = 4 * threadIdx.y;
+      T acc[4] = {T(0), T(0), T(0), T(0)};
+      auto rows = [&](auto wt) {  // wt(idx): the weight, from the parameter bank or wdev
+#pragma unroll 1
+        for (int t = 0; t < H + 3; ++t) {
+          const T* rowp = tile + (y0 + t) * TW + threadIdx.x;
+#pragma unroll 2
+          for (int p = 0; p < W; ++p) {
+            const T x = rowp[p];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int q = t - k;
+              if (q >= 0 && q < H) acc[k] = sg_mac(acc[k], wt(q * W + p), x);
+            }
+          }
+        }
+      };
+      if (a.count <= VMAX)
+        rows([&](int idx) { return a.v[idx]; });
+      else
+        rows([&](int idx) { return __ldg(a.wdev + idx); });
+      if (i < a.col1) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (j0 + y0 + k < a.row1) put_out(a, j0 + y0 + k, i, acc[k]);
+      }
+      return;
+    }
     if (i >= a.col1) return;
 #pragma unroll 1
     for (int k = 0; k < 4; ++k) {
