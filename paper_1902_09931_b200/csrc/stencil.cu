@@ -167,9 +167,11 @@ int launch_typed(const sg_slab_desc& d, const sg_extents& e, int fn, const doubl
     a.wdev = wtmp;
   }
   dim3 block(32, 8);
-  const size_t tileB = generic_tile_bytes<T>(e);
+  const bool weights = fn == SG_FN_NONE;
+  const size_t tileB = generic_tile_bytes<T>(e, weights);
   a.gtile = tileB > 0 ? 1 : 0;
-  dim3 grid((cols + 31) / 32, tileB > 0 ? (rows + 31) / 32 : (rows + 7) / 8);
+  const int gw = tileB > 0 ? generic_tile_cols(weights) : 32;
+  dim3 grid((cols + gw - 1) / gw, tileB > 0 ? (rows + 31) / 32 : (rows + 7) / 8);
   with_op<void>(fn, [&](auto op) { k_generic<T, decltype(op)><<<grid, block, tileB, s>>>(a); });
   check_launch("stencil generic kernel");
   if (wtmp) SG_CUDA(cudaFreeAsync(wtmp, s));

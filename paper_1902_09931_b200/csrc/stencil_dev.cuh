@@ -630,8 +630,10 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T
   if (a.gtile) {
     extern __shared__ __align__(16) unsigned char gsm[];
     T* tile = reinterpret_cast<T*>(gsm);
-    const int TW = 32 + W - 1, TH = 32 + H - 1;
-    const int i0 = a.col0 + blockIdx.x * 32, j0 = a.row0 + blockIdx.y * 32;
+    // weight windows: 64 output columns per CTA (two per thread)
+    constexpr int GW = sg_same<Op, OpWeights>::value && SG_GENERIC_ROWS4 ? 64 : 32;
+    const int TW = GW + W - 1, TH = 32 + H - 1;
+    const int i0 = a.col0 + blockIdx.x * GW, j0 = a.row0 + blockIdx.y * 32;
     const int tid = threadIdx.y * 32 + threadIdx.x;
     for (int e = tid; e < TW * TH; e += 256) {
       const int ty = e / TW, tx = e - ty * TW;
@@ -658,19 +660,44 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T
       // order). No lane-dependent exit before the loops (it would cost the
       // uniform datapath for the weights, cf. k_tma); lanes past col1
       // compute on clamped tile values and do not store.
+      // (and columns threadIdx.x, threadIdx.x + 32: each weight load feeds
+      // eight multiply-adds)
       const int y0 = 4 * threadIdx.y;
-      T acc[4] = {T(0), T(0), T(0), T(0)};
+      T acc[2][4] = {{T(0), T(0), T(0), T(0)}, {T(0), T(0), T(0), T(0)}};
       auto rows = [&](auto wt) {  // wt(idx): the weight, from the parameter bank or wdev
 #pragma unroll 1
         for (int t = 0; t < H + 3; ++t) {
           const T* rowp = tile + (y0 + t) * TW + threadIdx.x;
+          if (t >= 3 && t < H) {
+            // staged row t is tap row t - k of output k, for all four:
+            // no predicates, one running weight index per output
+            const int i0 = t * W, i1 = i0 - W, i2 = i1 - W, i3 = i2 - W;
+#pragma unroll 4
+            for (int p = 0; p < W; ++p) {
+              const T x0 = rowp[p], x1 = rowp[p + 32];
+              const T w0 = wt(i0 + p), w1 = wt(i1 + p), w2 = wt(i2 + p), w3 = wt(i3 + p);
+              acc[0][0] = sg_mac(acc[0][0], w0, x0);
+              acc[0][1] = sg_mac(acc[0][1], w1, x0);
+              acc[0][2] = sg_mac(acc[0][2], w2, x0);
+              acc[0][3] = sg_mac(acc[0][3], w3, x0);
+              acc[1][0] = sg_mac(acc[1][0], w0, x1);
+              acc[1][1] = sg_mac(acc[1][1], w1, x1);
+              acc[1][2] = sg_mac(acc[1][2], w2, x1);
+              acc[1][3] = sg_mac(acc[1][3], w3, x1);
+            }
+            continue;
+          }
 #pragma unroll 2
           for (int p = 0; p < W; ++p) {
-            const T x = rowp[p];
+            const T x0 = rowp[p], x1 = rowp[p + 32];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const int q = t - k;
-              if (q >= 0 && q < H) acc[k] = sg_mac(acc[k], wt(q * W + p), x);
+              if (q >= 0 && q < H) {
+                const T w = wt(q * W + p);
+                acc[0][k] = sg_mac(acc[0][k], w, x0);
+                acc[1][k] = sg_mac(acc[1][k], w, x1);
+              }
             }
           }
         }
@@ -679,11 +706,13 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T
         rows([&](int idx) { return a.v[idx]; });
       else
         rows([&](int idx) { return __ldg(a.wdev + idx); });
-      if (i < a.col1) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (j0 + y0 + k < a.row1) put_out(a, j0 + y0 + k, i, acc[k]);
-      }
+      for (int c = 0; c < 2; ++c)
+        if (i + 32 * c < a.col1) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (j0 + y0 + k < a.row1) put_out(a, j0 + y0 + k, i + 32 * c, acc[c][k]);
+        }
       return;
     }
     if (i >= a.col1) return;

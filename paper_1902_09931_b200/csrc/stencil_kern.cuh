@@ -64,11 +64,15 @@ inline bool stencil_pdl() {
   return v;
 }
 
-// k_generic's staged input tile (32 + W - 1) x (32 + H - 1) in bytes, or 0
-// when it would exceed 48 KB (taps are then read from global memory).
+// k_generic's staged input tile (GW + W - 1) x (32 + H - 1) in bytes, or 0
+// when it would exceed 48 KB (taps are then read from global memory); GW =
+// generic_tile_cols: 64 output columns per CTA for weight windows (two per
+// thread), 32 for functions.
+inline int generic_tile_cols(bool weights) { return weights && SG_GENERIC_ROWS4 ? 64 : 32; }
 template <typename T>
-size_t generic_tile_bytes(const sg_extents& e) {
-  const size_t b = static_cast<size_t>(32 + e.left + e.right) * (32 + e.top + e.bottom) * sizeof(T);
+size_t generic_tile_bytes(const sg_extents& e, bool weights = false) {
+  const size_t b = static_cast<size_t>(generic_tile_cols(weights) + e.left + e.right) * (32 + e.top + e.bottom) *
+                   sizeof(T);
   return b <= (48u << 10) ? b : 0;
 }
 
