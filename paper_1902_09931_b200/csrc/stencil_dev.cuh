@@ -330,16 +330,29 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #ifndef SG_TALL_H
 #define SG_TALL_H 8
 #endif
+// k_tma_g tall windows: 7 consumers too (16384^2 FP64, rolled ring: 9 x 9
+// odd rows 0.168 -> 0.179 of HBM, (0,8,8,0) 0.168 -> 0.186; no spills)
+#ifndef SG_TMAG_WARPS_TALL
+#define SG_TMAG_WARPS_TALL 7
+#endif
 constexpr int TMA_WARPS = SG_TMA_WARPS;
 // consumer warps of k_tma (window height H) and of k_tma_g (W x H window)
-__host__ __device__ constexpr int tma_nw(int H) {
-  return H >= SG_TALL_H ? SG_TMA_WARPS_TALL : H >= 5 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS;
+// (tall = at least SG_TALL_H rows and SG_TALL_TAPS taps: FP64-bound; a 1 x 9
+// column window streams and keeps the wide CTA — k_tma_g's odd-row (0,0,4,4)
+// 0.85 -> 0.58 of HBM on 7 consumers — and 5 x 9 on odd rows loses too,
+// 0.34 -> 0.29; scripts/exp/gtall_ab.sh)
+#ifndef SG_TALL_TAPS
+#define SG_TALL_TAPS 60
+#endif
+__host__ __device__ constexpr bool tma_tall(int W, int H) { return H >= SG_TALL_H && W * H >= SG_TALL_TAPS; }
+__host__ __device__ constexpr int tma_nw(int H, int W = 1) {
+  return tma_tall(W, H) ? SG_TMA_WARPS_TALL : H >= 5 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS;
 }
 // (k_tma_g: FP64 always on the 16-warp geometry — its odd-row store
 // realignment needs the registers: {3,1,0,0} on odd rows 0.76 -> 0.82 —
 // FP32 light windows stay on 17 warps: FP32 {3,1,0,0} 0.89 -> 0.69 with 16)
 __host__ __device__ constexpr int tmag_nw(int W, int H, int esz) {
-  return esz == 8 || W * H >= 9 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS;
+  return tma_tall(W, H) ? SG_TMAG_WARPS_TALL : esz == 8 || W * H >= 9 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS;
 }
 // Release of a ring stage by the consumers: every thread arrives on the
 // "empty" mbarrier (1), or each warp's lane 0 after __syncwarp (0).
@@ -351,7 +364,7 @@ template <typename T, int L, int R, int TP, int BT>
 struct TmaGeom {
   static constexpr int V = VecT<T>::V;
   static constexpr int SW = 32 * V;
-  static constexpr int NW = tma_nw(TP + BT + 1);
+  static constexpr int NW = tma_nw(TP + BT + 1, L + R + 1);
   static constexpr int CW = NW * SW;
   static constexpr int LP = ((L + V - 1) / V) * V;  // left pad, 16 B granules
   static constexpr int RP = ((R + V - 1) / V) * V;
