@@ -344,15 +344,18 @@ constexpr int TMA_WARPS = SG_TMA_WARPS;
 #ifndef SG_TALL_TAPS
 #define SG_TALL_TAPS 60
 #endif
-__host__ __device__ constexpr bool tma_tall(int W, int H) { return H >= SG_TALL_H && W * H >= SG_TALL_TAPS; }
-__host__ __device__ constexpr int tma_nw(int H, int W = 1) {
-  return tma_tall(W, H) ? SG_TMA_WARPS_TALL : H >= 5 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS;
+// FP64 only: FP32 9 x 9 on 7 consumers 0.39 -> 0.30 of HBM (gtall32_ab.sh)
+__host__ __device__ constexpr bool tma_tall(int W, int H, int esz) {
+  return esz == 8 && H >= SG_TALL_H && W * H >= SG_TALL_TAPS;
+}
+__host__ __device__ constexpr int tma_nw(int H, int W, int esz) {
+  return tma_tall(W, H, esz) ? SG_TMA_WARPS_TALL : H >= 5 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS;
 }
 // (k_tma_g: FP64 always on the 16-warp geometry — its odd-row store
 // realignment needs the registers: {3,1,0,0} on odd rows 0.76 -> 0.82 —
 // FP32 light windows stay on 17 warps: FP32 {3,1,0,0} 0.89 -> 0.69 with 16)
 __host__ __device__ constexpr int tmag_nw(int W, int H, int esz) {
-  return tma_tall(W, H) ? SG_TMAG_WARPS_TALL : esz == 8 || W * H >= 9 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS;
+  return tma_tall(W, H, esz) ? SG_TMAG_WARPS_TALL : esz == 8 || W * H >= 9 ? SG_TMA_WARPS_HEAVY : SG_TMA_WARPS;
 }
 // Release of a ring stage by the consumers: every thread arrives on the
 // "empty" mbarrier (1), or each warp's lane 0 after __syncwarp (0).
@@ -364,7 +367,7 @@ template <typename T, int L, int R, int TP, int BT>
 struct TmaGeom {
   static constexpr int V = VecT<T>::V;
   static constexpr int SW = 32 * V;
-  static constexpr int NW = tma_nw(TP + BT + 1, L + R + 1);
+  static constexpr int NW = tma_nw(TP + BT + 1, L + R + 1, static_cast<int>(sizeof(T)));
   static constexpr int CW = NW * SW;
   static constexpr int LP = ((L + V - 1) / V) * V;  // left pad, 16 B granules
   static constexpr int RP = ((R + V - 1) / V) * V;

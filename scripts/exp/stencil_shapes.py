@@ -17,7 +17,9 @@ peak = json.loads((Path(__file__).resolve().parents[2] / "MEASURED_PEAKS.json").
 shapes = [tuple(int(x) for x in s.split(",")) for s in sys.argv[1:]] or [
     (3, 1, 0, 0), (2, 1, 1, 2), (2, 2, 2, 2), (4, 4, 4, 4), (1, 1, 1, 1), (2, 2, 0, 0), (1, 2, 2, 1), (2, 2, 2, 1),
     (3, 3, 3, 3), (0, 0, 2, 2)]
-a = torch.rand((n, n), dtype=torch.float64, device="cuda")
+DT = torch.float32 if os.environ.get("SG_DT") == "f32" else torch.float64
+ESZ = 4 if DT == torch.float32 else 8
+a = torch.rand((n, n), dtype=DT, device="cuda")
 b = torch.zeros_like(a)
 rng = np.random.default_rng(0)
 for odd in (False, True):
@@ -42,6 +44,6 @@ for odd in (False, True):
         ms = e0.elapsed_time(e1) / reps
         print(json.dumps({"lib": os.environ.get("SG_LIB_PATH", "default"), "ext": ext, "nx": nxv,
                           "kind": plan.kernel_kind(), "ms": round(ms, 4),
-                          "hbm_frac": round(16 * n * nxv / (ms * 1e-3) / 1e9 / peak, 4),
+                          "hbm_frac": round(2 * ESZ * n * nxv / (ms * 1e-3) / 1e9 / peak, 4), "esz": ESZ,
                           "fp64_ops": 2 * nv}), flush=True)
         sg.destroy_plan(plan)
