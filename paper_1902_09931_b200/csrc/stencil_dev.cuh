@@ -92,6 +92,11 @@ __device__ __forceinline__ bool sg_store_vote(bool lane) {
 #ifndef SG_ROT_MIN_H
 #define SG_ROT_MIN_H 8
 #endif
+// FP32 from 7 rows (7 x 7 0.58 -> 0.62 of HBM, 5 x 7 0.74 -> 0.78; 5 x 5 on
+// odd rows loses: 0.64 -> 0.61; scripts/exp/rot32_ab.sh)
+#ifndef SG_ROT_MIN_H_F32
+#define SG_ROT_MIN_H_F32 7
+#endif
 
 // One input row e[0 .. V+W-1] of a weight window with H x V pending outputs:
 // pend[q] holds the output started q rows ago; this row is its tap row q.
@@ -510,7 +515,7 @@ __global__ void __launch_bounds__((TmaGeom<T, L, R, TP, BT>::NW + 1) * 32, (tma_
   // per row (pend[q] = the output started q rows ago) so the row loop stays
   // rolled — 9 unrolled rows of a 9 x 9 window are ~3.5 k instructions and
   // stalled on instruction fetch; the shift costs (H - 1) x V moves per row
-  constexpr bool ROT = ACC && H >= SG_ROT_MIN_H;
+  constexpr bool ROT = ACC && H >= (sizeof(T) == 4 ? SG_ROT_MIN_H_F32 : SG_ROT_MIN_H);
   T win[ACC ? 1 : H][E];  // ring: input row t lives in win[t % H]
   T pend[ACC ? H : 1][V];  // ACC: output started at local input row u lives in pend[u % H]
   T* __restrict__ orow = a.out + static_cast<long long>(ra - (H - 1)) * nx + xb;
@@ -1012,7 +1017,7 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
   const bool peers = a.peerUp != nullptr || a.peerDn != nullptr;
   const bool peerVec = nx % V == 0;  // peer rows share the output rows' phase only then
   constexpr bool ACC = sg_same<Op, OpWeights>::value && H >= SG_ACC_MIN_H;
-  constexpr bool ROT = ACC && H >= SG_ROT_MIN_H;  // (see k_tma)
+  constexpr bool ROT = ACC && H >= (sizeof(T) == 4 ? SG_ROT_MIN_H_F32 : SG_ROT_MIN_H);  // (see k_tma)
   T win[ACC ? 1 : H][E];   // ring: input row t lives in win[t % H]
   T pend[ACC ? H : 1][V];  // ACC: output started at local input row u lives in pend[u % H]
   RowWalk rw;
