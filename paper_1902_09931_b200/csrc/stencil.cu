@@ -172,6 +172,12 @@ int launch_typed(const sg_slab_desc& d, const sg_extents& e, int fn, const doubl
   a.gtile = tileB > 0 ? 1 : 0;
   const int gw = tileB > 0 ? generic_tile_cols(weights) : 32;
   dim3 grid((cols + gw - 1) / gw, tileB > 0 ? (rows + 31) / 32 : (rows + 7) / 8);
+  if (weights && tileB > (48u << 10)) {
+    static const cudaError_t optin =  // once per T (thread-safe static init)
+        cudaFuncSetAttribute(k_generic<T, OpWeights>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(SG_GENERIC_SMEM));
+    SG_CUDA(optin);
+  }
   with_op<void>(fn, [&](auto op) { k_generic<T, decltype(op)><<<grid, block, tileB, s>>>(a); });
   check_launch("stencil generic kernel");
   if (wtmp) SG_CUDA(cudaFreeAsync(wtmp, s));

@@ -127,6 +127,14 @@ __device__ __forceinline__ void sg_acc_rows_rot(T (&pend)[H][V], const T* __rest
 #ifndef SG_GENERIC_ROWS4
 #define SG_GENERIC_ROWS4 1
 #endif
+// ... and SG_GENERIC_NC columns per thread (32 apart)
+#ifndef SG_GENERIC_NC
+#define SG_GENERIC_NC 4
+#endif
+// k_generic's staged tile limit (dynamic shared memory, opted in beyond 48 KB)
+#ifndef SG_GENERIC_SMEM
+#define SG_GENERIC_SMEM (96 * 1024)
+#endif
 
 constexpr int VMAX = 256;       // values carried in the parameter bank
 constexpr int GENERIC_FN_MAX = 256;  // window taps a generic device function may see
@@ -652,7 +660,7 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T
     extern __shared__ __align__(16) unsigned char gsm[];
     T* tile = reinterpret_cast<T*>(gsm);
     // weight windows: 64 output columns per CTA (two per thread)
-    constexpr int GW = sg_same<Op, OpWeights>::value && SG_GENERIC_ROWS4 ? 64 : 32;
+    constexpr int GW = sg_same<Op, OpWeights>::value && SG_GENERIC_ROWS4 ? 32 * SG_GENERIC_NC : 32;
     const int TW = GW + W - 1, TH = 32 + H - 1;
     const int i0 = a.col0 + blockIdx.x * GW, j0 = a.row0 + blockIdx.y * 32;
     const int tid = threadIdx.y * 32 + threadIdx.x;
@@ -684,7 +692,12 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T
       // (and columns threadIdx.x, threadIdx.x + 32: each weight load feeds
       // eight multiply-adds)
       const int y0 = 4 * threadIdx.y;
-      T acc[2][4] = {{T(0), T(0), T(0), T(0)}, {T(0), T(0), T(0), T(0)}};
+      constexpr int NC = SG_GENERIC_NC;
+      T acc[NC][4];
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[c][k] = T(0);
       auto rows = [&](auto wt) {  // wt(idx): the weight, from the parameter bank or wdev
 #pragma unroll 1
         for (int t = 0; t < H + 3; ++t) {
@@ -695,29 +708,27 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T
             const int i0 = t * W, i1 = i0 - W, i2 = i1 - W, i3 = i2 - W;
 #pragma unroll 4
             for (int p = 0; p < W; ++p) {
-              const T x0 = rowp[p], x1 = rowp[p + 32];
               const T w0 = wt(i0 + p), w1 = wt(i1 + p), w2 = wt(i2 + p), w3 = wt(i3 + p);
-              acc[0][0] = sg_mac(acc[0][0], w0, x0);
-              acc[0][1] = sg_mac(acc[0][1], w1, x0);
-              acc[0][2] = sg_mac(acc[0][2], w2, x0);
-              acc[0][3] = sg_mac(acc[0][3], w3, x0);
-              acc[1][0] = sg_mac(acc[1][0], w0, x1);
-              acc[1][1] = sg_mac(acc[1][1], w1, x1);
-              acc[1][2] = sg_mac(acc[1][2], w2, x1);
-              acc[1][3] = sg_mac(acc[1][3], w3, x1);
+#pragma unroll
+              for (int c = 0; c < NC; ++c) {
+                const T x = rowp[p + 32 * c];
+                acc[c][0] = sg_mac(acc[c][0], w0, x);
+                acc[c][1] = sg_mac(acc[c][1], w1, x);
+                acc[c][2] = sg_mac(acc[c][2], w2, x);
+                acc[c][3] = sg_mac(acc[c][3], w3, x);
+              }
             }
             continue;
           }
 #pragma unroll 2
           for (int p = 0; p < W; ++p) {
-            const T x0 = rowp[p], x1 = rowp[p + 32];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const int q = t - k;
               if (q >= 0 && q < H) {
                 const T w = wt(q * W + p);
-                acc[0][k] = sg_mac(acc[0][k], w, x0);
-                acc[1][k] = sg_mac(acc[1][k], w, x1);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) acc[c][k] = sg_mac(acc[c][k], w, rowp[p + 32 * c]);
               }
             }
           }
@@ -728,7 +739,7 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ KArgs<T
       else
         rows([&](int idx) { return __ldg(a.wdev + idx); });
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
+      for (int c = 0; c < NC; ++c)
         if (i + 32 * c < a.col1) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)

@@ -65,15 +65,18 @@ inline bool stencil_pdl() {
 }
 
 // k_generic's staged input tile (GW + W - 1) x (32 + H - 1) in bytes, or 0
-// when it would exceed 48 KB (taps are then read from global memory); GW =
-// generic_tile_cols: 64 output columns per CTA for weight windows (two per
-// thread), 32 for functions.
-inline int generic_tile_cols(bool weights) { return weights && SG_GENERIC_ROWS4 ? 64 : 32; }
+// when it would exceed the limit (taps are then read from global memory); GW
+// = generic_tile_cols: 32 x SG_GENERIC_NC output columns per CTA for weight
+// windows (SG_GENERIC_NC per thread), 32 for functions. Weight tiles may use
+// up to SG_GENERIC_SMEM (the launcher opts in), function tiles 48 KB (the
+// NVRTC path launches them without the opt-in).
+inline int generic_tile_cols(bool weights) { return weights && SG_GENERIC_ROWS4 ? 32 * SG_GENERIC_NC : 32; }
 template <typename T>
 size_t generic_tile_bytes(const sg_extents& e, bool weights = false) {
   const size_t b = static_cast<size_t>(generic_tile_cols(weights) + e.left + e.right) * (32 + e.top + e.bottom) *
                    sizeof(T);
-  return b <= (48u << 10) ? b : 0;
+  const size_t lim = weights ? static_cast<size_t>(SG_GENERIC_SMEM) : (48u << 10);
+  return b <= lim ? b : 0;
 }
 
 inline int sm_count() {
