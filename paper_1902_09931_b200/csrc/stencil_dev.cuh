@@ -541,8 +541,14 @@ __global__ void __launch_bounds__((TmaGeom<T, L, R, TP, BT>::NW + 1) * 32, (tma_
     const int slot = g % STAGES;
     mbar_wait(&full[slot], (g / STAGES) & 1);
     const T* sbase = ring + slot * (RPS * ROW) + LP + warp * SW + lane * V;
-#pragma unroll(ROT ? 1 : RPS)
-    for (int k = 0; k < RPS; ++k) {
+    // rows of the stage: fully unrolled (plain `#pragma unroll`: an
+    // explicit factor changed ptxas' schedule, FP64 odd-row 3 x 3 0.94 ->
+    // 0.91 of HBM), or one rolled row at a time for ROT
+#pragma unroll 1
+    for (int kk = 0; kk < (ROT ? RPS : 1); ++kk)
+#pragma unroll
+    for (int k0 = 0; k0 < (ROT ? 1 : RPS); ++k0) {
+      const int k = kk + k0;
       const T* srow = sbase + k * ROW;
       T* e = win[ACC ? 0 : k % H];
       const VT c = *reinterpret_cast<const VT*>(srow);
@@ -1038,8 +1044,11 @@ __global__ void __launch_bounds__((TmaGGeom<T, W, H>::NW + 1) * 32, (tmag_min_bl
     const int slot = g % STAGES;
     mbar_wait(&full[slot], (g / STAGES) & 1);
     const T* sbase = ring + slot * (RPS * ROW) + HP + xo - a.left;
-#pragma unroll(ROT ? 1 : RPS)
-    for (int k = 0; k < RPS; ++k) {
+#pragma unroll 1
+    for (int kk = 0; kk < (ROT ? RPS : 1); ++kk)  // (see k_tma)
+#pragma unroll
+    for (int k0 = 0; k0 < (ROT ? 1 : RPS); ++k0) {
+      const int k = kk + k0;
       const int ph = static_cast<int>((inOff + static_cast<unsigned>(rw.cur) * unx) & (V - 1));
       rw.next(a.inRows, a.wrapY);
       const T* srow = sbase + k * ROW + ph;  // window column 0 of the lane's first output
